@@ -1,0 +1,241 @@
+/*
+ * rig_oracle.c -- CPU ORACLE for the row inner-product graph (G_RIP) and its
+ * cutsize.  TEST INFRASTRUCTURE ONLY: only tests/, __graft_entry__.smoke()
+ * and bench.py's cpu_baseline / --impl reference legs may load this library.
+ * The product path (paper_1710_07769_b200/) never links, imports or calls it,
+ * and shares no code, header, table or helper with it.
+ *
+ * It is the plain definition written out, in the paper's order:
+ *
+ *   PAPER.md:293-301  (§2.1, eq. E)    edge (v_i,v_j) iff r_i r_j^T != 0
+ *   PAPER.md:310-315  (§2.1, eq14)     cost(v_i,v_j) = |r_i r_j^T|
+ *   PAPER.md:317-318  (§2.1)           optional prescaling of rows to unit 2-norm
+ *   PAPER.md:321-325, 351-352 (§2.1)   G_RIP == graph of C = A A^T, diagonal ignored
+ *   PAPER.md:560-562  (§2.3)           C computed by basic (Gustavson) SpGEMM
+ *   PAPER.md:393-405, 1150-1154 (§2.2, eq. partcut)
+ *                                      cutsize(Pi) = sum of costs of cut edges
+ *
+ * Readings where the paper is silent:
+ *   - ordering contract: for each (i,j), c_ij = fma-chain over the shared
+ *     columns k in ASCENDING k, starting from +0.0 (c2 #4);
+ *   - scaling: ss = ascending-k fma chain of a_ik^2 from +0.0, nrm = sqrt(ss)
+ *     (IEEE correctly rounded), a_hat = a / nrm (IEEE division) (c2 #5);
+ *   - an edge is kept iff j != i and |c_ij| > drop_tol (strict), c2 #1-#3;
+ *   - cutsize sums each undirected cut edge once (stored j > i), Neumaier
+ *     compensated (c2 #8-#9).
+ *
+ * Build: gcc -O2 -ffp-contract=off -fno-fast-math (no DAZ/FTZ); fma() is the
+ * C99 correctly-rounded fused multiply-add.
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+#define ORC_OK 0
+#define ORC_ERR_INVALID (-1)
+#define ORC_ERR_ZERO_ROW (-3)
+#define ORC_ERR_NONFINITE (-4)
+#define ORC_ERR_NOMEM (-5)
+
+/* Row scaling to unit 2-norm, PAPER.md:317-318 (§2.1) and PAPER.md:628
+ * (§3.1: "row scaling on A to have 2-norm equal to exactly one").
+ * out may alias val.  Returns ORC_ERR_ZERO_ROW for an all-zero / empty row
+ * and ORC_ERR_NONFINITE when a value or a norm is not finite. */
+int orc_scale_rows(int64_t nrows, const int64_t *row_ptr, const double *val,
+                   double *out, double *norms /* may be NULL */) {
+    for (int64_t i = 0; i < nrows; ++i) {
+        double ss = +0.0;
+        for (int64_t p = row_ptr[i]; p < row_ptr[i + 1]; ++p) {
+            if (!isfinite(val[p])) return ORC_ERR_NONFINITE;
+            ss = fma(val[p], val[p], ss);
+        }
+        if (!isfinite(ss)) return ORC_ERR_NONFINITE;
+        if (ss == 0.0) return ORC_ERR_ZERO_ROW;
+        double nrm = sqrt(ss);
+        if (norms) norms[i] = nrm;
+        for (int64_t p = row_ptr[i]; p < row_ptr[i + 1]; ++p) out[p] = val[p] / nrm;
+    }
+    return ORC_OK;
+}
+
+/* Column access to A (CSC of A == CSR of A^T), required by Gustavson's
+ * row-by-row SpGEMM.  Stable counting sort: rows ascend
+ * within each column. */
+int orc_transpose(int64_t nrows, int64_t ncols, const int64_t *row_ptr,
+                  const int32_t *col_idx, const double *val, int64_t *col_ptr,
+                  int32_t *row_idx, double *valT) {
+    for (int64_t k = 0; k <= ncols; ++k) col_ptr[k] = 0;
+    int64_t nnz = row_ptr[nrows];
+    for (int64_t p = 0; p < nnz; ++p) {
+        if (col_idx[p] < 0 || col_idx[p] >= ncols) return ORC_ERR_INVALID;
+        col_ptr[col_idx[p] + 1] += 1;
+    }
+    for (int64_t k = 0; k < ncols; ++k) col_ptr[k + 1] += col_ptr[k];
+    int64_t *next = (int64_t *)malloc(sizeof(int64_t) * (size_t)(ncols > 0 ? ncols : 1));
+    if (!next) return ORC_ERR_NOMEM;
+    for (int64_t k = 0; k < ncols; ++k) next[k] = col_ptr[k];
+    for (int64_t i = 0; i < nrows; ++i) {
+        for (int64_t p = row_ptr[i]; p < row_ptr[i + 1]; ++p) {
+            int64_t q = next[col_idx[p]]++;
+            row_idx[q] = (int32_t)i;
+            valT[q] = val[p];
+        }
+    }
+    free(next);
+    return ORC_OK;
+}
+
+/* Intermediate products of Gustavson's A A^T for row i: f_i = sum over k in
+ * row i of nnz(column k).  Total P = sum_k nnz(col k)^2. */
+int64_t orc_row_products(int64_t nrows, const int64_t *row_ptr, const int32_t *col_idx,
+                         const int64_t *col_ptr, int64_t *f /* may be NULL */) {
+    int64_t total = 0;
+    for (int64_t i = 0; i < nrows; ++i) {
+        int64_t fi = 0;
+        for (int64_t p = row_ptr[i]; p < row_ptr[i + 1]; ++p)
+            fi += col_ptr[col_idx[p] + 1] - col_ptr[col_idx[p]];
+        if (f) f[i] = fi;
+        total += fi;
+    }
+    return total;
+}
+
+static int cmp_i32(const void *a, const void *b) {
+    int32_t x = *(const int32_t *)a, y = *(const int32_t *)b;
+    return (x > y) - (x < y);
+}
+
+/* G_RIP rows [row_begin, row_end) from the (already scaled, if requested)
+ * CSR of A and its CSC, by dense-accumulator Gustavson SpGEMM (PAPER.md:
+ * 560-562), keeping off-diagonal entries with |c_ij| > drop_tol as edges with
+ * cost |c_ij|.
+ *
+ * Outputs (malloc'ed here, released with orc_free):
+ *   *g_row_ptr  int64[nloc+1]  (local, starts at 0)
+ *   *g_col      int32[nnz]     ascending per row
+ *   *g_w        double[nnz]    |c_ij|
+ * Optional caller arrays (length nloc, may be NULL):
+ *   diag[]   c_ii (0.0 when row i is empty)
+ *   nnzc[]   structural nnz of row i of C including the diagonal
+ */
+int orc_build(int64_t nrows, int64_t ncols, const int64_t *row_ptr,
+              const int32_t *col_idx, const double *val, const int64_t *col_ptr,
+              const int32_t *row_idx, const double *valT, double drop_tol,
+              int64_t row_begin, int64_t row_end, int64_t **g_row_ptr,
+              int32_t **g_col, double **g_w, int64_t *g_nnz, double *diag,
+              int64_t *nnzc) {
+    (void)ncols;
+    if (row_begin < 0 || row_end > nrows || row_begin > row_end) return ORC_ERR_INVALID;
+    if (!(drop_tol >= 0.0)) return ORC_ERR_INVALID;
+    int64_t nloc = row_end - row_begin;
+    int64_t cap = 1024, len = 0;
+    double *acc = (double *)malloc(sizeof(double) * (size_t)(nrows > 0 ? nrows : 1));
+    int64_t *mark = (int64_t *)malloc(sizeof(int64_t) * (size_t)(nrows > 0 ? nrows : 1));
+    int32_t *touched = (int32_t *)malloc(sizeof(int32_t) * (size_t)(nrows > 0 ? nrows : 1));
+    int64_t *rp = (int64_t *)malloc(sizeof(int64_t) * (size_t)(nloc + 1));
+    int32_t *gc = (int32_t *)malloc(sizeof(int32_t) * (size_t)cap);
+    double *gw = (double *)malloc(sizeof(double) * (size_t)cap);
+    if (!acc || !mark || !touched || !rp || !gc || !gw) {
+        free(acc); free(mark); free(touched); free(rp); free(gc); free(gw);
+        return ORC_ERR_NOMEM;
+    }
+    for (int64_t j = 0; j < nrows; ++j) mark[j] = -1;
+    rp[0] = 0;
+    for (int64_t i = row_begin; i < row_end; ++i) {
+        int64_t nt = 0;
+        /* row i of C: for k in row i (ascending), for j in column k */
+        for (int64_t p = row_ptr[i]; p < row_ptr[i + 1]; ++p) {
+            int32_t k = col_idx[p];
+            double a_ik = val[p];
+            for (int64_t q = col_ptr[k]; q < col_ptr[k + 1]; ++q) {
+                int32_t j = row_idx[q];
+                if (mark[j] != i) {
+                    mark[j] = i;
+                    acc[j] = +0.0;
+                    touched[nt++] = j;
+                }
+                acc[j] = fma(a_ik, valT[q], acc[j]);
+            }
+        }
+        qsort(touched, (size_t)nt, sizeof(int32_t), cmp_i32);
+        if (diag) diag[i - row_begin] = 0.0;
+        if (nnzc) nnzc[i - row_begin] = nt;
+        for (int64_t t = 0; t < nt; ++t) {
+            int32_t j = touched[t];
+            double c = acc[j];
+            if (j == i) {
+                if (diag) diag[i - row_begin] = c;
+                continue;
+            }
+            double w = fabs(c);
+            if (!(w > drop_tol)) continue;
+            if (len == cap) {
+                cap *= 2;
+                int32_t *nc = (int32_t *)realloc(gc, sizeof(int32_t) * (size_t)cap);
+                if (nc) gc = nc;
+                double *nw = (double *)realloc(gw, sizeof(double) * (size_t)cap);
+                if (nw) gw = nw;
+                if (!nc || !nw) {
+                    free(acc); free(mark); free(touched); free(rp); free(gc); free(gw);
+                    return ORC_ERR_NOMEM;
+                }
+            }
+            gc[len] = j;
+            gw[len] = w;
+            ++len;
+        }
+        rp[i - row_begin + 1] = len;
+    }
+    free(acc);
+    free(mark);
+    free(touched);
+    *g_row_ptr = rp;
+    *g_col = gc;
+    *g_w = gw;
+    *g_nnz = len;
+    return ORC_OK;
+}
+
+void orc_free(void *p) { free(p); }
+
+/* Neumaier-compensated summation step. */
+static void neumaier(double *s, double *c, double x) {
+    double t = *s + x;
+    if (fabs(*s) >= fabs(x))
+        *c += (*s - t) + x;
+    else
+        *c += (x - t) + *s;
+    *s = t;
+}
+
+/* cutsize(Pi) = sum of cost(v_i,v_j) over cut edges (§2.2;
+ * PAPER.md:1150-1154, eq. partcut), each undirected edge counted once
+ * (stored (i,j) with j > i).  Also returns the total edge weight and the
+ * intra-block weight (the identity cut = total - intra is a test pin).
+ * Rows are [row_begin, row_begin + nloc) of the global graph; part has the
+ * global length.  Returns ORC_ERR_INVALID if a part id is outside [0, K). */
+int orc_cutsize(int64_t nloc, int64_t row_begin, const int64_t *g_row_ptr,
+                const int32_t *g_col, const double *g_w, int64_t n_global,
+                const int32_t *part, int32_t K, double *cut, double *total,
+                double *intra) {
+    for (int64_t v = 0; v < n_global; ++v)
+        if (part[v] < 0 || part[v] >= K) return ORC_ERR_INVALID;
+    double sc = 0.0, cc = 0.0, st = 0.0, ct = 0.0, si = 0.0, ci = 0.0;
+    for (int64_t r = 0; r < nloc; ++r) {
+        int64_t i = row_begin + r;
+        for (int64_t e = g_row_ptr[r]; e < g_row_ptr[r + 1]; ++e) {
+            int64_t j = g_col[e];
+            if (j <= i) continue;
+            neumaier(&st, &ct, g_w[e]);
+            if (part[i] != part[j])
+                neumaier(&sc, &cc, g_w[e]);
+            else
+                neumaier(&si, &ci, g_w[e]);
+        }
+    }
+    *cut = sc + cc;
+    if (total) *total = st + ct;
+    if (intra) *intra = si + ci;
+    return ORC_OK;
+}
