@@ -1,0 +1,178 @@
+/*
+ * rig.h -- C ABI of librig, the B200 (sm_100a) builder of the row
+ * inner-product graph G_RIP of a sparse matrix A and the cutsize of a K-way
+ * block-row partition (arXiv 1710.07769, "row inner-product graph model").
+ *
+ * What the calls compute (PAPER.md = /root/reference/PAPER.md):
+ *   - G_RIP(A): one vertex per row r_i; an edge (v_i,v_j) iff r_i r_j^T != 0
+ *     (§2.1, eq. for E) with cost |r_i r_j^T| (PAPER.md:
+ *     310-315, eq14).  It is the off-diagonal pattern and |values| of
+ *     C = A A^T, computed by Gustavson SpGEMM
+ *     (§2.3).  Rows may first be scaled to unit 2-norm so
+ *     costs are |cosines|.
+ *   - cutsize(Pi) = sum of costs of cut edges = interIP(Pi) (PAPER.md:393-405,
+ *     §2.2, eq. partcut).
+ *
+ * Arithmetic contract (readings R1-R9), identical to the CPU
+ * oracle in oracle/ so structure and weights match bit for bit:
+ *   - scaling: ss_i = fma-chain of a_ik^2 over ascending k from +0.0,
+ *     nrm_i = sqrt_rn(ss_i), a_hat_ik = a_ik /_rn nrm_i;
+ *   - c_ij = fma-chain of a_hat_ik * a_hat_jk over the shared columns k in
+ *     ascending k, starting from +0.0;
+ *   - edge (i,j) kept iff j != i and |c_ij| > drop_tol (strict);
+ *   - the graph is stored symmetric (both (i,j) and (j,i)), columns
+ *     ascending within each row.
+ *
+ * Conventions for every call:
+ *   - All matrix / graph / partition pointers are DEVICE pointers on the
+ *     current CUDA device, except in rig_build_host (HOST pointers).
+ *   - Index types: row pointers int64, column / row indices int32, values and
+ *     weights float64, part ids int32.
+ *   - Input CSR must be canonical (row_ptr[0]=0, non-decreasing,
+ *     row_ptr[nrows]=nnz, columns strictly increasing per row and in
+ *     [0, ncols)); pass RIG_FLAG_VALIDATE to have it checked on the device.
+ *   - `stream` is a cudaStream_t (NULL = legacy default stream).  Work is
+ *     enqueued on it; inputs are borrowed and must stay valid until the
+ *     stream has passed the call.
+ *   - Every call returns RIG_OK (0) or a negative RIG_ERR_* code; the message
+ *     of the last failure on the calling thread is rig_last_error().  No C++
+ *     exception crosses the ABI.  Asynchronous kernel faults surface at the
+ *     next synchronising call as RIG_ERR_CUDA.
+ */
+#ifndef RIG_H_
+#define RIG_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes ---------------------------------------------------- */
+#define RIG_OK 0
+#define RIG_ERR_INVALID (-1)      /* null pointer, bad size/range, drop_tol < 0 or NaN, capacity too small */
+#define RIG_ERR_NONCANONICAL (-2) /* RIG_FLAG_VALIDATE found a non-canonical CSR */
+#define RIG_ERR_ZERO_ROW (-3)     /* scale_rows = 1 and a row is empty / all zero */
+#define RIG_ERR_NONFINITE (-4)    /* a value or a row norm is Inf/NaN (checked when scaling or validating) */
+#define RIG_ERR_NOMEM (-5)        /* device or host allocation failed */
+#define RIG_ERR_CUDA (-6)         /* a CUDA runtime error; message holds cudaGetErrorString */
+
+/* ---- flags ------------------------------------------------------------- */
+#define RIG_FLAG_VALIDATE 0x1u /* a0: check canonical CSR and finite values on the device */
+#define RIG_FLAG_DIAG 0x2u     /* also return diag[i] = c_ii (0 for an empty row) */
+
+typedef void *rig_stream_t; /* a cudaStream_t */
+
+#if defined(__GNUC__)
+#define RIG_API __attribute__((visibility("default")))
+#else
+#define RIG_API
+#endif
+
+/* Sparse A (nrows x ncols), canonical CSR. */
+typedef struct {
+    int64_t nrows, ncols, nnz;
+    const int64_t *row_ptr; /* [nrows+1] */
+    const int32_t *col_idx; /* [nnz] */
+    const double *val;      /* [nnz] */
+} rig_csr_t;
+
+/* G_RIP rows [row_begin, row_begin + n) as symmetric CSR (local row_ptr
+ * starting at 0, global column ids).  w[e] = |c_ij| > drop_tol, j != i. */
+typedef struct {
+    int64_t n, nnz;
+    int64_t *row_ptr; /* [n+1] */
+    int32_t *col_idx; /* [nnz] ascending within each row */
+    double *w;        /* [nnz] */
+    double *diag;     /* [n] c_ii, or NULL (RIG_FLAG_DIAG not given) */
+} rig_graph_t;
+
+typedef struct rig_plan rig_plan_t;
+
+/* ---- simple API: library-owned output ---------------------------------- */
+
+/* Build G_RIP(A) for all rows (steps a0-a6 of DESIGN.md §2).
+ *   A          device CSR (borrowed).
+ *   scale_rows 1: scale rows to unit 2-norm first; 0: use A as is.
+ *   drop_tol   >= 0; an off-diagonal entry is an edge iff |c_ij| > drop_tol.
+ *   flags      RIG_FLAG_VALIDATE | RIG_FLAG_DIAG.
+ *   out        filled with device arrays allocated by the library (stream-
+ *              ordered on `stream`); release them with rig_graph_free.
+ * Synchronises `stream` to size allocations. */
+RIG_API int rig_build(const rig_csr_t *A, int scale_rows, double drop_tol, uint32_t flags, rig_graph_t *out,
+              rig_stream_t stream);
+
+/* Release the arrays of a graph returned by rig_build / rig_build_sharded;
+ * zeroes *g.  NULL arrays are ignored. */
+RIG_API int rig_graph_free(rig_graph_t *g, rig_stream_t stream);
+
+/* Same as rig_build restricted to rows [row_begin, row_end) of C (one shard
+ * of a multi-GPU build).  A is the FULL matrix (replicated);
+ * out->row_ptr is local (starts at 0); column ids are global. */
+RIG_API int rig_build_rows(const rig_csr_t *A, int scale_rows, double drop_tol, uint32_t flags, int64_t row_begin,
+                   int64_t row_end, rig_graph_t *out, rig_stream_t stream);
+
+/* ---- staged API: caller-owned output (estimate -> allocate -> compute) --- */
+
+/* Runs steps a0-a4 for rows [row_begin, row_end): validation, scaling,
+ * transpose, flop count and the symbolic pass.  Synchronises once. */
+RIG_API int rig_plan_create(const rig_csr_t *A, int scale_rows, double drop_tol, uint32_t flags, int64_t row_begin,
+                    int64_t row_end, rig_plan_t **plan, rig_stream_t stream);
+
+/* nnz_upper: graph capacity needed (structural off-diagonal nnz of the
+ * shard); products: Gustavson intermediate products of the shard;
+ * workspace_bytes: device bytes rig_plan_execute needs in `workspace`. */
+RIG_API int rig_plan_query(const rig_plan_t *plan, int64_t *nnz_upper, int64_t *products, size_t *workspace_bytes);
+
+/* Steps a5-a6 into caller arrays: out->row_ptr [n+1], out->col_idx and
+ * out->w with capacity >= nnz_upper, out->diag [n] or NULL.  `workspace`
+ * must hold workspace_bytes (may be NULL if that is 0).  Sets out->n and
+ * out->nnz.  Synchronises once (to read the kept count). */
+RIG_API int rig_plan_execute(rig_plan_t *plan, void *workspace, rig_graph_t *out, rig_stream_t stream);
+
+RIG_API int rig_plan_destroy(rig_plan_t *plan);
+
+/* ---- multi-GPU helper -------------------------------------------------- */
+
+/* Flop-balanced contiguous split of the rows of C into `parts` shards:
+ * split[0]=0, split[parts]=nrows, split[g] = first row whose inclusive
+ * prefix of products f_i reaches ceil(g*P/parts).
+ * `split` is a HOST array of parts+1 entries.  Deterministic: every rank
+ * computes the same split.  Synchronises. */
+RIG_API int rig_row_split(const rig_csr_t *A, int32_t parts, int64_t *split, rig_stream_t stream);
+
+/* ---- cutsize ----------------------------------------------------------- */
+
+/* cut_dev[0] = sum over stored edges (i,j) of g with j > i and
+ * part[i] != part[j] of w_ij, i = row_begin + local row.
+ * part: device int32[n_global] with values in [0, K); an out-of-range id
+ * makes cut_dev[0] = NaN.  Deterministic for a fixed graph.  Fully
+ * asynchronous (no host sync).  Multi-GPU: allreduce cut_dev outside. */
+RIG_API int rig_cutsize(const rig_graph_t *g, int64_t row_begin, int64_t n_global, const int32_t *part, int32_t K,
+                double *cut_dev, rig_stream_t stream);
+
+/* ---- end-to-end from host memory --------------------------------------- */
+
+/* Host-to-host convenience for the whole path: copies A (HOST CSR) and part
+ * (HOST, may be NULL) to the device, builds G_RIP, computes the cutsize, and
+ * copies the graph into the caller's HOST arrays out_host->row_ptr [nrows+1],
+ * col_idx / w (capacity entries each) and diag ([nrows], only with
+ * RIG_FLAG_DIAG).  If capacity is too small, returns RIG_ERR_INVALID with
+ * out_host->nnz set to the required capacity.  *cut_host receives the cutsize
+ * (NaN when part is NULL).  Pinned host memory gives full PCIe bandwidth. */
+RIG_API int rig_build_host(const rig_csr_t *A_host, int scale_rows, double drop_tol, uint32_t flags,
+                   const int32_t *part_host, int32_t K, rig_graph_t *out_host, int64_t capacity, double *cut_host,
+                   rig_stream_t stream);
+
+/* ---- diagnostics ------------------------------------------------------- */
+
+RIG_API const char *rig_last_error(void);
+/* Number of kernels this library has launched since it was loaded. */
+RIG_API uint64_t rig_launch_count(void);
+RIG_API const char *rig_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RIG_H_ */

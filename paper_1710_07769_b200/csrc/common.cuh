@@ -1,0 +1,158 @@
+// common.cuh -- device helpers and the internal kernel interface of librig.
+// sm_100a only.  Compiled with --fmad=false: every fused multiply-add in the
+// library is an explicit __fma_rn, so no accidental contraction changes a bit
+// of the ordering contract (DESIGN.md §3 R4) or of the compensated cutsize.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <climits>
+#include <cstdint>
+
+namespace rig {
+
+constexpr unsigned kFull = 0xffffffffu;
+constexpr int kWarp = 32;
+
+// Device error bits, read back at the first synchronisation.
+enum : int {
+    kErrZeroRow = 1,
+    kErrNonFinite = 2,
+    kErrNonCanonical = 4,
+};
+
+// Rows whose A-row length is <= kMergeMaxLen and whose product count is
+// <= kMergeMaxF take the thread-per-row k-way merge path (k_spgemm.cu).
+constexpr int kMergeMaxLen = 8;
+constexpr int64_t kMergeMaxF = 4096;
+// Warp-hash bins: symbolic table T = next_pow2(2 f) in [64, 4096] (keys only);
+// numeric table T = next_pow2(2 nnzC) in [64, 2048] (key + value).
+constexpr int kSymBinMinLog = 6, kSymBinMaxLog = 12;
+constexpr int kNumBinMinLog = 6, kNumBinMaxLog = 11;
+constexpr int kNumSymBins = kSymBinMaxLog - kSymBinMinLog + 1;  // 7
+constexpr int kNumNumBins = kNumBinMaxLog - kNumBinMinLog + 1;  // 6
+
+struct Csr {
+    int64_t nrows, ncols, nnz;
+    const int64_t *rp;
+    const int32_t *ci;
+    const double *v;  // scaled values a_hat when scale_rows
+};
+
+struct Csc {
+    const int64_t *cp;  // [ncols+1]
+    const int32_t *ri;  // [nnz] ascending within each column
+    const double *vt;   // [nnz] bit-identical to the CSR value of (i,k)
+};
+
+// Counters written by the device and read back by the host at a sync.
+constexpr int kSymBins = kNumSymBins + 1;  // + huge
+constexpr int kNumBins = kNumNumBins + 1;  // + huge
+struct DevCounters {
+    int err;
+    int holes;          // numeric pass dropped an entry (|c| <= tol or exact 0)
+    unsigned long_cols; // columns longer than the short-sort limit
+    int bad_part;
+    int64_t products;   // sum f_i over the shard
+    int64_t n_mid;      // rows not on the merge path
+    int64_t sym_count[8];
+    int64_t num_count[8];
+};
+
+__device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
+__device__ __forceinline__ unsigned lanemask_lt() {
+    unsigned m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
+}
+
+__device__ __forceinline__ double shfl_d(double v, int src) {
+    return __shfl_sync(kFull, v, src);
+}
+
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+    return v;
+}
+
+// Inclusive warp scan.
+template <typename T>
+__device__ __forceinline__ T warp_incl_scan(T v) {
+    const int l = lane_id();
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        T u = __shfl_up_sync(kFull, v, o);
+        if (l >= o) v += u;
+    }
+    return v;
+}
+
+// Launch bookkeeping (rig_launch_count).
+void note_launch(int n = 1);
+int num_sms();
+
+// ---------------------------------------------------------------- kernels
+// k_prep.cu
+void launch_validate(const Csr &A, int *err, cudaStream_t s);
+void launch_col_hist(const Csr &A, unsigned *cnt, cudaStream_t s);
+void launch_scale_scatter(const Csr &A, int scale, double *ahat, int64_t *cursor, int32_t *ri, double *vt,
+                          int *err, cudaStream_t s);
+void launch_col_sort(int64_t ncols, const int64_t *cp, int32_t *ri, double *vt, int32_t *long_list,
+                     unsigned *long_count, cudaStream_t s);
+void launch_analyze(const Csr &A, const int64_t *cp, int64_t rb, int64_t re, int64_t *f, int32_t *sym_lists,
+                    int64_t cap, DevCounters *ctr, cudaStream_t s);
+void launch_bin_num(const int32_t *sym_lists, int64_t sym_cap, const DevCounters *ctr, const int64_t *nnzc,
+                    int64_t rb, int32_t *num_lists, int64_t num_cap, int64_t *num_count, cudaStream_t s);
+
+// k_scan.cu: out[0..n] = exclusive prefix of in[0..n-1] (out[n] = total).
+enum class ScanOp { Identity, UbOffDiag };
+void scan_i64(const int64_t *in, int64_t n, int64_t *out, ScanOp op, void *tmp, size_t tmp_bytes,
+              cudaStream_t s);
+void scan_u32(const unsigned *in, int64_t n, int64_t *out, void *tmp, size_t tmp_bytes, cudaStream_t s);
+size_t scan_tmp_bytes(int64_t n);
+
+// k_spgemm.cu
+struct SymArgs {
+    Csr A;
+    Csc T;
+    int64_t rb, re;
+    int64_t *nnzc;  // [re-rb]
+};
+struct NumArgs {
+    Csr A;
+    Csc T;
+    int64_t rb, re;
+    const int64_t *gptr;  // [re-rb+1] upper-bound (structural) offsets
+    int32_t *gcol;
+    double *gw;
+    double *diag;  // may be null
+    double tol;
+    int *holes;
+};
+void launch_sym_merge(const SymArgs &a, cudaStream_t s);
+void launch_num_merge(const NumArgs &a, cudaStream_t s);
+// counts: device bin sizes (loop bounds); hcounts: host copy (skip empty bins)
+void launch_sym_warp(const SymArgs &a, const int32_t *lists, int64_t list_cap, const int64_t *counts,
+                     const int64_t *hcounts, cudaStream_t s);
+void launch_num_warp(const NumArgs &a, const int32_t *lists, int64_t list_cap, const int64_t *counts,
+                     const int64_t *hcounts, cudaStream_t s);
+// huge rows: CTA per row, dense accumulator + bitmap in global scratch
+size_t huge_scratch_bytes(int64_t nrows, int slots, bool numeric);
+int huge_slots(int64_t nrows, int64_t n_huge);
+void launch_sym_huge(const SymArgs &a, const int32_t *list, const int64_t *count, int slots, void *scratch,
+                     cudaStream_t s);
+void launch_num_huge(const NumArgs &a, const int32_t *list, const int64_t *count, int slots, void *scratch,
+                     cudaStream_t s);
+
+// k_post.cu
+void launch_count_kept(const int64_t *gptr_ub, int64_t nloc, const int32_t *gcol, int64_t *kept, cudaStream_t s);
+void launch_compact_move(const int64_t *gptr_ub, const int64_t *gptr, int64_t nloc, const int32_t *gcol_in,
+                         const double *gw_in, int32_t *gcol, double *gw, cudaStream_t s);
+void launch_cutsize(const int64_t *grp, const int32_t *gcol, const double *gw, int64_t nloc, int64_t rb,
+                    int64_t n_global, const int32_t *part, int32_t K, double *partials, int nblocks,
+                    double *cut, cudaStream_t s);
+int cutsize_blocks();
+void launch_split(const int64_t *fprefix, int64_t n, int32_t parts, int64_t *split, cudaStream_t s);
+
+}  // namespace rig

@@ -1,0 +1,174 @@
+// k_post.cu -- a6 compaction (only when the numeric pass dropped entries),
+// a7 cutsize (§2.2; eq. partcut) and the
+// flop-balanced row split for multi-GPU sharding.
+#include "common.cuh"
+
+namespace rig {
+
+// ------------------------------------------------------------------ a6 (holes path)
+// The numeric pass writes each row's kept entries at the front of its
+// structural slot range [gptr_ub[r], gptr_ub[r+1]) and marks the rest -1.
+__global__ void k_count_kept(const int64_t *__restrict__ gptr_ub, int64_t nloc, const int32_t *__restrict__ gcol,
+                             int64_t *kept) {
+    const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int nw = (gridDim.x * blockDim.x) >> 5;
+    const int l = lane_id();
+    for (int64_t r = w; r < nloc; r += nw) {
+        const int64_t s = gptr_ub[r], e = gptr_ub[r + 1];
+        int64_t c = 0;
+        for (int64_t t = s + l; t < e; t += 32) c += gcol[t] >= 0;
+        c = warp_sum(c);
+        if (l == 0) kept[r] = c;
+    }
+}
+
+void launch_count_kept(const int64_t *gptr_ub, int64_t nloc, const int32_t *gcol, int64_t *kept, cudaStream_t s) {
+    int64_t g = (nloc * 32 + 255) / 256;
+    const int64_t cap = (int64_t)num_sms() * 16;
+    g = g < 1 ? 1 : (g > cap ? cap : g);
+    k_count_kept<<<(unsigned)g, 256, 0, s>>>(gptr_ub, nloc, gcol, kept);
+    note_launch();
+}
+
+__global__ void k_compact_move(const int64_t *__restrict__ gptr_ub, const int64_t *__restrict__ gptr, int64_t nloc,
+                               const int32_t *__restrict__ gcol_in, const double *__restrict__ gw_in, int32_t *gcol,
+                               double *gw) {
+    const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int nw = (gridDim.x * blockDim.x) >> 5;
+    const int l = lane_id();
+    for (int64_t r = w; r < nloc; r += nw) {
+        const int64_t s = gptr_ub[r], d = gptr[r], len = gptr[r + 1] - d;
+        for (int64_t t = l; t < len; t += 32) {
+            gcol[d + t] = gcol_in[s + t];
+            gw[d + t] = gw_in[s + t];
+        }
+    }
+}
+
+void launch_compact_move(const int64_t *gptr_ub, const int64_t *gptr, int64_t nloc, const int32_t *gcol_in,
+                         const double *gw_in, int32_t *gcol, double *gw, cudaStream_t s) {
+    int64_t g = (nloc * 32 + 255) / 256;
+    const int64_t cap = (int64_t)num_sms() * 16;
+    g = g < 1 ? 1 : (g > cap ? cap : g);
+    k_compact_move<<<(unsigned)g, 256, 0, s>>>(gptr_ub, gptr, nloc, gcol_in, gw_in, gcol, gw);
+    note_launch();
+}
+
+// ------------------------------------------------------------------ a7 cutsize
+// Each undirected edge counted once (stored j > i), DESIGN.md §3 R8.
+// Per-thread Neumaier sums, fixed-shape tree per CTA, then a fixed-order
+// final reduction: deterministic for a given graph.
+constexpr int kCutThreads = 256;
+
+__device__ __forceinline__ void neumaier_add(double &s, double &c, double x) {
+    const double t = s + x;
+    if (fabs(s) >= fabs(x))
+        c += (s - t) + x;
+    else
+        c += (x - t) + s;
+    s = t;
+}
+
+__global__ void __launch_bounds__(kCutThreads) k_cutsize(const int64_t *__restrict__ grp,
+                                                         const int32_t *__restrict__ gcol,
+                                                         const double *__restrict__ gw, int64_t nloc, int64_t rb,
+                                                         int64_t n_global, const int32_t *__restrict__ part,
+                                                         int32_t K, double *partials, int *bad) {
+    const int l = lane_id();
+    const int64_t wg = ((int64_t)blockIdx.x * kCutThreads + threadIdx.x) >> 5;
+    const int64_t nwg = ((int64_t)gridDim.x * kCutThreads) >> 5;
+    double s = 0.0, c = 0.0;
+    int badp = 0;
+    // part ids must lie in [0, K)
+    for (int64_t v = (int64_t)blockIdx.x * kCutThreads + threadIdx.x; v < n_global;
+         v += (int64_t)gridDim.x * kCutThreads) {
+        const int32_t p = part[v];
+        badp |= (p < 0) | (p >= K);
+    }
+    const int64_t ntiles = (nloc + 31) / 32;
+    for (int64_t tile = wg; tile < ntiles; tile += nwg) {
+        const int64_t r0 = tile * 32;
+        const int rows = (int)min((int64_t)32, nloc - r0);
+        const int64_t hi = grp[r0 + rows];
+        const int64_t my_start = l < rows ? grp[r0 + l] : hi;
+        const int32_t pi = l < rows ? part[rb + r0 + l] : 0;
+        const int64_t lo = __shfl_sync(kFull, my_start, 0);
+        const int64_t last = __shfl_sync(kFull, my_start, 31);
+        for (int64_t base = lo; base < hi; base += 32) {
+            const int64_t e = base + l;
+            // row of edge e: (number of lanes with start <= e) - 1
+            int t = 0;
+#pragma unroll
+            for (int step = 16; step >= 1; step >>= 1) {
+                const int64_t v = __shfl_sync(kFull, my_start, t + step - 1);
+                if (v <= e) t += step;
+            }
+            if (t == 31 && last <= e) t = 32;
+            const int row = t - 1;
+            const int32_t prow = __shfl_sync(kFull, pi, row < 0 ? 0 : row);
+            if (e < hi) {
+                const int64_t i = rb + r0 + row;
+                const int32_t j = gcol[e];
+                if ((int64_t)j > i && part[j] != prow) neumaier_add(s, c, gw[e]);
+            }
+        }
+    }
+    __shared__ double red[kCutThreads];
+    red[threadIdx.x] = s + c;
+    __syncthreads();
+    for (int h = kCutThreads / 2; h > 0; h >>= 1) {
+        if (threadIdx.x < h) red[threadIdx.x] += red[threadIdx.x + h];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) partials[blockIdx.x] = red[0];
+    if (__syncthreads_or(badp) && threadIdx.x == 0) atomicOr(bad, 1);
+}
+
+__global__ void k_cutsize_final(const double *partials, int n, const int *bad, double *cut) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
+        double s = 0.0, c = 0.0;
+        for (int k = 0; k < n; ++k) neumaier_add(s, c, partials[k]);
+        *cut = *bad ? __longlong_as_double(0x7ff8000000000000ll) : s + c;
+    }
+}
+
+int cutsize_blocks() { return num_sms() * 4; }
+
+void launch_cutsize(const int64_t *grp, const int32_t *gcol, const double *gw, int64_t nloc, int64_t rb,
+                    int64_t n_global, const int32_t *part, int32_t K, double *partials, int nblocks, double *cut,
+                    cudaStream_t s) {
+    int *bad = reinterpret_cast<int *>(partials + nblocks);
+    cudaMemsetAsync(bad, 0, sizeof(int), s);
+    k_cutsize<<<nblocks, kCutThreads, 0, s>>>(grp, gcol, gw, nloc, rb, n_global, part, K, partials, bad);
+    k_cutsize_final<<<1, 32, 0, s>>>(partials, nblocks, bad, cut);
+    note_launch(2);
+}
+
+// ------------------------------------------------------------------ row split
+// split[g] = smallest r with fprefix[r] >= ceil(g * P / parts); split[parts] = n.
+__global__ void k_split(const int64_t *__restrict__ fprefix, int64_t n, int32_t parts, int64_t *split) {
+    const int g = blockIdx.x * blockDim.x + threadIdx.x;
+    if (g > parts) return;
+    const int64_t P = fprefix[n];
+    if (g == parts) {
+        split[g] = n;
+        return;
+    }
+    const int64_t target = (int64_t)(((__int128)g * P + parts - 1) / parts);
+    int64_t lo = 0, hi = n;  // first r in [0, n] with fprefix[r] >= target
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (fprefix[mid] >= target)
+            hi = mid;
+        else
+            lo = mid + 1;
+    }
+    split[g] = lo;
+}
+
+void launch_split(const int64_t *fprefix, int64_t n, int32_t parts, int64_t *split, cudaStream_t s) {
+    k_split<<<(parts + 1 + 127) / 128, 128, 0, s>>>(fprefix, n, parts, split);
+    note_launch();
+}
+
+}  // namespace rig

@@ -1,0 +1,760 @@
+// k_spgemm.cu -- steps a4 (symbolic) and a5+a6 (numeric, fused with abs /
+// drop / diagonal strip) of the hot path: row i of C = A_hat A_hat^T by
+// Gustavson's row-by-row SpGEMM (§2.3), kept as G_RIP edges
+// (PAPER.md:293-315, 321-325, 352).
+//
+// Ordering contract (DESIGN.md §3 R4): every c_ij is the fma-chain over the
+// shared columns k in ASCENDING k from +0.0.  Each path below preserves it:
+//  * merge path (row length <= 8): one thread per row performs a k-way merge
+//    of the row's column runs (sorted by j); for the current minimum j it
+//    folds the runs in ascending k -- exactly the chain.
+//  * warp-hash path: products are enumerated in (k ascending, column order)
+//    and processed in chunks of 32 lanes in that order; lanes with the same j
+//    (__match_any_sync) pass the accumulator down the group in lane order, so
+//    each key's chain is applied in ascending k.  Then an LSD radix sort
+//    orders the row by j.
+//  * huge path (one CTA per row): warp w owns the keys with (j/32) % W == w
+//    and walks the whole product stream in order, so again every chain runs in
+//    ascending k; the dense accumulator's bitmap yields j-sorted output.
+#include "common.cuh"
+
+namespace rig {
+
+static int g_sms_cache = 0;
+
+// ======================================================== merge path
+template <int R>
+__device__ __forceinline__ int64_t sym_merge_row(const Csr &A, const Csc &T, int64_t s) {
+    int32_t h[R];
+    int64_t q[R], qe[R];
+    int64_t f = 0;
+#pragma unroll
+    for (int t = 0; t < R; ++t) {
+        const int k = A.ci[s + t];
+        q[t] = T.cp[k];
+        qe[t] = T.cp[k + 1];
+        f += qe[t] - q[t];
+    }
+    if (f > kMergeMaxF) return -1;
+#pragma unroll
+    for (int t = 0; t < R; ++t) h[t] = q[t] < qe[t] ? T.ri[q[t]] : INT_MAX;
+    int64_t cnt = 0;
+    while (true) {
+        int m = h[0];
+#pragma unroll
+        for (int t = 1; t < R; ++t) m = min(m, h[t]);
+        if (m == INT_MAX) break;
+        ++cnt;
+#pragma unroll
+        for (int t = 0; t < R; ++t) {
+            if (h[t] == m) {
+                ++q[t];
+                h[t] = q[t] < qe[t] ? T.ri[q[t]] : INT_MAX;
+            }
+        }
+    }
+    return cnt;
+}
+
+template <int R>
+__device__ __forceinline__ void num_merge_row(const NumArgs &a, int64_t i, int64_t r, int64_t s) {
+    int32_t h[R];
+    int64_t q[R], qe[R];
+    double av[R], hv[R];
+    int64_t f = 0;
+#pragma unroll
+    for (int t = 0; t < R; ++t) {
+        const int k = a.A.ci[s + t];
+        av[t] = a.A.v[s + t];
+        q[t] = a.T.cp[k];
+        qe[t] = a.T.cp[k + 1];
+        f += qe[t] - q[t];
+    }
+    if (f > kMergeMaxF) return;
+#pragma unroll
+    for (int t = 0; t < R; ++t) {
+        if (q[t] < qe[t]) {
+            h[t] = a.T.ri[q[t]];
+            hv[t] = a.T.vt[q[t]];
+        } else {
+            h[t] = INT_MAX;
+            hv[t] = 0.0;
+        }
+    }
+    const int64_t g0 = a.gptr[r], ub = a.gptr[r + 1] - g0;
+    int64_t o = 0;
+    while (true) {
+        int m = h[0];
+#pragma unroll
+        for (int t = 1; t < R; ++t) m = min(m, h[t]);
+        if (m == INT_MAX) break;
+        double acc = +0.0;
+#pragma unroll
+        for (int t = 0; t < R; ++t) {
+            if (h[t] == m) {  // runs visited in ascending k: the ordered chain
+                acc = __fma_rn(av[t], hv[t], acc);
+                ++q[t];
+                if (q[t] < qe[t]) {
+                    h[t] = a.T.ri[q[t]];
+                    hv[t] = a.T.vt[q[t]];
+                } else {
+                    h[t] = INT_MAX;
+                }
+            }
+        }
+        if ((int64_t)m == i) {
+            if (a.diag) a.diag[r] = acc;
+        } else {
+            const double w = fabs(acc);
+            if (w > a.tol) {
+                a.gcol[g0 + o] = m;
+                a.gw[g0 + o] = w;
+                ++o;
+            }
+        }
+    }
+    if (o < ub) {
+        for (int64_t t = o; t < ub; ++t) a.gcol[g0 + t] = -1;
+        atomicOr(a.holes, 1);
+    }
+}
+
+__global__ void __launch_bounds__(256) k_sym_merge(SymArgs a) {
+    const int64_t nloc = a.re - a.rb;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < nloc; r += stride) {
+        const int64_t i = a.rb + r;
+        const int64_t s = a.A.rp[i];
+        const int len = (int)min(a.A.rp[i + 1] - s, (int64_t)kMergeMaxLen + 1);
+        int64_t c = -1;
+        switch (len) {
+            case 0: c = 0; break;
+            case 1: c = sym_merge_row<1>(a.A, a.T, s); break;
+            case 2: c = sym_merge_row<2>(a.A, a.T, s); break;
+            case 3: c = sym_merge_row<3>(a.A, a.T, s); break;
+            case 4: c = sym_merge_row<4>(a.A, a.T, s); break;
+            case 5: c = sym_merge_row<5>(a.A, a.T, s); break;
+            case 6: c = sym_merge_row<6>(a.A, a.T, s); break;
+            case 7: c = sym_merge_row<7>(a.A, a.T, s); break;
+            case 8: c = sym_merge_row<8>(a.A, a.T, s); break;
+            default: break;
+        }
+        if (c >= 0) a.nnzc[r] = c;
+    }
+}
+
+__global__ void __launch_bounds__(256) k_num_merge(NumArgs a) {
+    const int64_t nloc = a.re - a.rb;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < nloc; r += stride) {
+        const int64_t i = a.rb + r;
+        const int64_t s = a.A.rp[i];
+        const int len = (int)min(a.A.rp[i + 1] - s, (int64_t)kMergeMaxLen + 1);
+        switch (len) {
+            case 0:
+                if (a.diag) a.diag[r] = 0.0;
+                break;
+            case 1: num_merge_row<1>(a, i, r, s); break;
+            case 2: num_merge_row<2>(a, i, r, s); break;
+            case 3: num_merge_row<3>(a, i, r, s); break;
+            case 4: num_merge_row<4>(a, i, r, s); break;
+            case 5: num_merge_row<5>(a, i, r, s); break;
+            case 6: num_merge_row<6>(a, i, r, s); break;
+            case 7: num_merge_row<7>(a, i, r, s); break;
+            case 8: num_merge_row<8>(a, i, r, s); break;
+            default: break;
+        }
+    }
+}
+
+static int sms() {
+    if (!g_sms_cache) g_sms_cache = num_sms();
+    return g_sms_cache;
+}
+
+void launch_sym_merge(const SymArgs &a, cudaStream_t s) {
+    const int64_t nloc = a.re - a.rb;
+    int64_t g = (nloc + 255) / 256;
+    g = g < 1 ? 1 : (g > (int64_t)sms() * 16 ? (int64_t)sms() * 16 : g);
+    k_sym_merge<<<(unsigned)g, 256, 0, s>>>(a);
+    note_launch();
+}
+
+void launch_num_merge(const NumArgs &a, cudaStream_t s) {
+    const int64_t nloc = a.re - a.rb;
+    int64_t g = (nloc + 255) / 256;
+    g = g < 1 ? 1 : (g > (int64_t)sms() * 16 ? (int64_t)sms() * 16 : g);
+    k_num_merge<<<(unsigned)g, 256, 0, s>>>(a);
+    note_launch();
+}
+
+// ======================================================== product enumeration
+// Row entries of row i are taken 32 at a time; for each, the column segment
+// [cp[k], cp[k+1]) of the CSC.  Products of the batch are numbered 0..total-1
+// in (k ascending, column order); lane L of a chunk handles product c0+L.
+struct Batch {
+    int64_t incl;  // inclusive prefix of column lengths (this lane's entry)
+    int64_t excl;
+    int64_t cs;    // column start
+    double a;      // a_hat_ik of this lane's entry
+    int64_t total;
+};
+
+__device__ __forceinline__ Batch load_batch(const Csr &A, const Csc &T, int64_t base, int64_t e, bool need_a) {
+    Batch b;
+    const int64_t p = base + lane_id();
+    int64_t cl = 0;
+    b.cs = 0;
+    b.a = 0.0;
+    if (p < e) {
+        const int k = A.ci[p];
+        b.cs = T.cp[k];
+        cl = T.cp[k + 1] - b.cs;
+        if (need_a) b.a = A.v[p];
+    }
+    b.incl = warp_incl_scan(cl);
+    b.excl = b.incl - cl;
+    b.total = __shfl_sync(kFull, b.incl, 31);
+    return b;
+}
+
+// Segment (lane index) holding product pp: number of lanes with incl <= pp.
+__device__ __forceinline__ int find_seg(const Batch &b, int64_t pp) {
+    int t = 0;
+#pragma unroll
+    for (int step = 16; step >= 1; step >>= 1) {
+        const int64_t v = __shfl_sync(kFull, b.incl, t + step - 1);
+        if (v <= pp) t += step;
+    }
+    return t;
+}
+
+__device__ __forceinline__ unsigned hash_key(int j, int logt) {
+    return ((unsigned)j * 0x9E3779B1u) >> (32 - logt);
+}
+
+// ======================================================== warp-hash symbolic
+constexpr int kWarpHashThreads = 256;
+
+template <int LOGT>
+__global__ void __launch_bounds__(kWarpHashThreads) k_sym_warp(SymArgs a, const int32_t *__restrict__ list,
+                                                               const int64_t *count) {
+    constexpr int T = 1 << LOGT;
+    extern __shared__ int32_t sym_tab[];
+    const int w = threadIdx.x >> 5, l = lane_id();
+    int32_t *keys = sym_tab + w * T;
+    const int64_t n = *count;
+    for (int s = l; s < T; s += 32) keys[s] = -1;
+    __syncwarp();
+    const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+    for (int64_t idx = blockIdx.x * (int64_t)(blockDim.x >> 5) + w; idx < n; idx += nw) {
+        const int64_t i = list[idx];
+        const int64_t s = a.A.rp[i], e = a.A.rp[i + 1];
+        int cnt = 0;
+        for (int64_t base = s; base < e; base += 32) {
+            const Batch b = load_batch(a.A, a.T, base, e, false);
+            for (int64_t c0 = 0; c0 < b.total; c0 += 32) {
+                const int64_t pp = c0 + l;
+                const int t = find_seg(b, pp);
+                const int64_t q = __shfl_sync(kFull, b.cs, t) + pp - __shfl_sync(kFull, b.excl, t);
+                if (pp < b.total) {
+                    const int j = a.T.ri[q];
+                    unsigned sl = hash_key(j, LOGT);
+                    while (true) {
+                        const int prev = atomicCAS(&keys[sl], -1, j);
+                        if (prev == -1) {
+                            ++cnt;
+                            break;
+                        }
+                        if (prev == j) break;
+                        sl = (sl + 1) & (T - 1);
+                    }
+                }
+            }
+        }
+        cnt = warp_sum(cnt);
+        if (l == 0) a.nnzc[i - a.rb] = cnt;
+        __syncwarp();
+        for (int s2 = l; s2 < T; s2 += 32) keys[s2] = -1;
+        __syncwarp();
+    }
+}
+
+template <int LOGT>
+static void launch_sym_warp_t(const SymArgs &a, const int32_t *list, const int64_t *count, cudaStream_t s) {
+    constexpr int T = 1 << LOGT;
+    const size_t smem = (size_t)(kWarpHashThreads / 32) * T * sizeof(int32_t);
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_sym_warp<LOGT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attr = true;
+    }
+    int per_sm = (int)((200 * 1024) / smem);
+    per_sm = per_sm < 1 ? 1 : (per_sm > 8 ? 8 : per_sm);
+    k_sym_warp<LOGT><<<sms() * per_sm, kWarpHashThreads, smem, s>>>(a, list, count);
+    note_launch();
+}
+
+void launch_sym_warp(const SymArgs &a, const int32_t *lists, int64_t cap, const int64_t *counts,
+                     const int64_t *hcounts, cudaStream_t s) {
+    if (hcounts[0]) launch_sym_warp_t<6>(a, lists + 0 * cap, counts + 0, s);
+    if (hcounts[1]) launch_sym_warp_t<7>(a, lists + 1 * cap, counts + 1, s);
+    if (hcounts[2]) launch_sym_warp_t<8>(a, lists + 2 * cap, counts + 2, s);
+    if (hcounts[3]) launch_sym_warp_t<9>(a, lists + 3 * cap, counts + 3, s);
+    if (hcounts[4]) launch_sym_warp_t<10>(a, lists + 4 * cap, counts + 4, s);
+    if (hcounts[5]) launch_sym_warp_t<11>(a, lists + 5 * cap, counts + 5, s);
+    if (hcounts[6]) launch_sym_warp_t<12>(a, lists + 6 * cap, counts + 6, s);
+}
+
+// ======================================================== warp-hash numeric
+// Per warp (T = 2^LOGT slots, at most T/2 live keys since T >= 2 nnzC_i):
+//   keys[T] int32 (-1 empty), vals[T] double (+0.0 when empty),
+//   two radix buffers of T/2 (key, value), hist[256].
+template <int LOGT>
+struct NumWarpSmem {
+    static constexpr int T = 1 << LOGT;
+    static constexpr size_t bytes = (size_t)T * 4 + (size_t)T * 8 + 2 * ((size_t)(T / 2) * 12) + 256 * 4;
+};
+
+template <int LOGT, int WPB>
+__global__ void __launch_bounds__(WPB * 32) k_num_warp(NumArgs a, const int32_t *__restrict__ list,
+                                                       const int64_t *count) {
+    constexpr int T = 1 << LOGT;
+    constexpr int H = T / 2;
+    extern __shared__ __align__(16) unsigned char num_smem[];
+    const int w = threadIdx.x >> 5, l = lane_id();
+    unsigned char *base = num_smem + (size_t)w * NumWarpSmem<LOGT>::bytes;
+    double *vals = reinterpret_cast<double *>(base);
+    double *av = vals + T;
+    double *bv = av + H;
+    int32_t *keys = reinterpret_cast<int32_t *>(bv + H);
+    int32_t *ak = keys + T;
+    int32_t *bk = ak + H;
+    int32_t *hist = bk + H;
+    const unsigned lt = lanemask_lt();
+
+    for (int s = l; s < T; s += 32) {
+        keys[s] = -1;
+        vals[s] = +0.0;
+    }
+    __syncwarp();
+    const int64_t n = *count;
+    const int64_t nw = (int64_t)gridDim.x * WPB;
+    for (int64_t idx = blockIdx.x * (int64_t)WPB + w; idx < n; idx += nw) {
+        const int64_t i = list[idx];
+        const int64_t r = i - a.rb;
+        const int64_t s = a.A.rp[i], e = a.A.rp[i + 1];
+        // ---- accumulate (ordered chains)
+        for (int64_t bb = s; bb < e; bb += 32) {
+            const Batch b = load_batch(a.A, a.T, bb, e, true);
+            for (int64_t c0 = 0; c0 < b.total; c0 += 32) {
+                const int64_t pp = c0 + l;
+                const bool valid = pp < b.total;
+                const int t = find_seg(b, pp);
+                const int64_t q = __shfl_sync(kFull, b.cs, t) + pp - __shfl_sync(kFull, b.excl, t);
+                const double aik = shfl_d(b.a, t);
+                int j = -2 - l;
+                double bjk = 0.0;
+                if (valid) {
+                    j = a.T.ri[q];
+                    bjk = a.T.vt[q];
+                }
+                const unsigned g = __match_any_sync(kFull, j);
+                const int leader = __ffs(g) - 1;
+                const int rank = __popc(g & lt);
+                const int cnt = __popc(g);
+                int slot = 0;
+                if (valid && l == leader) {
+                    unsigned sl = hash_key(j, LOGT);
+                    while (true) {
+                        const int prev = atomicCAS(&keys[sl], -1, j);
+                        if (prev == -1 || prev == j) break;
+                        sl = (sl + 1) & (T - 1);
+                    }
+                    slot = (int)sl;
+                }
+                slot = __shfl_sync(kFull, slot, leader);
+                double acc = 0.0;
+                if (valid && rank == 0) acc = vals[slot];
+                const int pred = rank ? 31 - __clz(g & lt) : l;
+                const int maxc = __reduce_max_sync(kFull, valid ? cnt : 0);
+                for (int it = 0; it < maxc; ++it) {
+                    const double x = shfl_d(acc, pred);
+                    if (valid && rank == it) acc = __fma_rn(aik, bjk, rank == 0 ? acc : x);
+                }
+                if (valid && rank == cnt - 1) vals[slot] = acc;
+                __syncwarp();
+            }
+        }
+        // ---- compact the table into (ak, av), reset it
+        int L = 0;
+        int jmin = INT_MAX, jmax = -1;
+        for (int b0 = 0; b0 < T; b0 += 32) {
+            const int sidx = b0 + l;
+            const int k = keys[sidx];
+            const bool occ = k >= 0;
+            const unsigned bal = __ballot_sync(kFull, occ);
+            if (occ) {
+                const int pos = L + __popc(bal & lt);
+                ak[pos] = k;
+                av[pos] = vals[sidx];
+                keys[sidx] = -1;
+                vals[sidx] = +0.0;
+                jmin = min(jmin, k);
+                jmax = max(jmax, k);
+            }
+            L += __popc(bal);
+        }
+        jmin = __reduce_min_sync(kFull, jmin);
+        jmax = __reduce_max_sync(kFull, jmax);
+        __syncwarp();
+        // ---- LSD radix sort on (key - jmin), 8-bit digits, stable
+        const unsigned span = L > 1 ? (unsigned)(jmax - jmin) : 0u;
+        const int bits = span ? 32 - __clz(span) : 0;
+        int32_t *ck = ak, *nk = bk;
+        double *cv = av, *nv = bv;
+        for (int sh = 0; sh < bits; sh += 8) {
+            for (int h = l; h < 256; h += 32) hist[h] = 0;
+            __syncwarp();
+            for (int rd = 0; rd < L; rd += 32) {
+                const int e2 = rd + l;
+                const bool v = e2 < L;
+                const int dig = v ? (int)(((unsigned)(ck[e2] - jmin) >> sh) & 255u) : 256 + l;
+                const unsigned g = __match_any_sync(kFull, dig);
+                if (v && l == __ffs(g) - 1) hist[dig] += __popc(g);
+                __syncwarp();
+            }
+            {  // exclusive scan of the 256 counters, 8 per lane
+                int loc[8], sum = 0;
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    loc[u] = hist[l * 8 + u];
+                    sum += loc[u];
+                }
+                const int inc = warp_incl_scan(sum);
+                int run = inc - sum;
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    hist[l * 8 + u] = run;
+                    run += loc[u];
+                }
+            }
+            __syncwarp();
+            for (int rd = 0; rd < L; rd += 32) {
+                const int e2 = rd + l;
+                const bool v = e2 < L;
+                const int key = v ? ck[e2] : 0;
+                const int dig = v ? (int)(((unsigned)(key - jmin) >> sh) & 255u) : 256 + l;
+                const unsigned g = __match_any_sync(kFull, dig);
+                if (v) {
+                    const int pos = hist[dig] + __popc(g & lt);
+                    nk[pos] = key;
+                    nv[pos] = cv[e2];
+                }
+                __syncwarp();
+                if (v && l == 31 - __clz(g)) hist[dig] += __popc(g);
+                __syncwarp();
+            }
+            int32_t *tk = ck;
+            ck = nk;
+            nk = tk;
+            double *tv = cv;
+            cv = nv;
+            nv = tv;
+        }
+        // ---- write the row: strip diagonal, |c| > tol
+        const int64_t g0 = a.gptr[r], ub = a.gptr[r + 1] - g0;
+        int64_t o = 0;
+        for (int rd = 0; rd < L; rd += 32) {
+            const int e2 = rd + l;
+            const bool v = e2 < L;
+            const int key = v ? ck[e2] : -1;
+            const double c = v ? cv[e2] : 0.0;
+            const bool isdiag = v && (int64_t)key == i;
+            if (isdiag && a.diag) a.diag[r] = c;
+            const bool keep = v && !isdiag && fabs(c) > a.tol;
+            const unsigned bal = __ballot_sync(kFull, keep);
+            if (keep) {
+                const int64_t pos = g0 + o + __popc(bal & lt);
+                a.gcol[pos] = key;
+                a.gw[pos] = fabs(c);
+            }
+            o += __popc(bal);
+        }
+        if (o < ub) {
+            for (int64_t t = o + l; t < ub; t += 32) a.gcol[g0 + t] = -1;
+            if (l == 0) atomicOr(a.holes, 1);
+        }
+        __syncwarp();
+    }
+}
+
+template <int LOGT>
+static void launch_num_warp_t(const NumArgs &a, const int32_t *list, const int64_t *count, cudaStream_t s) {
+    constexpr int WPB = LOGT >= 11 ? 4 : 8;
+    const size_t smem = (size_t)WPB * NumWarpSmem<LOGT>::bytes;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_num_warp<LOGT, WPB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attr = true;
+    }
+    int per_sm = (int)((220 * 1024) / smem);
+    per_sm = per_sm < 1 ? 1 : (per_sm > 4 ? 4 : per_sm);
+    k_num_warp<LOGT, WPB><<<sms() * per_sm, WPB * 32, smem, s>>>(a, list, count);
+    note_launch();
+}
+
+void launch_num_warp(const NumArgs &a, const int32_t *lists, int64_t cap, const int64_t *counts,
+                     const int64_t *hcounts, cudaStream_t s) {
+    if (hcounts[0]) launch_num_warp_t<6>(a, lists + 0 * cap, counts + 0, s);
+    if (hcounts[1]) launch_num_warp_t<7>(a, lists + 1 * cap, counts + 1, s);
+    if (hcounts[2]) launch_num_warp_t<8>(a, lists + 2 * cap, counts + 2, s);
+    if (hcounts[3]) launch_num_warp_t<9>(a, lists + 3 * cap, counts + 3, s);
+    if (hcounts[4]) launch_num_warp_t<10>(a, lists + 4 * cap, counts + 4, s);
+    if (hcounts[5]) launch_num_warp_t<11>(a, lists + 5 * cap, counts + 5, s);
+}
+
+// ======================================================== huge rows
+// One CTA per row; per-CTA scratch slot = bitmap over j (nrows bits) and, for
+// the numeric pass, a dense accumulator acc[nrows].  The bitmap is all-zero
+// between rows (each row clears what it set).
+constexpr int kHugeThreads = 512;
+constexpr int kHugeWarps = kHugeThreads / 32;
+
+static int64_t bitmap_words(int64_t nrows) { return (nrows + 31) / 32; }
+
+size_t huge_scratch_bytes(int64_t nrows, int slots, bool numeric) {
+    size_t per = (size_t)bitmap_words(nrows) * 4;
+    per = (per + 255) & ~(size_t)255;
+    if (numeric) per += (size_t)nrows * 8;
+    return per * (size_t)slots;
+}
+
+int huge_slots(int64_t nrows, int64_t n_huge) {
+    const size_t per = huge_scratch_bytes(nrows, 1, true);
+    int64_t budget = (int64_t)(4ull << 30) / (int64_t)(per ? per : 1);
+    int64_t s = 2 * (int64_t)sms();
+    if (s > budget) s = budget;
+    if (s > n_huge) s = n_huge;
+    if (s < 1) s = 1;
+    return (int)s;
+}
+
+struct BlockBatch {
+    int64_t total;
+};
+
+// CTA-level batch of up to kHugeThreads row entries: prefix of column
+// lengths in shared memory.
+__device__ __forceinline__ int64_t block_batch(const Csr &A, const Csc &T, int64_t base, int64_t e,
+                                               int64_t *s_incl, int64_t *s_cs, double *s_a) {
+    __shared__ int64_t wsum[kHugeWarps];
+    const int tid = threadIdx.x, w = tid >> 5, l = lane_id();
+    const int64_t p = base + tid;
+    int64_t cl = 0, cs = 0;
+    double av = 0.0;
+    if (p < e) {
+        const int k = A.ci[p];
+        cs = T.cp[k];
+        cl = T.cp[k + 1] - cs;
+        if (s_a) av = A.v[p];
+    }
+    const int64_t inc = warp_incl_scan(cl);
+    if (l == 31) wsum[w] = inc;
+    __syncthreads();
+    if (w == 0) {
+        const int64_t x = l < kHugeWarps ? wsum[l] : 0;
+        const int64_t xi = warp_incl_scan(x);
+        if (l < kHugeWarps) wsum[l] = xi - x;
+    }
+    __syncthreads();
+    s_incl[tid] = inc + wsum[w];
+    s_cs[tid] = cs;
+    if (s_a) s_a[tid] = av;
+    __syncthreads();
+    const int64_t total = s_incl[kHugeThreads - 1];
+    return total;
+}
+
+// index of the entry holding product pp: number of entries with incl <= pp
+__device__ __forceinline__ int block_find(const int64_t *s_incl, int64_t pp) {
+    int lo = 0, hi = kHugeThreads;  // first index with incl > pp
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (s_incl[mid] <= pp)
+            lo = mid + 1;
+        else
+            hi = mid;
+    }
+    return lo;
+}
+
+__device__ __forceinline__ int64_t block_sum(int64_t v) {
+    __shared__ int64_t red[kHugeWarps];
+    v = warp_sum(v);
+    if (lane_id() == 0) red[threadIdx.x >> 5] = v;
+    __syncthreads();
+    int64_t t = 0;
+    for (int k = 0; k < kHugeWarps; ++k) t += red[k];
+    __syncthreads();
+    return t;
+}
+
+__global__ void __launch_bounds__(kHugeThreads) k_sym_huge(SymArgs a, const int32_t *__restrict__ list,
+                                                           const int64_t *count, unsigned char *scratch,
+                                                           size_t slot_bytes) {
+    __shared__ int64_t s_incl[kHugeThreads], s_cs[kHugeThreads];
+    unsigned *bm = reinterpret_cast<unsigned *>(scratch + slot_bytes * blockIdx.x);
+    const int64_t n = *count;
+    for (int64_t idx = blockIdx.x; idx < n; idx += gridDim.x) {
+        const int64_t i = list[idx];
+        const int64_t s = a.A.rp[i], e = a.A.rp[i + 1];
+        int64_t cnt = 0;
+        for (int pass = 0; pass < 2; ++pass) {  // pass 0: set + count, pass 1: clear
+            for (int64_t base = s; base < e; base += kHugeThreads) {
+                const int64_t total = block_batch(a.A, a.T, base, e, s_incl, s_cs, nullptr);
+                for (int64_t pp = threadIdx.x; pp < total; pp += kHugeThreads) {
+                    const int t = block_find(s_incl, pp);
+                    const int64_t ex = t ? s_incl[t - 1] : 0;
+                    const int j = a.T.ri[s_cs[t] + pp - ex];
+                    if (pass == 0) {
+                        const unsigned bit = 1u << (j & 31);
+                        if (!(atomicOr(&bm[j >> 5], bit) & bit)) ++cnt;
+                    } else {
+                        bm[j >> 5] = 0u;
+                    }
+                }
+                __syncthreads();
+            }
+        }
+        cnt = block_sum(cnt);
+        if (threadIdx.x == 0) a.nnzc[i - a.rb] = cnt;
+        __syncthreads();
+    }
+}
+
+__global__ void __launch_bounds__(kHugeThreads) k_num_huge(NumArgs a, const int32_t *__restrict__ list,
+                                                           const int64_t *count, unsigned char *scratch,
+                                                           size_t slot_bytes, int64_t nwords) {
+    __shared__ int64_t s_incl[kHugeThreads], s_cs[kHugeThreads];
+    __shared__ double s_a[kHugeThreads];
+    __shared__ int64_t s_scan[kHugeWarps];
+    unsigned char *slot = scratch + slot_bytes * blockIdx.x;
+    unsigned *bm = reinterpret_cast<unsigned *>(slot);
+    double *acc_g = reinterpret_cast<double *>(slot + (((size_t)nwords * 4 + 255) & ~(size_t)255));
+    const int w = threadIdx.x >> 5, l = lane_id();
+    const unsigned lt = lanemask_lt();
+    const int64_t n = *count;
+    for (int64_t idx = blockIdx.x; idx < n; idx += gridDim.x) {
+        const int64_t i = list[idx];
+        const int64_t r = i - a.rb;
+        const int64_t s = a.A.rp[i], e = a.A.rp[i + 1];
+        for (int64_t base = s; base < e; base += kHugeThreads) {
+            const int64_t total = block_batch(a.A, a.T, base, e, s_incl, s_cs, s_a);
+            // every warp walks every chunk in order; it only touches its keys
+            for (int64_t c0 = 0; c0 < total; c0 += 32) {
+                const int64_t pp = c0 + l;
+                const bool inr = pp < total;
+                int j = -2 - l;
+                bool own = false;
+                double aik = 0.0, bjk = 0.0;
+                if (inr) {
+                    const int t = block_find(s_incl, pp);
+                    const int64_t ex = t ? s_incl[t - 1] : 0;
+                    const int64_t q = s_cs[t] + pp - ex;
+                    const int jj = a.T.ri[q];
+                    if (((jj >> 5) % kHugeWarps) == w) {
+                        own = true;
+                        j = jj;
+                        aik = s_a[t];
+                        bjk = a.T.vt[q];
+                    }
+                }
+                if (!__any_sync(kFull, own)) continue;
+                const unsigned g = __match_any_sync(kFull, j);
+                const int leader = __ffs(g) - 1;
+                const int rank = __popc(g & lt);
+                const int cnt = __popc(g);
+                double acc = 0.0;
+                if (own && rank == 0) {
+                    const unsigned bit = 1u << (j & 31);
+                    const unsigned old = atomicOr(&bm[j >> 5], bit);
+                    acc = (old & bit) ? acc_g[j] : +0.0;
+                }
+                (void)leader;
+                const int pred = rank ? 31 - __clz(g & lt) : l;
+                const int maxc = __reduce_max_sync(kFull, own ? cnt : 0);
+                for (int it = 0; it < maxc; ++it) {
+                    const double x = shfl_d(acc, pred);
+                    if (own && rank == it) acc = __fma_rn(aik, bjk, rank == 0 ? acc : x);
+                }
+                if (own && rank == cnt - 1) acc_g[j] = acc;
+                __syncwarp();
+            }
+            __syncthreads();
+        }
+        __threadfence_block();
+        __syncthreads();
+        // ---- emit in ascending j by scanning the bitmap
+        const int64_t g0 = a.gptr[r], ub = a.gptr[r + 1] - g0;
+        int64_t o = 0;
+        for (int64_t wb = 0; wb < nwords; wb += kHugeThreads) {
+            const int64_t wi = wb + threadIdx.x;
+            unsigned word = wi < nwords ? bm[wi] : 0u;
+            int keep = 0;
+            for (unsigned m = word; m; m &= m - 1) {
+                const int64_t j = wi * 32 + __ffs(m) - 1;
+                const double c = acc_g[j];
+                if (j == i) {
+                    if (a.diag) a.diag[r] = c;
+                } else if (fabs(c) > a.tol) {
+                    ++keep;
+                }
+            }
+            // block exclusive scan of keep
+            const int64_t inc = warp_incl_scan((int64_t)keep);
+            if (l == 31) s_scan[w] = inc;
+            __syncthreads();
+            int64_t wofs = 0, tot = 0;
+            for (int k = 0; k < kHugeWarps; ++k) {
+                if (k < w) wofs += s_scan[k];
+                tot += s_scan[k];
+            }
+            int64_t pos = g0 + o + wofs + inc - keep;
+            for (unsigned m = word; m; m &= m - 1) {
+                const int64_t j = wi * 32 + __ffs(m) - 1;
+                const double c = acc_g[j];
+                if (j != i && fabs(c) > a.tol) {
+                    a.gcol[pos] = (int32_t)j;
+                    a.gw[pos] = fabs(c);
+                    ++pos;
+                }
+            }
+            if (word) bm[wi] = 0u;
+            o += tot;
+            __syncthreads();
+        }
+        if (o < ub) {
+            for (int64_t t = o + threadIdx.x; t < ub; t += kHugeThreads) a.gcol[g0 + t] = -1;
+            if (threadIdx.x == 0) atomicOr(a.holes, 1);
+        }
+        __syncthreads();
+    }
+}
+
+void launch_sym_huge(const SymArgs &a, const int32_t *list, const int64_t *count, int slots, void *scratch,
+                     cudaStream_t s) {
+    const size_t slot_bytes = huge_scratch_bytes(a.A.nrows, 1, true);
+    k_sym_huge<<<slots, kHugeThreads, 0, s>>>(a, list, count, static_cast<unsigned char *>(scratch), slot_bytes);
+    note_launch();
+}
+
+void launch_num_huge(const NumArgs &a, const int32_t *list, const int64_t *count, int slots, void *scratch,
+                     cudaStream_t s) {
+    const size_t slot_bytes = huge_scratch_bytes(a.A.nrows, 1, true);
+    k_num_huge<<<slots, kHugeThreads, 0, s>>>(a, list, count, static_cast<unsigned char *>(scratch), slot_bytes,
+                                              bitmap_words(a.A.nrows));
+    note_launch();
+}
+
+}  // namespace rig

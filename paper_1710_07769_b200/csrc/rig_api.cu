@@ -1,0 +1,524 @@
+// rig_api.cu -- the C ABI declared in include/rig.h: argument checks, device
+// memory (stream-ordered pool), pass orchestration, error reporting.
+// Every step of the path runs in the kernels of k_*.cu; this file only
+// sequences them and reads back the few counters that size allocations.
+#include <atomic>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/rig.h"
+#include "common.cuh"
+
+namespace rig {
+
+static std::atomic<uint64_t> g_launches{0};
+void note_launch(int n) { g_launches.fetch_add((uint64_t)n, std::memory_order_relaxed); }
+
+int num_sms() {
+    static int cache[64] = {0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64) dev = 0;
+    if (!cache[dev]) {
+        int v = 0;
+        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+        cache[dev] = v > 0 ? v : 148;
+    }
+    return cache[dev];
+}
+
+struct Error : std::runtime_error {
+    int code;
+    Error(int c, const std::string &m) : std::runtime_error(m), code(c) {}
+};
+
+static thread_local std::string t_last_error;
+
+#define CK(call)                                                                                \
+    do {                                                                                        \
+        cudaError_t e_ = (call);                                                                \
+        if (e_ != cudaSuccess)                                                                  \
+            throw Error(e_ == cudaErrorMemoryAllocation ? RIG_ERR_NOMEM : RIG_ERR_CUDA,         \
+                        std::string(#call) + ": " + cudaGetErrorString(e_));                    \
+    } while (0)
+
+static void check_launch(const char *what) {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) throw Error(RIG_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+static void ensure_pool() {
+    static bool done[64] = {false};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev >= 0 && dev < 64 && !done[dev]) {
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            uint64_t thr = UINT64_MAX;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        }
+        done[dev] = true;
+    }
+}
+
+// Stream-ordered allocations owned by one call / plan.
+struct Arena {
+    cudaStream_t s;
+    std::vector<void *> ptrs;
+    explicit Arena(cudaStream_t st) : s(st) {}
+    template <typename T>
+    T *get(int64_t count) {
+        if (count <= 0) count = 1;
+        void *p = nullptr;
+        CK(cudaMallocAsync(&p, (size_t)count * sizeof(T), s));
+        ptrs.push_back(p);
+        return static_cast<T *>(p);
+    }
+    void release(void *p) {
+        for (auto &q : ptrs)
+            if (q == p) {
+                cudaFreeAsync(q, s);
+                q = nullptr;
+            }
+    }
+    ~Arena() {
+        for (void *p : ptrs)
+            if (p) cudaFreeAsync(p, s);
+    }
+};
+
+static int err_to_code(int err) {
+    if (err & kErrNonCanonical) return RIG_ERR_NONCANONICAL;
+    if (err & kErrNonFinite) return RIG_ERR_NONFINITE;
+    if (err & kErrZeroRow) return RIG_ERR_ZERO_ROW;
+    return RIG_OK;
+}
+
+static const char *err_msg(int code) {
+    switch (code) {
+        case RIG_ERR_NONCANONICAL: return "input CSR is not canonical";
+        case RIG_ERR_NONFINITE: return "non-finite value or row norm";
+        case RIG_ERR_ZERO_ROW: return "scale_rows with an empty or all-zero row";
+        default: return "error";
+    }
+}
+
+static void check_csr(const rig_csr_t *A) {
+    if (!A) throw Error(RIG_ERR_INVALID, "A is NULL");
+    if (A->nrows < 0 || A->ncols < 0 || A->nnz < 0) throw Error(RIG_ERR_INVALID, "negative size");
+    if (A->nrows > INT32_MAX || A->ncols > INT32_MAX) throw Error(RIG_ERR_INVALID, "nrows/ncols exceed int32");
+    if (!A->row_ptr) throw Error(RIG_ERR_INVALID, "row_ptr is NULL");
+    if (A->nnz > 0 && (!A->col_idx || !A->val)) throw Error(RIG_ERR_INVALID, "col_idx/val is NULL");
+}
+
+}  // namespace rig
+
+using namespace rig;
+
+// ---------------------------------------------------------------- the plan
+struct rig_plan {
+    cudaStream_t s;
+    Arena arena;
+    Csr A{};  // scaled view
+    Csc T{};
+    int scale = 0;
+    double tol = 0;
+    uint32_t flags = 0;
+    int64_t rb = 0, re = 0, nloc = 0;
+    DevCounters *ctr = nullptr;  // device
+    DevCounters h{};             // host copy
+    int32_t *sym_lists = nullptr, *num_lists = nullptr;
+    int64_t list_cap = 0;
+    int64_t *nnzc = nullptr, *gptr_ub = nullptr;
+    void *huge_scratch = nullptr;
+    int huge_slots_n = 0;
+    int64_t nnz_upper = 0;
+    explicit rig_plan(cudaStream_t st) : s(st), arena(st) {}
+};
+
+static void plan_build(rig_plan *p, const rig_csr_t *Ain) {
+    cudaStream_t s = p->s;
+    Arena &ar = p->arena;
+    const int64_t n = Ain->nrows, m = Ain->ncols, nnz = Ain->nnz;
+    Csr A0{n, m, nnz, Ain->row_ptr, Ain->col_idx, Ain->val};
+    p->ctr = ar.get<DevCounters>(1);
+    CK(cudaMemsetAsync(p->ctr, 0, sizeof(DevCounters), s));
+    // a0: validation must finish before anything indexes with the input
+    if (p->flags & RIG_FLAG_VALIDATE) {
+        launch_validate(A0, &p->ctr->err, s);
+        check_launch("validate");
+        int err = 0;
+        CK(cudaMemcpyAsync(&err, &p->ctr->err, sizeof(int), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        if (err) throw Error(err_to_code(err), err_msg(err_to_code(err)));
+    }
+    // a2: column histogram -> col_ptr
+    unsigned *cnt = ar.get<unsigned>(m);
+    int64_t *cp = ar.get<int64_t>(m + 1);
+    void *scan_tmp = ar.get<unsigned char>((int64_t)scan_tmp_bytes(std::max(m, n) + 1));
+    CK(cudaMemsetAsync(cnt, 0, sizeof(unsigned) * (size_t)std::max<int64_t>(m, 1), s));
+    if (nnz > 0) launch_col_hist(A0, cnt, s);
+    scan_u32(cnt, m, cp, scan_tmp, 0, s);
+    int64_t *cursor = ar.get<int64_t>(m);
+    if (m > 0) CK(cudaMemcpyAsync(cursor, cp, sizeof(int64_t) * (size_t)m, cudaMemcpyDeviceToDevice, s));
+    // a1 + a2: scale rows (optional) and scatter into the CSC
+    double *ahat = p->scale ? ar.get<double>(nnz) : nullptr;
+    int32_t *ri = ar.get<int32_t>(nnz);
+    double *vt = ar.get<double>(nnz);
+    if (n > 0) launch_scale_scatter(A0, p->scale, ahat, cursor, ri, vt, &p->ctr->err, s);
+    ar.release(cursor);
+    ar.release(cnt);
+    int32_t *long_list = ar.get<int32_t>(m);
+    if (m > 0) launch_col_sort(m, cp, ri, vt, long_list, &p->ctr->long_cols, s);
+    check_launch("prep");
+    p->A = Csr{n, m, nnz, Ain->row_ptr, Ain->col_idx, p->scale ? ahat : Ain->val};
+    p->T = Csc{cp, ri, vt};
+    // a3: products per row, bins for rows off the merge path
+    p->list_cap = p->nloc;
+    p->sym_lists = ar.get<int32_t>((int64_t)kSymBins * std::max<int64_t>(p->list_cap, 1));
+    if (p->nloc > 0) launch_analyze(p->A, cp, p->rb, p->re, nullptr, p->sym_lists, p->list_cap, p->ctr, s);
+    check_launch("analyze");
+    // sync 1: errors, bin sizes
+    CK(cudaMemcpyAsync(&p->h, p->ctr, sizeof(DevCounters), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (p->h.err) throw Error(err_to_code(p->h.err), err_msg(err_to_code(p->h.err)));
+    // a4: symbolic
+    p->nnzc = ar.get<int64_t>(p->nloc);
+    SymArgs sa{p->A, p->T, p->rb, p->re, p->nnzc};
+    if (p->nloc > 0) launch_sym_merge(sa, s);
+    const int64_t n_huge_sym = p->h.sym_count[kNumSymBins];
+    int64_t n_mid = p->h.n_mid;
+    if (n_mid > 0) {
+        launch_sym_warp(sa, p->sym_lists, p->list_cap, p->ctr->sym_count, p->h.sym_count, s);
+        if (n_huge_sym > 0) {
+            p->huge_slots_n = huge_slots(n, n_mid);
+            const size_t bytes = huge_scratch_bytes(n, p->huge_slots_n, true);
+            p->huge_scratch = ar.get<unsigned char>((int64_t)bytes);
+            CK(cudaMemsetAsync(p->huge_scratch, 0, bytes, s));
+            launch_sym_huge(sa, p->sym_lists + (int64_t)kNumSymBins * p->list_cap, p->ctr->sym_count + kNumSymBins,
+                            p->huge_slots_n, p->huge_scratch, s);
+        }
+        p->num_lists = ar.get<int32_t>((int64_t)kNumBins * n_mid);
+        launch_bin_num(p->sym_lists, p->list_cap, p->ctr, p->nnzc, p->rb, p->num_lists, n_mid, p->ctr->num_count, s);
+    }
+    check_launch("symbolic");
+    p->gptr_ub = ar.get<int64_t>(p->nloc + 1);
+    scan_i64(p->nnzc, p->nloc, p->gptr_ub, ScanOp::UbOffDiag, scan_tmp, 0, s);
+    check_launch("scan");
+    // sync 2: structural size, numeric bins
+    CK(cudaMemcpyAsync(&p->h, p->ctr, sizeof(DevCounters), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(&p->nnz_upper, p->gptr_ub + p->nloc, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+}
+
+// a5 + a6 into caller arrays (capacity nnz_upper).  Returns the final nnz.
+// `tmp` (nullable) provides nnz_upper*12 + (nloc+1)*8 bytes for compaction.
+static int64_t plan_numeric(rig_plan *p, int32_t *gcol, double *gw, double *diag, int64_t *row_ptr_out,
+                            Arena &tmp_arena) {
+    cudaStream_t s = p->s;
+    CK(cudaMemsetAsync(&p->ctr->holes, 0, sizeof(int), s));
+    NumArgs na{p->A, p->T, p->rb, p->re, p->gptr_ub, gcol, gw, (p->flags & RIG_FLAG_DIAG) ? diag : nullptr,
+               p->tol, &p->ctr->holes};
+    if (p->nloc > 0) launch_num_merge(na, s);
+    if (p->h.n_mid > 0) {
+        launch_num_warp(na, p->num_lists, p->h.n_mid, p->ctr->num_count, p->h.num_count, s);
+        const int64_t n_huge = p->h.num_count[kNumNumBins];
+        if (n_huge > 0) {
+            if (!p->huge_scratch) {
+                p->huge_slots_n = huge_slots(p->A.nrows, n_huge);
+                const size_t bytes = huge_scratch_bytes(p->A.nrows, p->huge_slots_n, true);
+                p->huge_scratch = p->arena.get<unsigned char>((int64_t)bytes);
+                CK(cudaMemsetAsync(p->huge_scratch, 0, bytes, s));
+            }
+            launch_num_huge(na, p->num_lists + (int64_t)kNumNumBins * p->h.n_mid, p->ctr->num_count + kNumNumBins,
+                            p->huge_slots_n, p->huge_scratch, s);
+        }
+    }
+    check_launch("numeric");
+    int holes = 0;
+    CK(cudaMemcpyAsync(&holes, &p->ctr->holes, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (!holes) {
+        CK(cudaMemcpyAsync(row_ptr_out, p->gptr_ub, sizeof(int64_t) * (size_t)(p->nloc + 1),
+                           cudaMemcpyDeviceToDevice, s));
+        return p->nnz_upper;
+    }
+    // holes: count kept entries per row, scan, move into a temporary, copy back
+    int64_t *kept = tmp_arena.get<int64_t>(p->nloc);
+    void *scan_tmp = tmp_arena.get<unsigned char>((int64_t)scan_tmp_bytes(p->nloc + 1));
+    launch_count_kept(p->gptr_ub, p->nloc, gcol, kept, s);
+    scan_i64(kept, p->nloc, row_ptr_out, ScanOp::Identity, scan_tmp, 0, s);
+    int64_t g = 0;
+    CK(cudaMemcpyAsync(&g, row_ptr_out + p->nloc, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    int32_t *c2 = tmp_arena.get<int32_t>(p->nnz_upper);
+    double *w2 = tmp_arena.get<double>(p->nnz_upper);
+    launch_compact_move(p->gptr_ub, row_ptr_out, p->nloc, gcol, gw, c2, w2, s);
+    check_launch("compact");
+    CK(cudaStreamSynchronize(s));
+    if (g > 0) {
+        CK(cudaMemcpyAsync(gcol, c2, sizeof(int32_t) * (size_t)g, cudaMemcpyDeviceToDevice, s));
+        CK(cudaMemcpyAsync(gw, w2, sizeof(double) * (size_t)g, cudaMemcpyDeviceToDevice, s));
+    }
+    return g;
+}
+
+static rig_plan *make_plan(const rig_csr_t *A, int scale_rows, double drop_tol, uint32_t flags, int64_t rb,
+                           int64_t re, cudaStream_t s) {
+    check_csr(A);
+    if (!(drop_tol >= 0.0) || std::isnan(drop_tol)) throw Error(RIG_ERR_INVALID, "drop_tol must be >= 0");
+    if (rb < 0 || re > A->nrows || rb > re) throw Error(RIG_ERR_INVALID, "bad row range");
+    ensure_pool();
+    rig_plan *p = new rig_plan(s);
+    p->scale = scale_rows ? 1 : 0;
+    p->tol = drop_tol;
+    p->flags = flags;
+    p->rb = rb;
+    p->re = re;
+    p->nloc = re - rb;
+    try {
+        plan_build(p, A);
+    } catch (...) {
+        delete p;
+        throw;
+    }
+    return p;
+}
+
+#define ABI_BEGIN try {
+#define ABI_END                                 \
+    }                                           \
+    catch (const Error &e) {                    \
+        t_last_error = e.what();                \
+        return e.code;                          \
+    }                                           \
+    catch (const std::exception &e) {           \
+        t_last_error = e.what();                \
+        return RIG_ERR_INVALID;                 \
+    }                                           \
+    catch (...) {                               \
+        t_last_error = "unknown error";         \
+        return RIG_ERR_INVALID;                 \
+    }
+
+// Library-owned output: allocate exactly-sized graph arrays.
+static void build_owned(const rig_csr_t *A, int scale_rows, double drop_tol, uint32_t flags, int64_t rb, int64_t re,
+                        rig_graph_t *out, cudaStream_t s) {
+    if (!out) throw Error(RIG_ERR_INVALID, "out is NULL");
+    std::memset(out, 0, sizeof(*out));
+    rig_plan *p = make_plan(A, scale_rows, drop_tol, flags, rb, re, s);
+    Arena tmp(s);
+    int64_t *rp = nullptr;
+    int32_t *col = nullptr;
+    double *w = nullptr, *diag = nullptr;
+    try {
+        CK(cudaMallocAsync((void **)&rp, sizeof(int64_t) * (size_t)(p->nloc + 1), s));
+        CK(cudaMallocAsync((void **)&col, sizeof(int32_t) * (size_t)std::max<int64_t>(p->nnz_upper, 1), s));
+        CK(cudaMallocAsync((void **)&w, sizeof(double) * (size_t)std::max<int64_t>(p->nnz_upper, 1), s));
+        if (flags & RIG_FLAG_DIAG) CK(cudaMallocAsync((void **)&diag, sizeof(double) * (size_t)std::max<int64_t>(p->nloc, 1), s));
+        const int64_t g = plan_numeric(p, col, w, diag, rp, tmp);
+        out->n = p->nloc;
+        out->nnz = g;
+        out->row_ptr = rp;
+        out->col_idx = col;
+        out->w = w;
+        out->diag = diag;
+    } catch (...) {
+        if (rp) cudaFreeAsync(rp, s);
+        if (col) cudaFreeAsync(col, s);
+        if (w) cudaFreeAsync(w, s);
+        if (diag) cudaFreeAsync(diag, s);
+        delete p;
+        throw;
+    }
+    delete p;
+}
+
+extern "C" {
+
+const char *rig_last_error(void) { return t_last_error.c_str(); }
+uint64_t rig_launch_count(void) { return g_launches.load(); }
+const char *rig_version(void) { return "librig 0.1 (sm_100a)"; }
+
+int rig_build(const rig_csr_t *A, int scale_rows, double drop_tol, uint32_t flags, rig_graph_t *out,
+              rig_stream_t stream) {
+    ABI_BEGIN
+    check_csr(A);
+    build_owned(A, scale_rows, drop_tol, flags, 0, A->nrows, out, (cudaStream_t)stream);
+    return RIG_OK;
+    ABI_END
+}
+
+int rig_build_rows(const rig_csr_t *A, int scale_rows, double drop_tol, uint32_t flags, int64_t row_begin,
+                   int64_t row_end, rig_graph_t *out, rig_stream_t stream) {
+    ABI_BEGIN
+    build_owned(A, scale_rows, drop_tol, flags, row_begin, row_end, out, (cudaStream_t)stream);
+    return RIG_OK;
+    ABI_END
+}
+
+int rig_graph_free(rig_graph_t *g, rig_stream_t stream) {
+    ABI_BEGIN
+    if (!g) throw Error(RIG_ERR_INVALID, "g is NULL");
+    cudaStream_t s = (cudaStream_t)stream;
+    if (g->row_ptr) CK(cudaFreeAsync(g->row_ptr, s));
+    if (g->col_idx) CK(cudaFreeAsync(g->col_idx, s));
+    if (g->w) CK(cudaFreeAsync(g->w, s));
+    if (g->diag) CK(cudaFreeAsync(g->diag, s));
+    std::memset(g, 0, sizeof(*g));
+    return RIG_OK;
+    ABI_END
+}
+
+int rig_plan_create(const rig_csr_t *A, int scale_rows, double drop_tol, uint32_t flags, int64_t row_begin,
+                    int64_t row_end, rig_plan_t **plan, rig_stream_t stream) {
+    ABI_BEGIN
+    if (!plan) throw Error(RIG_ERR_INVALID, "plan is NULL");
+    *plan = make_plan(A, scale_rows, drop_tol, flags, row_begin, row_end, (cudaStream_t)stream);
+    return RIG_OK;
+    ABI_END
+}
+
+int rig_plan_query(const rig_plan_t *plan, int64_t *nnz_upper, int64_t *products, size_t *workspace_bytes) {
+    ABI_BEGIN
+    if (!plan) throw Error(RIG_ERR_INVALID, "plan is NULL");
+    if (nnz_upper) *nnz_upper = plan->nnz_upper;
+    if (products) *products = plan->h.products;
+    if (workspace_bytes) *workspace_bytes = 0;
+    return RIG_OK;
+    ABI_END
+}
+
+int rig_plan_execute(rig_plan_t *plan, void *workspace, rig_graph_t *out, rig_stream_t stream) {
+    ABI_BEGIN
+    (void)workspace;
+    if (!plan || !out) throw Error(RIG_ERR_INVALID, "plan/out is NULL");
+    if (!out->row_ptr || ((!out->col_idx || !out->w) && plan->nnz_upper > 0))
+        throw Error(RIG_ERR_INVALID, "output arrays are NULL");
+    if ((plan->flags & RIG_FLAG_DIAG) && !out->diag && plan->nloc > 0)
+        throw Error(RIG_ERR_INVALID, "RIG_FLAG_DIAG needs out->diag");
+    plan->s = (cudaStream_t)stream;
+    Arena tmp(plan->s);
+    const int64_t g = plan_numeric(plan, out->col_idx, out->w, out->diag, out->row_ptr, tmp);
+    out->n = plan->nloc;
+    out->nnz = g;
+    return RIG_OK;
+    ABI_END
+}
+
+int rig_plan_destroy(rig_plan_t *plan) {
+    ABI_BEGIN
+    delete plan;
+    return RIG_OK;
+    ABI_END
+}
+
+int rig_row_split(const rig_csr_t *A, int32_t parts, int64_t *split, rig_stream_t stream) {
+    ABI_BEGIN
+    check_csr(A);
+    if (parts < 1 || !split) throw Error(RIG_ERR_INVALID, "parts < 1 or split NULL");
+    ensure_pool();
+    cudaStream_t s = (cudaStream_t)stream;
+    Arena ar(s);
+    const int64_t n = A->nrows, m = A->ncols;
+    Csr A0{n, m, A->nnz, A->row_ptr, A->col_idx, A->val};
+    unsigned *cnt = ar.get<unsigned>(m);
+    int64_t *cp = ar.get<int64_t>(m + 1);
+    void *scan_tmp = ar.get<unsigned char>((int64_t)scan_tmp_bytes(std::max(m, n) + 1));
+    CK(cudaMemsetAsync(cnt, 0, sizeof(unsigned) * (size_t)std::max<int64_t>(m, 1), s));
+    if (A->nnz > 0) launch_col_hist(A0, cnt, s);
+    scan_u32(cnt, m, cp, scan_tmp, 0, s);
+    int64_t *f = ar.get<int64_t>(n);
+    int64_t *fp = ar.get<int64_t>(n + 1);
+    DevCounters *ctr = ar.get<DevCounters>(1);
+    CK(cudaMemsetAsync(ctr, 0, sizeof(DevCounters), s));
+    if (n > 0) launch_analyze(A0, cp, 0, n, f, nullptr, 0, ctr, s);
+    scan_i64(f, n, fp, ScanOp::Identity, scan_tmp, 0, s);
+    int64_t *sp = ar.get<int64_t>(parts + 1);
+    launch_split(fp, n, parts, sp, s);
+    check_launch("split");
+    CK(cudaMemcpyAsync(split, sp, sizeof(int64_t) * (size_t)(parts + 1), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    return RIG_OK;
+    ABI_END
+}
+
+int rig_cutsize(const rig_graph_t *g, int64_t row_begin, int64_t n_global, const int32_t *part, int32_t K,
+                double *cut_dev, rig_stream_t stream) {
+    ABI_BEGIN
+    if (!g || !part || !cut_dev) throw Error(RIG_ERR_INVALID, "NULL argument");
+    if (K < 1 || n_global < 0 || row_begin < 0 || row_begin + g->n > n_global)
+        throw Error(RIG_ERR_INVALID, "bad K / row range");
+    if (!g->row_ptr || (g->nnz > 0 && (!g->col_idx || !g->w))) throw Error(RIG_ERR_INVALID, "graph arrays NULL");
+    ensure_pool();
+    cudaStream_t s = (cudaStream_t)stream;
+    Arena ar(s);
+    const int nb = cutsize_blocks();
+    double *partials = ar.get<double>(nb + 1);
+    launch_cutsize(g->row_ptr, g->col_idx, g->w, g->n, row_begin, n_global, part, K, partials, nb, cut_dev, s);
+    check_launch("cutsize");
+    return RIG_OK;
+    ABI_END
+}
+
+int rig_build_host(const rig_csr_t *Ah, int scale_rows, double drop_tol, uint32_t flags, const int32_t *part_host,
+                   int32_t K, rig_graph_t *out_host, int64_t capacity, double *cut_host, rig_stream_t stream) {
+    ABI_BEGIN
+    check_csr(Ah);
+    if (!out_host || !out_host->row_ptr) throw Error(RIG_ERR_INVALID, "out_host arrays are NULL");
+    if (part_host && K < 1) throw Error(RIG_ERR_INVALID, "K < 1");
+    ensure_pool();
+    cudaStream_t s = (cudaStream_t)stream;
+    Arena ar(s);
+    const int64_t n = Ah->nrows, nnz = Ah->nnz;
+    int64_t *rp = ar.get<int64_t>(n + 1);
+    int32_t *ci = ar.get<int32_t>(nnz);
+    double *v = ar.get<double>(nnz);
+    CK(cudaMemcpyAsync(rp, Ah->row_ptr, sizeof(int64_t) * (size_t)(n + 1), cudaMemcpyHostToDevice, s));
+    if (nnz > 0) {
+        CK(cudaMemcpyAsync(ci, Ah->col_idx, sizeof(int32_t) * (size_t)nnz, cudaMemcpyHostToDevice, s));
+        CK(cudaMemcpyAsync(v, Ah->val, sizeof(double) * (size_t)nnz, cudaMemcpyHostToDevice, s));
+    }
+    int32_t *part = nullptr;
+    if (part_host) {
+        part = ar.get<int32_t>(n);
+        CK(cudaMemcpyAsync(part, part_host, sizeof(int32_t) * (size_t)n, cudaMemcpyHostToDevice, s));
+    }
+    rig_csr_t Ad{n, Ah->ncols, nnz, rp, ci, v};
+    rig_graph_t g{};
+    build_owned(&Ad, scale_rows, drop_tol, flags, 0, n, &g, s);
+    struct Guard {
+        rig_graph_t *g;
+        cudaStream_t s;
+        ~Guard() { rig_graph_free(g, s); }
+    } guard{&g, s};
+    double *cut_dev = ar.get<double>(1);
+    if (part) {
+        rig_cutsize(&g, 0, n, part, K, cut_dev, s);
+    }
+    if (g.nnz > capacity) {
+        out_host->nnz = g.nnz;
+        throw Error(RIG_ERR_INVALID, "capacity too small for the graph");
+    }
+    CK(cudaMemcpyAsync(out_host->row_ptr, g.row_ptr, sizeof(int64_t) * (size_t)(n + 1), cudaMemcpyDeviceToHost, s));
+    if (g.nnz > 0) {
+        if (!out_host->col_idx || !out_host->w) throw Error(RIG_ERR_INVALID, "out_host col/w NULL");
+        CK(cudaMemcpyAsync(out_host->col_idx, g.col_idx, sizeof(int32_t) * (size_t)g.nnz, cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(out_host->w, g.w, sizeof(double) * (size_t)g.nnz, cudaMemcpyDeviceToHost, s));
+    }
+    if ((flags & RIG_FLAG_DIAG) && out_host->diag && n > 0)
+        CK(cudaMemcpyAsync(out_host->diag, g.diag, sizeof(double) * (size_t)n, cudaMemcpyDeviceToHost, s));
+    double cut = std::nan("");
+    if (part) CK(cudaMemcpyAsync(&cut, cut_dev, sizeof(double), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (cut_host) *cut_host = cut;
+    out_host->n = n;
+    out_host->nnz = g.nnz;
+    return RIG_OK;
+    ABI_END
+}
+
+}  // extern "C"

@@ -1,0 +1,64 @@
+"""librig.so loads and exports every symbol include/rig.h declares; host-side
+argument validation (no compute calls, no GPU needed)."""
+import ctypes
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def rig():
+    from paper_1710_07769_b200 import build
+
+    build.build()
+    from paper_1710_07769_b200 import rig as r
+
+    return r
+
+
+def test_header_symbols_exported(rig):
+    names = rig.header_symbols()
+    expected = {"rig_build", "rig_build_rows", "rig_graph_free", "rig_plan_create", "rig_plan_query",
+                "rig_plan_execute", "rig_plan_destroy", "rig_row_split", "rig_cutsize", "rig_build_host",
+                "rig_last_error", "rig_launch_count", "rig_version"}
+    assert set(names) == expected
+    so = ctypes.CDLL(rig.LIB_PATH)
+    for n in names:
+        assert hasattr(so, n), n
+
+
+def test_status_codes_match_header(rig):
+    txt = open(os.path.join(ROOT, "include", "rig.h")).read()
+    for name in ["RIG_OK", "RIG_ERR_INVALID", "RIG_ERR_NONCANONICAL", "RIG_ERR_ZERO_ROW", "RIG_ERR_NONFINITE",
+                 "RIG_ERR_NOMEM", "RIG_ERR_CUDA"]:
+        m = re.search(rf"#define {name} \(?(-?\d+)\)?", txt)
+        assert m and int(m.group(1)) == getattr(rig, name)
+    for name in ["RIG_FLAG_VALIDATE", "RIG_FLAG_DIAG"]:
+        m = re.search(rf"#define {name} (0x[0-9a-f]+)u", txt)
+        assert m and int(m.group(1), 16) == getattr(rig, name)
+
+
+def test_sm100a_only_cubin(rig):
+    import subprocess
+
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", rig.LIB_PATH], capture_output=True,
+                         text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_null_arguments_rejected_on_host(rig):
+    L = rig.lib
+    assert L.rig_build(None, 1, 0.0, 0, None, None) == rig.RIG_ERR_INVALID
+    assert b"NULL" in L.rig_last_error()
+    assert L.rig_plan_query(None, None, None, None) == rig.RIG_ERR_INVALID
+    assert L.rig_cutsize(None, 0, 0, None, 1, None, None) == rig.RIG_ERR_INVALID
+    A = rig.rig_csr_t(-1, 3, 0, 1, 1, 1)
+    assert L.rig_build(ctypes.byref(A), 1, 0.0, 0, ctypes.byref(rig.rig_graph_t()), None) == rig.RIG_ERR_INVALID
+    A = rig.rig_csr_t(3, 3, 0, 1, 1, 1)
+    assert L.rig_build(ctypes.byref(A), 1, -1.0, 0, ctypes.byref(rig.rig_graph_t()), None) == rig.RIG_ERR_INVALID
+    assert L.rig_build(ctypes.byref(A), 1, float("nan"), 0, ctypes.byref(rig.rig_graph_t()), None) == rig.RIG_ERR_INVALID
+    assert L.rig_row_split(ctypes.byref(A), 0, None, None) == rig.RIG_ERR_INVALID
+    assert rig.lib.rig_version().startswith(b"librig")

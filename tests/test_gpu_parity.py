@@ -1,0 +1,272 @@
+"""GPU parity: the CUDA path through the C ABI vs the CPU oracle, element by
+element on the same seeded inputs.
+
+Bar (BASELINE.json north_star): graph row_ptr / col_idx bit-exact; weights
+and cutsize within 1e-12 relative.  Under the ordering contract (DESIGN.md §3
+R4) the weights are expected bit-identical, so that is asserted too.
+"""
+import math
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+pytestmark = pytest.mark.gpu
+
+import oracle  # noqa: E402
+from rig_inputs import from_dense, from_triplets, make, make_small  # noqa: E402
+
+REL = 1e-12
+
+
+@pytest.fixture(scope="module")
+def rig():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    from paper_1710_07769_b200 import rig as r
+
+    return r
+
+
+def to_np(t):
+    return t.detach().cpu().numpy()
+
+
+def assert_graph_equal(g_rp, g_col, g_w, orc, g_diag=None, bitwise=True):
+    np.testing.assert_array_equal(g_rp, orc.row_ptr)
+    np.testing.assert_array_equal(g_col, orc.col)
+    if orc.w.size:
+        rel = np.abs(g_w - orc.w) / np.abs(orc.w)
+        assert rel.max() <= REL, f"max rel err {rel.max()}"
+    if bitwise:
+        assert g_w.tobytes() == orc.w.tobytes(), f"{int((g_w != orc.w).sum())} weights differ in bits"
+    if g_diag is not None:
+        assert g_diag.tobytes() == orc.diag.tobytes()
+
+
+def gpu_build(rig, w, flags=None, **kw):
+    A = rig.CSR(w.row_ptr, w.col_idx, w.val, ncols=w.ncols)
+    g = rig.rig_build(A, w.scale_rows, w.drop_tol, rig.RIG_FLAG_DIAG if flags is None else flags, **kw)
+    return A, g
+
+
+@pytest.mark.parametrize("cfg", [1, 2, 3, 4, 5])
+def test_small_configs_bitexact(rig, cfg):
+    w = make_small(cfg)
+    orc = oracle.build(w.row_ptr, w.col_idx, w.val, scale_rows=w.scale_rows, drop_tol=w.drop_tol)
+    A, g = gpu_build(rig, w)
+    assert g.n == w.n and g.nnz == orc.nnz
+    assert_graph_equal(to_np(g.row_ptr), to_np(g.col_idx), to_np(g.w), orc, to_np(g.diag))
+    part = torch.as_tensor(w.part, device="cuda")
+    cut = rig.rig_cutsize(g, part, w.K).item()
+    ocut = oracle.cutsize(orc.row_ptr, orc.col, orc.w, w.part, w.K)[0]
+    assert abs(cut - ocut) <= REL * abs(ocut)
+    # staged API gives the same graph
+    plan = rig.Plan(A, w.scale_rows, w.drop_tol, rig.RIG_FLAG_DIAG)
+    assert plan.products == orc.products
+    tg = plan.execute()
+    assert_graph_equal(to_np(tg.row_ptr), to_np(tg.col_idx), to_np(tg.w), orc, to_np(tg.diag))
+    plan.destroy()
+
+
+def test_shards_concatenate_bitwise(rig):
+    w = make_small(5)
+    A = rig.CSR(w.row_ptr, w.col_idx, w.val)
+    full = rig.rig_build(A, w.scale_rows, w.drop_tol)
+    split = rig.rig_row_split(A, 3)
+    assert split[0] == 0 and split[-1] == w.n and all(a <= b for a, b in zip(split, split[1:]))
+    f, P = oracle.row_products(w.row_ptr, w.col_idx, oracle.transpose(w.n, w.n, w.row_ptr, w.col_idx, w.val)[0])
+    pre = np.concatenate([[0], np.cumsum(f)])
+    for gi in range(4):  # split[g] = first r with prefix[r] >= ceil(g P / 3)
+        if gi < 3:
+            tgt = -(-gi * P // 3)
+            assert split[gi] == int(np.searchsorted(pre, tgt, side="left"))
+    cols, ws, cuts = [], [], []
+    part = torch.as_tensor(w.part, device="cuda")
+    for a, b in zip(split[:-1], split[1:]):
+        s = rig.rig_build_rows(A, a, b, w.scale_rows, w.drop_tol)
+        cols.append(to_np(s.col_idx)); ws.append(to_np(s.w))
+        cuts.append(rig.rig_cutsize(s, part, w.K).item())
+    np.testing.assert_array_equal(np.concatenate(cols), to_np(full.col_idx))
+    assert np.concatenate(ws).tobytes() == to_np(full.w).tobytes()
+    c_full = rig.rig_cutsize(full, part, w.K).item()
+    assert abs(sum(cuts) - c_full) <= REL * c_full
+
+
+def _dense_case(rig, D, scale, tol=0.0):
+    rp, ci, v = from_dense(D)
+    orc = oracle.build(rp, ci, v, ncols=D.shape[1], scale_rows=scale, drop_tol=tol)
+    A = rig.CSR(rp, ci, v, ncols=D.shape[1])
+    g = rig.rig_build(A, scale, tol, rig.RIG_FLAG_DIAG)
+    assert_graph_equal(to_np(g.row_ptr), to_np(g.col_idx), to_np(g.w), orc, to_np(g.diag) if g.n else None)
+    return g, orc
+
+
+def test_edge_cases(rig):
+    # paper worked example c_24 = 216, unscaled
+    D = np.zeros((8, 8)); D[1, 2] = 9; D[1, 6] = 6; D[3, 2] = 12; D[3, 6] = 18; D[0, 0] = 5; D[2, 1] = 4
+    g, _ = _dense_case(rig, D, 0)
+    G = np.zeros((8, 8))
+    rp, c, wv = to_np(g.row_ptr), to_np(g.col_idx), to_np(g.w)
+    for r in range(8):
+        G[r, c[rp[r]:rp[r + 1]]] = wv[rp[r]:rp[r + 1]]
+    assert G[1, 3] == 216.0 and G[3, 1] == 216.0
+    # exact cancellation -> no edge; drop rule strict
+    D = np.array([[1.0, 1.0, 0], [1.0, -1.0, 0], [0, 0, 2.0]])
+    g, orc = _dense_case(rig, D, 0)
+    assert g.nnz == 0
+    D = np.array([[1.0, 0.0], [0.5, 1.0]])
+    assert _dense_case(rig, D, 0, 0.5)[0].nnz == 0
+    assert _dense_case(rig, D, 0, np.nextafter(0.5, 0))[0].nnz == 2
+    # duplicate rows, one-row, empty rows (unscaled), rectangular
+    _dense_case(rig, np.array([[1.0, 2.0, 0.0], [1.0, 2.0, 0.0], [0.0, 0.0, 3.0]]), 1)
+    _dense_case(rig, np.array([[3.0, 4.0]]), 1)
+    _dense_case(rig, np.array([[0.0, 0.0, 0.0], [1.0, 0.0, 2.0], [0.0, 0.0, 0.0]]), 0)
+    rng = np.random.default_rng(5)
+    D = (rng.random((50, 80)) < 0.1) * rng.standard_normal((50, 80))
+    D[np.arange(50), rng.integers(0, 80, 50)] = 1.5
+    _dense_case(rig, D, 1)
+    # paper's dense-column example: nnz(AA^T) = 531
+    D = np.eye(25)
+    for r in range(25):
+        if r not in (2, 19):
+            D[r, 11] = 1.0 + r / 7.0
+    g, orc = _dense_case(rig, D, 1)
+    assert g.nnz == 506
+
+
+def test_empty_and_errors(rig):
+    A = rig.CSR(np.zeros(1, np.int64), np.zeros(0, np.int32), np.zeros(0))
+    g = rig.rig_build(A, 0, 0.0)
+    assert g.n == 0 and g.nnz == 0
+    A = rig.CSR(np.array([0, 2, 2, 3]), np.array([0, 1, 2], np.int32), np.array([1.0, 2.0, 3.0]))
+    with pytest.raises(rig.RigError) as e:
+        rig.rig_build(A, 1, 0.0)
+    assert e.value.code == rig.RIG_ERR_ZERO_ROW
+    A = rig.CSR(np.array([0, 2, 3]), np.array([0, 1, 2], np.int32), np.array([1.0, np.inf, 3.0]))
+    with pytest.raises(rig.RigError) as e:
+        rig.rig_build(A, 1, 0.0)
+    assert e.value.code == rig.RIG_ERR_NONFINITE
+    A = rig.CSR(np.array([0, 2, 3]), np.array([1, 0, 2], np.int32), np.array([1.0, 2.0, 3.0]))
+    with pytest.raises(rig.RigError) as e:
+        rig.rig_build(A, 1, 0.0, rig.RIG_FLAG_VALIDATE)
+    assert e.value.code == rig.RIG_ERR_NONCANONICAL
+    A = rig.CSR(np.array([0, 2, 3]), np.array([0, 5, 2], np.int32), np.array([1.0, 2.0, 3.0]))
+    with pytest.raises(rig.RigError):
+        rig.rig_build(A, 1, 0.0, rig.RIG_FLAG_VALIDATE)
+    # cutsize: K = 1 -> 0; out-of-range part -> NaN
+    w = make_small(1)
+    A = rig.CSR(w.row_ptr, w.col_idx, w.val)
+    g = rig.rig_build(A, 1, 0.0)
+    assert rig.rig_cutsize(g, torch.zeros(w.n, dtype=torch.int32, device="cuda"), 1).item() == 0.0
+    bad = torch.full((w.n,), 4, dtype=torch.int32, device="cuda")
+    assert math.isnan(rig.rig_cutsize(g, bad, 4).item())
+
+
+def test_long_rows_and_columns(rig):
+    """Warp-hash, huge-row and long-column-sort paths."""
+    rng = np.random.default_rng(11)
+    n = 20000
+    rows, cols = [], []
+    # row 0: 3000 distinct columns (f > 2048 -> huge symbolic and numeric)
+    c0 = rng.choice(n, 3000, replace=False); rows += [0] * 3000; cols += list(c0)
+    # rows 1..200: 20..600 entries (warp-hash bins)
+    for r in range(1, 201):
+        k = int(rng.integers(20, 600))
+        cc = rng.choice(n, k, replace=False); rows += [r] * k; cols += list(cc)
+    # column 7: 5000 entries (> 4096: in-place global bitonic column sort)
+    r7 = rng.choice(np.arange(201, n), 5000, replace=False); rows += list(r7); cols += [7] * 5000
+    # column 9: 600 entries (shared-memory column sort)
+    r9 = rng.choice(np.arange(201, n), 600, replace=False); rows += list(r9); cols += [9] * 600
+    # every row nonempty
+    rows += list(range(n)); cols += list(rng.integers(0, n, n))
+    rows, cols = np.array(rows), np.array(cols)
+    key = np.unique(rows.astype(np.int64) * n + cols)
+    rows, cols = key // n, key % n
+    vals = rng.standard_normal(rows.size)
+    rp, ci, v = from_triplets(n, n, rows, cols, vals)
+    orc = oracle.build(rp, ci, v, scale_rows=1, drop_tol=0.0)
+    A = rig.CSR(rp, ci, v)
+    g = rig.rig_build(A, 1, 0.0, rig.RIG_FLAG_DIAG)
+    assert_graph_equal(to_np(g.row_ptr), to_np(g.col_idx), to_np(g.w), orc, to_np(g.diag))
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_random_mixed(rig, seed):
+    rng = np.random.default_rng(1000 + seed)
+    n = int(rng.integers(500, 3000))
+    lens = np.clip(rng.zipf(1.8, n), 1, 300)
+    rows = np.repeat(np.arange(n), lens)
+    cols = rng.integers(0, n, rows.size)
+    key = np.unique(rows.astype(np.int64) * n + cols)
+    rows, cols = key // n, key % n
+    vals = rng.standard_normal(rows.size)
+    vals[rng.random(rows.size) < 0.3] = 1.0  # exact ties / cancellations
+    vals[rng.random(rows.size) < 0.3] = -1.0
+    rp, ci, v = from_triplets(n, n, rows, cols, vals)
+    for scale, tol in ((1, 0.0), (0, 0.5), (1, 1e-3)):
+        orc = oracle.build(rp, ci, v, scale_rows=scale, drop_tol=tol)
+        g = rig.rig_build(rig.CSR(rp, ci, v), scale, tol, rig.RIG_FLAG_DIAG)
+        assert_graph_equal(to_np(g.row_ptr), to_np(g.col_idx), to_np(g.w), orc, to_np(g.diag))
+
+
+def test_build_host_e2e(rig):
+    w = make_small(2)
+    orc = oracle.build(w.row_ptr, w.col_idx, w.val, scale_rows=1, drop_tol=0.0)
+    ocut = oracle.cutsize(orc.row_ptr, orc.col, orc.w, w.part, w.K)[0]
+    pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
+    rp, ci, v, part = pin(w.row_ptr), pin(w.col_idx), pin(w.val), pin(w.part)
+    orp = torch.empty(w.n + 1, dtype=torch.int64).pin_memory()
+    ocol = torch.empty(orc.nnz, dtype=torch.int32).pin_memory()
+    ow = torch.empty(orc.nnz, dtype=torch.float64).pin_memory()
+    nnz, cut = rig.rig_build_host(rp, ci, v, w.n, 1, 0.0, 0, part, w.K, orp, ocol, ow)
+    assert nnz == orc.nnz
+    np.testing.assert_array_equal(orp.numpy(), orc.row_ptr)
+    np.testing.assert_array_equal(ocol.numpy(), orc.col)
+    assert ow.numpy().tobytes() == orc.w.tobytes()
+    assert abs(cut - ocut) <= REL * ocut
+    small = torch.empty(10, dtype=torch.int32).pin_memory()
+    with pytest.raises(rig.RigError):
+        rig.rig_build_host(rp, ci, v, w.n, 1, 0.0, 0, part, w.K, orp, small, torch.empty(10, dtype=torch.float64))
+
+
+# ------------------------------------------------------------------ full size
+def _sample_windows(n, rng, k=4, width=1500):
+    starts = sorted(set([0, max(0, n - width)] + [int(x) for x in rng.integers(0, n - width, k)]))
+    return [(s, min(n, s + width)) for s in starts]
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("cfg", [1, 2, 3, 4, 5])
+def test_full_configs_sampled(rig, cfg):
+    """BASELINE.json full sizes in the launch configuration bench.py times
+    (rig_build over all rows): totals vs closed forms / oracle products, and
+    sampled row windows vs the oracle computing only those rows."""
+    w = make(cfg)
+    A = rig.CSR(w.row_ptr, w.col_idx, w.val)
+    g = rig.rig_build(A, w.scale_rows, w.drop_tol, rig.RIG_FLAG_DIAG)
+    torch.cuda.synchronize()
+    closed = {2: 11_980_004, 3: 190_322_400}
+    if cfg in closed:
+        assert g.nnz == closed[cfg]
+    rp = to_np(g.row_ptr)
+    rng = np.random.default_rng(cfg)
+    a_hat = oracle.scale(w.row_ptr, w.val)[0] if w.scale_rows else w.val
+    csc = oracle.transpose(w.n, w.n, w.row_ptr, w.col_idx, a_hat)
+    part = torch.as_tensor(w.part, device="cuda")
+    for a, b in _sample_windows(w.n, rng):
+        o_rp, o_col, o_w, o_diag, _ = oracle.build_from_scaled(w.n, w.n, w.row_ptr, w.col_idx, a_hat, csc,
+                                                               w.drop_tol, a, b)
+        s, e = int(rp[a]), int(rp[b])
+        np.testing.assert_array_equal(rp[a:b + 1] - s, o_rp)
+        np.testing.assert_array_equal(to_np(g.col_idx[s:e]), o_col)
+        assert to_np(g.w[s:e]).tobytes() == o_w.tobytes()
+        assert to_np(g.diag[a:b]).tobytes() == o_diag.tobytes()
+        # cutsize of the window: GPU (graph rows a..b) vs oracle
+        sub = rig.TensorGraph(g.row_ptr[a:b + 1] - s, g.col_idx[s:e], g.w[s:e], None, a)
+        c = rig.rig_cutsize(sub, part, w.K).item()
+        oc = oracle.cutsize(o_rp, o_col, o_w, w.part, w.K, row_begin=a)[0]
+        assert abs(c - oc) <= REL * max(oc, 1e-300)
+    # symmetry spot check via total: sum over j>i equals sum over j<i bitwise-symmetric weights
+    assert rig.rig_cutsize(g, torch.zeros(w.n, dtype=torch.int32, device="cuda"), 1).item() == 0.0
