@@ -1,0 +1,365 @@
+#!/usr/bin/env python
+"""Benchmark: one step = the whole hot path over
+one synthetic matrix resident in HBM: rig_build (scale, transpose, analyze,
+symbolic, numeric fused with abs/drop/diag-strip, compaction if needed) +
+rig_cutsize (+ NCCL allreduce of the cut when N > 1).
+
+Workload (N=1): BASELINE.json configs[1] -- 2-D convection-diffusion-like
+5-point stencil, n = 1,000,000.  Metric: A.A^T intermediate
+products per second (P / step time), plus build ms and the numeric pass's
+fraction of the measured HBM roofline.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--impl reference]
+N > 1: launch with torchrun (one rank per GPU); rows of C are sharded by
+flop count (rig_row_split), the cut is allreduced over NCCL, the time is the
+max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "A·A^T intermediate products/s and row-graph build ms; % of HBM roofline"
+L2_FLUSH_BYTES = 512 << 20
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", type=int, default=2, help="BASELINE.json config id (1-based); default configs[1]")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--soak-seconds", type=float, default=1.5,
+                    help="untimed steps before the timed region so clocks are sampled under load")
+    return ap.parse_args()
+
+
+def numeric_alg_bytes(n, nnz_a, nnz_c):
+    """read A CSR + read A_hat^T CSC + read row_ptr_C +
+    write C once = 24(n+1) + 24 nnzA + 12 nnzC (perfect L2 reuse of gathers)."""
+    return 24 * (n + 1) + 24 * nnz_a + 12 * nnz_c
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def load_traffic(cfg):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of the numeric
+    kernel from the committed ncu --set full summary, if present."""
+    p = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    try:
+        with open(p) as fh:
+            d = json.load(fh)
+        e = d.get("numeric", {}).get(f"config{cfg}")
+        return (float(e["dram_bytes"]), e.get("source")) if e else (None, None)
+    except Exception:
+        return None, None
+
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, dev_index):
+        self.dev = dev_index
+        self.proc = None
+        self.lines = []
+        self.mark = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits", "-lms", "100",
+                 "-i", str(self.dev)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            threading.Thread(target=self._read, daemon=True).start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append((time.time(), line.strip()))
+
+    def begin_load(self):
+        self.mark = time.time()
+
+    def stop(self):
+        end = time.time()
+        if self.proc:
+            time.sleep(0.15)
+            self.proc.terminate()
+            try:
+                self.proc.wait(2)
+            except Exception:
+                self.proc.kill()
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for t, line in self.lines:
+            if self.mark is None or t < self.mark or t > end + 0.2:
+                continue
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def cpu_baseline(w, seconds):
+    """The oracle as it stands (single-threaded C, oracle/), timed on this
+    host on repetitions of the full workload, bounded to ~`seconds`."""
+    import oracle
+
+    reps, t0 = 0, time.perf_counter()
+    P = None
+    while True:
+        g = oracle.build(w.row_ptr, w.col_idx, w.val, scale_rows=w.scale_rows, drop_tol=w.drop_tol)
+        oracle.cutsize(g.row_ptr, g.col, g.w, w.part, w.K)
+        P = g.products
+        reps += 1
+        el = time.perf_counter() - t0
+        if el >= seconds or reps >= 50:
+            break
+    return {"value": P * reps / el, "unit": "products/s", "cores": 1, "kind": "oracle",
+            "sample": f"full {w.name} workload (scale+CSC+Gustavson+cutsize) x {reps} in {el:.1f}s",
+            "ms_per_step": 1e3 * el / reps}
+
+
+def run_reference(args):
+    """--impl reference: the CPU oracle (the only reference this tier has)
+    timed as it stands on the host cores, on our arm's config/metric."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from rig_inputs import make
+
+    w = make(args.config)
+    import oracle
+
+    oracle.build_lib()
+    for _ in range(max(0, min(args.warmup, 1))):
+        oracle.build(w.row_ptr, w.col_idx, w.val, scale_rows=w.scale_rows, drop_tol=w.drop_tol)
+    times, P = [], None
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        g = oracle.build(w.row_ptr, w.col_idx, w.val, scale_rows=w.scale_rows, drop_tol=w.drop_tol)
+        oracle.cutsize(g.row_ptr, g.col, g.w, w.part, w.K)
+        times.append(time.perf_counter() - t0)
+        P = g.products
+    t = sum(times) / len(times)
+    v = P / t
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "products/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"{w.name} (BASELINE configs[{w.cfg_id - 1}])", "n": w.n, "nnz_A": w.nnz,
+                       "products": P, "K": w.K},
+            "cpu_baseline": {"value": v, "unit": "products/s", "cores": 1, "kind": "oracle",
+                             "sample": f"full {w.name} workload per step (scale+CSC+Gustavson+cutsize)"},
+            "e2e": {"value": v, "unit": "products/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import numpy as np
+    import torch
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.gpus != world and world > 1:
+        print(f"warning: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    from paper_1710_07769_b200 import rig
+    from rig_inputs import make
+
+    w = make(args.config)
+    stream = torch.cuda.current_stream()
+    A = rig.CSR(w.row_ptr, w.col_idx, w.val)
+    part = torch.as_tensor(w.part, device="cuda")
+    split = rig.rig_row_split(A, world) if world > 1 else [0, w.n]
+    rb, re = split[rank], split[rank + 1]
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.int32, device="cuda")
+
+    def step():
+        if world > 1:
+            g = rig.rig_build_rows(A, rb, re, w.scale_rows, w.drop_tol)
+        else:
+            g = rig.rig_build(A, w.scale_rows, w.drop_tol)
+        cut = rig.rig_cutsize(g, part, w.K, n_global=w.n)
+        if world > 1:
+            dist.all_reduce(cut)
+        return g, cut
+
+    # warm-up
+    for _ in range(max(args.warmup, 3)):
+        g, cut = step()
+    torch.cuda.synchronize()
+    nnz_local = g.nnz
+    # products of this shard / of the whole matrix (plan query == oracle-free count)
+    plan = rig.Plan(A, w.scale_rows, w.drop_tol, 0, rb, re)
+    P_local = plan.products
+    plan.destroy()
+    P_total = P_local
+    g_total = nnz_local
+    if world > 1:
+        t = torch.tensor([P_local, nnz_local], dtype=torch.int64, device="cuda")
+        dist.all_reduce(t)
+        P_total, g_total = int(t[0]), int(t[1])
+    # structural nnz(C) incl. diagonal = graph nnz + nonempty rows when nothing was dropped
+    nnz_c = g_total + int((np.diff(w.row_ptr) > 0).sum())
+
+    clocks = ClockSampler(local)
+    clocks.start()
+    clocks.begin_load()
+    t_end = time.time() + args.soak_seconds
+    while time.time() < t_end:
+        flush.zero_()
+        step()
+    torch.cuda.synchronize()
+
+    # ---- timed region: exactly K steps, L2 flushed between steps
+    rig.lib.rig_profile_read(None, None)
+    rig.lib.rig_profile_enable(1)
+    launches0 = rig.launch_count()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    for k in range(args.steps):
+        flush.zero_()
+        ev[k][0].record(stream)
+        g, cut = step()
+        ev[k][1].record(stream)
+        del g
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    launches = rig.launch_count() - launches0
+    rig.lib.rig_profile_enable(0)
+    import ctypes
+
+    pms = (ctypes.c_double * 12)()
+    pcnt = (ctypes.c_int64 * 12)()
+    rig.lib.rig_profile_read(pms, pcnt)
+    clk = clocks.stop()
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    my_ms = sum(step_ms) / len(step_ms)
+    pass_ms = {rig.lib.rig_pass_name(i).decode(): pms[i] / args.steps for i in range(12) if pcnt[i]}
+    num_ms = pass_ms.get("numeric", float("nan"))
+    if dist:
+        t = torch.tensor([my_ms, num_ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        my_ms, num_ms = float(t[0]), float(t[1])
+    cut_val = float(cut.item())
+
+    # ---- e2e through the C ABI from pinned host buffers (N=1 path)
+    e2e = None
+    if world == 1:
+        pin = lambda a: torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
+        hrp, hci, hv, hpart = pin(w.row_ptr), pin(w.col_idx), pin(w.val), pin(w.part)
+        orp = torch.empty(w.n + 1, dtype=torch.int64).pin_memory()
+        ocol = torch.empty(max(g_total, 1), dtype=torch.int32).pin_memory()
+        ow = torch.empty(max(g_total, 1), dtype=torch.float64).pin_memory()
+        for _ in range(2):
+            rig.rig_build_host(hrp, hci, hv, w.n, w.scale_rows, w.drop_tol, 0, hpart, w.K, orp, ocol, ow)
+        e_ms = []
+        for _ in range(max(3, min(args.steps, 10))):
+            flush.zero_()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            nn, ccut = rig.rig_build_host(hrp, hci, hv, w.n, w.scale_rows, w.drop_tol, 0, hpart, w.K, orp, ocol, ow)
+            b.record(stream)
+            torch.cuda.synchronize()
+            e_ms.append(a.elapsed_time(b))
+        em = sum(e_ms) / len(e_ms)
+        h2d = 8 * (w.n + 1) + 12 * w.nnz + 4 * w.n
+        d2h = 8 * (w.n + 1) + 12 * nn + 8
+        e2e = {"value": P_total / (em * 1e-3), "unit": "products/s", "ms_per_step": em, "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": d2h}
+
+    if rank != 0:
+        if dist:
+            dist.destroy_process_group()
+        return
+
+    peak, peak_src = load_peaks()
+    alg = numeric_alg_bytes(w.n, w.nnz, nnz_c) / max(world, 1) if world > 1 else numeric_alg_bytes(w.n, w.nnz, nnz_c)
+    achieved = alg / (num_ms * 1e-3) / 1e9
+    traffic, traffic_src = load_traffic(args.config)
+    line = {
+        "metric": METRIC,
+        "value": P_total / (my_ms * 1e-3),
+        "unit": "products/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": my_ms,
+        "higher_is_better": True,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": f"{w.name} (BASELINE configs[{w.cfg_id - 1}])", "n": w.n, "nnz_A": w.nnz,
+                   "products": P_total, "nnz_C": nnz_c, "graph_nnz": g_total, "K": w.K,
+                   "scale_rows": w.scale_rows, "drop_tol": w.drop_tol,
+                   "l2": f"flushed between timed steps ({L2_FLUSH_BYTES >> 20} MiB write)",
+                   "parallelism": f"rows of C sharded over {world} GPU(s), flop-balanced; NCCL allreduce of cut"
+                   if world > 1 else "1 GPU"},
+        "build_ms": my_ms - pass_ms.get("cutsize", 0.0),
+        "pass_ms": pass_ms,
+        "cut": cut_val,
+        "roofline": {"bound": "hbm", "kernel": "numeric (k_num_merge: a5+a6 fused)",
+                     "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": traffic, "alg_bytes": alg,
+                     "alg_bytes_formula": "SURVEY §8(d) F1 = 24(n+1) + 24 nnzA + 12 nnzC",
+                     "peak_source": peak_src, "traffic_source": traffic_src},
+        "gpu_launches": launches,
+        "clocks": clk,
+    }
+    if e2e:
+        line["e2e"] = e2e
+    if world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(w, args.cpu_seconds)
+    print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

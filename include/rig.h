@@ -167,6 +167,16 @@ RIG_API int rig_build_host(const rig_csr_t *A_host, int scale_rows, double drop_
 
 /* ---- diagnostics ------------------------------------------------------- */
 
+/* Per-pass device timing.  While enabled, every pass of rig_build /
+ * rig_plan_* / rig_cutsize records a CUDA event pair on the stream it runs
+ * on.  rig_profile_read waits for those events and returns, per pass id in
+ * [0, RIG_NPASS), the summed milliseconds and the number of occurrences since
+ * the previous read (then clears them).  Pass names: rig_pass_name. */
+#define RIG_NPASS 12
+RIG_API int rig_profile_enable(int on);
+RIG_API int rig_profile_read(double *ms, int64_t *count);
+RIG_API const char *rig_pass_name(int pass);
+
 RIG_API const char *rig_last_error(void);
 /* Number of kernels this library has launched since it was loaded. */
 RIG_API uint64_t rig_launch_count(void);

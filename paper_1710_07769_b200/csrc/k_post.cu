@@ -124,12 +124,19 @@ __global__ void __launch_bounds__(kCutThreads) k_cutsize(const int64_t *__restri
     if (__syncthreads_or(badp) && threadIdx.x == 0) atomicOr(bad, 1);
 }
 
-__global__ void k_cutsize_final(const double *partials, int n, const int *bad, double *cut) {
-    if (threadIdx.x == 0 && blockIdx.x == 0) {
-        double s = 0.0, c = 0.0;
-        for (int k = 0; k < n; ++k) neumaier_add(s, c, partials[k]);
-        *cut = *bad ? __longlong_as_double(0x7ff8000000000000ll) : s + c;
+// One CTA: strided Neumaier sums, then a fixed-shape tree (deterministic).
+__global__ void __launch_bounds__(kCutThreads) k_cutsize_final(const double *partials, int n, const int *bad,
+                                                               double *cut) {
+    double s = 0.0, c = 0.0;
+    for (int k = threadIdx.x; k < n; k += kCutThreads) neumaier_add(s, c, partials[k]);
+    __shared__ double red[kCutThreads];
+    red[threadIdx.x] = s + c;
+    __syncthreads();
+    for (int h = kCutThreads / 2; h > 0; h >>= 1) {
+        if (threadIdx.x < h) red[threadIdx.x] += red[threadIdx.x + h];
+        __syncthreads();
     }
+    if (threadIdx.x == 0) *cut = *bad ? __longlong_as_double(0x7ff8000000000000ll) : red[0];
 }
 
 int cutsize_blocks() { return num_sms() * 4; }
@@ -140,7 +147,7 @@ void launch_cutsize(const int64_t *grp, const int32_t *gcol, const double *gw, i
     int *bad = reinterpret_cast<int *>(partials + nblocks);
     cudaMemsetAsync(bad, 0, sizeof(int), s);
     k_cutsize<<<nblocks, kCutThreads, 0, s>>>(grp, gcol, gw, nloc, rb, n_global, part, K, partials, bad);
-    k_cutsize_final<<<1, 32, 0, s>>>(partials, nblocks, bad, cut);
+    k_cutsize_final<<<1, kCutThreads, 0, s>>>(partials, nblocks, bad, cut);
     note_launch(2);
 }
 

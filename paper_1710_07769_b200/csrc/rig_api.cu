@@ -4,6 +4,7 @@
 // sequences them and reads back the few counters that size allocations.
 #include <atomic>
 #include <cmath>
+#include <mutex>
 #include <cstdio>
 #include <cstring>
 #include <stdexcept>
@@ -30,6 +31,69 @@ int num_sms() {
     }
     return cache[dev];
 }
+
+// ---------------------------------------------------------------- profiling
+enum Pass {
+    P_VALIDATE = 0,
+    P_COLPTR,      // column histogram + scan
+    P_SCATTER,     // a1 scale + a2 scatter
+    P_COLSORT,
+    P_ANALYZE,     // a3
+    P_SYMBOLIC,    // a4 (+ numeric binning)
+    P_UBSCAN,
+    P_NUMERIC,     // a5 + a6 (fused)
+    P_COMPACT,     // a6 holes path
+    P_CUTSIZE,     // a7
+    P_SPLIT,
+    P_OTHER,
+};
+static const char *kPassNames[RIG_NPASS] = {"validate", "colptr",   "scale_scatter", "colsort",
+                                            "analyze",  "symbolic", "ub_scan",       "numeric",
+                                            "compact",  "cutsize",  "split",         "other"};
+static std::mutex g_prof_mu;
+static std::atomic<bool> g_prof_on{false};
+struct ProfRec {
+    int pass;
+    cudaEvent_t a, b;
+};
+static std::vector<ProfRec> g_recs;
+static std::vector<std::pair<int, cudaEvent_t>> g_pool;  // (device, event)
+
+static cudaEvent_t ev_get() {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    {
+        std::lock_guard<std::mutex> lk(g_prof_mu);
+        for (size_t k = 0; k < g_pool.size(); ++k)
+            if (g_pool[k].first == dev) {
+                cudaEvent_t e = g_pool[k].second;
+                g_pool.erase(g_pool.begin() + (long)k);
+                return e;
+            }
+    }
+    cudaEvent_t e = nullptr;
+    cudaEventCreate(&e);
+    return e;
+}
+
+struct Prof {
+    int pass;
+    cudaStream_t s;
+    cudaEvent_t a = nullptr;
+    Prof(int p, cudaStream_t st) : pass(p), s(st) {
+        if (g_prof_on.load(std::memory_order_relaxed)) {
+            a = ev_get();
+            cudaEventRecord(a, s);
+        }
+    }
+    ~Prof() {
+        if (!a) return;
+        cudaEvent_t b = ev_get();
+        cudaEventRecord(b, s);
+        std::lock_guard<std::mutex> lk(g_prof_mu);
+        g_recs.push_back({pass, a, b});
+    }
+};
 
 struct Error : std::runtime_error {
     int code;
@@ -149,6 +213,7 @@ static void plan_build(rig_plan *p, const rig_csr_t *Ain) {
     CK(cudaMemsetAsync(p->ctr, 0, sizeof(DevCounters), s));
     // a0: validation must finish before anything indexes with the input
     if (p->flags & RIG_FLAG_VALIDATE) {
+        Prof pf(P_VALIDATE, s);
         launch_validate(A0, &p->ctr->err, s);
         check_launch("validate");
         int err = 0;
@@ -160,27 +225,39 @@ static void plan_build(rig_plan *p, const rig_csr_t *Ain) {
     unsigned *cnt = ar.get<unsigned>(m);
     int64_t *cp = ar.get<int64_t>(m + 1);
     void *scan_tmp = ar.get<unsigned char>((int64_t)scan_tmp_bytes(std::max(m, n) + 1));
-    CK(cudaMemsetAsync(cnt, 0, sizeof(unsigned) * (size_t)std::max<int64_t>(m, 1), s));
-    if (nnz > 0) launch_col_hist(A0, cnt, s);
-    scan_u32(cnt, m, cp, scan_tmp, 0, s);
     int64_t *cursor = ar.get<int64_t>(m);
-    if (m > 0) CK(cudaMemcpyAsync(cursor, cp, sizeof(int64_t) * (size_t)m, cudaMemcpyDeviceToDevice, s));
+    {
+        Prof pf(P_COLPTR, s);
+        CK(cudaMemsetAsync(cnt, 0, sizeof(unsigned) * (size_t)std::max<int64_t>(m, 1), s));
+        if (nnz > 0) launch_col_hist(A0, cnt, s);
+        scan_u32(cnt, m, cp, scan_tmp, 0, s);
+        if (m > 0) CK(cudaMemcpyAsync(cursor, cp, sizeof(int64_t) * (size_t)m, cudaMemcpyDeviceToDevice, s));
+    }
     // a1 + a2: scale rows (optional) and scatter into the CSC
     double *ahat = p->scale ? ar.get<double>(nnz) : nullptr;
     int32_t *ri = ar.get<int32_t>(nnz);
     double *vt = ar.get<double>(nnz);
-    if (n > 0) launch_scale_scatter(A0, p->scale, ahat, cursor, ri, vt, &p->ctr->err, s);
+    if (n > 0) {
+        Prof pf(P_SCATTER, s);
+        launch_scale_scatter(A0, p->scale, ahat, cursor, ri, vt, &p->ctr->err, s);
+    }
     ar.release(cursor);
     ar.release(cnt);
     int32_t *long_list = ar.get<int32_t>(m);
-    if (m > 0) launch_col_sort(m, cp, ri, vt, long_list, &p->ctr->long_cols, s);
+    if (m > 0) {
+        Prof pf(P_COLSORT, s);
+        launch_col_sort(m, cp, ri, vt, long_list, &p->ctr->long_cols, s);
+    }
     check_launch("prep");
     p->A = Csr{n, m, nnz, Ain->row_ptr, Ain->col_idx, p->scale ? ahat : Ain->val};
     p->T = Csc{cp, ri, vt};
     // a3: products per row, bins for rows off the merge path
     p->list_cap = p->nloc;
     p->sym_lists = ar.get<int32_t>((int64_t)kSymBins * std::max<int64_t>(p->list_cap, 1));
-    if (p->nloc > 0) launch_analyze(p->A, cp, p->rb, p->re, nullptr, p->sym_lists, p->list_cap, p->ctr, s);
+    if (p->nloc > 0) {
+        Prof pf(P_ANALYZE, s);
+        launch_analyze(p->A, cp, p->rb, p->re, nullptr, p->sym_lists, p->list_cap, p->ctr, s);
+    }
     check_launch("analyze");
     // sync 1: errors, bin sizes
     CK(cudaMemcpyAsync(&p->h, p->ctr, sizeof(DevCounters), cudaMemcpyDeviceToHost, s));
@@ -189,6 +266,7 @@ static void plan_build(rig_plan *p, const rig_csr_t *Ain) {
     // a4: symbolic
     p->nnzc = ar.get<int64_t>(p->nloc);
     SymArgs sa{p->A, p->T, p->rb, p->re, p->nnzc};
+    Prof *pf_sym = new Prof(P_SYMBOLIC, s);
     if (p->nloc > 0) launch_sym_merge(sa, s);
     const int64_t n_huge_sym = p->h.sym_count[kNumSymBins];
     int64_t n_mid = p->h.n_mid;
@@ -205,9 +283,13 @@ static void plan_build(rig_plan *p, const rig_csr_t *Ain) {
         p->num_lists = ar.get<int32_t>((int64_t)kNumBins * n_mid);
         launch_bin_num(p->sym_lists, p->list_cap, p->ctr, p->nnzc, p->rb, p->num_lists, n_mid, p->ctr->num_count, s);
     }
+    delete pf_sym;
     check_launch("symbolic");
     p->gptr_ub = ar.get<int64_t>(p->nloc + 1);
-    scan_i64(p->nnzc, p->nloc, p->gptr_ub, ScanOp::UbOffDiag, scan_tmp, 0, s);
+    {
+        Prof pf(P_UBSCAN, s);
+        scan_i64(p->nnzc, p->nloc, p->gptr_ub, ScanOp::UbOffDiag, scan_tmp, 0, s);
+    }
     check_launch("scan");
     // sync 2: structural size, numeric bins
     CK(cudaMemcpyAsync(&p->h, p->ctr, sizeof(DevCounters), cudaMemcpyDeviceToHost, s));
@@ -220,6 +302,7 @@ static void plan_build(rig_plan *p, const rig_csr_t *Ain) {
 static int64_t plan_numeric(rig_plan *p, int32_t *gcol, double *gw, double *diag, int64_t *row_ptr_out,
                             Arena &tmp_arena) {
     cudaStream_t s = p->s;
+    Prof *pf_num = new Prof(P_NUMERIC, s);
     CK(cudaMemsetAsync(&p->ctr->holes, 0, sizeof(int), s));
     NumArgs na{p->A, p->T, p->rb, p->re, p->gptr_ub, gcol, gw, (p->flags & RIG_FLAG_DIAG) ? diag : nullptr,
                p->tol, &p->ctr->holes};
@@ -238,6 +321,7 @@ static int64_t plan_numeric(rig_plan *p, int32_t *gcol, double *gw, double *diag
                             p->huge_slots_n, p->huge_scratch, s);
         }
     }
+    delete pf_num;
     check_launch("numeric");
     int holes = 0;
     CK(cudaMemcpyAsync(&holes, &p->ctr->holes, sizeof(int), cudaMemcpyDeviceToHost, s));
@@ -248,6 +332,7 @@ static int64_t plan_numeric(rig_plan *p, int32_t *gcol, double *gw, double *diag
         return p->nnz_upper;
     }
     // holes: count kept entries per row, scan, move into a temporary, copy back
+    Prof pf_c(P_COMPACT, s);
     int64_t *kept = tmp_arena.get<int64_t>(p->nloc);
     void *scan_tmp = tmp_arena.get<unsigned char>((int64_t)scan_tmp_bytes(p->nloc + 1));
     launch_count_kept(p->gptr_ub, p->nloc, gcol, kept, s);
@@ -340,6 +425,40 @@ static void build_owned(const rig_csr_t *A, int scale_rows, double drop_tol, uin
 extern "C" {
 
 const char *rig_last_error(void) { return t_last_error.c_str(); }
+
+int rig_profile_enable(int on) {
+    g_prof_on.store(on != 0);
+    return RIG_OK;
+}
+
+int rig_profile_read(double *ms, int64_t *count) {
+    ABI_BEGIN
+    std::vector<ProfRec> recs;
+    {
+        std::lock_guard<std::mutex> lk(g_prof_mu);
+        recs.swap(g_recs);
+    }
+    for (int k = 0; k < RIG_NPASS; ++k) {
+        if (ms) ms[k] = 0.0;
+        if (count) count[k] = 0;
+    }
+    int dev = 0;
+    cudaGetDevice(&dev);
+    for (auto &r : recs) {
+        CK(cudaEventSynchronize(r.b));
+        float t = 0.f;
+        CK(cudaEventElapsedTime(&t, r.a, r.b));
+        if (ms) ms[r.pass] += (double)t;
+        if (count) count[r.pass] += 1;
+        std::lock_guard<std::mutex> lk(g_prof_mu);
+        g_pool.push_back({dev, r.a});
+        g_pool.push_back({dev, r.b});
+    }
+    return RIG_OK;
+    ABI_END
+}
+
+const char *rig_pass_name(int pass) { return (pass >= 0 && pass < RIG_NPASS) ? kPassNames[pass] : "?"; }
 uint64_t rig_launch_count(void) { return g_launches.load(); }
 const char *rig_version(void) { return "librig 0.1 (sm_100a)"; }
 
@@ -458,6 +577,7 @@ int rig_cutsize(const rig_graph_t *g, int64_t row_begin, int64_t n_global, const
     Arena ar(s);
     const int nb = cutsize_blocks();
     double *partials = ar.get<double>(nb + 1);
+    Prof pf(P_CUTSIZE, s);
     launch_cutsize(g->row_ptr, g->col_idx, g->w, g->n, row_begin, n_global, part, K, partials, nb, cut_dev, s);
     check_launch("cutsize");
     return RIG_OK;

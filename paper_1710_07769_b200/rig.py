@@ -61,6 +61,10 @@ def _load():
     L.rig_last_error.restype = ctypes.c_char_p
     L.rig_launch_count.restype = ctypes.c_uint64
     L.rig_version.restype = ctypes.c_char_p
+    L.rig_profile_enable.argtypes = [ctypes.c_int]
+    L.rig_profile_read.argtypes = [P, P]
+    L.rig_pass_name.argtypes = [ctypes.c_int]
+    L.rig_pass_name.restype = ctypes.c_char_p
     return L
 
 
@@ -112,17 +116,40 @@ class _Cai:
                                          "version": 3, "strides": None, "stream": None}
 
 
+class _GraphOwner:
+    """Owns the library-allocated arrays of one graph; freed (rig_graph_free,
+    stream-ordered on the current stream) when the Graph and every tensor view
+    of it are gone.  Holds no reference back to them: no reference cycle."""
+
+    def __init__(self, g: rig_graph_t):
+        self.g = g
+
+    def __del__(self):
+        try:
+            if self.g is not None:
+                lib.rig_graph_free(ctypes.byref(self.g), _stream())
+                self.g = None
+        except Exception:
+            pass
+
+
 class Graph:
     """G_RIP rows [row_begin, row_begin+n): library-owned device arrays
-    (rig_build), released by rig_graph_free when garbage collected."""
+    (rig_build) exposed as torch views."""
 
     def __init__(self, g: rig_graph_t, row_begin: int, stream):
-        self._g = g
+        self._owner = _GraphOwner(g)
+        self._g = rig_graph_t(g.n, g.nnz, g.row_ptr, g.col_idx, g.w, g.diag)
         self.row_begin = row_begin
-        self._stream = stream
         self.n, self.nnz = int(g.n), int(g.nnz)
         dev = torch.device("cuda", torch.cuda.current_device())
-        mk = lambda p, n, t, dt: torch.as_tensor(_Cai(p, n, t, self), device=dev) if n else torch.empty(0, dtype=dt, device=dev)
+        own = self._owner
+
+        def mk(p, n, t, dt):
+            if not n:
+                return torch.empty(0, dtype=dt, device=dev)
+            return torch.as_tensor(_Cai(p, n, t, own), device=dev)
+
         self.row_ptr = mk(g.row_ptr, self.n + 1, "<i8", torch.int64)
         self.col_idx = mk(g.col_idx, self.nnz, "<i4", torch.int32)
         self.w = mk(g.w, self.nnz, "<f8", torch.float64)
@@ -130,18 +157,6 @@ class Graph:
 
     def c(self):
         return self._g
-
-    def free(self):
-        if self._g is not None and (self._g.row_ptr or self._g.col_idx):
-            self.row_ptr = self.col_idx = self.w = self.diag = None
-            lib.rig_graph_free(ctypes.byref(self._g), _stream())
-        self._g = None
-
-    def __del__(self):
-        try:
-            self.free()
-        except Exception:
-            pass
 
 
 class TensorGraph:
