@@ -51,7 +51,7 @@ struct DevCounters {
     int err;
     int holes;          // numeric pass dropped an entry (|c| <= tol or exact 0)
     unsigned long_cols; // columns longer than the short-sort limit
-    int bad_part;
+    int max_len;        // longest A row (in the shard) on the merge path
     int64_t products;   // sum f_i over the shard
     int64_t n_mid;      // rows not on the merge path
     int64_t sym_count[8];
@@ -130,8 +130,9 @@ struct NumArgs {
     double tol;
     int *holes;
 };
-void launch_sym_merge(const SymArgs &a, cudaStream_t s);
-void launch_num_merge(const NumArgs &a, cudaStream_t s);
+// maxlen: longest A row on the merge path in the shard (DevCounters::max_len)
+void launch_sym_merge(const SymArgs &a, int maxlen, cudaStream_t s);
+void launch_num_merge(const NumArgs &a, int maxlen, cudaStream_t s);
 // counts: device bin sizes (loop bounds); hcounts: host copy (skip empty bins)
 void launch_sym_warp(const SymArgs &a, const int32_t *lists, int64_t list_cap, const int64_t *counts,
                      const int64_t *hcounts, cudaStream_t s);

@@ -94,22 +94,33 @@ __global__ void __launch_bounds__(kCutThreads) k_cutsize(const int64_t *__restri
         const int32_t pi = l < rows ? part[rb + r0 + l] : 0;
         const int64_t lo = __shfl_sync(kFull, my_start, 0);
         const int64_t last = __shfl_sync(kFull, my_start, 31);
-        for (int64_t base = lo; base < hi; base += 32) {
-            const int64_t e = base + l;
-            // row of edge e: (number of lanes with start <= e) - 1
-            int t = 0;
+        constexpr int U = 4;  // chunks of 32 edges in flight per iteration
+        for (int64_t base = lo; base < hi; base += 32 * U) {
+            int32_t j[U], pj[U];
+            double wv[U];
+            int64_t e[U];
 #pragma unroll
-            for (int step = 16; step >= 1; step >>= 1) {
-                const int64_t v = __shfl_sync(kFull, my_start, t + step - 1);
-                if (v <= e) t += step;
+            for (int u = 0; u < U; ++u) {
+                e[u] = base + 32 * u + l;
+                const bool v = e[u] < hi;
+                j[u] = v ? gcol[e[u]] : 0;
+                wv[u] = v ? gw[e[u]] : 0.0;
             }
-            if (t == 31 && last <= e) t = 32;
-            const int row = t - 1;
-            const int32_t prow = __shfl_sync(kFull, pi, row < 0 ? 0 : row);
-            if (e < hi) {
-                const int64_t i = rb + r0 + row;
-                const int32_t j = gcol[e];
-                if ((int64_t)j > i && part[j] != prow) neumaier_add(s, c, gw[e]);
+#pragma unroll
+            for (int u = 0; u < U; ++u) pj[u] = e[u] < hi ? part[j[u]] : 0;
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                // row of edge e: (number of lanes with start <= e) - 1
+                int t = 0;
+#pragma unroll
+                for (int step = 16; step >= 1; step >>= 1) {
+                    const int64_t v = __shfl_sync(kFull, my_start, t + step - 1);
+                    if (v <= e[u]) t += step;
+                }
+                if (t == 31 && last <= e[u]) t = 32;
+                const int row = t - 1;
+                const int32_t prow = __shfl_sync(kFull, pi, row < 0 ? 0 : row);
+                if (e[u] < hi && (int64_t)j[u] > rb + r0 + row && pj[u] != prow) neumaier_add(s, c, wv[u]);
             }
         }
     }
@@ -139,7 +150,7 @@ __global__ void __launch_bounds__(kCutThreads) k_cutsize_final(const double *par
     if (threadIdx.x == 0) *cut = *bad ? __longlong_as_double(0x7ff8000000000000ll) : red[0];
 }
 
-int cutsize_blocks() { return num_sms() * 4; }
+int cutsize_blocks() { return num_sms() * 8; }
 
 void launch_cutsize(const int64_t *grp, const int32_t *gcol, const double *gw, int64_t nloc, int64_t rb,
                     int64_t n_global, const int32_t *part, int32_t K, double *partials, int nblocks, double *cut,

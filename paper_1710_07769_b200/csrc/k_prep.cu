@@ -83,7 +83,27 @@ __global__ void k_scale_scatter(Csr A, int scale, double *__restrict__ ahat, int
             }
             nrm = __dsqrt_rn(ss);
         }
-        for (int64_t p = s; p < e; ++p) {
+        // four independent atomics in flight per thread
+        int64_t p = s;
+        for (; p + 4 <= e; p += 4) {
+            int k[4];
+            double x[4];
+            unsigned long long q[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                k[u] = A.ci[p + u];
+                x[u] = scale ? __ddiv_rn(A.v[p + u], nrm) : A.v[p + u];
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) q[u] = atomicAdd((unsigned long long *)&cursor[k[u]], 1ull);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                if (scale) ahat[p + u] = x[u];
+                ri[q[u]] = (int32_t)i;
+                vt[q[u]] = x[u];
+            }
+        }
+        for (; p < e; ++p) {
             const double x = scale ? __ddiv_rn(A.v[p], nrm) : A.v[p];
             if (scale) ahat[p] = x;
             const int k = A.ci[p];
@@ -105,6 +125,22 @@ void launch_scale_scatter(const Csr &A, int scale, double *ahat, int64_t *cursor
 // needs each column's rows ascending.  Short columns: insertion sort by one
 // thread; long ones go to a list sorted by a CTA.
 constexpr int kShortCol = 32;
+constexpr int kRegCol = 8;
+
+// Odd-even transposition network on registers (static indices only).
+template <int N>
+__device__ __forceinline__ void sort_regs(int32_t (&k)[N], double (&v)[N]) {
+#pragma unroll
+    for (int r = 0; r < N; ++r) {
+#pragma unroll
+        for (int i = r & 1; i + 1 < N; i += 2) {
+            const bool sw = k[i] > k[i + 1];
+            const int32_t ka = sw ? k[i + 1] : k[i], kb = sw ? k[i] : k[i + 1];
+            const double va = sw ? v[i + 1] : v[i], vb = sw ? v[i] : v[i + 1];
+            k[i] = ka; k[i + 1] = kb; v[i] = va; v[i + 1] = vb;
+        }
+    }
+}
 
 __global__ void k_col_sort_short(int64_t ncols, const int64_t *__restrict__ cp, int32_t *ri, double *vt,
                                  int32_t *long_list, unsigned *long_count) {
@@ -113,6 +149,27 @@ __global__ void k_col_sort_short(int64_t ncols, const int64_t *__restrict__ cp, 
         const int64_t s = cp[k], len = cp[k + 1] - s;
         if (len > kShortCol) {
             long_list[atomicAdd(long_count, 1u)] = (int32_t)k;
+            continue;
+        }
+        if (len <= kRegCol) {
+            int32_t kk[kRegCol];
+            double vv[kRegCol];
+            bool sorted = true;
+#pragma unroll
+            for (int t = 0; t < kRegCol; ++t) {
+                kk[t] = t < len ? ri[s + t] : INT_MAX;
+                vv[t] = t < len ? vt[s + t] : 0.0;
+                if (t > 0) sorted &= kk[t - 1] <= kk[t];
+            }
+            if (sorted) continue;
+            sort_regs<kRegCol>(kk, vv);
+#pragma unroll
+            for (int t = 0; t < kRegCol; ++t) {
+                if (t < len) {
+                    ri[s + t] = kk[t];
+                    vt[s + t] = vv[t];
+                }
+            }
             continue;
         }
         for (int64_t a = 1; a < len; ++a) {
@@ -230,6 +287,7 @@ __global__ void k_analyze(Csr A, const int64_t *__restrict__ cp, int64_t rb, int
     const int64_t nloc = re - rb;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     int64_t local = 0;
+    int maxlen = 0;
     for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < nloc; r += stride) {
         const int64_t i = rb + r;
         const int64_t s = A.rp[i], e = A.rp[i + 1];
@@ -240,7 +298,9 @@ __global__ void k_analyze(Csr A, const int64_t *__restrict__ cp, int64_t rb, int
         }
         if (f) f[r] = fi;
         local += fi;
-        if (sym_lists && !(e - s <= kMergeMaxLen && fi <= kMergeMaxF)) {
+        const bool merge = e - s <= kMergeMaxLen && fi <= kMergeMaxF;
+        if (merge) maxlen = max(maxlen, (int)(e - s));
+        if (sym_lists && !merge) {
             int lg = ceil_log2_2x(fi);
             if (lg < kSymBinMinLog) lg = kSymBinMinLog;
             const int b = lg > kSymBinMaxLog ? kNumSymBins : lg - kSymBinMinLog;
@@ -249,6 +309,8 @@ __global__ void k_analyze(Csr A, const int64_t *__restrict__ cp, int64_t rb, int
             atomicAdd((unsigned long long *)&ctr->n_mid, 1ull);
         }
     }
+    maxlen = __reduce_max_sync(kFull, maxlen);
+    if (lane_id() == 0 && maxlen) atomicMax(&ctr->max_len, maxlen);
     local = warp_sum(local);
     __shared__ int64_t part[32];
     if (lane_id() == 0) part[threadIdx.x >> 5] = local;

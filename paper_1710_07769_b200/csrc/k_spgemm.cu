@@ -23,16 +23,20 @@ namespace rig {
 static int g_sms_cache = 0;
 
 // ======================================================== merge path
-template <int R>
+// One thread per row i.  The row's R column runs (column k of A_hat^T, rows j
+// ascending) are merged; for the current minimum j the runs holding it are
+// folded in ascending k: c_ij = fma(a_ik, a_jk, c_ij) -- the ordered chain.
+// IdxT: int32 CSC offsets when nnz < 2^31 (fewer registers), else int64.
+template <int R, typename IdxT>
 __device__ __forceinline__ int64_t sym_merge_row(const Csr &A, const Csc &T, int64_t s) {
     int32_t h[R];
-    int64_t q[R], qe[R];
+    IdxT q[R], qe[R];
     int64_t f = 0;
 #pragma unroll
     for (int t = 0; t < R; ++t) {
         const int k = A.ci[s + t];
-        q[t] = T.cp[k];
-        qe[t] = T.cp[k + 1];
+        q[t] = (IdxT)T.cp[k];
+        qe[t] = (IdxT)T.cp[k + 1];
         f += qe[t] - q[t];
     }
     if (f > kMergeMaxF) return -1;
@@ -56,18 +60,21 @@ __device__ __forceinline__ int64_t sym_merge_row(const Csr &A, const Csc &T, int
     return cnt;
 }
 
-template <int R>
-__device__ __forceinline__ void num_merge_row(const NumArgs &a, int64_t i, int64_t r, int64_t s) {
+// Writes the kept entries of row i to (oc, ow)[0..), pads the structural
+// slots it did not fill ([kept, ub)) with col = -1 and raises *holes.
+template <int R, typename IdxT>
+__device__ __forceinline__ void num_merge_row(const NumArgs &a, int64_t i, int64_t r, int64_t s, int32_t *oc,
+                                              double *ow, int64_t ub) {
     int32_t h[R];
-    int64_t q[R], qe[R];
+    IdxT q[R], qe[R];
     double av[R], hv[R];
     int64_t f = 0;
 #pragma unroll
     for (int t = 0; t < R; ++t) {
         const int k = a.A.ci[s + t];
         av[t] = a.A.v[s + t];
-        q[t] = a.T.cp[k];
-        qe[t] = a.T.cp[k + 1];
+        q[t] = (IdxT)a.T.cp[k];
+        qe[t] = (IdxT)a.T.cp[k + 1];
         f += qe[t] - q[t];
     }
     if (f > kMergeMaxF) return;
@@ -81,7 +88,6 @@ __device__ __forceinline__ void num_merge_row(const NumArgs &a, int64_t i, int64
             hv[t] = 0.0;
         }
     }
-    const int64_t g0 = a.gptr[r], ub = a.gptr[r + 1] - g0;
     int64_t o = 0;
     while (true) {
         int m = h[0];
@@ -107,19 +113,24 @@ __device__ __forceinline__ void num_merge_row(const NumArgs &a, int64_t i, int64
         } else {
             const double w = fabs(acc);
             if (w > a.tol) {
-                a.gcol[g0 + o] = m;
-                a.gw[g0 + o] = w;
+                oc[o] = m;
+                ow[o] = w;
                 ++o;
             }
         }
     }
     if (o < ub) {
-        for (int64_t t = o; t < ub; ++t) a.gcol[g0 + t] = -1;
+        for (int64_t t = o; t < ub; ++t) oc[t] = -1;
         atomicOr(a.holes, 1);
     }
 }
 
-__global__ void __launch_bounds__(256) k_sym_merge(SymArgs a) {
+constexpr int kMergeThreads = 256;
+constexpr int kMergeWarps = kMergeThreads / 32;
+constexpr int kStageCap = 448;  // staged graph entries per warp (12 B each)
+
+template <int RMAX, typename IdxT>
+__global__ void __launch_bounds__(kMergeThreads) k_sym_merge(SymArgs a) {
     const int64_t nloc = a.re - a.rb;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < nloc; r += stride) {
@@ -129,40 +140,67 @@ __global__ void __launch_bounds__(256) k_sym_merge(SymArgs a) {
         int64_t c = -1;
         switch (len) {
             case 0: c = 0; break;
-            case 1: c = sym_merge_row<1>(a.A, a.T, s); break;
-            case 2: c = sym_merge_row<2>(a.A, a.T, s); break;
-            case 3: c = sym_merge_row<3>(a.A, a.T, s); break;
-            case 4: c = sym_merge_row<4>(a.A, a.T, s); break;
-            case 5: c = sym_merge_row<5>(a.A, a.T, s); break;
-            case 6: c = sym_merge_row<6>(a.A, a.T, s); break;
-            case 7: c = sym_merge_row<7>(a.A, a.T, s); break;
-            case 8: c = sym_merge_row<8>(a.A, a.T, s); break;
+            case 1: c = sym_merge_row<1, IdxT>(a.A, a.T, s); break;
+            case 2: c = sym_merge_row<2, IdxT>(a.A, a.T, s); break;
+            case 3: c = sym_merge_row<3, IdxT>(a.A, a.T, s); break;
+            case 4: c = sym_merge_row<4, IdxT>(a.A, a.T, s); break;
+            case 5: if constexpr (RMAX >= 5) c = sym_merge_row<5, IdxT>(a.A, a.T, s); break;
+            case 6: if constexpr (RMAX >= 6) c = sym_merge_row<6, IdxT>(a.A, a.T, s); break;
+            case 7: if constexpr (RMAX >= 7) c = sym_merge_row<7, IdxT>(a.A, a.T, s); break;
+            case 8: if constexpr (RMAX >= 8) c = sym_merge_row<8, IdxT>(a.A, a.T, s); break;
             default: break;
         }
         if (c >= 0) a.nnzc[r] = c;
     }
 }
 
-__global__ void __launch_bounds__(256) k_num_merge(NumArgs a) {
+// Each warp takes 32 consecutive rows (one per lane).  Their graph slots are
+// contiguous, so when they fit kStageCap the lanes write into shared memory
+// and the warp streams the range out with coalesced stores.
+template <int RMAX, typename IdxT>
+__global__ void __launch_bounds__(kMergeThreads) k_num_merge(NumArgs a) {
+    __shared__ int32_t st_col[kMergeWarps][kStageCap];
+    __shared__ double st_w[kMergeWarps][kStageCap];
+    const int w = threadIdx.x >> 5, l = lane_id();
     const int64_t nloc = a.re - a.rb;
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < nloc; r += stride) {
-        const int64_t i = a.rb + r;
-        const int64_t s = a.A.rp[i];
-        const int len = (int)min(a.A.rp[i + 1] - s, (int64_t)kMergeMaxLen + 1);
-        switch (len) {
-            case 0:
-                if (a.diag) a.diag[r] = 0.0;
-                break;
-            case 1: num_merge_row<1>(a, i, r, s); break;
-            case 2: num_merge_row<2>(a, i, r, s); break;
-            case 3: num_merge_row<3>(a, i, r, s); break;
-            case 4: num_merge_row<4>(a, i, r, s); break;
-            case 5: num_merge_row<5>(a, i, r, s); break;
-            case 6: num_merge_row<6>(a, i, r, s); break;
-            case 7: num_merge_row<7>(a, i, r, s); break;
-            case 8: num_merge_row<8>(a, i, r, s); break;
-            default: break;
+    const int64_t ntiles = (nloc + 31) / 32;
+    for (int64_t tile = (int64_t)blockIdx.x * kMergeWarps + w; tile < ntiles;
+         tile += (int64_t)gridDim.x * kMergeWarps) {
+        const int64_t r0 = tile * 32;
+        const int rows = (int)min((int64_t)32, nloc - r0);
+        const int64_t r = r0 + l;
+        const int64_t g0 = a.gptr[r0];
+        const int64_t span = a.gptr[r0 + rows] - g0;
+        const bool staged = span <= kStageCap;
+        if (l < rows) {
+            const int64_t i = a.rb + r;
+            const int64_t s = a.A.rp[i];
+            const int len = (int)min(a.A.rp[i + 1] - s, (int64_t)kMergeMaxLen + 1);
+            const int64_t gr = a.gptr[r], ub = a.gptr[r + 1] - gr;
+            int32_t *oc = staged ? &st_col[w][gr - g0] : a.gcol + gr;
+            double *ow = staged ? &st_w[w][gr - g0] : a.gw + gr;
+            switch (len) {
+                case 0:
+                    if (a.diag) a.diag[r] = 0.0;
+                    break;
+                case 1: num_merge_row<1, IdxT>(a, i, r, s, oc, ow, ub); break;
+                case 2: num_merge_row<2, IdxT>(a, i, r, s, oc, ow, ub); break;
+                case 3: num_merge_row<3, IdxT>(a, i, r, s, oc, ow, ub); break;
+                case 4: num_merge_row<4, IdxT>(a, i, r, s, oc, ow, ub); break;
+                case 5: if constexpr (RMAX >= 5) num_merge_row<5, IdxT>(a, i, r, s, oc, ow, ub); break;
+                case 6: if constexpr (RMAX >= 6) num_merge_row<6, IdxT>(a, i, r, s, oc, ow, ub); break;
+                case 7: if constexpr (RMAX >= 7) num_merge_row<7, IdxT>(a, i, r, s, oc, ow, ub); break;
+                case 8: if constexpr (RMAX >= 8) num_merge_row<8, IdxT>(a, i, r, s, oc, ow, ub); break;
+                default: break;
+            }
+        }
+        if (staged) {
+            __syncwarp();
+            for (int64_t t = l; t < span; t += 32) {
+                a.gcol[g0 + t] = st_col[w][t];
+                a.gw[g0 + t] = st_w[w][t];
+            }
+            __syncwarp();
         }
     }
 }
@@ -172,20 +210,48 @@ static int sms() {
     return g_sms_cache;
 }
 
-void launch_sym_merge(const SymArgs &a, cudaStream_t s) {
-    const int64_t nloc = a.re - a.rb;
-    int64_t g = (nloc + 255) / 256;
-    g = g < 1 ? 1 : (g > (int64_t)sms() * 16 ? (int64_t)sms() * 16 : g);
-    k_sym_merge<<<(unsigned)g, 256, 0, s>>>(a);
+template <int RMAX, typename IdxT>
+static void launch_merge_t(const SymArgs *sa, const NumArgs *na, cudaStream_t s) {
+    if (sa) {
+        const int64_t nloc = sa->re - sa->rb;
+        int64_t g = (nloc + kMergeThreads - 1) / kMergeThreads;
+        g = g < 1 ? 1 : (g > (int64_t)sms() * 16 ? (int64_t)sms() * 16 : g);
+        k_sym_merge<RMAX, IdxT><<<(unsigned)g, kMergeThreads, 0, s>>>(*sa);
+    } else {
+        const int64_t nloc = na->re - na->rb;
+        int64_t g = (nloc + kMergeThreads - 1) / kMergeThreads;
+        g = g < 1 ? 1 : (g > (int64_t)sms() * 16 ? (int64_t)sms() * 16 : g);
+        k_num_merge<RMAX, IdxT><<<(unsigned)g, kMergeThreads, 0, s>>>(*na);
+    }
     note_launch();
 }
 
-void launch_num_merge(const NumArgs &a, cudaStream_t s) {
-    const int64_t nloc = a.re - a.rb;
-    int64_t g = (nloc + 255) / 256;
-    g = g < 1 ? 1 : (g > (int64_t)sms() * 16 ? (int64_t)sms() * 16 : g);
-    k_num_merge<<<(unsigned)g, 256, 0, s>>>(a);
-    note_launch();
+template <typename IdxT>
+static void launch_merge_r(int maxlen, const SymArgs *sa, const NumArgs *na, cudaStream_t s) {
+    if (maxlen <= 4)
+        launch_merge_t<4, IdxT>(sa, na, s);
+    else if (maxlen == 5)
+        launch_merge_t<5, IdxT>(sa, na, s);
+    else if (maxlen == 6)
+        launch_merge_t<6, IdxT>(sa, na, s);
+    else if (maxlen == 7)
+        launch_merge_t<7, IdxT>(sa, na, s);
+    else
+        launch_merge_t<8, IdxT>(sa, na, s);
+}
+
+void launch_sym_merge(const SymArgs &a, int maxlen, cudaStream_t s) {
+    if (a.A.nnz <= INT32_MAX)
+        launch_merge_r<int32_t>(maxlen, &a, nullptr, s);
+    else
+        launch_merge_r<int64_t>(maxlen, &a, nullptr, s);
+}
+
+void launch_num_merge(const NumArgs &a, int maxlen, cudaStream_t s) {
+    if (a.A.nnz <= INT32_MAX)
+        launch_merge_r<int32_t>(maxlen, nullptr, &a, s);
+    else
+        launch_merge_r<int64_t>(maxlen, nullptr, &a, s);
 }
 
 // ======================================================== product enumeration

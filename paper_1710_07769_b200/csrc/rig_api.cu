@@ -267,7 +267,7 @@ static void plan_build(rig_plan *p, const rig_csr_t *Ain) {
     p->nnzc = ar.get<int64_t>(p->nloc);
     SymArgs sa{p->A, p->T, p->rb, p->re, p->nnzc};
     Prof *pf_sym = new Prof(P_SYMBOLIC, s);
-    if (p->nloc > 0) launch_sym_merge(sa, s);
+    if (p->nloc > 0) launch_sym_merge(sa, p->h.max_len, s);
     const int64_t n_huge_sym = p->h.sym_count[kNumSymBins];
     int64_t n_mid = p->h.n_mid;
     if (n_mid > 0) {
@@ -306,7 +306,7 @@ static int64_t plan_numeric(rig_plan *p, int32_t *gcol, double *gw, double *diag
     CK(cudaMemsetAsync(&p->ctr->holes, 0, sizeof(int), s));
     NumArgs na{p->A, p->T, p->rb, p->re, p->gptr_ub, gcol, gw, (p->flags & RIG_FLAG_DIAG) ? diag : nullptr,
                p->tol, &p->ctr->holes};
-    if (p->nloc > 0) launch_num_merge(na, s);
+    if (p->nloc > 0) launch_num_merge(na, p->h.max_len, s);
     if (p->h.n_mid > 0) {
         launch_num_warp(na, p->num_lists, p->h.n_mid, p->ctr->num_count, p->h.num_count, s);
         const int64_t n_huge = p->h.num_count[kNumNumBins];
