@@ -216,14 +216,13 @@ def main():
     rb, re = split[rank], split[rank + 1]
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.int32, device="cuda")
 
+    cut_buf = torch.empty(1, dtype=torch.float64, device="cuda")
+
     def step():
+        # the whole hot path through the C ABI: a1-a6 (build) + a7 (cutsize)
+        g, cut = rig.rig_build_cut(A, part, w.K, rb, re, w.scale_rows, w.drop_tol, out=cut_buf)
         if world > 1:
-            g = rig.rig_build_rows(A, rb, re, w.scale_rows, w.drop_tol)
-        else:
-            g = rig.rig_build(A, w.scale_rows, w.drop_tol)
-        cut = rig.rig_cutsize(g, part, w.K, n_global=w.n)
-        if world > 1:
-            dist.all_reduce(cut)
+            dist.all_reduce(cut)  # a8: NCCL allreduce of the partial cutsizes
         return g, cut
 
     # warm-up

@@ -113,6 +113,15 @@ RIG_API int rig_graph_free(rig_graph_t *g, rig_stream_t stream);
 RIG_API int rig_build_rows(const rig_csr_t *A, int scale_rows, double drop_tol, uint32_t flags, int64_t row_begin,
                    int64_t row_end, rig_graph_t *out, rig_stream_t stream);
 
+/* Build + score in one call (the whole hot path): rig_build_rows
+ * for rows [row_begin, row_end), then the cutsize of `part` (device int32
+ * [A->nrows], ids in [0, K)) over those rows into cut_dev[0] (device double),
+ * enqueued behind the numeric pass before the final synchronisation.
+ * Multi-GPU: each rank passes its shard and allreduces cut_dev. */
+RIG_API int rig_build_cut(const rig_csr_t *A, int scale_rows, double drop_tol, uint32_t flags, int64_t row_begin,
+                          int64_t row_end, const int32_t *part, int32_t K, rig_graph_t *out, double *cut_dev,
+                          rig_stream_t stream);
+
 /* ---- staged API: caller-owned output (estimate -> allocate -> compute) --- */
 
 /* Runs steps a0-a4 for rows [row_begin, row_end): validation, scaling,

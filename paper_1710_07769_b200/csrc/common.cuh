@@ -129,7 +129,52 @@ struct NumArgs {
     double *diag;  // may be null
     double tol;
     int *holes;
+    // fused a7 (optional, part == nullptr: off): every kept edge (i,j) with
+    // j > i and part[i] != part[j] is added to a per-thread Neumaier sum; each
+    // CTA writes its sum to cutp[blockIdx.x] (deterministic order).
+    const int32_t *part;
+    int32_t K;
+    double *cutp;
+    int *bad_part;
+    int *cut_used;  // this launch's number of written partials (= gridDim.x)
 };
+
+// Neumaier-compensated running sum (compiled with --fmad=false).
+struct Comp {
+    double s = 0.0, c = 0.0;
+    __device__ __forceinline__ void add(double x) {
+        const double t = s + x;
+        if (fabs(s) >= fabs(x))
+            c += (s - t) + x;
+        else
+            c += (x - t) + s;
+        s = t;
+    }
+    __device__ __forceinline__ double value() const { return s + c; }
+};
+
+// Sum of one double per thread over the CTA in a fixed tree order; thread 0
+// gets the result.  All threads must call it.
+template <int NT>
+__device__ __forceinline__ double block_tree_sum(double v) {
+    __shared__ double red[NT];
+    red[threadIdx.x] = v;
+    __syncthreads();
+#pragma unroll
+    for (int h = NT / 2; h > 0; h >>= 1) {
+        if ((int)threadIdx.x < h) red[threadIdx.x] += red[threadIdx.x + h];
+        __syncthreads();
+    }
+    const double r = red[0];
+    __syncthreads();
+    return r;
+}
+
+// Cut slots reserved per numeric launch in the fused-cut partials array.
+constexpr int kCutSlotsPerLaunch = 4096;
+constexpr int kCutLaunches = 8;  // merge + 6 warp bins + huge
+// a3 + a4(merge rows) fused: products, merge-row nnzC, bins for the others
+void launch_analyze_sym(const SymArgs &a, int32_t *sym_lists, int64_t cap, DevCounters *ctr, cudaStream_t s);
 // maxlen: longest A row on the merge path in the shard (DevCounters::max_len)
 void launch_sym_merge(const SymArgs &a, int maxlen, cudaStream_t s);
 void launch_num_merge(const NumArgs &a, int maxlen, cudaStream_t s);
@@ -154,6 +199,9 @@ void launch_cutsize(const int64_t *grp, const int32_t *gcol, const double *gw, i
                     int64_t n_global, const int32_t *part, int32_t K, double *partials, int nblocks,
                     double *cut, cudaStream_t s);
 int cutsize_blocks();
+// final fixed-order reduction of cut partials (NaN if *bad)
+void launch_cut_final(const double *partials, const int *used, int nseg, int stride, const int *bad, double *cut,
+                      cudaStream_t s);
 void launch_split(const int64_t *fprefix, int64_t n, int32_t parts, int64_t *split, cudaStream_t s);
 
 }  // namespace rig

@@ -107,7 +107,8 @@ __global__ void __launch_bounds__(kCutThreads) k_cutsize(const int64_t *__restri
                 wv[u] = v ? gw[e[u]] : 0.0;
             }
 #pragma unroll
-            for (int u = 0; u < U; ++u) pj[u] = e[u] < hi ? part[j[u]] : 0;
+            // j < 0 marks an unfilled slot of the upper-bound layout: skipped
+            for (int u = 0; u < U; ++u) pj[u] = (e[u] < hi && j[u] >= 0) ? part[j[u]] : 0;
 #pragma unroll
             for (int u = 0; u < U; ++u) {
                 // row of edge e: (number of lanes with start <= e) - 1
@@ -151,6 +152,31 @@ __global__ void __launch_bounds__(kCutThreads) k_cutsize_final(const double *par
 }
 
 int cutsize_blocks() { return num_sms() * 8; }
+
+// Fused-cut partials: nseg segments of `stride` slots, segment g holding
+// used[g] partials.  Fixed order: deterministic.
+__global__ void __launch_bounds__(kCutThreads) k_cut_final_seg(const double *partials, const int *used, int nseg,
+                                                               int stride, const int *bad, double *cut) {
+    double s = 0.0, c = 0.0;
+    for (int g = 0; g < nseg; ++g) {
+        const int n = used[g];
+        for (int k = threadIdx.x; k < n; k += kCutThreads) neumaier_add(s, c, partials[(int64_t)g * stride + k]);
+    }
+    __shared__ double red[kCutThreads];
+    red[threadIdx.x] = s + c;
+    __syncthreads();
+    for (int h = kCutThreads / 2; h > 0; h >>= 1) {
+        if (threadIdx.x < h) red[threadIdx.x] += red[threadIdx.x + h];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *cut = *bad ? __longlong_as_double(0x7ff8000000000000ll) : red[0];
+}
+
+void launch_cut_final(const double *partials, const int *used, int nseg, int stride, const int *bad, double *cut,
+                      cudaStream_t s) {
+    k_cut_final_seg<<<1, kCutThreads, 0, s>>>(partials, used, nseg, stride, bad, cut);
+    note_launch();
+}
 
 void launch_cutsize(const int64_t *grp, const int32_t *gcol, const double *gw, int64_t nloc, int64_t rb,
                     int64_t n_global, const int32_t *part, int32_t K, double *partials, int nblocks, double *cut,

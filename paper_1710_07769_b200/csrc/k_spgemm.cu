@@ -62,9 +62,10 @@ __device__ __forceinline__ int64_t sym_merge_row(const Csr &A, const Csc &T, int
 
 // Writes the kept entries of row i to (oc, ow)[0..), pads the structural
 // slots it did not fill ([kept, ub)) with col = -1 and raises *holes.
+// With a.part set, kept edges (i,j), j > i, part[j] != pi also go to `cut`.
 template <int R, typename IdxT>
 __device__ __forceinline__ void num_merge_row(const NumArgs &a, int64_t i, int64_t r, int64_t s, int32_t *oc,
-                                              double *ow, int64_t ub) {
+                                              double *ow, int64_t ub, Comp &cut, int32_t pi, int &badp) {
     int32_t h[R];
     IdxT q[R], qe[R];
     double av[R], hv[R];
@@ -116,6 +117,11 @@ __device__ __forceinline__ void num_merge_row(const NumArgs &a, int64_t i, int64
                 oc[o] = m;
                 ow[o] = w;
                 ++o;
+                if (a.part && (int64_t)m > i) {
+                    const int32_t pj = a.part[m];
+                    badp |= (pj < 0) | (pj >= a.K);
+                    if (pj != pi) cut.add(w);
+                }
             }
         }
     }
@@ -164,6 +170,8 @@ __global__ void __launch_bounds__(kMergeThreads) k_num_merge(NumArgs a) {
     const int w = threadIdx.x >> 5, l = lane_id();
     const int64_t nloc = a.re - a.rb;
     const int64_t ntiles = (nloc + 31) / 32;
+    Comp cut;
+    int badp = 0;
     for (int64_t tile = (int64_t)blockIdx.x * kMergeWarps + w; tile < ntiles;
          tile += (int64_t)gridDim.x * kMergeWarps) {
         const int64_t r0 = tile * 32;
@@ -179,18 +187,23 @@ __global__ void __launch_bounds__(kMergeThreads) k_num_merge(NumArgs a) {
             const int64_t gr = a.gptr[r], ub = a.gptr[r + 1] - gr;
             int32_t *oc = staged ? &st_col[w][gr - g0] : a.gcol + gr;
             double *ow = staged ? &st_w[w][gr - g0] : a.gw + gr;
+            int32_t pi = 0;
+            if (a.part) {
+                pi = a.part[i];
+                badp |= (pi < 0) | (pi >= a.K);
+            }
             switch (len) {
                 case 0:
                     if (a.diag) a.diag[r] = 0.0;
                     break;
-                case 1: num_merge_row<1, IdxT>(a, i, r, s, oc, ow, ub); break;
-                case 2: num_merge_row<2, IdxT>(a, i, r, s, oc, ow, ub); break;
-                case 3: num_merge_row<3, IdxT>(a, i, r, s, oc, ow, ub); break;
-                case 4: num_merge_row<4, IdxT>(a, i, r, s, oc, ow, ub); break;
-                case 5: if constexpr (RMAX >= 5) num_merge_row<5, IdxT>(a, i, r, s, oc, ow, ub); break;
-                case 6: if constexpr (RMAX >= 6) num_merge_row<6, IdxT>(a, i, r, s, oc, ow, ub); break;
-                case 7: if constexpr (RMAX >= 7) num_merge_row<7, IdxT>(a, i, r, s, oc, ow, ub); break;
-                case 8: if constexpr (RMAX >= 8) num_merge_row<8, IdxT>(a, i, r, s, oc, ow, ub); break;
+                case 1: num_merge_row<1, IdxT>(a, i, r, s, oc, ow, ub, cut, pi, badp); break;
+                case 2: num_merge_row<2, IdxT>(a, i, r, s, oc, ow, ub, cut, pi, badp); break;
+                case 3: num_merge_row<3, IdxT>(a, i, r, s, oc, ow, ub, cut, pi, badp); break;
+                case 4: num_merge_row<4, IdxT>(a, i, r, s, oc, ow, ub, cut, pi, badp); break;
+                case 5: if constexpr (RMAX >= 5) num_merge_row<5, IdxT>(a, i, r, s, oc, ow, ub, cut, pi, badp); break;
+                case 6: if constexpr (RMAX >= 6) num_merge_row<6, IdxT>(a, i, r, s, oc, ow, ub, cut, pi, badp); break;
+                case 7: if constexpr (RMAX >= 7) num_merge_row<7, IdxT>(a, i, r, s, oc, ow, ub, cut, pi, badp); break;
+                case 8: if constexpr (RMAX >= 8) num_merge_row<8, IdxT>(a, i, r, s, oc, ow, ub, cut, pi, badp); break;
                 default: break;
             }
         }
@@ -203,11 +216,81 @@ __global__ void __launch_bounds__(kMergeThreads) k_num_merge(NumArgs a) {
             __syncwarp();
         }
     }
+    if (a.part) {  // fused a7: per-CTA partial of the cut
+        const double v = block_tree_sum<kMergeThreads>(cut.value());
+        if (threadIdx.x == 0) {
+            a.cutp[blockIdx.x] = v;
+            if (blockIdx.x == 0) *a.cut_used = (int)gridDim.x;
+        }
+        if (__syncthreads_or(badp) && threadIdx.x == 0) atomicOr(a.bad_part, 1);
+    }
 }
 
 static int sms() {
     if (!g_sms_cache) g_sms_cache = num_sms();
     return g_sms_cache;
+}
+
+// a3 + a4 fused for the merge path: per row, f_i = sum of column lengths;
+// merge-path rows get their structural nnz(C_i) right away, the others are
+// binned for the warp-hash / huge symbolic kernels by ceil(log2(2 f_i)).
+template <typename IdxT>
+__global__ void __launch_bounds__(kMergeThreads) k_analyze_sym(SymArgs a, int32_t *sym_lists, int64_t cap,
+                                                               DevCounters *ctr) {
+    const int64_t nloc = a.re - a.rb;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    int64_t local = 0;
+    int maxlen = 0;
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < nloc; r += stride) {
+        const int64_t i = a.rb + r;
+        const int64_t s = a.A.rp[i], e = a.A.rp[i + 1];
+        int64_t fi = 0;
+        for (int64_t p = s; p < e; ++p) {
+            const int k = a.A.ci[p];
+            fi += a.T.cp[k + 1] - a.T.cp[k];
+        }
+        local += fi;
+        const int len = (int)min(e - s, (int64_t)kMergeMaxLen + 1);
+        if (len <= kMergeMaxLen && fi <= kMergeMaxF) {
+            maxlen = max(maxlen, len);
+            int64_t c = 0;
+            switch (len) {
+                case 1: c = sym_merge_row<1, IdxT>(a.A, a.T, s); break;
+                case 2: c = sym_merge_row<2, IdxT>(a.A, a.T, s); break;
+                case 3: c = sym_merge_row<3, IdxT>(a.A, a.T, s); break;
+                case 4: c = sym_merge_row<4, IdxT>(a.A, a.T, s); break;
+                case 5: c = sym_merge_row<5, IdxT>(a.A, a.T, s); break;
+                case 6: c = sym_merge_row<6, IdxT>(a.A, a.T, s); break;
+                case 7: c = sym_merge_row<7, IdxT>(a.A, a.T, s); break;
+                case 8: c = sym_merge_row<8, IdxT>(a.A, a.T, s); break;
+                default: break;
+            }
+            a.nnzc[r] = c;
+        } else {
+            const int64_t m2 = 2 * (fi > 1 ? fi : 1);
+            int lg = 64 - __clzll(m2 - 1);
+            if (lg < kSymBinMinLog) lg = kSymBinMinLog;
+            const int b = lg > kSymBinMaxLog ? kNumSymBins : lg - kSymBinMinLog;
+            const unsigned long long pos = atomicAdd((unsigned long long *)&ctr->sym_count[b], 1ull);
+            sym_lists[b * cap + (int64_t)pos] = (int32_t)i;
+            atomicAdd((unsigned long long *)&ctr->n_mid, 1ull);
+        }
+    }
+    maxlen = __reduce_max_sync(kFull, maxlen);
+    if (lane_id() == 0 && maxlen) atomicMax(&ctr->max_len, maxlen);
+    local = warp_sum(local);
+    if (lane_id() == 0 && local) atomicAdd((unsigned long long *)&ctr->products, (unsigned long long)local);
+}
+
+void launch_analyze_sym(const SymArgs &a, int32_t *sym_lists, int64_t cap, DevCounters *ctr, cudaStream_t s) {
+    const int64_t nloc = a.re - a.rb;
+    int64_t g = (nloc + kMergeThreads - 1) / kMergeThreads;
+    g = g < 1 ? 1 : (g > (int64_t)sms() * 16 ? (int64_t)sms() * 16 : g);
+    if (a.A.nnz <= INT32_MAX)
+        k_analyze_sym<int32_t><<<(unsigned)g, kMergeThreads, 0, s>>>(a, sym_lists, cap, ctr);
+    else
+        k_analyze_sym<int64_t><<<(unsigned)g, kMergeThreads, 0, s>>>(a, sym_lists, cap, ctr);
+    note_launch();
 }
 
 template <int RMAX, typename IdxT>
@@ -398,6 +481,8 @@ __global__ void __launch_bounds__(WPB * 32) k_num_warp(NumArgs a, const int32_t 
     int32_t *bk = ak + H;
     int32_t *hist = bk + H;
     const unsigned lt = lanemask_lt();
+    Comp cut;
+    int badp = 0;
 
     for (int s = l; s < T; s += 32) {
         keys[s] = -1;
@@ -528,8 +613,13 @@ __global__ void __launch_bounds__(WPB * 32) k_num_warp(NumArgs a, const int32_t 
             cv = nv;
             nv = tv;
         }
-        // ---- write the row: strip diagonal, |c| > tol
+        // ---- write the row: strip diagonal, |c| > tol (+ fused cut)
         const int64_t g0 = a.gptr[r], ub = a.gptr[r + 1] - g0;
+        int32_t pi = 0;
+        if (a.part) {
+            pi = a.part[i];
+            badp |= (pi < 0) | (pi >= a.K);
+        }
         int64_t o = 0;
         for (int rd = 0; rd < L; rd += 32) {
             const int e2 = rd + l;
@@ -544,6 +634,11 @@ __global__ void __launch_bounds__(WPB * 32) k_num_warp(NumArgs a, const int32_t 
                 const int64_t pos = g0 + o + __popc(bal & lt);
                 a.gcol[pos] = key;
                 a.gw[pos] = fabs(c);
+                if (a.part && (int64_t)key > i) {
+                    const int32_t pj = a.part[key];
+                    badp |= (pj < 0) | (pj >= a.K);
+                    if (pj != pi) cut.add(fabs(c));
+                }
             }
             o += __popc(bal);
         }
@@ -552,6 +647,14 @@ __global__ void __launch_bounds__(WPB * 32) k_num_warp(NumArgs a, const int32_t 
             if (l == 0) atomicOr(a.holes, 1);
         }
         __syncwarp();
+    }
+    if (a.part) {
+        const double v = block_tree_sum<WPB * 32>(cut.value());
+        if (threadIdx.x == 0) {
+            a.cutp[blockIdx.x] = v;
+            if (blockIdx.x == 0) *a.cut_used = (int)gridDim.x;
+        }
+        if (__syncthreads_or(badp) && threadIdx.x == 0) atomicOr(a.bad_part, 1);
     }
 }
 
@@ -572,12 +675,21 @@ static void launch_num_warp_t(const NumArgs &a, const int32_t *list, const int64
 
 void launch_num_warp(const NumArgs &a, const int32_t *lists, int64_t cap, const int64_t *counts,
                      const int64_t *hcounts, cudaStream_t s) {
-    if (hcounts[0]) launch_num_warp_t<6>(a, lists + 0 * cap, counts + 0, s);
-    if (hcounts[1]) launch_num_warp_t<7>(a, lists + 1 * cap, counts + 1, s);
-    if (hcounts[2]) launch_num_warp_t<8>(a, lists + 2 * cap, counts + 2, s);
-    if (hcounts[3]) launch_num_warp_t<9>(a, lists + 3 * cap, counts + 3, s);
-    if (hcounts[4]) launch_num_warp_t<10>(a, lists + 4 * cap, counts + 4, s);
-    if (hcounts[5]) launch_num_warp_t<11>(a, lists + 5 * cap, counts + 5, s);
+    // fused-cut partial slots: launch slot 0 = merge, 1..6 = these bins, 7 = huge
+    NumArgs b[6];
+    for (int k = 0; k < 6; ++k) {
+        b[k] = a;
+        if (a.cutp) {
+            b[k].cutp = a.cutp + (int64_t)(1 + k) * kCutSlotsPerLaunch;
+            b[k].cut_used = a.cut_used + 1 + k;
+        }
+    }
+    if (hcounts[0]) launch_num_warp_t<6>(b[0], lists + 0 * cap, counts + 0, s);
+    if (hcounts[1]) launch_num_warp_t<7>(b[1], lists + 1 * cap, counts + 1, s);
+    if (hcounts[2]) launch_num_warp_t<8>(b[2], lists + 2 * cap, counts + 2, s);
+    if (hcounts[3]) launch_num_warp_t<9>(b[3], lists + 3 * cap, counts + 3, s);
+    if (hcounts[4]) launch_num_warp_t<10>(b[4], lists + 4 * cap, counts + 4, s);
+    if (hcounts[5]) launch_num_warp_t<11>(b[5], lists + 5 * cap, counts + 5, s);
 }
 
 // ======================================================== huge rows
@@ -711,6 +823,8 @@ __global__ void __launch_bounds__(kHugeThreads) k_num_huge(NumArgs a, const int3
     const int w = threadIdx.x >> 5, l = lane_id();
     const unsigned lt = lanemask_lt();
     const int64_t n = *count;
+    Comp cut;
+    int badp = 0;
     for (int64_t idx = blockIdx.x; idx < n; idx += gridDim.x) {
         const int64_t i = list[idx];
         const int64_t r = i - a.rb;
@@ -761,8 +875,13 @@ __global__ void __launch_bounds__(kHugeThreads) k_num_huge(NumArgs a, const int3
         }
         __threadfence_block();
         __syncthreads();
-        // ---- emit in ascending j by scanning the bitmap
+        // ---- emit in ascending j by scanning the bitmap (+ fused cut)
         const int64_t g0 = a.gptr[r], ub = a.gptr[r + 1] - g0;
+        int32_t pi = 0;
+        if (a.part) {
+            pi = a.part[i];
+            badp |= (pi < 0) | (pi >= a.K);
+        }
         int64_t o = 0;
         for (int64_t wb = 0; wb < nwords; wb += kHugeThreads) {
             const int64_t wi = wb + threadIdx.x;
@@ -794,6 +913,11 @@ __global__ void __launch_bounds__(kHugeThreads) k_num_huge(NumArgs a, const int3
                     a.gcol[pos] = (int32_t)j;
                     a.gw[pos] = fabs(c);
                     ++pos;
+                    if (a.part && j > i) {
+                        const int32_t pj = a.part[j];
+                        badp |= (pj < 0) | (pj >= a.K);
+                        if (pj != pi) cut.add(fabs(c));
+                    }
                 }
             }
             if (word) bm[wi] = 0u;
@@ -805,6 +929,14 @@ __global__ void __launch_bounds__(kHugeThreads) k_num_huge(NumArgs a, const int3
             if (threadIdx.x == 0) atomicOr(a.holes, 1);
         }
         __syncthreads();
+    }
+    if (a.part) {
+        const double v = block_tree_sum<kHugeThreads>(cut.value());
+        if (threadIdx.x == 0) {
+            a.cutp[blockIdx.x] = v;
+            if (blockIdx.x == 0) *a.cut_used = (int)gridDim.x;
+        }
+        if (__syncthreads_or(badp) && threadIdx.x == 0) atomicOr(a.bad_part, 1);
     }
 }
 
@@ -818,7 +950,12 @@ void launch_sym_huge(const SymArgs &a, const int32_t *list, const int64_t *count
 void launch_num_huge(const NumArgs &a, const int32_t *list, const int64_t *count, int slots, void *scratch,
                      cudaStream_t s) {
     const size_t slot_bytes = huge_scratch_bytes(a.A.nrows, 1, true);
-    k_num_huge<<<slots, kHugeThreads, 0, s>>>(a, list, count, static_cast<unsigned char *>(scratch), slot_bytes,
+    NumArgs b = a;
+    if (a.cutp) {
+        b.cutp = a.cutp + (int64_t)7 * kCutSlotsPerLaunch;
+        b.cut_used = a.cut_used + 7;
+    }
+    k_num_huge<<<slots, kHugeThreads, 0, s>>>(b, list, count, static_cast<unsigned char *>(scratch), slot_bytes,
                                               bitmap_words(a.A.nrows));
     note_launch();
 }

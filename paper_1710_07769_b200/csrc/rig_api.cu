@@ -204,7 +204,7 @@ struct rig_plan {
     explicit rig_plan(cudaStream_t st) : s(st), arena(st) {}
 };
 
-static void plan_build(rig_plan *p, const rig_csr_t *Ain) {
+static void plan_build(rig_plan *p, const rig_csr_t *Ain, int64_t *gptr_out, bool exact) {
     cudaStream_t s = p->s;
     Arena &ar = p->arena;
     const int64_t n = Ain->nrows, m = Ain->ncols, nnz = Ain->nnz;
@@ -251,97 +251,138 @@ static void plan_build(rig_plan *p, const rig_csr_t *Ain) {
     check_launch("prep");
     p->A = Csr{n, m, nnz, Ain->row_ptr, Ain->col_idx, p->scale ? ahat : Ain->val};
     p->T = Csc{cp, ri, vt};
-    // a3: products per row, bins for rows off the merge path
+    // a3 + a4 (merge rows): products, structural nnz(C_i), bins for the rest
     p->list_cap = p->nloc;
     p->sym_lists = ar.get<int32_t>((int64_t)kSymBins * std::max<int64_t>(p->list_cap, 1));
+    p->nnzc = ar.get<int64_t>(p->nloc);
+    SymArgs sa{p->A, p->T, p->rb, p->re, p->nnzc};
     if (p->nloc > 0) {
         Prof pf(P_ANALYZE, s);
-        launch_analyze(p->A, cp, p->rb, p->re, nullptr, p->sym_lists, p->list_cap, p->ctr, s);
+        launch_analyze_sym(sa, p->sym_lists, p->list_cap, p->ctr, s);
     }
     check_launch("analyze");
-    // sync 1: errors, bin sizes
+    // sync 1: errors, products, bin sizes
     CK(cudaMemcpyAsync(&p->h, p->ctr, sizeof(DevCounters), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     if (p->h.err) throw Error(err_to_code(p->h.err), err_msg(err_to_code(p->h.err)));
-    // a4: symbolic
-    p->nnzc = ar.get<int64_t>(p->nloc);
-    SymArgs sa{p->A, p->T, p->rb, p->re, p->nnzc};
-    Prof *pf_sym = new Prof(P_SYMBOLIC, s);
-    if (p->nloc > 0) launch_sym_merge(sa, p->h.max_len, s);
-    const int64_t n_huge_sym = p->h.sym_count[kNumSymBins];
-    int64_t n_mid = p->h.n_mid;
+    // a4 for rows off the merge path
+    const int64_t n_mid = p->h.n_mid;
     if (n_mid > 0) {
+        Prof pf(P_SYMBOLIC, s);
         launch_sym_warp(sa, p->sym_lists, p->list_cap, p->ctr->sym_count, p->h.sym_count, s);
-        if (n_huge_sym > 0) {
-            p->huge_slots_n = huge_slots(n, n_mid);
+        // rows with f > 1024 may need the huge numeric path too (nnzC <= f)
+        if (p->h.sym_count[kNumSymBins] + p->h.sym_count[kNumSymBins - 1] > 0) {
+            p->huge_slots_n = huge_slots(n, p->h.sym_count[kNumSymBins] + p->h.sym_count[kNumSymBins - 1]);
             const size_t bytes = huge_scratch_bytes(n, p->huge_slots_n, true);
             p->huge_scratch = ar.get<unsigned char>((int64_t)bytes);
             CK(cudaMemsetAsync(p->huge_scratch, 0, bytes, s));
+        }
+        if (p->h.sym_count[kNumSymBins] > 0)
             launch_sym_huge(sa, p->sym_lists + (int64_t)kNumSymBins * p->list_cap, p->ctr->sym_count + kNumSymBins,
                             p->huge_slots_n, p->huge_scratch, s);
-        }
         p->num_lists = ar.get<int32_t>((int64_t)kNumBins * n_mid);
         launch_bin_num(p->sym_lists, p->list_cap, p->ctr, p->nnzc, p->rb, p->num_lists, n_mid, p->ctr->num_count, s);
     }
-    delete pf_sym;
     check_launch("symbolic");
-    p->gptr_ub = ar.get<int64_t>(p->nloc + 1);
+    p->gptr_ub = gptr_out ? gptr_out : ar.get<int64_t>(p->nloc + 1);
     {
         Prof pf(P_UBSCAN, s);
         scan_i64(p->nnzc, p->nloc, p->gptr_ub, ScanOp::UbOffDiag, scan_tmp, 0, s);
     }
     check_launch("scan");
-    // sync 2: structural size, numeric bins
-    CK(cudaMemcpyAsync(&p->h, p->ctr, sizeof(DevCounters), cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpyAsync(&p->nnz_upper, p->gptr_ub + p->nloc, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
+    p->nnz_upper = -1;
+    if (exact) {  // sync 2 (staged API): exact capacity for the caller
+        CK(cudaMemcpyAsync(&p->nnz_upper, p->gptr_ub + p->nloc, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+    }
 }
 
-// a5 + a6 into caller arrays (capacity nnz_upper).  Returns the final nnz.
-// `tmp` (nullable) provides nnz_upper*12 + (nloc+1)*8 bytes for compaction.
+struct CutReq {
+    const int32_t *part = nullptr;
+    int32_t K = 0;
+    int64_t n_global = 0;
+    double *cut_dev = nullptr;
+};
+
+// a5 + a6 into caller arrays (capacity >= structural off-diagonal nnz); the
+// optional cutsize (a7) is enqueued right behind the numeric pass -- it skips
+// unfilled slots (col < 0) -- so it costs no extra synchronisation.
+// Returns the final nnz.  Synchronises once (twice if entries were dropped).
 static int64_t plan_numeric(rig_plan *p, int32_t *gcol, double *gw, double *diag, int64_t *row_ptr_out,
-                            Arena &tmp_arena) {
+                            Arena &tmp_arena, const CutReq *cut) {
     cudaStream_t s = p->s;
-    Prof *pf_num = new Prof(P_NUMERIC, s);
-    CK(cudaMemsetAsync(&p->ctr->holes, 0, sizeof(int), s));
-    NumArgs na{p->A, p->T, p->rb, p->re, p->gptr_ub, gcol, gw, (p->flags & RIG_FLAG_DIAG) ? diag : nullptr,
-               p->tol, &p->ctr->holes};
-    if (p->nloc > 0) launch_num_merge(na, p->h.max_len, s);
-    if (p->h.n_mid > 0) {
-        launch_num_warp(na, p->num_lists, p->h.n_mid, p->ctr->num_count, p->h.num_count, s);
-        const int64_t n_huge = p->h.num_count[kNumNumBins];
-        if (n_huge > 0) {
-            if (!p->huge_scratch) {
-                p->huge_slots_n = huge_slots(p->A.nrows, n_huge);
-                const size_t bytes = huge_scratch_bytes(p->A.nrows, p->huge_slots_n, true);
-                p->huge_scratch = p->arena.get<unsigned char>((int64_t)bytes);
-                CK(cudaMemsetAsync(p->huge_scratch, 0, bytes, s));
-            }
-            launch_num_huge(na, p->num_lists + (int64_t)kNumNumBins * p->h.n_mid, p->ctr->num_count + kNumNumBins,
-                            p->huge_slots_n, p->huge_scratch, s);
-        }
+    double *cutp = nullptr;
+    int *badp = nullptr, *used = nullptr;
+    if (cut) {  // fused a7: per-CTA partials of every numeric launch, used counts, bad-id flag
+        const int64_t nslots = (int64_t)kCutLaunches * kCutSlotsPerLaunch;
+        cutp = tmp_arena.get<double>(nslots + 8);
+        used = reinterpret_cast<int *>(cutp + nslots);  // [kCutLaunches] ints
+        badp = used + kCutLaunches;
+        CK(cudaMemsetAsync(used, 0, sizeof(int) * (kCutLaunches + 1), s));
     }
-    delete pf_num;
-    check_launch("numeric");
+    {
+        Prof pf(P_NUMERIC, s);
+        CK(cudaMemsetAsync(&p->ctr->holes, 0, sizeof(int), s));
+        NumArgs na{p->A,
+                   p->T,
+                   p->rb,
+                   p->re,
+                   p->gptr_ub,
+                   gcol,
+                   gw,
+                   (p->flags & RIG_FLAG_DIAG) ? diag : nullptr,
+                   p->tol,
+                   &p->ctr->holes,
+                   cut ? cut->part : nullptr,
+                   cut ? cut->K : 0,
+                   cutp,
+                   badp,
+                   used};
+        if (p->nloc > 0) launch_num_merge(na, p->h.max_len, s);
+        if (p->h.n_mid > 0) {
+            // numeric bin sizes are device-side; empty bins exit immediately
+            int64_t all[8] = {1, 1, 1, 1, 1, 1, 1, 1};
+            launch_num_warp(na, p->num_lists, p->h.n_mid, p->ctr->num_count, all, s);
+            if (p->huge_scratch)
+                launch_num_huge(na, p->num_lists + (int64_t)kNumNumBins * p->h.n_mid,
+                                p->ctr->num_count + kNumNumBins, p->huge_slots_n, p->huge_scratch, s);
+        }
+        check_launch("numeric");
+    }
+    if (cut) {
+        Prof pf(P_CUTSIZE, s);
+        launch_cut_final(cutp, used, kCutLaunches, kCutSlotsPerLaunch, badp, cut->cut_dev, s);
+        check_launch("cut_final");
+    }
     int holes = 0;
+    int64_t ub = 0;
     CK(cudaMemcpyAsync(&holes, &p->ctr->holes, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(&ub, p->gptr_ub + p->nloc, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
+    p->nnz_upper = ub;
     if (!holes) {
-        CK(cudaMemcpyAsync(row_ptr_out, p->gptr_ub, sizeof(int64_t) * (size_t)(p->nloc + 1),
-                           cudaMemcpyDeviceToDevice, s));
-        return p->nnz_upper;
+        if (row_ptr_out != p->gptr_ub)
+            CK(cudaMemcpyAsync(row_ptr_out, p->gptr_ub, sizeof(int64_t) * (size_t)(p->nloc + 1),
+                               cudaMemcpyDeviceToDevice, s));
+        return ub;
     }
     // holes: count kept entries per row, scan, move into a temporary, copy back
     Prof pf_c(P_COMPACT, s);
+    const int64_t *ubp = p->gptr_ub;
+    if (row_ptr_out == p->gptr_ub) {  // keep the structural offsets for the move
+        int64_t *copy = tmp_arena.get<int64_t>(p->nloc + 1);
+        CK(cudaMemcpyAsync(copy, p->gptr_ub, sizeof(int64_t) * (size_t)(p->nloc + 1), cudaMemcpyDeviceToDevice, s));
+        ubp = copy;
+    }
     int64_t *kept = tmp_arena.get<int64_t>(p->nloc);
     void *scan_tmp = tmp_arena.get<unsigned char>((int64_t)scan_tmp_bytes(p->nloc + 1));
-    launch_count_kept(p->gptr_ub, p->nloc, gcol, kept, s);
+    launch_count_kept(ubp, p->nloc, gcol, kept, s);
     scan_i64(kept, p->nloc, row_ptr_out, ScanOp::Identity, scan_tmp, 0, s);
     int64_t g = 0;
     CK(cudaMemcpyAsync(&g, row_ptr_out + p->nloc, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
-    int32_t *c2 = tmp_arena.get<int32_t>(p->nnz_upper);
-    double *w2 = tmp_arena.get<double>(p->nnz_upper);
-    launch_compact_move(p->gptr_ub, row_ptr_out, p->nloc, gcol, gw, c2, w2, s);
+    int32_t *c2 = tmp_arena.get<int32_t>(ub);
+    double *w2 = tmp_arena.get<double>(ub);
+    launch_compact_move(ubp, row_ptr_out, p->nloc, gcol, gw, c2, w2, s);
     check_launch("compact");
     CK(cudaStreamSynchronize(s));
     if (g > 0) {
@@ -351,8 +392,8 @@ static int64_t plan_numeric(rig_plan *p, int32_t *gcol, double *gw, double *diag
     return g;
 }
 
-static rig_plan *make_plan(const rig_csr_t *A, int scale_rows, double drop_tol, uint32_t flags, int64_t rb,
-                           int64_t re, cudaStream_t s) {
+static rig_plan *new_plan(const rig_csr_t *A, int scale_rows, double drop_tol, uint32_t flags, int64_t rb,
+                          int64_t re, cudaStream_t s) {
     check_csr(A);
     if (!(drop_tol >= 0.0) || std::isnan(drop_tol)) throw Error(RIG_ERR_INVALID, "drop_tol must be >= 0");
     if (rb < 0 || re > A->nrows || rb > re) throw Error(RIG_ERR_INVALID, "bad row range");
@@ -364,8 +405,14 @@ static rig_plan *make_plan(const rig_csr_t *A, int scale_rows, double drop_tol, 
     p->rb = rb;
     p->re = re;
     p->nloc = re - rb;
+    return p;
+}
+
+static rig_plan *make_plan(const rig_csr_t *A, int scale_rows, double drop_tol, uint32_t flags, int64_t rb,
+                           int64_t re, cudaStream_t s) {
+    rig_plan *p = new_plan(A, scale_rows, drop_tol, flags, rb, re, s);
     try {
-        plan_build(p, A);
+        plan_build(p, A, nullptr, true);
     } catch (...) {
         delete p;
         throw;
@@ -389,22 +436,26 @@ static rig_plan *make_plan(const rig_csr_t *A, int scale_rows, double drop_tol, 
         return RIG_ERR_INVALID;                 \
     }
 
-// Library-owned output: allocate exactly-sized graph arrays.
+// Library-owned output.  The graph arrays are sized from the product count P
+// (known at the first sync; P >= nnz(C) >= graph nnz), so the numeric pass
+// follows the symbolic scan without a host round trip.
 static void build_owned(const rig_csr_t *A, int scale_rows, double drop_tol, uint32_t flags, int64_t rb, int64_t re,
-                        rig_graph_t *out, cudaStream_t s) {
+                        rig_graph_t *out, cudaStream_t s, const CutReq *cut) {
     if (!out) throw Error(RIG_ERR_INVALID, "out is NULL");
     std::memset(out, 0, sizeof(*out));
-    rig_plan *p = make_plan(A, scale_rows, drop_tol, flags, rb, re, s);
+    rig_plan *p = new_plan(A, scale_rows, drop_tol, flags, rb, re, s);
     Arena tmp(s);
     int64_t *rp = nullptr;
     int32_t *col = nullptr;
     double *w = nullptr, *diag = nullptr;
     try {
         CK(cudaMallocAsync((void **)&rp, sizeof(int64_t) * (size_t)(p->nloc + 1), s));
-        CK(cudaMallocAsync((void **)&col, sizeof(int32_t) * (size_t)std::max<int64_t>(p->nnz_upper, 1), s));
-        CK(cudaMallocAsync((void **)&w, sizeof(double) * (size_t)std::max<int64_t>(p->nnz_upper, 1), s));
+        plan_build(p, A, rp, false);
+        const int64_t cap = std::max<int64_t>(p->h.products, 1);
+        CK(cudaMallocAsync((void **)&col, sizeof(int32_t) * (size_t)cap, s));
+        CK(cudaMallocAsync((void **)&w, sizeof(double) * (size_t)cap, s));
         if (flags & RIG_FLAG_DIAG) CK(cudaMallocAsync((void **)&diag, sizeof(double) * (size_t)std::max<int64_t>(p->nloc, 1), s));
-        const int64_t g = plan_numeric(p, col, w, diag, rp, tmp);
+        const int64_t g = plan_numeric(p, col, w, diag, rp, tmp, cut);
         out->n = p->nloc;
         out->nnz = g;
         out->row_ptr = rp;
@@ -466,7 +517,7 @@ int rig_build(const rig_csr_t *A, int scale_rows, double drop_tol, uint32_t flag
               rig_stream_t stream) {
     ABI_BEGIN
     check_csr(A);
-    build_owned(A, scale_rows, drop_tol, flags, 0, A->nrows, out, (cudaStream_t)stream);
+    build_owned(A, scale_rows, drop_tol, flags, 0, A->nrows, out, (cudaStream_t)stream, nullptr);
     return RIG_OK;
     ABI_END
 }
@@ -474,7 +525,24 @@ int rig_build(const rig_csr_t *A, int scale_rows, double drop_tol, uint32_t flag
 int rig_build_rows(const rig_csr_t *A, int scale_rows, double drop_tol, uint32_t flags, int64_t row_begin,
                    int64_t row_end, rig_graph_t *out, rig_stream_t stream) {
     ABI_BEGIN
-    build_owned(A, scale_rows, drop_tol, flags, row_begin, row_end, out, (cudaStream_t)stream);
+    build_owned(A, scale_rows, drop_tol, flags, row_begin, row_end, out, (cudaStream_t)stream, nullptr);
+    return RIG_OK;
+    ABI_END
+}
+
+int rig_build_cut(const rig_csr_t *A, int scale_rows, double drop_tol, uint32_t flags, int64_t row_begin,
+                  int64_t row_end, const int32_t *part, int32_t K, rig_graph_t *out, double *cut_dev,
+                  rig_stream_t stream) {
+    ABI_BEGIN
+    check_csr(A);
+    if (!part || !cut_dev) throw Error(RIG_ERR_INVALID, "part/cut_dev is NULL");
+    if (K < 1) throw Error(RIG_ERR_INVALID, "K < 1");
+    CutReq cr;
+    cr.part = part;
+    cr.K = K;
+    cr.n_global = A->nrows;
+    cr.cut_dev = cut_dev;
+    build_owned(A, scale_rows, drop_tol, flags, row_begin, row_end, out, (cudaStream_t)stream, &cr);
     return RIG_OK;
     ABI_END
 }
@@ -521,7 +589,7 @@ int rig_plan_execute(rig_plan_t *plan, void *workspace, rig_graph_t *out, rig_st
         throw Error(RIG_ERR_INVALID, "RIG_FLAG_DIAG needs out->diag");
     plan->s = (cudaStream_t)stream;
     Arena tmp(plan->s);
-    const int64_t g = plan_numeric(plan, out->col_idx, out->w, out->diag, out->row_ptr, tmp);
+    const int64_t g = plan_numeric(plan, out->col_idx, out->w, out->diag, out->row_ptr, tmp, nullptr);
     out->n = plan->nloc;
     out->nnz = g;
     return RIG_OK;
@@ -609,16 +677,18 @@ int rig_build_host(const rig_csr_t *Ah, int scale_rows, double drop_tol, uint32_
     }
     rig_csr_t Ad{n, Ah->ncols, nnz, rp, ci, v};
     rig_graph_t g{};
-    build_owned(&Ad, scale_rows, drop_tol, flags, 0, n, &g, s);
+    double *cut_dev = ar.get<double>(1);
+    CutReq cr;
+    cr.part = part;
+    cr.K = K;
+    cr.n_global = n;
+    cr.cut_dev = cut_dev;
+    build_owned(&Ad, scale_rows, drop_tol, flags, 0, n, &g, s, part ? &cr : nullptr);
     struct Guard {
         rig_graph_t *g;
         cudaStream_t s;
         ~Guard() { rig_graph_free(g, s); }
     } guard{&g, s};
-    double *cut_dev = ar.get<double>(1);
-    if (part) {
-        rig_cutsize(&g, 0, n, part, K, cut_dev, s);
-    }
     if (g.nnz > capacity) {
         out_host->nnz = g.nnz;
         throw Error(RIG_ERR_INVALID, "capacity too small for the graph");

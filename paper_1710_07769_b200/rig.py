@@ -50,6 +50,7 @@ def _load():
     P, I64, I32, U32, D = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_uint32, ctypes.c_double
     L.rig_build.argtypes = [P, ctypes.c_int, D, U32, P, P]
     L.rig_build_rows.argtypes = [P, ctypes.c_int, D, U32, I64, I64, P, P]
+    L.rig_build_cut.argtypes = [P, ctypes.c_int, D, U32, I64, I64, P, I32, P, P, P]
     L.rig_graph_free.argtypes = [P, P]
     L.rig_plan_create.argtypes = [P, ctypes.c_int, D, U32, I64, I64, P, P]
     L.rig_plan_query.argtypes = [P, P, P, P]
@@ -135,25 +136,39 @@ class _GraphOwner:
 
 class Graph:
     """G_RIP rows [row_begin, row_begin+n): library-owned device arrays
-    (rig_build) exposed as torch views."""
+    (rig_build) exposed as torch views, created on first access."""
 
     def __init__(self, g: rig_graph_t, row_begin: int, stream):
         self._owner = _GraphOwner(g)
         self._g = rig_graph_t(g.n, g.nnz, g.row_ptr, g.col_idx, g.w, g.diag)
         self.row_begin = row_begin
         self.n, self.nnz = int(g.n), int(g.nnz)
-        dev = torch.device("cuda", torch.cuda.current_device())
-        own = self._owner
+        self._views = {}
 
-        def mk(p, n, t, dt):
-            if not n:
-                return torch.empty(0, dtype=dt, device=dev)
-            return torch.as_tensor(_Cai(p, n, t, own), device=dev)
+    def _view(self, name, ptr, n, typestr, dt):
+        v = self._views.get(name)
+        if v is None:
+            dev = torch.device("cuda", torch.cuda.current_device())
+            v = (torch.as_tensor(_Cai(ptr, n, typestr, self._owner), device=dev) if n
+                 else torch.empty(0, dtype=dt, device=dev))
+            self._views[name] = v
+        return v
 
-        self.row_ptr = mk(g.row_ptr, self.n + 1, "<i8", torch.int64)
-        self.col_idx = mk(g.col_idx, self.nnz, "<i4", torch.int32)
-        self.w = mk(g.w, self.nnz, "<f8", torch.float64)
-        self.diag = mk(g.diag, self.n, "<f8", torch.float64) if g.diag else None
+    @property
+    def row_ptr(self):
+        return self._view("row_ptr", self._g.row_ptr, self.n + 1, "<i8", torch.int64)
+
+    @property
+    def col_idx(self):
+        return self._view("col_idx", self._g.col_idx, self.nnz, "<i4", torch.int32)
+
+    @property
+    def w(self):
+        return self._view("w", self._g.w, self.nnz, "<f8", torch.float64)
+
+    @property
+    def diag(self):
+        return self._view("diag", self._g.diag, self.n, "<f8", torch.float64) if self._g.diag else None
 
     def c(self):
         return self._g
@@ -186,6 +201,20 @@ def rig_build_rows(A: CSR, row_begin, row_end, scale_rows=1, drop_tol=0.0, flags
     _check(lib.rig_build_rows(ctypes.byref(A.c()), int(scale_rows), float(drop_tol), int(flags), int(row_begin),
                               int(row_end), ctypes.byref(g), s))
     return Graph(g, int(row_begin), stream)
+
+
+def rig_build_cut(A: CSR, part: torch.Tensor, K: int, row_begin=0, row_end=None, scale_rows=1, drop_tol=0.0,
+                  flags=0, out=None, stream=None):
+    """Whole hot path in one call: graph rows [row_begin, row_end) and the
+    cutsize of `part` over them (device float64[1], asynchronous value)."""
+    g = rig_graph_t()
+    row_end = A.nrows if row_end is None else int(row_end)
+    if out is None:
+        out = torch.empty(1, dtype=torch.float64, device=part.device)
+    _check(lib.rig_build_cut(ctypes.byref(A.c()), int(scale_rows), float(drop_tol), int(flags), int(row_begin),
+                             row_end, ctypes.c_void_p(part.data_ptr()), int(K), ctypes.byref(g),
+                             ctypes.c_void_p(out.data_ptr()), _stream(stream)))
+    return Graph(g, int(row_begin), stream), out
 
 
 class Plan:

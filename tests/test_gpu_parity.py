@@ -70,6 +70,34 @@ def test_small_configs_bitexact(rig, cfg):
     plan.destroy()
 
 
+@pytest.mark.parametrize("cfg", [1, 3, 5])
+def test_build_cut_fused(rig, cfg):
+    """rig_build_cut (cutsize enqueued on the upper-bound layout) == oracle."""
+    w = make_small(cfg)
+    orc = oracle.build(w.row_ptr, w.col_idx, w.val, scale_rows=w.scale_rows, drop_tol=w.drop_tol)
+    ocut = oracle.cutsize(orc.row_ptr, orc.col, orc.w, w.part, w.K)[0]
+    A = rig.CSR(w.row_ptr, w.col_idx, w.val)
+    part = torch.as_tensor(w.part, device="cuda")
+    g, cut = rig.rig_build_cut(A, part, w.K, 0, w.n, w.scale_rows, w.drop_tol)
+    assert_graph_equal(to_np(g.row_ptr), to_np(g.col_idx), to_np(g.w), orc)
+    assert abs(cut.item() - ocut) <= REL * ocut
+    # holes (dropped entries) before the compaction: the cut must skip them
+    tol = float(np.quantile(orc.w, 0.3))
+    orc2 = oracle.build(w.row_ptr, w.col_idx, w.val, scale_rows=w.scale_rows, drop_tol=tol)
+    ocut2 = oracle.cutsize(orc2.row_ptr, orc2.col, orc2.w, w.part, w.K)[0]
+    g2, cut2 = rig.rig_build_cut(A, part, w.K, 0, w.n, w.scale_rows, tol)
+    assert_graph_equal(to_np(g2.row_ptr), to_np(g2.col_idx), to_np(g2.w), orc2)
+    assert abs(cut2.item() - ocut2) <= REL * ocut2
+    # a shard
+    a, b = w.n // 3, 2 * w.n // 3
+    o3 = oracle.build(w.row_ptr, w.col_idx, w.val, scale_rows=w.scale_rows, drop_tol=w.drop_tol, row_begin=a,
+                      row_end=b)
+    oc3 = oracle.cutsize(o3.row_ptr, o3.col, o3.w, w.part, w.K, row_begin=a)[0]
+    g3, cut3 = rig.rig_build_cut(A, part, w.K, a, b, w.scale_rows, w.drop_tol)
+    assert_graph_equal(to_np(g3.row_ptr), to_np(g3.col_idx), to_np(g3.w), o3)
+    assert abs(cut3.item() - oc3) <= REL * oc3
+
+
 def test_shards_concatenate_bitwise(rig):
     w = make_small(5)
     A = rig.CSR(w.row_ptr, w.col_idx, w.val)
