@@ -95,9 +95,9 @@ int num_sms();
 // ---------------------------------------------------------------- kernels
 // k_prep.cu
 void launch_validate(const Csr &A, int *err, cudaStream_t s);
-void launch_col_hist(const Csr &A, unsigned *cnt, cudaStream_t s);
-void launch_scale_scatter(const Csr &A, int scale, double *ahat, int64_t *cursor, int32_t *ri, double *vt,
-                          int *err, cudaStream_t s);
+void launch_col_hist(const Csr &A, unsigned *cnt, unsigned *rank /*nullable*/, cudaStream_t s);
+void launch_scale_scatter(const Csr &A, int scale, double *ahat, const int64_t *cp, const unsigned *rank,
+                          int32_t *ri, double *vt, int *err, cudaStream_t s);
 void launch_col_sort(int64_t ncols, const int64_t *cp, int32_t *ri, double *vt, int32_t *long_list,
                      unsigned *long_count, cudaStream_t s);
 void launch_analyze(const Csr &A, const int64_t *cp, int64_t rb, int64_t re, int64_t *f, int32_t *sym_lists,

@@ -45,14 +45,27 @@ void launch_validate(const Csr &A, int *err, cudaStream_t s) {
 }
 
 // ------------------------------------------------------------------ a2 (histogram)
-__global__ void k_col_hist(const int32_t *__restrict__ ci, int64_t nnz, unsigned *cnt) {
+// Column counts; with `rank`, also each entry's arrival slot in its column
+// (the returned old count), so the scatter needs no atomics.
+__global__ void k_col_hist(const int32_t *__restrict__ ci, int64_t nnz, unsigned *cnt, unsigned *rank) {
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < nnz; p += stride)
-        atomicAdd(&cnt[ci[p]], 1u);
+    int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (rank) {
+        for (; p + 3 * stride < nnz; p += 4 * stride) {  // 4 returning atomics in flight
+            unsigned r[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) r[u] = atomicAdd(&cnt[ci[p + u * stride]], 1u);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) rank[p + u * stride] = r[u];
+        }
+        for (; p < nnz; p += stride) rank[p] = atomicAdd(&cnt[ci[p]], 1u);
+    } else {
+        for (; p < nnz; p += stride) atomicAdd(&cnt[ci[p]], 1u);
+    }
 }
 
-void launch_col_hist(const Csr &A, unsigned *cnt, cudaStream_t s) {
-    k_col_hist<<<grid_for(A.nnz, 256, 16), 256, 0, s>>>(A.ci, A.nnz, cnt);
+void launch_col_hist(const Csr &A, unsigned *cnt, unsigned *rank, cudaStream_t s) {
+    k_col_hist<<<grid_for(A.nnz, 256, 16), 256, 0, s>>>(A.ci, A.nnz, cnt, rank);
     note_launch();
 }
 
@@ -61,8 +74,9 @@ void launch_col_hist(const Csr &A, unsigned *cnt, cudaStream_t s) {
 // +0.0; nrm_i = sqrt_rn(ss_i); a_hat = a /_rn nrm_i (DESIGN.md §3 R5).
 // Fused with the CSC scatter: each thread owns one row, so the scaled value
 // written to the CSR copy and to the CSC slot is the same double.
-__global__ void k_scale_scatter(Csr A, int scale, double *__restrict__ ahat, int64_t *cursor, int32_t *ri,
-                                double *vt, int *err) {
+// Slot of entry p in the CSC: cp[ci[p]] + rank[p] (rank from k_col_hist).
+__global__ void k_scale_scatter(Csr A, int scale, double *__restrict__ ahat, const int64_t *__restrict__ cp,
+                                const unsigned *__restrict__ rank, int32_t *ri, double *vt, int *err) {
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < A.nrows; i += stride) {
         const int64_t s = A.rp[i], e = A.rp[i + 1];
@@ -83,40 +97,19 @@ __global__ void k_scale_scatter(Csr A, int scale, double *__restrict__ ahat, int
             }
             nrm = __dsqrt_rn(ss);
         }
-        // four independent atomics in flight per thread
-        int64_t p = s;
-        for (; p + 4 <= e; p += 4) {
-            int k[4];
-            double x[4];
-            unsigned long long q[4];
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                k[u] = A.ci[p + u];
-                x[u] = scale ? __ddiv_rn(A.v[p + u], nrm) : A.v[p + u];
-            }
-#pragma unroll
-            for (int u = 0; u < 4; ++u) q[u] = atomicAdd((unsigned long long *)&cursor[k[u]], 1ull);
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                if (scale) ahat[p + u] = x[u];
-                ri[q[u]] = (int32_t)i;
-                vt[q[u]] = x[u];
-            }
-        }
-        for (; p < e; ++p) {
+        for (int64_t p = s; p < e; ++p) {
             const double x = scale ? __ddiv_rn(A.v[p], nrm) : A.v[p];
             if (scale) ahat[p] = x;
-            const int k = A.ci[p];
-            const unsigned long long q = atomicAdd((unsigned long long *)&cursor[k], 1ull);
+            const int64_t q = cp[A.ci[p]] + rank[p];
             ri[q] = (int32_t)i;
             vt[q] = x;
         }
     }
 }
 
-void launch_scale_scatter(const Csr &A, int scale, double *ahat, int64_t *cursor, int32_t *ri, double *vt,
-                          int *err, cudaStream_t s) {
-    k_scale_scatter<<<grid_for(A.nrows, 128, 16), 128, 0, s>>>(A, scale, ahat, cursor, ri, vt, err);
+void launch_scale_scatter(const Csr &A, int scale, double *ahat, const int64_t *cp, const unsigned *rank,
+                          int32_t *ri, double *vt, int *err, cudaStream_t s) {
+    k_scale_scatter<<<grid_for(A.nrows, 128, 16), 128, 0, s>>>(A, scale, ahat, cp, rank, ri, vt, err);
     note_launch();
 }
 
@@ -158,10 +151,11 @@ __global__ void k_col_sort_short(int64_t ncols, const int64_t *__restrict__ cp, 
 #pragma unroll
             for (int t = 0; t < kRegCol; ++t) {
                 kk[t] = t < len ? ri[s + t] : INT_MAX;
-                vv[t] = t < len ? vt[s + t] : 0.0;
                 if (t > 0) sorted &= kk[t - 1] <= kk[t];
             }
-            if (sorted) continue;
+            if (sorted) continue;  // values are only read when the keys need sorting
+#pragma unroll
+            for (int t = 0; t < kRegCol; ++t) vv[t] = t < len ? vt[s + t] : 0.0;
             sort_regs<kRegCol>(kk, vv);
 #pragma unroll
             for (int t = 0; t < kRegCol; ++t) {

@@ -1,14 +1,19 @@
 // rig_api.cu -- the C ABI declared in include/rig.h: argument checks, device
-// memory (stream-ordered pool), pass orchestration, error reporting.
-// Every step of the path runs in the kernels of k_*.cu; this file only
-// sequences them and reads back the few counters that size allocations.
+// memory, pass orchestration, error reporting.  Every step of the path runs
+// in the kernels of k_*.cu; this file only sequences them and reads back the
+// few counters that size allocations.
+//
+// Host-overhead budget: a build makes one workspace
+// allocation per phase (stream-ordered pool), two memsets, two host syncs
+// (reading counters into pinned host memory) and ~10 kernel launches.
 #include <atomic>
 #include <cmath>
-#include <mutex>
 #include <cstdio>
 #include <cstring>
+#include <mutex>
 #include <stdexcept>
 #include <string>
+#include <unordered_map>
 #include <vector>
 
 #include "../../include/rig.h"
@@ -35,15 +40,15 @@ int num_sms() {
 // ---------------------------------------------------------------- profiling
 enum Pass {
     P_VALIDATE = 0,
-    P_COLPTR,      // column histogram + scan
-    P_SCATTER,     // a1 scale + a2 scatter
-    P_COLSORT,
-    P_ANALYZE,     // a3
-    P_SYMBOLIC,    // a4 (+ numeric binning)
-    P_UBSCAN,
-    P_NUMERIC,     // a5 + a6 (fused)
-    P_COMPACT,     // a6 holes path
-    P_CUTSIZE,     // a7
+    P_COLPTR,    // column histogram (+ ranks) + scan
+    P_SCATTER,   // a1 scale + a2 scatter
+    P_COLSORT,   // a2 per-column order
+    P_ANALYZE,   // a3 + a4 for merge-path rows
+    P_SYMBOLIC,  // a4 for the other rows (+ numeric binning)
+    P_UBSCAN,    // graph row pointers
+    P_NUMERIC,   // a5 + a6 (+ fused a7 partials)
+    P_COMPACT,   // a6 holes path
+    P_CUTSIZE,   // a7 (standalone kernel or fused final reduction)
     P_SPLIT,
     P_OTHER,
 };
@@ -51,7 +56,7 @@ static const char *kPassNames[RIG_NPASS] = {"validate", "colptr",   "scale_scatt
                                             "analyze",  "symbolic", "ub_scan",       "numeric",
                                             "compact",  "cutsize",  "split",         "other"};
 static std::mutex g_prof_mu;
-static std::atomic<bool> g_prof_on{false};
+static std::atomic<uint32_t> g_prof_mask{0};
 struct ProfRec {
     int pass;
     cudaEvent_t a, b;
@@ -76,12 +81,13 @@ static cudaEvent_t ev_get() {
     return e;
 }
 
+// CUDA event pair around one pass on the stream it runs on (when enabled).
 struct Prof {
     int pass;
     cudaStream_t s;
     cudaEvent_t a = nullptr;
     Prof(int p, cudaStream_t st) : pass(p), s(st) {
-        if (g_prof_on.load(std::memory_order_relaxed)) {
+        if (g_prof_mask.load(std::memory_order_relaxed) & (1u << p)) {
             a = ev_get();
             cudaEventRecord(a, s);
         }
@@ -129,31 +135,57 @@ static void ensure_pool() {
     }
 }
 
+// Pinned host staging for the counters read back at syncs (per thread).
+struct HostStage {
+    DevCounters ctr;
+    int64_t v[4];
+    int holes;
+};
+static HostStage *host_stage() {
+    static thread_local HostStage *hs = nullptr;
+    if (!hs) {
+        void *p = nullptr;
+        if (cudaMallocHost(&p, sizeof(HostStage)) != cudaSuccess) throw Error(RIG_ERR_NOMEM, "cudaMallocHost");
+        hs = static_cast<HostStage *>(p);
+    }
+    return hs;
+}
+
+// Bump layout over one allocation: add() records 256-byte aligned offsets.
+struct Layout {
+    size_t bytes = 0;
+    size_t add(size_t n) {
+        const size_t off = bytes;
+        bytes += (n + 255) & ~(size_t)255;
+        return off;
+    }
+};
+
 // Stream-ordered allocations owned by one call / plan.
 struct Arena {
     cudaStream_t s;
     std::vector<void *> ptrs;
     explicit Arena(cudaStream_t st) : s(st) {}
+    unsigned char *raw(size_t bytes) {
+        void *p = nullptr;
+        CK(cudaMallocAsync(&p, bytes ? bytes : 256, s));
+        ptrs.push_back(p);
+        return static_cast<unsigned char *>(p);
+    }
     template <typename T>
     T *get(int64_t count) {
-        if (count <= 0) count = 1;
-        void *p = nullptr;
-        CK(cudaMallocAsync(&p, (size_t)count * sizeof(T), s));
-        ptrs.push_back(p);
-        return static_cast<T *>(p);
-    }
-    void release(void *p) {
-        for (auto &q : ptrs)
-            if (q == p) {
-                cudaFreeAsync(q, s);
-                q = nullptr;
-            }
+        return reinterpret_cast<T *>(raw((size_t)(count > 0 ? count : 1) * sizeof(T)));
     }
     ~Arena() {
         for (void *p : ptrs)
             if (p) cudaFreeAsync(p, s);
     }
 };
+
+// Library-owned graphs: row_ptr and the (col, w, diag) block are two
+// allocations; rig_graph_free looks the block up by row_ptr.
+static std::mutex g_own_mu;
+static std::unordered_map<void *, void *> g_owned;
 
 static int err_to_code(int err) {
     if (err & kErrNonCanonical) return RIG_ERR_NONCANONICAL;
@@ -194,7 +226,7 @@ struct rig_plan {
     uint32_t flags = 0;
     int64_t rb = 0, re = 0, nloc = 0;
     DevCounters *ctr = nullptr;  // device
-    DevCounters h{};             // host copy
+    DevCounters h{};             // host copy (after sync 1)
     int32_t *sym_lists = nullptr, *num_lists = nullptr;
     int64_t list_cap = 0;
     int64_t *nnzc = nullptr, *gptr_ub = nullptr;
@@ -204,46 +236,66 @@ struct rig_plan {
     explicit rig_plan(cudaStream_t st) : s(st), arena(st) {}
 };
 
+// Steps a0-a4 for rows [rb, re).  The graph row pointers (structural
+// upper-bound offsets) go to gptr_out when given.  exact: also read back
+// nnz_upper (staged API; one more sync).
 static void plan_build(rig_plan *p, const rig_csr_t *Ain, int64_t *gptr_out, bool exact) {
     cudaStream_t s = p->s;
-    Arena &ar = p->arena;
-    const int64_t n = Ain->nrows, m = Ain->ncols, nnz = Ain->nnz;
+    const int64_t n = Ain->nrows, m = Ain->ncols, nnz = Ain->nnz, nloc = p->nloc;
     Csr A0{n, m, nnz, Ain->row_ptr, Ain->col_idx, Ain->val};
-    p->ctr = ar.get<DevCounters>(1);
-    CK(cudaMemsetAsync(p->ctr, 0, sizeof(DevCounters), s));
+    // ---- phase-A workspace (one allocation, one memset of the zeroed head)
+    Layout L;
+    const size_t o_ctr = L.add(sizeof(DevCounters));
+    const size_t o_cnt = L.add(sizeof(unsigned) * (size_t)m);
+    const size_t o_st1 = L.add(scan_tmp_bytes(m));
+    const size_t o_st2 = L.add(scan_tmp_bytes(nloc));
+    const size_t zero_bytes = L.bytes;
+    const size_t o_cp = L.add(sizeof(int64_t) * (size_t)(m + 1));
+    const size_t o_rank = L.add(sizeof(unsigned) * (size_t)nnz);
+    const size_t o_ahat = p->scale ? L.add(sizeof(double) * (size_t)nnz) : 0;
+    const size_t o_ri = L.add(sizeof(int32_t) * (size_t)nnz);
+    const size_t o_vt = L.add(sizeof(double) * (size_t)nnz);
+    const size_t o_long = L.add(sizeof(int32_t) * (size_t)m);
+    const size_t o_sym = L.add(sizeof(int32_t) * (size_t)kSymBins * (size_t)std::max<int64_t>(nloc, 1));
+    const size_t o_nnzc = L.add(sizeof(int64_t) * (size_t)nloc);
+    const size_t o_gptr = gptr_out ? 0 : L.add(sizeof(int64_t) * (size_t)(nloc + 1));
+    unsigned char *ws = p->arena.raw(L.bytes);
+    CK(cudaMemsetAsync(ws, 0, zero_bytes, s));
+    p->ctr = reinterpret_cast<DevCounters *>(ws + o_ctr);
+    unsigned *cnt = reinterpret_cast<unsigned *>(ws + o_cnt);
+    int64_t *cp = reinterpret_cast<int64_t *>(ws + o_cp);
+    unsigned *rank = reinterpret_cast<unsigned *>(ws + o_rank);
+    double *ahat = p->scale ? reinterpret_cast<double *>(ws + o_ahat) : nullptr;
+    int32_t *ri = reinterpret_cast<int32_t *>(ws + o_ri);
+    double *vt = reinterpret_cast<double *>(ws + o_vt);
+    int32_t *long_list = reinterpret_cast<int32_t *>(ws + o_long);
+    p->sym_lists = reinterpret_cast<int32_t *>(ws + o_sym);
+    p->nnzc = reinterpret_cast<int64_t *>(ws + o_nnzc);
+    p->gptr_ub = gptr_out ? gptr_out : reinterpret_cast<int64_t *>(ws + o_gptr);
+    p->list_cap = nloc;
+    HostStage *hs = host_stage();
+
     // a0: validation must finish before anything indexes with the input
     if (p->flags & RIG_FLAG_VALIDATE) {
         Prof pf(P_VALIDATE, s);
         launch_validate(A0, &p->ctr->err, s);
         check_launch("validate");
-        int err = 0;
-        CK(cudaMemcpyAsync(&err, &p->ctr->err, sizeof(int), cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(&hs->ctr.err, &p->ctr->err, sizeof(int), cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
+        const int err = hs->ctr.err;
         if (err) throw Error(err_to_code(err), err_msg(err_to_code(err)));
     }
-    // a2: column histogram -> col_ptr
-    unsigned *cnt = ar.get<unsigned>(m);
-    int64_t *cp = ar.get<int64_t>(m + 1);
-    void *scan_tmp = ar.get<unsigned char>((int64_t)scan_tmp_bytes(std::max(m, n) + 1));
-    int64_t *cursor = ar.get<int64_t>(m);
+    // a2: column counts + arrival ranks -> col_ptr
     {
         Prof pf(P_COLPTR, s);
-        CK(cudaMemsetAsync(cnt, 0, sizeof(unsigned) * (size_t)std::max<int64_t>(m, 1), s));
-        if (nnz > 0) launch_col_hist(A0, cnt, s);
-        scan_u32(cnt, m, cp, scan_tmp, 0, s);
-        if (m > 0) CK(cudaMemcpyAsync(cursor, cp, sizeof(int64_t) * (size_t)m, cudaMemcpyDeviceToDevice, s));
+        if (nnz > 0) launch_col_hist(A0, cnt, rank, s);
+        scan_u32(cnt, m, cp, ws + o_st1, 0, s);
     }
     // a1 + a2: scale rows (optional) and scatter into the CSC
-    double *ahat = p->scale ? ar.get<double>(nnz) : nullptr;
-    int32_t *ri = ar.get<int32_t>(nnz);
-    double *vt = ar.get<double>(nnz);
     if (n > 0) {
         Prof pf(P_SCATTER, s);
-        launch_scale_scatter(A0, p->scale, ahat, cursor, ri, vt, &p->ctr->err, s);
+        launch_scale_scatter(A0, p->scale, ahat, cp, rank, ri, vt, &p->ctr->err, s);
     }
-    ar.release(cursor);
-    ar.release(cnt);
-    int32_t *long_list = ar.get<int32_t>(m);
     if (m > 0) {
         Prof pf(P_COLSORT, s);
         launch_col_sort(m, cp, ri, vt, long_list, &p->ctr->long_cols, s);
@@ -252,18 +304,16 @@ static void plan_build(rig_plan *p, const rig_csr_t *Ain, int64_t *gptr_out, boo
     p->A = Csr{n, m, nnz, Ain->row_ptr, Ain->col_idx, p->scale ? ahat : Ain->val};
     p->T = Csc{cp, ri, vt};
     // a3 + a4 (merge rows): products, structural nnz(C_i), bins for the rest
-    p->list_cap = p->nloc;
-    p->sym_lists = ar.get<int32_t>((int64_t)kSymBins * std::max<int64_t>(p->list_cap, 1));
-    p->nnzc = ar.get<int64_t>(p->nloc);
     SymArgs sa{p->A, p->T, p->rb, p->re, p->nnzc};
-    if (p->nloc > 0) {
+    if (nloc > 0) {
         Prof pf(P_ANALYZE, s);
         launch_analyze_sym(sa, p->sym_lists, p->list_cap, p->ctr, s);
     }
     check_launch("analyze");
     // sync 1: errors, products, bin sizes
-    CK(cudaMemcpyAsync(&p->h, p->ctr, sizeof(DevCounters), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(&hs->ctr, p->ctr, sizeof(DevCounters), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
+    p->h = hs->ctr;
     if (p->h.err) throw Error(err_to_code(p->h.err), err_msg(err_to_code(p->h.err)));
     // a4 for rows off the merge path
     const int64_t n_mid = p->h.n_mid;
@@ -271,58 +321,67 @@ static void plan_build(rig_plan *p, const rig_csr_t *Ain, int64_t *gptr_out, boo
         Prof pf(P_SYMBOLIC, s);
         launch_sym_warp(sa, p->sym_lists, p->list_cap, p->ctr->sym_count, p->h.sym_count, s);
         // rows with f > 1024 may need the huge numeric path too (nnzC <= f)
-        if (p->h.sym_count[kNumSymBins] + p->h.sym_count[kNumSymBins - 1] > 0) {
-            p->huge_slots_n = huge_slots(n, p->h.sym_count[kNumSymBins] + p->h.sym_count[kNumSymBins - 1]);
-            const size_t bytes = huge_scratch_bytes(n, p->huge_slots_n, true);
-            p->huge_scratch = ar.get<unsigned char>((int64_t)bytes);
-            CK(cudaMemsetAsync(p->huge_scratch, 0, bytes, s));
+        const int64_t n_big = p->h.sym_count[kNumSymBins] + p->h.sym_count[kNumSymBins - 1];
+        Layout LB;
+        const size_t o_num = LB.add(sizeof(int32_t) * (size_t)kNumBins * (size_t)n_mid);
+        size_t o_huge = 0, huge_bytes = 0;
+        if (n_big > 0) {
+            p->huge_slots_n = huge_slots(n, n_big);
+            huge_bytes = huge_scratch_bytes(n, p->huge_slots_n, true);
+            o_huge = LB.add(huge_bytes);
+        }
+        unsigned char *wb = p->arena.raw(LB.bytes);
+        p->num_lists = reinterpret_cast<int32_t *>(wb + o_num);
+        if (n_big > 0) {
+            p->huge_scratch = wb + o_huge;
+            CK(cudaMemsetAsync(p->huge_scratch, 0, huge_bytes, s));
         }
         if (p->h.sym_count[kNumSymBins] > 0)
             launch_sym_huge(sa, p->sym_lists + (int64_t)kNumSymBins * p->list_cap, p->ctr->sym_count + kNumSymBins,
                             p->huge_slots_n, p->huge_scratch, s);
-        p->num_lists = ar.get<int32_t>((int64_t)kNumBins * n_mid);
         launch_bin_num(p->sym_lists, p->list_cap, p->ctr, p->nnzc, p->rb, p->num_lists, n_mid, p->ctr->num_count, s);
     }
     check_launch("symbolic");
-    p->gptr_ub = gptr_out ? gptr_out : ar.get<int64_t>(p->nloc + 1);
     {
         Prof pf(P_UBSCAN, s);
-        scan_i64(p->nnzc, p->nloc, p->gptr_ub, ScanOp::UbOffDiag, scan_tmp, 0, s);
+        scan_i64(p->nnzc, nloc, p->gptr_ub, ScanOp::UbOffDiag, ws + o_st2, 0, s);
     }
     check_launch("scan");
     p->nnz_upper = -1;
     if (exact) {  // sync 2 (staged API): exact capacity for the caller
-        CK(cudaMemcpyAsync(&p->nnz_upper, p->gptr_ub + p->nloc, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(&hs->v[0], p->gptr_ub + nloc, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
+        p->nnz_upper = hs->v[0];
     }
 }
 
 struct CutReq {
     const int32_t *part = nullptr;
     int32_t K = 0;
-    int64_t n_global = 0;
     double *cut_dev = nullptr;
 };
 
 // a5 + a6 into caller arrays (capacity >= structural off-diagonal nnz); the
-// optional cutsize (a7) is enqueued right behind the numeric pass -- it skips
-// unfilled slots (col < 0) -- so it costs no extra synchronisation.
+// optional cutsize (a7) is fused into the numeric kernels and reduced right
+// behind them, so it costs no extra synchronisation.
 // Returns the final nnz.  Synchronises once (twice if entries were dropped).
 static int64_t plan_numeric(rig_plan *p, int32_t *gcol, double *gw, double *diag, int64_t *row_ptr_out,
                             Arena &tmp_arena, const CutReq *cut) {
     cudaStream_t s = p->s;
-    double *cutp = nullptr;
-    int *badp = nullptr, *used = nullptr;
-    if (cut) {  // fused a7: per-CTA partials of every numeric launch, used counts, bad-id flag
-        const int64_t nslots = (int64_t)kCutLaunches * kCutSlotsPerLaunch;
-        cutp = tmp_arena.get<double>(nslots + 8);
-        used = reinterpret_cast<int *>(cutp + nslots);  // [kCutLaunches] ints
-        badp = used + kCutLaunches;
-        CK(cudaMemsetAsync(used, 0, sizeof(int) * (kCutLaunches + 1), s));
-    }
+    // zeroed: holes flag, fused-cut used counts + bad flag; then the partials
+    Layout L;
+    const size_t o_holes = L.add(sizeof(int));
+    const size_t o_used = L.add(sizeof(int) * (kCutLaunches + 1));
+    const size_t zero_bytes = L.bytes;
+    const size_t o_cutp = cut ? L.add(sizeof(double) * (size_t)kCutLaunches * kCutSlotsPerLaunch) : 0;
+    unsigned char *wn = tmp_arena.raw(L.bytes);
+    CK(cudaMemsetAsync(wn, 0, zero_bytes, s));
+    int *holes_d = reinterpret_cast<int *>(wn + o_holes);
+    int *used = reinterpret_cast<int *>(wn + o_used);
+    int *badp = used + kCutLaunches;
+    double *cutp = cut ? reinterpret_cast<double *>(wn + o_cutp) : nullptr;
     {
         Prof pf(P_NUMERIC, s);
-        CK(cudaMemsetAsync(&p->ctr->holes, 0, sizeof(int), s));
         NumArgs na{p->A,
                    p->T,
                    p->rb,
@@ -332,7 +391,7 @@ static int64_t plan_numeric(rig_plan *p, int32_t *gcol, double *gw, double *diag
                    gw,
                    (p->flags & RIG_FLAG_DIAG) ? diag : nullptr,
                    p->tol,
-                   &p->ctr->holes,
+                   holes_d,
                    cut ? cut->part : nullptr,
                    cut ? cut->K : 0,
                    cutp,
@@ -341,7 +400,7 @@ static int64_t plan_numeric(rig_plan *p, int32_t *gcol, double *gw, double *diag
         if (p->nloc > 0) launch_num_merge(na, p->h.max_len, s);
         if (p->h.n_mid > 0) {
             // numeric bin sizes are device-side; empty bins exit immediately
-            int64_t all[8] = {1, 1, 1, 1, 1, 1, 1, 1};
+            const int64_t all[8] = {1, 1, 1, 1, 1, 1, 1, 1};
             launch_num_warp(na, p->num_lists, p->h.n_mid, p->ctr->num_count, all, s);
             if (p->huge_scratch)
                 launch_num_huge(na, p->num_lists + (int64_t)kNumNumBins * p->h.n_mid,
@@ -354,11 +413,12 @@ static int64_t plan_numeric(rig_plan *p, int32_t *gcol, double *gw, double *diag
         launch_cut_final(cutp, used, kCutLaunches, kCutSlotsPerLaunch, badp, cut->cut_dev, s);
         check_launch("cut_final");
     }
-    int holes = 0;
-    int64_t ub = 0;
-    CK(cudaMemcpyAsync(&holes, &p->ctr->holes, sizeof(int), cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpyAsync(&ub, p->gptr_ub + p->nloc, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    HostStage *hs = host_stage();
+    CK(cudaMemcpyAsync(&hs->holes, holes_d, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(&hs->v[0], p->gptr_ub + p->nloc, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
+    const int holes = hs->holes;
+    const int64_t ub = hs->v[0];
     p->nnz_upper = ub;
     if (!holes) {
         if (row_ptr_out != p->gptr_ub)
@@ -368,23 +428,29 @@ static int64_t plan_numeric(rig_plan *p, int32_t *gcol, double *gw, double *diag
     }
     // holes: count kept entries per row, scan, move into a temporary, copy back
     Prof pf_c(P_COMPACT, s);
+    Layout LC;
+    const size_t o_copy = LC.add(sizeof(int64_t) * (size_t)(p->nloc + 1));
+    const size_t o_kept = LC.add(sizeof(int64_t) * (size_t)p->nloc);
+    const size_t o_st = LC.add(scan_tmp_bytes(p->nloc));
+    const size_t o_c2 = LC.add(sizeof(int32_t) * (size_t)ub);
+    const size_t o_w2 = LC.add(sizeof(double) * (size_t)ub);
+    unsigned char *wc = tmp_arena.raw(LC.bytes);
     const int64_t *ubp = p->gptr_ub;
     if (row_ptr_out == p->gptr_ub) {  // keep the structural offsets for the move
-        int64_t *copy = tmp_arena.get<int64_t>(p->nloc + 1);
+        int64_t *copy = reinterpret_cast<int64_t *>(wc + o_copy);
         CK(cudaMemcpyAsync(copy, p->gptr_ub, sizeof(int64_t) * (size_t)(p->nloc + 1), cudaMemcpyDeviceToDevice, s));
         ubp = copy;
     }
-    int64_t *kept = tmp_arena.get<int64_t>(p->nloc);
-    void *scan_tmp = tmp_arena.get<unsigned char>((int64_t)scan_tmp_bytes(p->nloc + 1));
+    int64_t *kept = reinterpret_cast<int64_t *>(wc + o_kept);
+    int32_t *c2 = reinterpret_cast<int32_t *>(wc + o_c2);
+    double *w2 = reinterpret_cast<double *>(wc + o_w2);
     launch_count_kept(ubp, p->nloc, gcol, kept, s);
-    scan_i64(kept, p->nloc, row_ptr_out, ScanOp::Identity, scan_tmp, 0, s);
-    int64_t g = 0;
-    CK(cudaMemcpyAsync(&g, row_ptr_out + p->nloc, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
-    int32_t *c2 = tmp_arena.get<int32_t>(ub);
-    double *w2 = tmp_arena.get<double>(ub);
+    scan_i64(kept, p->nloc, row_ptr_out, ScanOp::Identity, wc + o_st, 0, s);
+    CK(cudaMemcpyAsync(&hs->v[1], row_ptr_out + p->nloc, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
     launch_compact_move(ubp, row_ptr_out, p->nloc, gcol, gw, c2, w2, s);
     check_launch("compact");
     CK(cudaStreamSynchronize(s));
+    const int64_t g = hs->v[1];
     if (g > 0) {
         CK(cudaMemcpyAsync(gcol, c2, sizeof(int32_t) * (size_t)g, cudaMemcpyDeviceToDevice, s));
         CK(cudaMemcpyAsync(gw, w2, sizeof(double) * (size_t)g, cudaMemcpyDeviceToDevice, s));
@@ -436,9 +502,27 @@ static rig_plan *make_plan(const rig_csr_t *A, int scale_rows, double drop_tol, 
         return RIG_ERR_INVALID;                 \
     }
 
-// Library-owned output.  The graph arrays are sized from the product count P
-// (known at the first sync; P >= nnz(C) >= graph nnz), so the numeric pass
-// follows the symbolic scan without a host round trip.
+static void free_owned(rig_graph_t *g, cudaStream_t s) {
+    void *block = nullptr;
+    bool found = false;
+    {
+        std::lock_guard<std::mutex> lk(g_own_mu);
+        auto it = g_owned.find(g->row_ptr);
+        if (it != g_owned.end()) {
+            block = it->second;
+            g_owned.erase(it);
+            found = true;
+        }
+    }
+    if (!found) throw Error(RIG_ERR_INVALID, "graph was not allocated by rig_build*");
+    CK(cudaFreeAsync(g->row_ptr, s));
+    if (block) CK(cudaFreeAsync(block, s));
+    std::memset(g, 0, sizeof(*g));
+}
+
+// Library-owned output.  The (col, w, diag) block is sized from the product
+// count P (known at the first sync; P >= nnz(C) >= graph nnz), so the numeric
+// pass follows the symbolic scan without a host round trip.
 static void build_owned(const rig_csr_t *A, int scale_rows, double drop_tol, uint32_t flags, int64_t rb, int64_t re,
                         rig_graph_t *out, cudaStream_t s, const CutReq *cut) {
     if (!out) throw Error(RIG_ERR_INVALID, "out is NULL");
@@ -446,15 +530,19 @@ static void build_owned(const rig_csr_t *A, int scale_rows, double drop_tol, uin
     rig_plan *p = new_plan(A, scale_rows, drop_tol, flags, rb, re, s);
     Arena tmp(s);
     int64_t *rp = nullptr;
-    int32_t *col = nullptr;
-    double *w = nullptr, *diag = nullptr;
+    unsigned char *block = nullptr;
     try {
         CK(cudaMallocAsync((void **)&rp, sizeof(int64_t) * (size_t)(p->nloc + 1), s));
         plan_build(p, A, rp, false);
         const int64_t cap = std::max<int64_t>(p->h.products, 1);
-        CK(cudaMallocAsync((void **)&col, sizeof(int32_t) * (size_t)cap, s));
-        CK(cudaMallocAsync((void **)&w, sizeof(double) * (size_t)cap, s));
-        if (flags & RIG_FLAG_DIAG) CK(cudaMallocAsync((void **)&diag, sizeof(double) * (size_t)std::max<int64_t>(p->nloc, 1), s));
+        Layout L;
+        const size_t o_col = L.add(sizeof(int32_t) * (size_t)cap);
+        const size_t o_w = L.add(sizeof(double) * (size_t)cap);
+        const size_t o_diag = (flags & RIG_FLAG_DIAG) ? L.add(sizeof(double) * (size_t)std::max<int64_t>(p->nloc, 1)) : 0;
+        CK(cudaMallocAsync((void **)&block, L.bytes, s));
+        int32_t *col = reinterpret_cast<int32_t *>(block + o_col);
+        double *w = reinterpret_cast<double *>(block + o_w);
+        double *diag = (flags & RIG_FLAG_DIAG) ? reinterpret_cast<double *>(block + o_diag) : nullptr;
         const int64_t g = plan_numeric(p, col, w, diag, rp, tmp, cut);
         out->n = p->nloc;
         out->nnz = g;
@@ -462,11 +550,11 @@ static void build_owned(const rig_csr_t *A, int scale_rows, double drop_tol, uin
         out->col_idx = col;
         out->w = w;
         out->diag = diag;
+        std::lock_guard<std::mutex> lk(g_own_mu);
+        g_owned[rp] = block;
     } catch (...) {
         if (rp) cudaFreeAsync(rp, s);
-        if (col) cudaFreeAsync(col, s);
-        if (w) cudaFreeAsync(w, s);
-        if (diag) cudaFreeAsync(diag, s);
+        if (block) cudaFreeAsync(block, s);
         delete p;
         throw;
     }
@@ -478,7 +566,9 @@ extern "C" {
 const char *rig_last_error(void) { return t_last_error.c_str(); }
 
 int rig_profile_enable(int on) {
-    g_prof_on.store(on != 0);
+    // on: 0 = off, 1 = every pass, otherwise a bit mask (bit p = pass p) | 2^31
+    const uint32_t u = (uint32_t)on;
+    g_prof_mask.store(u == 1u ? 0xffffffffu : (u & 0x7fffffffu));
     return RIG_OK;
 }
 
@@ -511,7 +601,7 @@ int rig_profile_read(double *ms, int64_t *count) {
 
 const char *rig_pass_name(int pass) { return (pass >= 0 && pass < RIG_NPASS) ? kPassNames[pass] : "?"; }
 uint64_t rig_launch_count(void) { return g_launches.load(); }
-const char *rig_version(void) { return "librig 0.1 (sm_100a)"; }
+const char *rig_version(void) { return "librig 0.2 (sm_100a)"; }
 
 int rig_build(const rig_csr_t *A, int scale_rows, double drop_tol, uint32_t flags, rig_graph_t *out,
               rig_stream_t stream) {
@@ -540,7 +630,6 @@ int rig_build_cut(const rig_csr_t *A, int scale_rows, double drop_tol, uint32_t 
     CutReq cr;
     cr.part = part;
     cr.K = K;
-    cr.n_global = A->nrows;
     cr.cut_dev = cut_dev;
     build_owned(A, scale_rows, drop_tol, flags, row_begin, row_end, out, (cudaStream_t)stream, &cr);
     return RIG_OK;
@@ -550,12 +639,11 @@ int rig_build_cut(const rig_csr_t *A, int scale_rows, double drop_tol, uint32_t 
 int rig_graph_free(rig_graph_t *g, rig_stream_t stream) {
     ABI_BEGIN
     if (!g) throw Error(RIG_ERR_INVALID, "g is NULL");
-    cudaStream_t s = (cudaStream_t)stream;
-    if (g->row_ptr) CK(cudaFreeAsync(g->row_ptr, s));
-    if (g->col_idx) CK(cudaFreeAsync(g->col_idx, s));
-    if (g->w) CK(cudaFreeAsync(g->w, s));
-    if (g->diag) CK(cudaFreeAsync(g->diag, s));
-    std::memset(g, 0, sizeof(*g));
+    if (!g->row_ptr) {
+        std::memset(g, 0, sizeof(*g));
+        return RIG_OK;
+    }
+    free_owned(g, (cudaStream_t)stream);
     return RIG_OK;
     ABI_END
 }
@@ -574,7 +662,7 @@ int rig_plan_query(const rig_plan_t *plan, int64_t *nnz_upper, int64_t *products
     if (!plan) throw Error(RIG_ERR_INVALID, "plan is NULL");
     if (nnz_upper) *nnz_upper = plan->nnz_upper;
     if (products) *products = plan->h.products;
-    if (workspace_bytes) *workspace_bytes = 0;
+    if (workspace_bytes) *workspace_bytes = 0;  // temporaries are stream-ordered pool allocations
     return RIG_OK;
     ABI_END
 }
@@ -612,19 +700,29 @@ int rig_row_split(const rig_csr_t *A, int32_t parts, int64_t *split, rig_stream_
     Arena ar(s);
     const int64_t n = A->nrows, m = A->ncols;
     Csr A0{n, m, A->nnz, A->row_ptr, A->col_idx, A->val};
-    unsigned *cnt = ar.get<unsigned>(m);
-    int64_t *cp = ar.get<int64_t>(m + 1);
-    void *scan_tmp = ar.get<unsigned char>((int64_t)scan_tmp_bytes(std::max(m, n) + 1));
-    CK(cudaMemsetAsync(cnt, 0, sizeof(unsigned) * (size_t)std::max<int64_t>(m, 1), s));
-    if (A->nnz > 0) launch_col_hist(A0, cnt, s);
-    scan_u32(cnt, m, cp, scan_tmp, 0, s);
-    int64_t *f = ar.get<int64_t>(n);
-    int64_t *fp = ar.get<int64_t>(n + 1);
-    DevCounters *ctr = ar.get<DevCounters>(1);
-    CK(cudaMemsetAsync(ctr, 0, sizeof(DevCounters), s));
+    Layout L;
+    const size_t o_ctr = L.add(sizeof(DevCounters));
+    const size_t o_cnt = L.add(sizeof(unsigned) * (size_t)m);
+    const size_t o_st1 = L.add(scan_tmp_bytes(m));
+    const size_t o_st2 = L.add(scan_tmp_bytes(n));
+    const size_t zero_bytes = L.bytes;
+    const size_t o_cp = L.add(sizeof(int64_t) * (size_t)(m + 1));
+    const size_t o_f = L.add(sizeof(int64_t) * (size_t)n);
+    const size_t o_fp = L.add(sizeof(int64_t) * (size_t)(n + 1));
+    const size_t o_sp = L.add(sizeof(int64_t) * (size_t)(parts + 1));
+    unsigned char *ws = ar.raw(L.bytes);
+    CK(cudaMemsetAsync(ws, 0, zero_bytes, s));
+    DevCounters *ctr = reinterpret_cast<DevCounters *>(ws + o_ctr);
+    unsigned *cnt = reinterpret_cast<unsigned *>(ws + o_cnt);
+    int64_t *cp = reinterpret_cast<int64_t *>(ws + o_cp);
+    int64_t *f = reinterpret_cast<int64_t *>(ws + o_f);
+    int64_t *fp = reinterpret_cast<int64_t *>(ws + o_fp);
+    int64_t *sp = reinterpret_cast<int64_t *>(ws + o_sp);
+    Prof pf(P_SPLIT, s);
+    if (A->nnz > 0) launch_col_hist(A0, cnt, nullptr, s);
+    scan_u32(cnt, m, cp, ws + o_st1, 0, s);
     if (n > 0) launch_analyze(A0, cp, 0, n, f, nullptr, 0, ctr, s);
-    scan_i64(f, n, fp, ScanOp::Identity, scan_tmp, 0, s);
-    int64_t *sp = ar.get<int64_t>(parts + 1);
+    scan_i64(f, n, fp, ScanOp::Identity, ws + o_st2, 0, s);
     launch_split(fp, n, parts, sp, s);
     check_launch("split");
     CK(cudaMemcpyAsync(split, sp, sizeof(int64_t) * (size_t)(parts + 1), cudaMemcpyDeviceToHost, s));
@@ -662,32 +760,40 @@ int rig_build_host(const rig_csr_t *Ah, int scale_rows, double drop_tol, uint32_
     cudaStream_t s = (cudaStream_t)stream;
     Arena ar(s);
     const int64_t n = Ah->nrows, nnz = Ah->nnz;
-    int64_t *rp = ar.get<int64_t>(n + 1);
-    int32_t *ci = ar.get<int32_t>(nnz);
-    double *v = ar.get<double>(nnz);
+    Layout L;
+    const size_t o_rp = L.add(sizeof(int64_t) * (size_t)(n + 1));
+    const size_t o_ci = L.add(sizeof(int32_t) * (size_t)nnz);
+    const size_t o_v = L.add(sizeof(double) * (size_t)nnz);
+    const size_t o_part = L.add(sizeof(int32_t) * (size_t)n);
+    const size_t o_cut = L.add(sizeof(double));
+    unsigned char *ws = ar.raw(L.bytes);
+    int64_t *rp = reinterpret_cast<int64_t *>(ws + o_rp);
+    int32_t *ci = reinterpret_cast<int32_t *>(ws + o_ci);
+    double *v = reinterpret_cast<double *>(ws + o_v);
+    int32_t *part = part_host ? reinterpret_cast<int32_t *>(ws + o_part) : nullptr;
+    double *cut_dev = reinterpret_cast<double *>(ws + o_cut);
     CK(cudaMemcpyAsync(rp, Ah->row_ptr, sizeof(int64_t) * (size_t)(n + 1), cudaMemcpyHostToDevice, s));
     if (nnz > 0) {
         CK(cudaMemcpyAsync(ci, Ah->col_idx, sizeof(int32_t) * (size_t)nnz, cudaMemcpyHostToDevice, s));
         CK(cudaMemcpyAsync(v, Ah->val, sizeof(double) * (size_t)nnz, cudaMemcpyHostToDevice, s));
     }
-    int32_t *part = nullptr;
-    if (part_host) {
-        part = ar.get<int32_t>(n);
-        CK(cudaMemcpyAsync(part, part_host, sizeof(int32_t) * (size_t)n, cudaMemcpyHostToDevice, s));
-    }
+    if (part) CK(cudaMemcpyAsync(part, part_host, sizeof(int32_t) * (size_t)n, cudaMemcpyHostToDevice, s));
     rig_csr_t Ad{n, Ah->ncols, nnz, rp, ci, v};
     rig_graph_t g{};
-    double *cut_dev = ar.get<double>(1);
     CutReq cr;
     cr.part = part;
     cr.K = K;
-    cr.n_global = n;
     cr.cut_dev = cut_dev;
     build_owned(&Ad, scale_rows, drop_tol, flags, 0, n, &g, s, part ? &cr : nullptr);
     struct Guard {
         rig_graph_t *g;
         cudaStream_t s;
-        ~Guard() { rig_graph_free(g, s); }
+        ~Guard() {
+            try {
+                free_owned(g, s);
+            } catch (...) {
+            }
+        }
     } guard{&g, s};
     if (g.nnz > capacity) {
         out_host->nnz = g.nnz;
@@ -701,9 +807,11 @@ int rig_build_host(const rig_csr_t *Ah, int scale_rows, double drop_tol, uint32_
     }
     if ((flags & RIG_FLAG_DIAG) && out_host->diag && n > 0)
         CK(cudaMemcpyAsync(out_host->diag, g.diag, sizeof(double) * (size_t)n, cudaMemcpyDeviceToHost, s));
-    double cut = std::nan("");
-    if (part) CK(cudaMemcpyAsync(&cut, cut_dev, sizeof(double), cudaMemcpyDeviceToHost, s));
+    HostStage *hs = host_stage();
+    if (part) CK(cudaMemcpyAsync(&hs->v[2], cut_dev, sizeof(double), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
+    double cut = std::nan("");
+    if (part) std::memcpy(&cut, &hs->v[2], sizeof(double));
     if (cut_host) *cut_host = cut;
     out_host->n = n;
     out_host->nnz = g.nnz;
