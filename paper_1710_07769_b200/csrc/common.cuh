@@ -137,6 +137,7 @@ struct NumArgs {
     double *cutp;
     int *bad_part;
     int *cut_used;  // this launch's number of written partials (= gridDim.x)
+    int stage_cap;  // merge path: staged graph entries per warp (set by the launcher)
 };
 
 // Neumaier-compensated running sum (compiled with --fmad=false).
@@ -168,6 +169,21 @@ __device__ __forceinline__ double block_tree_sum(double v) {
     const double r = red[0];
     __syncthreads();
     return r;
+}
+
+// Merge-path output staging (entries per warp), see stage_cap_for().
+constexpr int kMinStageCap = 256, kMaxStageCap = 1536;
+// Staging capacity from the mean products per row (P / rows): a 32-row tile
+// writes about 32 * nnz(C_i) <= 32 * f_i entries; stencil-like rows have
+// f_i ~ 2 nnz(C_i), so 0.6 * 32 * P/rows leaves headroom.  Tiles that do not
+// fit fall back to direct global stores (correct, slower).
+inline int stage_cap_for(int64_t products, int64_t rows) {
+    const double mean = rows > 0 ? (double)products / (double)rows : 0.0;
+    int64_t cap = (int64_t)(0.6 * 32.0 * mean) + 32;
+    cap = (cap + 31) / 32 * 32;
+    if (cap < kMinStageCap) cap = kMinStageCap;
+    if (cap > kMaxStageCap) cap = kMaxStageCap;
+    return (int)cap;
 }
 
 // Cut slots reserved per numeric launch in the fused-cut partials array.

@@ -72,44 +72,73 @@ void launch_col_hist(const Csr &A, unsigned *cnt, unsigned *rank, cudaStream_t s
 // ------------------------------------------------------------------ a1 + a2 (scatter)
 // a1: ss_i = fma-chain of a_ik^2 in ascending k from
 // +0.0; nrm_i = sqrt_rn(ss_i); a_hat = a /_rn nrm_i (DESIGN.md §3 R5).
-// Fused with the CSC scatter: each thread owns one row, so the scaled value
-// written to the CSR copy and to the CSC slot is the same double.
-// Slot of entry p in the CSC: cp[ci[p]] + rank[p] (rank from k_col_hist).
-__global__ void k_scale_scatter(Csr A, int scale, double *__restrict__ ahat, const int64_t *__restrict__ cp,
-                                const unsigned *__restrict__ rank, int32_t *ri, double *vt, int *err) {
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < A.nrows; i += stride) {
-        const int64_t s = A.rp[i], e = A.rp[i + 1];
+// Fused with the CSC scatter so the scaled value written to the CSR copy and
+// to the CSC slot is the same double.  Slot of entry p in the CSC:
+// cp[ci[p]] + rank[p] (rank from k_col_hist).
+// Warp-tile variant: a warp owns 32 consecutive rows.  Lane l computes the
+// norm of row r0+l (the ordered fma chain is per row and sequential), then the
+// warp walks the tile's entries [rp[r0], rp[r0+32]) 32 at a time: coalesced
+// loads of col / value / rank, coalesced a_hat stores, scattered CSC stores.
+__global__ void __launch_bounds__(256) k_scale_scatter_tile(Csr A, int scale, double *__restrict__ ahat,
+                                                            const int64_t *__restrict__ cp,
+                                                            const unsigned *__restrict__ rank, int32_t *ri,
+                                                            double *vt, int *err) {
+    const int l = lane_id();
+    const int64_t ntiles = (A.nrows + 31) / 32;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t tile = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; tile < ntiles; tile += nw) {
+        const int64_t r0 = tile * 32;
+        const int rows = (int)min((int64_t)32, A.nrows - r0);
+        const int64_t hi = A.rp[r0 + rows];
+        const int64_t my_s = l < rows ? A.rp[r0 + l] : hi;
+        const int64_t my_e = l < rows ? A.rp[r0 + l + 1] : hi;
         double nrm = 1.0;
-        if (scale) {
+        int bad = 0;
+        if (scale && l < rows) {
             double ss = +0.0;
-            for (int64_t p = s; p < e; ++p) {
+            for (int64_t p = my_s; p < my_e; ++p) {
                 const double a = A.v[p];
                 ss = __fma_rn(a, a, ss);
             }
-            if (!isfinite(ss)) {
-                atomicOr(err, kErrNonFinite);
-                continue;
-            }
-            if (ss == 0.0) {
-                atomicOr(err, kErrZeroRow);
-                continue;
-            }
-            nrm = __dsqrt_rn(ss);
+            if (!isfinite(ss))
+                bad = kErrNonFinite;
+            else if (ss == 0.0)
+                bad = kErrZeroRow;
+            else
+                nrm = __dsqrt_rn(ss);
         }
-        for (int64_t p = s; p < e; ++p) {
-            const double x = scale ? __ddiv_rn(A.v[p], nrm) : A.v[p];
-            if (scale) ahat[p] = x;
-            const int64_t q = cp[A.ci[p]] + rank[p];
-            ri[q] = (int32_t)i;
-            vt[q] = x;
+        if (bad) atomicOr(err, bad);
+        const int64_t lo = __shfl_sync(kFull, my_s, 0);
+        const int64_t last = __shfl_sync(kFull, my_s, 31);
+        for (int64_t base = lo; base < hi; base += 32) {
+            const int64_t p = base + l;
+            // row of entry p: (number of lanes with start <= p) - 1
+            int t = 0;
+#pragma unroll
+            for (int step = 16; step >= 1; step >>= 1) {
+                const int64_t v = __shfl_sync(kFull, my_s, t + step - 1);
+                if (v <= p) t += step;
+            }
+            if (t == 31 && last <= p) t = 32;
+            const int row = t > 0 ? t - 1 : 0;
+            const double rn = __shfl_sync(kFull, nrm, row);
+            if (p < hi) {
+                const double x = scale ? __ddiv_rn(A.v[p], rn) : A.v[p];
+                if (scale) ahat[p] = x;
+                const int64_t q = cp[A.ci[p]] + rank[p];
+                ri[q] = (int32_t)(r0 + row);
+                vt[q] = x;
+            }
         }
     }
 }
 
 void launch_scale_scatter(const Csr &A, int scale, double *ahat, const int64_t *cp, const unsigned *rank,
                           int32_t *ri, double *vt, int *err, cudaStream_t s) {
-    k_scale_scatter<<<grid_for(A.nrows, 128, 16), 128, 0, s>>>(A, scale, ahat, cp, rank, ri, vt, err);
+    int64_t g = (A.nrows + 255) / 256;  // 8 tiles of 32 rows per CTA
+    const int64_t cap = (int64_t)num_sms() * 8;
+    g = g < 1 ? 1 : (g > cap ? cap : g);
+    k_scale_scatter_tile<<<(unsigned)g, 256, 0, s>>>(A, scale, ahat, cp, rank, ri, vt, err);
     note_launch();
 }
 

@@ -133,7 +133,7 @@ __device__ __forceinline__ void num_merge_row(const NumArgs &a, int64_t i, int64
 
 constexpr int kMergeThreads = 256;
 constexpr int kMergeWarps = kMergeThreads / 32;
-constexpr int kStageCap = 448;  // staged graph entries per warp (12 B each)
+// staged graph entries per warp: NumArgs::stage_cap (dynamic shared memory)
 
 template <int RMAX, typename IdxT>
 __global__ void __launch_bounds__(kMergeThreads) k_sym_merge(SymArgs a) {
@@ -161,13 +161,15 @@ __global__ void __launch_bounds__(kMergeThreads) k_sym_merge(SymArgs a) {
 }
 
 // Each warp takes 32 consecutive rows (one per lane).  Their graph slots are
-// contiguous, so when they fit kStageCap the lanes write into shared memory
+// contiguous, so when they fit the stage capacity the lanes write into shared memory
 // and the warp streams the range out with coalesced stores.
 template <int RMAX, typename IdxT>
 __global__ void __launch_bounds__(kMergeThreads) k_num_merge(NumArgs a) {
-    __shared__ int32_t st_col[kMergeWarps][kStageCap];
-    __shared__ double st_w[kMergeWarps][kStageCap];
+    extern __shared__ __align__(16) unsigned char merge_smem[];
+    const int cap = a.stage_cap;
     const int w = threadIdx.x >> 5, l = lane_id();
+    double *st_wp = reinterpret_cast<double *>(merge_smem) + (size_t)w * cap;
+    int32_t *st_cp = reinterpret_cast<int32_t *>(merge_smem + (size_t)kMergeWarps * cap * sizeof(double)) + (size_t)w * cap;
     const int64_t nloc = a.re - a.rb;
     const int64_t ntiles = (nloc + 31) / 32;
     Comp cut;
@@ -179,14 +181,14 @@ __global__ void __launch_bounds__(kMergeThreads) k_num_merge(NumArgs a) {
         const int64_t r = r0 + l;
         const int64_t g0 = a.gptr[r0];
         const int64_t span = a.gptr[r0 + rows] - g0;
-        const bool staged = span <= kStageCap;
+        const bool staged = span <= cap;
         if (l < rows) {
             const int64_t i = a.rb + r;
             const int64_t s = a.A.rp[i];
             const int len = (int)min(a.A.rp[i + 1] - s, (int64_t)kMergeMaxLen + 1);
             const int64_t gr = a.gptr[r], ub = a.gptr[r + 1] - gr;
-            int32_t *oc = staged ? &st_col[w][gr - g0] : a.gcol + gr;
-            double *ow = staged ? &st_w[w][gr - g0] : a.gw + gr;
+            int32_t *oc = staged ? st_cp + (gr - g0) : a.gcol + gr;
+            double *ow = staged ? st_wp + (gr - g0) : a.gw + gr;
             int32_t pi = 0;
             if (a.part) {
                 pi = a.part[i];
@@ -210,8 +212,8 @@ __global__ void __launch_bounds__(kMergeThreads) k_num_merge(NumArgs a) {
         if (staged) {
             __syncwarp();
             for (int64_t t = l; t < span; t += 32) {
-                a.gcol[g0 + t] = st_col[w][t];
-                a.gw[g0 + t] = st_w[w][t];
+                a.gcol[g0 + t] = st_cp[t];
+                a.gw[g0 + t] = st_wp[t];
             }
             __syncwarp();
         }
@@ -304,7 +306,14 @@ static void launch_merge_t(const SymArgs *sa, const NumArgs *na, cudaStream_t s)
         const int64_t nloc = na->re - na->rb;
         int64_t g = (nloc + kMergeThreads - 1) / kMergeThreads;
         g = g < 1 ? 1 : (g > (int64_t)sms() * 16 ? (int64_t)sms() * 16 : g);
-        k_num_merge<RMAX, IdxT><<<(unsigned)g, kMergeThreads, 0, s>>>(*na);
+        const size_t smem = (size_t)kMergeWarps * (size_t)na->stage_cap * (sizeof(double) + sizeof(int32_t));
+        static bool attr = false;
+        if (!attr) {
+            cudaFuncSetAttribute(k_num_merge<RMAX, IdxT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)(kMergeWarps * kMaxStageCap * (sizeof(double) + sizeof(int32_t))));
+            attr = true;
+        }
+        k_num_merge<RMAX, IdxT><<<(unsigned)g, kMergeThreads, smem, s>>>(*na);
     }
     note_launch();
 }

@@ -396,7 +396,8 @@ static int64_t plan_numeric(rig_plan *p, int32_t *gcol, double *gw, double *diag
                    cut ? cut->K : 0,
                    cutp,
                    badp,
-                   used};
+                   used,
+                   stage_cap_for(p->h.products, p->nloc)};
         if (p->nloc > 0) launch_num_merge(na, p->h.max_len, s);
         if (p->h.n_mid > 0) {
             // numeric bin sizes are device-side; empty bins exit immediately
