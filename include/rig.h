@@ -181,6 +181,12 @@ RIG_API int rig_build_host(const rig_csr_t *A_host, int scale_rows, double drop_
  * on.  rig_profile_read waits for those events and returns, per pass id in
  * [0, RIG_NPASS), the summed milliseconds and the number of occurrences since
  * the previous read (then clears them).  Pass names: rig_pass_name. */
+/* The simple API (rig_build*, rig_build_host) keeps its internal work
+ * buffers in a grow-only cache per calling thread, device and stream, reused
+ * in stream order by the next build.  rig_trim releases the calling thread's
+ * cache (stream-ordered frees). */
+RIG_API int rig_trim(void);
+
 #define RIG_NPASS 12
 RIG_API int rig_profile_enable(int on);
 RIG_API int rig_profile_read(double *ms, int64_t *count);

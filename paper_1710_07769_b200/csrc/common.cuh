@@ -38,11 +38,14 @@ struct Csr {
     const double *v;  // scaled values a_hat when scale_rows
 };
 
+// CSC of A_hat with one sentinel per column: column k occupies
+// [cp[k] + k, cp[k+1] + k) (rows ascending) and ri[cp[k+1] + k] = INT_MAX.
 struct Csc {
-    const int64_t *cp;  // [ncols+1]
-    const int32_t *ri;  // [nnz] ascending within each column
-    const double *vt;   // [nnz] bit-identical to the CSR value of (i,k)
+    const int64_t *cp;  // [ncols+1] entry counts prefix (without sentinels)
+    const int32_t *ri;  // [nnz + ncols]
+    const double *vt;   // [nnz + ncols] bit-identical to the CSR value of (i,k)
 };
+__device__ __forceinline__ int64_t csc_begin(const Csc &T, int k) { return T.cp[k] + k; }
 
 // Counters written by the device and read back by the host at a sync.
 constexpr int kSymBins = kNumSymBins + 1;  // + huge
@@ -96,10 +99,11 @@ int num_sms();
 // k_prep.cu
 void launch_validate(const Csr &A, int *err, cudaStream_t s);
 void launch_col_hist(const Csr &A, unsigned *cnt, unsigned *rank /*nullable*/, cudaStream_t s);
-void launch_scale_scatter(const Csr &A, int scale, double *ahat, const int64_t *cp, const unsigned *rank,
-                          int32_t *ri, double *vt, int *err, cudaStream_t s);
-void launch_col_sort(int64_t ncols, const int64_t *cp, int32_t *ri, double *vt, int32_t *long_list,
-                     unsigned *long_count, cudaStream_t s);
+// k_transpose.cu: bucketed a1 + a2 (see there for the CSC layout with sentinels)
+int64_t transpose_buckets(int64_t nnz, int64_t ncols);
+constexpr size_t kTransposeRecBytes = 16;
+void launch_transpose(const Csr &A, int scale, const int64_t *cp, double *ahat, unsigned long long *bcur,
+                      void *rec, unsigned *gcur, int32_t *ri, double *vt, int *err, cudaStream_t s);
 void launch_analyze(const Csr &A, const int64_t *cp, int64_t rb, int64_t re, int64_t *f, int32_t *sym_lists,
                     int64_t cap, DevCounters *ctr, cudaStream_t s);
 void launch_bin_num(const int32_t *sym_lists, int64_t sym_cap, const DevCounters *ctr, const int64_t *nnzc,

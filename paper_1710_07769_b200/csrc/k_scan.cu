@@ -10,6 +10,8 @@ constexpr int kScanThreads = 256;
 constexpr int kScanItems = 16;
 constexpr int64_t kTile = (int64_t)kScanThreads * kScanItems;
 
+__device__ __forceinline__ int pad(int i) { return i + (i >> 4); }
+
 template <typename T>
 __device__ __forceinline__ int64_t scan_load(const T *in, int64_t i, ScanOp op) {
     int64_t x = (int64_t)in[i];
@@ -60,7 +62,7 @@ template <typename T>
 __global__ void __launch_bounds__(kScanThreads) k_tile_scan(const T *__restrict__ in, int64_t n, ScanOp op,
                                                             const int64_t *__restrict__ tile_sums, int64_t ntiles,
                                                             int64_t *out) {
-    __shared__ int64_t sv[kTile];
+    __shared__ int64_t sv[kTile + kTile / 16];  // padded: conflict-free blocked <-> striped transpose
     __shared__ int64_t tot_s, pre_s;
     // prefix of the earlier tiles' totals
     int64_t pre = 0;
@@ -72,7 +74,7 @@ __global__ void __launch_bounds__(kScanThreads) k_tile_scan(const T *__restrict_
 #pragma unroll
     for (int j = 0; j < kScanItems; ++j) {  // coalesced blocked load
         const int64_t i = base + (int64_t)j * kScanThreads + threadIdx.x;
-        sv[j * kScanThreads + threadIdx.x] = i < n ? scan_load(in, i, op) : 0;
+        sv[pad(j * kScanThreads + threadIdx.x)] = i < n ? scan_load(in, i, op) : 0;
     }
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -84,21 +86,21 @@ __global__ void __launch_bounds__(kScanThreads) k_tile_scan(const T *__restrict_
     int64_t s = 0;
 #pragma unroll
     for (int j = 0; j < kScanItems; ++j) {
-        v[j] = sv[threadIdx.x * kScanItems + j];
+        v[j] = sv[pad(threadIdx.x * kScanItems + j)];
         s += v[j];
     }
     const int64_t ex = block_excl_scan(s, &tot_s);  // (contains __syncthreads: pre_s visible after)
     int64_t run = pre_s + ex;
 #pragma unroll
     for (int j = 0; j < kScanItems; ++j) {
-        sv[threadIdx.x * kScanItems + j] = run;
+        sv[pad(threadIdx.x * kScanItems + j)] = run;
         run += v[j];
     }
     __syncthreads();
 #pragma unroll
     for (int j = 0; j < kScanItems; ++j) {
         const int64_t i = base + (int64_t)j * kScanThreads + threadIdx.x;
-        if (i < n) out[i] = sv[j * kScanThreads + threadIdx.x];
+        if (i < n) out[i] = sv[pad(j * kScanThreads + threadIdx.x)];
     }
     if (blockIdx.x == ntiles - 1 && threadIdx.x == 0) out[n] = pre_s + tot_s;
 }

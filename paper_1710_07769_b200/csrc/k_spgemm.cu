@@ -27,21 +27,22 @@ static int g_sms_cache = 0;
 // ascending) are merged; for the current minimum j the runs holding it are
 // folded in ascending k: c_ij = fma(a_ik, a_jk, c_ij) -- the ordered chain.
 // IdxT: int32 CSC offsets when nnz < 2^31 (fewer registers), else int64.
+// Columns end in an INT_MAX sentinel (csc_begin), so a run needs no end bound.
 template <int R, typename IdxT>
 __device__ __forceinline__ int64_t sym_merge_row(const Csr &A, const Csc &T, int64_t s) {
     int32_t h[R];
-    IdxT q[R], qe[R];
+    IdxT q[R];
     int64_t f = 0;
 #pragma unroll
     for (int t = 0; t < R; ++t) {
         const int k = A.ci[s + t];
-        q[t] = (IdxT)T.cp[k];
-        qe[t] = (IdxT)T.cp[k + 1];
-        f += qe[t] - q[t];
+        const int64_t c0 = T.cp[k], c1 = T.cp[k + 1];
+        q[t] = (IdxT)(c0 + k);
+        f += c1 - c0;
     }
     if (f > kMergeMaxF) return -1;
 #pragma unroll
-    for (int t = 0; t < R; ++t) h[t] = q[t] < qe[t] ? T.ri[q[t]] : INT_MAX;
+    for (int t = 0; t < R; ++t) h[t] = T.ri[q[t]];
     int64_t cnt = 0;
     while (true) {
         int m = h[0];
@@ -51,10 +52,7 @@ __device__ __forceinline__ int64_t sym_merge_row(const Csr &A, const Csc &T, int
         ++cnt;
 #pragma unroll
         for (int t = 0; t < R; ++t) {
-            if (h[t] == m) {
-                ++q[t];
-                h[t] = q[t] < qe[t] ? T.ri[q[t]] : INT_MAX;
-            }
+            if (h[t] == m) h[t] = T.ri[++q[t]];
         }
     }
     return cnt;
@@ -67,27 +65,22 @@ template <int R, typename IdxT>
 __device__ __forceinline__ void num_merge_row(const NumArgs &a, int64_t i, int64_t r, int64_t s, int32_t *oc,
                                               double *ow, int64_t ub, Comp &cut, int32_t pi, int &badp) {
     int32_t h[R];
-    IdxT q[R], qe[R];
+    IdxT q[R];
     double av[R], hv[R];
     int64_t f = 0;
 #pragma unroll
     for (int t = 0; t < R; ++t) {
         const int k = a.A.ci[s + t];
         av[t] = a.A.v[s + t];
-        q[t] = (IdxT)a.T.cp[k];
-        qe[t] = (IdxT)a.T.cp[k + 1];
-        f += qe[t] - q[t];
+        const int64_t c0 = a.T.cp[k], c1 = a.T.cp[k + 1];
+        q[t] = (IdxT)(c0 + k);
+        f += c1 - c0;
     }
     if (f > kMergeMaxF) return;
 #pragma unroll
     for (int t = 0; t < R; ++t) {
-        if (q[t] < qe[t]) {
-            h[t] = a.T.ri[q[t]];
-            hv[t] = a.T.vt[q[t]];
-        } else {
-            h[t] = INT_MAX;
-            hv[t] = 0.0;
-        }
+        h[t] = a.T.ri[q[t]];
+        hv[t] = a.T.vt[q[t]];
     }
     int64_t o = 0;
     while (true) {
@@ -101,12 +94,8 @@ __device__ __forceinline__ void num_merge_row(const NumArgs &a, int64_t i, int64
             if (h[t] == m) {  // runs visited in ascending k: the ordered chain
                 acc = __fma_rn(av[t], hv[t], acc);
                 ++q[t];
-                if (q[t] < qe[t]) {
-                    h[t] = a.T.ri[q[t]];
-                    hv[t] = a.T.vt[q[t]];
-                } else {
-                    h[t] = INT_MAX;
-                }
+                h[t] = a.T.ri[q[t]];  // the column's sentinel stops the run
+                hv[t] = a.T.vt[q[t]];
             }
         }
         if ((int64_t)m == i) {
@@ -247,9 +236,13 @@ __global__ void __launch_bounds__(kMergeThreads) k_analyze_sym(SymArgs a, int32_
         const int64_t i = a.rb + r;
         const int64_t s = a.A.rp[i], e = a.A.rp[i + 1];
         int64_t fi = 0;
-        for (int64_t p = s; p < e; ++p) {
-            const int k = a.A.ci[p];
-            fi += a.T.cp[k + 1] - a.T.cp[k];
+        for (int64_t p0 = s; p0 < e; p0 += 8) {  // 8 independent gathers in flight
+            int k[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) k[u] = p0 + u < e ? a.A.ci[p0 + u] : -1;
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+                if (k[u] >= 0) fi += a.T.cp[k[u] + 1] - a.T.cp[k[u]];
         }
         local += fi;
         const int len = (int)min(e - s, (int64_t)kMergeMaxLen + 1);
@@ -366,8 +359,9 @@ __device__ __forceinline__ Batch load_batch(const Csr &A, const Csc &T, int64_t 
     b.a = 0.0;
     if (p < e) {
         const int k = A.ci[p];
-        b.cs = T.cp[k];
-        cl = T.cp[k + 1] - b.cs;
+        const int64_t c0 = T.cp[k];
+        cl = T.cp[k + 1] - c0;
+        b.cs = c0 + k;  // sentinel layout (csc_begin)
         if (need_a) b.a = A.v[p];
     }
     b.incl = warp_incl_scan(cl);
@@ -742,8 +736,9 @@ __device__ __forceinline__ int64_t block_batch(const Csr &A, const Csc &T, int64
     double av = 0.0;
     if (p < e) {
         const int k = A.ci[p];
-        cs = T.cp[k];
-        cl = T.cp[k + 1] - cs;
+        const int64_t c0 = T.cp[k];
+        cl = T.cp[k + 1] - c0;
+        cs = c0 + k;  // sentinel layout (csc_begin)
         if (s_a) av = A.v[p];
     }
     const int64_t inc = warp_incl_scan(cl);

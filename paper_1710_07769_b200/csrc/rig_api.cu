@@ -182,6 +182,48 @@ struct Arena {
     }
 };
 
+// Grow-only per-thread workspace cache for the simple API's internal buffers
+// (phase A, phase B, numeric temporaries): consecutive builds on the same
+// device and stream reuse them in stream order, so the hot loop makes no
+// allocator calls besides the returned graph.  rig_trim() releases them.
+struct WsCache {
+    int dev = -1;
+    void *p[3] = {nullptr, nullptr, nullptr};
+    size_t n[3] = {0, 0, 0};
+    cudaStream_t s[3] = {nullptr, nullptr, nullptr};
+};
+static thread_local WsCache t_ws;
+
+static void ws_trim() {
+    for (int k = 0; k < 3; ++k) {
+        if (t_ws.p[k]) cudaFreeAsync(t_ws.p[k], t_ws.s[k]);
+        t_ws.p[k] = nullptr;
+        t_ws.n[k] = 0;
+    }
+}
+
+static unsigned char *ws_get(int slot, size_t bytes, cudaStream_t s) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (t_ws.dev != dev) {
+        if (t_ws.dev >= 0) {  // another device: release on that device
+            int cur = dev;
+            cudaSetDevice(t_ws.dev);
+            ws_trim();
+            cudaSetDevice(cur);
+        }
+        t_ws.dev = dev;
+    }
+    if (t_ws.p[slot] && t_ws.n[slot] >= bytes && t_ws.s[slot] == s) return static_cast<unsigned char *>(t_ws.p[slot]);
+    if (t_ws.p[slot]) CK(cudaFreeAsync(t_ws.p[slot], t_ws.s[slot]));
+    t_ws.p[slot] = nullptr;
+    const size_t want = bytes + bytes / 8 + 4096;  // headroom for slightly larger inputs
+    CK(cudaMallocAsync(&t_ws.p[slot], want, s));
+    t_ws.n[slot] = want;
+    t_ws.s[slot] = s;
+    return static_cast<unsigned char *>(t_ws.p[slot]);
+}
+
 // Library-owned graphs: row_ptr and the (col, w, diag) block are two
 // allocations; rig_graph_free looks the block up by row_ptr.
 static std::mutex g_own_mu;
@@ -233,6 +275,7 @@ struct rig_plan {
     void *huge_scratch = nullptr;
     int huge_slots_n = 0;
     int64_t nnz_upper = 0;
+    bool cached = false;  // simple API: internal buffers from the per-thread cache
     explicit rig_plan(cudaStream_t st) : s(st), arena(st) {}
 };
 
@@ -249,26 +292,25 @@ static void plan_build(rig_plan *p, const rig_csr_t *Ain, int64_t *gptr_out, boo
     const size_t o_cnt = L.add(sizeof(unsigned) * (size_t)m);
     const size_t o_st1 = L.add(scan_tmp_bytes(m));
     const size_t o_st2 = L.add(scan_tmp_bytes(nloc));
+    const size_t o_bcur = L.add(sizeof(unsigned long long) * (size_t)transpose_buckets(nnz, m));
+    const size_t o_gcur = L.add(sizeof(unsigned) * (size_t)m);
     const size_t zero_bytes = L.bytes;
     const size_t o_cp = L.add(sizeof(int64_t) * (size_t)(m + 1));
-    const size_t o_rank = L.add(sizeof(unsigned) * (size_t)nnz);
+    const size_t o_rec = L.add(kTransposeRecBytes * (size_t)nnz);
     const size_t o_ahat = p->scale ? L.add(sizeof(double) * (size_t)nnz) : 0;
-    const size_t o_ri = L.add(sizeof(int32_t) * (size_t)nnz);
-    const size_t o_vt = L.add(sizeof(double) * (size_t)nnz);
-    const size_t o_long = L.add(sizeof(int32_t) * (size_t)m);
+    const size_t o_ri = L.add(sizeof(int32_t) * (size_t)(nnz + m));  // + one sentinel per column
+    const size_t o_vt = L.add(sizeof(double) * (size_t)(nnz + m));
     const size_t o_sym = L.add(sizeof(int32_t) * (size_t)kSymBins * (size_t)std::max<int64_t>(nloc, 1));
     const size_t o_nnzc = L.add(sizeof(int64_t) * (size_t)nloc);
     const size_t o_gptr = gptr_out ? 0 : L.add(sizeof(int64_t) * (size_t)(nloc + 1));
-    unsigned char *ws = p->arena.raw(L.bytes);
+    unsigned char *ws = p->cached ? ws_get(0, L.bytes, s) : p->arena.raw(L.bytes);
     CK(cudaMemsetAsync(ws, 0, zero_bytes, s));
     p->ctr = reinterpret_cast<DevCounters *>(ws + o_ctr);
     unsigned *cnt = reinterpret_cast<unsigned *>(ws + o_cnt);
     int64_t *cp = reinterpret_cast<int64_t *>(ws + o_cp);
-    unsigned *rank = reinterpret_cast<unsigned *>(ws + o_rank);
     double *ahat = p->scale ? reinterpret_cast<double *>(ws + o_ahat) : nullptr;
     int32_t *ri = reinterpret_cast<int32_t *>(ws + o_ri);
     double *vt = reinterpret_cast<double *>(ws + o_vt);
-    int32_t *long_list = reinterpret_cast<int32_t *>(ws + o_long);
     p->sym_lists = reinterpret_cast<int32_t *>(ws + o_sym);
     p->nnzc = reinterpret_cast<int64_t *>(ws + o_nnzc);
     p->gptr_ub = gptr_out ? gptr_out : reinterpret_cast<int64_t *>(ws + o_gptr);
@@ -285,20 +327,17 @@ static void plan_build(rig_plan *p, const rig_csr_t *Ain, int64_t *gptr_out, boo
         const int err = hs->ctr.err;
         if (err) throw Error(err_to_code(err), err_msg(err_to_code(err)));
     }
-    // a2: column counts + arrival ranks -> col_ptr
+    // a2: column counts -> col_ptr
     {
         Prof pf(P_COLPTR, s);
-        if (nnz > 0) launch_col_hist(A0, cnt, rank, s);
+        if (nnz > 0) launch_col_hist(A0, cnt, nullptr, s);
         scan_u32(cnt, m, cp, ws + o_st1, 0, s);
     }
-    // a1 + a2: scale rows (optional) and scatter into the CSC
-    if (n > 0) {
+    // a1 + a2: scale rows (optional), bucketed transpose into the CSC
+    {
         Prof pf(P_SCATTER, s);
-        launch_scale_scatter(A0, p->scale, ahat, cp, rank, ri, vt, &p->ctr->err, s);
-    }
-    if (m > 0) {
-        Prof pf(P_COLSORT, s);
-        launch_col_sort(m, cp, ri, vt, long_list, &p->ctr->long_cols, s);
+        launch_transpose(A0, p->scale, cp, ahat, reinterpret_cast<unsigned long long *>(ws + o_bcur), ws + o_rec,
+                         reinterpret_cast<unsigned *>(ws + o_gcur), ri, vt, &p->ctr->err, s);
     }
     check_launch("prep");
     p->A = Csr{n, m, nnz, Ain->row_ptr, Ain->col_idx, p->scale ? ahat : Ain->val};
@@ -330,7 +369,7 @@ static void plan_build(rig_plan *p, const rig_csr_t *Ain, int64_t *gptr_out, boo
             huge_bytes = huge_scratch_bytes(n, p->huge_slots_n, true);
             o_huge = LB.add(huge_bytes);
         }
-        unsigned char *wb = p->arena.raw(LB.bytes);
+        unsigned char *wb = p->cached ? ws_get(1, LB.bytes, s) : p->arena.raw(LB.bytes);
         p->num_lists = reinterpret_cast<int32_t *>(wb + o_num);
         if (n_big > 0) {
             p->huge_scratch = wb + o_huge;
@@ -374,7 +413,7 @@ static int64_t plan_numeric(rig_plan *p, int32_t *gcol, double *gw, double *diag
     const size_t o_used = L.add(sizeof(int) * (kCutLaunches + 1));
     const size_t zero_bytes = L.bytes;
     const size_t o_cutp = cut ? L.add(sizeof(double) * (size_t)kCutLaunches * kCutSlotsPerLaunch) : 0;
-    unsigned char *wn = tmp_arena.raw(L.bytes);
+    unsigned char *wn = p->cached ? ws_get(2, L.bytes, s) : tmp_arena.raw(L.bytes);
     CK(cudaMemsetAsync(wn, 0, zero_bytes, s));
     int *holes_d = reinterpret_cast<int *>(wn + o_holes);
     int *used = reinterpret_cast<int *>(wn + o_used);
@@ -529,6 +568,7 @@ static void build_owned(const rig_csr_t *A, int scale_rows, double drop_tol, uin
     if (!out) throw Error(RIG_ERR_INVALID, "out is NULL");
     std::memset(out, 0, sizeof(*out));
     rig_plan *p = new_plan(A, scale_rows, drop_tol, flags, rb, re, s);
+    p->cached = true;
     Arena tmp(s);
     int64_t *rp = nullptr;
     unsigned char *block = nullptr;
@@ -601,6 +641,13 @@ int rig_profile_read(double *ms, int64_t *count) {
 }
 
 const char *rig_pass_name(int pass) { return (pass >= 0 && pass < RIG_NPASS) ? kPassNames[pass] : "?"; }
+
+int rig_trim(void) {
+    ABI_BEGIN
+    ws_trim();
+    return RIG_OK;
+    ABI_END
+}
 uint64_t rig_launch_count(void) { return g_launches.load(); }
 const char *rig_version(void) { return "librig 0.2 (sm_100a)"; }
 
