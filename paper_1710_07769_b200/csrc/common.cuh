@@ -106,7 +106,7 @@ void launch_transpose(const Csr &A, int scale, const int64_t *cp, double *ahat, 
                       void *rec, unsigned *gcur, int32_t *ri, double *vt, int *err, cudaStream_t s);
 void launch_analyze(const Csr &A, const int64_t *cp, int64_t rb, int64_t re, int64_t *f, int32_t *sym_lists,
                     int64_t cap, DevCounters *ctr, cudaStream_t s);
-void launch_bin_num(const int32_t *sym_lists, int64_t sym_cap, const DevCounters *ctr, const int64_t *nnzc,
+void launch_bin_num(const int32_t *sym_lists, int64_t sym_cap, const DevCounters *ctr, const int32_t *farc,
                     int64_t rb, int32_t *num_lists, int64_t num_cap, int64_t *num_count, cudaStream_t s);
 
 // k_scan.cu: out[0..n] = exclusive prefix of in[0..n-1] (out[n] = total).
@@ -122,6 +122,7 @@ struct SymArgs {
     Csc T;
     int64_t rb, re;
     int64_t *nnzc;  // [re-rb]
+    int32_t *farc;  // [re-rb] distinct far keys (warp path; numeric binning)
 };
 struct NumArgs {
     Csr A;
@@ -205,6 +206,7 @@ void launch_num_warp(const NumArgs &a, const int32_t *lists, int64_t list_cap, c
                      const int64_t *hcounts, cudaStream_t s);
 // huge rows: CTA per row, dense accumulator + bitmap in global scratch
 size_t huge_scratch_bytes(int64_t nrows, int slots, bool numeric);
+size_t huge_bitmap_bytes(int64_t nrows, int slots);  // zeroed prefix of the scratch
 int huge_slots(int64_t nrows, int64_t n_huge);
 void launch_sym_huge(const SymArgs &a, const int32_t *list, const int64_t *count, int slots, void *scratch,
                      cudaStream_t s);

@@ -129,14 +129,14 @@ void launch_analyze(const Csr &A, const int64_t *cp, int64_t rb, int64_t re, int
 // Numeric bins by nnzC_i: table T = 2^ceil(log2(2 nnzC_i)) in [64, 2048];
 // larger -> huge bin (index 6).
 __global__ void k_bin_num(const int32_t *__restrict__ sym_lists, int64_t sym_cap, const DevCounters *ctr,
-                          const int64_t *__restrict__ nnzc, int64_t rb, int32_t *num_lists, int64_t num_cap,
+                          const int32_t *__restrict__ farc, int64_t rb, int32_t *num_lists, int64_t num_cap,
                           int64_t *num_count) {
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int b = 0; b < kSymBins; ++b) {
         const int64_t n = ctr->sym_count[b];
         for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += stride) {
             const int32_t i = sym_lists[b * sym_cap + t];
-            int lg = ceil_log2_2x(nnzc[i - rb]);
+            int lg = ceil_log2_2x(farc[i - rb]);
             if (lg < kNumBinMinLog) lg = kNumBinMinLog;
             const int nb = lg > kNumBinMaxLog ? kNumNumBins : lg - kNumBinMinLog;
             const unsigned long long pos = atomicAdd((unsigned long long *)&num_count[nb], 1ull);
@@ -145,9 +145,9 @@ __global__ void k_bin_num(const int32_t *__restrict__ sym_lists, int64_t sym_cap
     }
 }
 
-void launch_bin_num(const int32_t *sym_lists, int64_t sym_cap, const DevCounters *ctr, const int64_t *nnzc,
+void launch_bin_num(const int32_t *sym_lists, int64_t sym_cap, const DevCounters *ctr, const int32_t *farc,
                     int64_t rb, int32_t *num_lists, int64_t num_cap, int64_t *num_count, cudaStream_t s) {
-    k_bin_num<<<grid_for(num_cap, 256), 256, 0, s>>>(sym_lists, sym_cap, ctr, nnzc, rb, num_lists, num_cap,
+    k_bin_num<<<grid_for(num_cap, 256), 256, 0, s>>>(sym_lists, sym_cap, ctr, farc, rb, num_lists, num_cap,
                                                       num_count);
     note_launch();
 }

@@ -381,12 +381,50 @@ __device__ __forceinline__ int find_seg(const Batch &b, int64_t pp) {
     return t;
 }
 
+// One product per lane for the chunk [c0, c0+32) of a batch.  The lane's
+// segment (row entry) comes from an OR-reduced bitmask of the segment starts
+// that fall inside the chunk -- no shuffle search.
+struct Chunk {
+    bool valid;
+    int j;
+    double b;  // a_hat_jk
+    double a;  // a_hat_ik
+};
+
+template <bool NEED_VAL>
+__device__ __forceinline__ Chunk fetch_chunk(const Csc &T, const Batch &b, int64_t c0) {
+    const int l = lane_id();
+    const int64_t rel = b.excl - c0;
+    const unsigned starts = __reduce_or_sync(kFull, (rel > 0 && rel < 32) ? (1u << (int)rel) : 0u);
+    const int seg0 = __popc(__ballot_sync(kFull, b.incl <= c0));
+    const int seg = (seg0 + __popc(starts & ((2u << l) - 1u))) & 31;
+    const int64_t pp = c0 + l;
+    Chunk c;
+    c.valid = pp < b.total;
+    const int64_t q = __shfl_sync(kFull, b.cs - b.excl, seg) + pp;
+    c.a = NEED_VAL ? shfl_d(b.a, seg) : 0.0;
+    c.j = c.valid ? T.ri[q] : -2 - l;
+    c.b = (NEED_VAL && c.valid) ? T.vt[q] : 0.0;
+    return c;
+}
+
 __device__ __forceinline__ unsigned hash_key(int j, int logt) {
     return ((unsigned)j * 0x9E3779B1u) >> (32 - logt);
 }
 
-// ======================================================== warp-hash symbolic
-constexpr int kWarpHashThreads = 256;
+// ======================================================== warp paths
+// Rows off the merge path.  Keys j inside the row's window
+// [i - kWinHalf, i + kWinHalf) go to a direct-mapped window (occupancy bitmap
+// + values): no hashing, and already in order for the output.  Other ("far")
+// keys use an open-addressing table in shared memory.  Banded rows (config 5)
+// keep most keys in the window; random rows (config 4) keep most in the table.
+// Chunks are software-pipelined: the next chunk's gathers are issued before
+// the current chunk is accumulated.
+constexpr int kWarpHashThreads = 128;  // 4 warps per CTA, many CTAs per SM
+constexpr int kWinHalf = 128;
+constexpr int kWin = 2 * kWinHalf;
+constexpr int kWinWords = kWin / 32;
+constexpr int kFarHuge = 1 << 30;  // farc marker: route the numeric pass to the huge path
 
 template <int LOGT>
 __global__ void __launch_bounds__(kWarpHashThreads) k_sym_warp(SymArgs a, const int32_t *__restrict__ list,
@@ -394,40 +432,63 @@ __global__ void __launch_bounds__(kWarpHashThreads) k_sym_warp(SymArgs a, const 
     constexpr int T = 1 << LOGT;
     extern __shared__ int32_t sym_tab[];
     const int w = threadIdx.x >> 5, l = lane_id();
-    int32_t *keys = sym_tab + w * T;
+    int32_t *keys = sym_tab + w * (T + kWinWords);
+    unsigned *wbits = reinterpret_cast<unsigned *>(keys + T);
     const int64_t n = *count;
     for (int s = l; s < T; s += 32) keys[s] = -1;
+    if (l < kWinWords) wbits[l] = 0u;
     __syncwarp();
     const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
     for (int64_t idx = blockIdx.x * (int64_t)(blockDim.x >> 5) + w; idx < n; idx += nw) {
         const int64_t i = list[idx];
         const int64_t s = a.A.rp[i], e = a.A.rp[i + 1];
-        int cnt = 0;
+        const int64_t wbase = i - kWinHalf;
+        int nnear = 0, nfar = 0;
         for (int64_t base = s; base < e; base += 32) {
             const Batch b = load_batch(a.A, a.T, base, e, false);
+            Chunk cur = fetch_chunk<false>(a.T, b, 0);
             for (int64_t c0 = 0; c0 < b.total; c0 += 32) {
-                const int64_t pp = c0 + l;
-                const int t = find_seg(b, pp);
-                const int64_t q = __shfl_sync(kFull, b.cs, t) + pp - __shfl_sync(kFull, b.excl, t);
-                if (pp < b.total) {
-                    const int j = a.T.ri[q];
-                    unsigned sl = hash_key(j, LOGT);
+                Chunk nxt = cur;
+                if (c0 + 32 < b.total) nxt = fetch_chunk<false>(a.T, b, c0 + 32);
+                const int64_t d = (int64_t)cur.j - wbase;
+                const bool near = cur.valid && d >= 0 && d < kWin;
+                // window: one OR per touched bitmap word (no same-word atomics)
+                unsigned touched = __reduce_or_sync(kFull, near ? (1u << (int)(d >> 5)) : 0u);
+                while (touched) {
+                    const int wd = __ffs(touched) - 1;
+                    touched &= touched - 1;
+                    const unsigned m = __reduce_or_sync(kFull, (near && (d >> 5) == wd) ? (1u << (int)(d & 31)) : 0u);
+                    if (l == 0) {
+                        const unsigned old = wbits[wd];
+                        nnear += __popc(m & ~old);
+                        wbits[wd] = old | m;
+                    }
+                }
+                if (cur.valid && !near) {
+                    unsigned sl = hash_key(cur.j, LOGT);
                     while (true) {
-                        const int prev = atomicCAS(&keys[sl], -1, j);
+                        const int prev = atomicCAS(&keys[sl], -1, cur.j);
                         if (prev == -1) {
-                            ++cnt;
+                            ++nfar;
                             break;
                         }
-                        if (prev == j) break;
+                        if (prev == cur.j) break;
                         sl = (sl + 1) & (T - 1);
                     }
                 }
+                __syncwarp();
+                cur = nxt;
             }
         }
-        cnt = warp_sum(cnt);
-        if (l == 0) a.nnzc[i - a.rb] = cnt;
+        nnear = warp_sum(nnear);
+        nfar = warp_sum(nfar);
+        if (l == 0) {
+            a.nnzc[i - a.rb] = nnear + nfar;
+            a.farc[i - a.rb] = nfar;
+        }
         __syncwarp();
         for (int s2 = l; s2 < T; s2 += 32) keys[s2] = -1;
+        if (l < kWinWords) wbits[l] = 0u;
         __syncwarp();
     }
 }
@@ -435,14 +496,14 @@ __global__ void __launch_bounds__(kWarpHashThreads) k_sym_warp(SymArgs a, const 
 template <int LOGT>
 static void launch_sym_warp_t(const SymArgs &a, const int32_t *list, const int64_t *count, cudaStream_t s) {
     constexpr int T = 1 << LOGT;
-    const size_t smem = (size_t)(kWarpHashThreads / 32) * T * sizeof(int32_t);
+    const size_t smem = (size_t)(kWarpHashThreads / 32) * (T + kWinWords) * sizeof(int32_t);
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(k_sym_warp<LOGT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         attr = true;
     }
     int per_sm = (int)((200 * 1024) / smem);
-    per_sm = per_sm < 1 ? 1 : (per_sm > 8 ? 8 : per_sm);
+    per_sm = per_sm < 1 ? 1 : (per_sm > 16 ? 16 : per_sm);
     k_sym_warp<LOGT><<<sms() * per_sm, kWarpHashThreads, smem, s>>>(a, list, count);
     note_launch();
 }
@@ -458,31 +519,33 @@ void launch_sym_warp(const SymArgs &a, const int32_t *lists, int64_t cap, const 
     if (hcounts[6]) launch_sym_warp_t<12>(a, lists + 6 * cap, counts + 6, s);
 }
 
-// ======================================================== warp-hash numeric
-// Per warp (T = 2^LOGT slots, at most T/2 live keys since T >= 2 nnzC_i):
-//   keys[T] int32 (-1 empty), vals[T] double (+0.0 when empty),
-//   two radix buffers of T/2 (key, value), hist[256].
+// Numeric, per warp (T = 2^LOGT far-table slots >= 2 * far keys):
+//   wv[kWin] window values, vals[T] / keys[T] far table (+0.0 / -1 when
+//   empty; reused as the second radix buffer), radix buffer of T/2
+//   (key, value), window bitmap, hist[256].
 template <int LOGT>
 struct NumWarpSmem {
     static constexpr int T = 1 << LOGT;
-    static constexpr size_t bytes = (size_t)T * 4 + (size_t)T * 8 + 2 * ((size_t)(T / 2) * 12) + 256 * 4;
+    static constexpr size_t bytes =
+        (size_t)kWin * 8 + (size_t)T * 8 + (size_t)T * 4 + (size_t)(T / 2) * 12 + kWinWords * 4 + 256 * 4;
 };
 
-template <int LOGT, int WPB>
-__global__ void __launch_bounds__(WPB * 32) k_num_warp(NumArgs a, const int32_t *__restrict__ list,
-                                                       const int64_t *count) {
+template <int LOGT>
+__global__ void __launch_bounds__(kWarpHashThreads) k_num_warp(NumArgs a, const int32_t *__restrict__ list,
+                                                               const int64_t *count) {
     constexpr int T = 1 << LOGT;
     constexpr int H = T / 2;
+    constexpr int WPB = kWarpHashThreads / 32;
     extern __shared__ __align__(16) unsigned char num_smem[];
     const int w = threadIdx.x >> 5, l = lane_id();
     unsigned char *base = num_smem + (size_t)w * NumWarpSmem<LOGT>::bytes;
-    double *vals = reinterpret_cast<double *>(base);
+    double *wv = reinterpret_cast<double *>(base);
+    double *vals = wv + kWin;
     double *av = vals + T;
-    double *bv = av + H;
-    int32_t *keys = reinterpret_cast<int32_t *>(bv + H);
+    int32_t *keys = reinterpret_cast<int32_t *>(av + H);
     int32_t *ak = keys + T;
-    int32_t *bk = ak + H;
-    int32_t *hist = bk + H;
+    unsigned *wbits = reinterpret_cast<unsigned *>(ak + H);
+    int32_t *hist = reinterpret_cast<int32_t *>(wbits + kWinWords);
     const unsigned lt = lanemask_lt();
     Comp cut;
     int badp = 0;
@@ -491,6 +554,7 @@ __global__ void __launch_bounds__(WPB * 32) k_num_warp(NumArgs a, const int32_t 
         keys[s] = -1;
         vals[s] = +0.0;
     }
+    if (l < kWinWords) wbits[l] = 0u;
     __syncwarp();
     const int64_t n = *count;
     const int64_t nw = (int64_t)gridDim.x * WPB;
@@ -498,27 +562,38 @@ __global__ void __launch_bounds__(WPB * 32) k_num_warp(NumArgs a, const int32_t 
         const int64_t i = list[idx];
         const int64_t r = i - a.rb;
         const int64_t s = a.A.rp[i], e = a.A.rp[i + 1];
+        const int64_t wbase = i - kWinHalf;
         // ---- accumulate (ordered chains)
         for (int64_t bb = s; bb < e; bb += 32) {
             const Batch b = load_batch(a.A, a.T, bb, e, true);
+            Chunk cur = fetch_chunk<true>(a.T, b, 0);
             for (int64_t c0 = 0; c0 < b.total; c0 += 32) {
-                const int64_t pp = c0 + l;
-                const bool valid = pp < b.total;
-                const int t = find_seg(b, pp);
-                const int64_t q = __shfl_sync(kFull, b.cs, t) + pp - __shfl_sync(kFull, b.excl, t);
-                const double aik = shfl_d(b.a, t);
-                int j = -2 - l;
-                double bjk = 0.0;
-                if (valid) {
-                    j = a.T.ri[q];
-                    bjk = a.T.vt[q];
-                }
+                Chunk nxt = cur;
+                if (c0 + 32 < b.total) nxt = fetch_chunk<true>(a.T, b, c0 + 32);
+                const bool valid = cur.valid;
+                const int j = cur.j;
+                const int64_t d = (int64_t)j - wbase;
+                const bool near = valid && d >= 0 && d < kWin;
                 const unsigned g = __match_any_sync(kFull, j);
                 const int leader = __ffs(g) - 1;
                 const int rank = __popc(g & lt);
                 const int cnt = __popc(g);
-                int slot = 0;
-                if (valid && l == leader) {
+                const bool lead = valid && l == leader;
+                int slot = near ? (int)d : 0;
+                double acc = 0.0;
+                if (lead && near) {  // first touch of a window key starts its chain at +0.0
+                    acc = ((wbits[slot >> 5] >> (slot & 31)) & 1u) ? wv[slot] : +0.0;
+                }
+                __syncwarp();  // old bits read before the bitmap update
+                unsigned touched = __reduce_or_sync(kFull, (lead && near) ? (1u << (slot >> 5)) : 0u);
+                while (touched) {
+                    const int wd = __ffs(touched) - 1;
+                    touched &= touched - 1;
+                    const unsigned m =
+                        __reduce_or_sync(kFull, (lead && near && (slot >> 5) == wd) ? (1u << (slot & 31)) : 0u);
+                    if (l == 0) wbits[wd] |= m;
+                }
+                if (lead && !near) {
                     unsigned sl = hash_key(j, LOGT);
                     while (true) {
                         const int prev = atomicCAS(&keys[sl], -1, j);
@@ -526,21 +601,26 @@ __global__ void __launch_bounds__(WPB * 32) k_num_warp(NumArgs a, const int32_t 
                         sl = (sl + 1) & (T - 1);
                     }
                     slot = (int)sl;
+                    acc = vals[slot];
                 }
                 slot = __shfl_sync(kFull, slot, leader);
-                double acc = 0.0;
-                if (valid && rank == 0) acc = vals[slot];
                 const int pred = rank ? 31 - __clz(g & lt) : l;
                 const int maxc = __reduce_max_sync(kFull, valid ? cnt : 0);
                 for (int it = 0; it < maxc; ++it) {
                     const double x = shfl_d(acc, pred);
-                    if (valid && rank == it) acc = __fma_rn(aik, bjk, rank == 0 ? acc : x);
+                    if (valid && rank == it) acc = __fma_rn(cur.a, cur.b, rank == 0 ? acc : x);
                 }
-                if (valid && rank == cnt - 1) vals[slot] = acc;
+                if (valid && rank == cnt - 1) {
+                    if (near)
+                        wv[slot] = acc;
+                    else
+                        vals[slot] = acc;
+                }
                 __syncwarp();
+                cur = nxt;
             }
         }
-        // ---- compact the table into (ak, av), reset it
+        // ---- far keys: compact the table into (ak, av)
         int L = 0;
         int jmin = INT_MAX, jmax = -1;
         for (int b0 = 0; b0 < T; b0 += 32) {
@@ -552,8 +632,6 @@ __global__ void __launch_bounds__(WPB * 32) k_num_warp(NumArgs a, const int32_t 
                 const int pos = L + __popc(bal & lt);
                 ak[pos] = k;
                 av[pos] = vals[sidx];
-                keys[sidx] = -1;
-                vals[sidx] = +0.0;
                 jmin = min(jmin, k);
                 jmax = max(jmax, k);
             }
@@ -562,11 +640,12 @@ __global__ void __launch_bounds__(WPB * 32) k_num_warp(NumArgs a, const int32_t 
         jmin = __reduce_min_sync(kFull, jmin);
         jmax = __reduce_max_sync(kFull, jmax);
         __syncwarp();
-        // ---- LSD radix sort on (key - jmin), 8-bit digits, stable
+        // ---- LSD radix sort of the far keys on (key - jmin), 8-bit digits,
+        // stable; the (now copied-out) table region is the second buffer
         const unsigned span = L > 1 ? (unsigned)(jmax - jmin) : 0u;
         const int bits = span ? 32 - __clz(span) : 0;
-        int32_t *ck = ak, *nk = bk;
-        double *cv = av, *nv = bv;
+        int32_t *ck = ak, *nk = keys;
+        double *cv = av, *nv = vals;
         for (int sh = 0; sh < bits; sh += 8) {
             for (int h = l; h < 256; h += 32) hist[h] = 0;
             __syncwarp();
@@ -578,7 +657,7 @@ __global__ void __launch_bounds__(WPB * 32) k_num_warp(NumArgs a, const int32_t 
                 if (v && l == __ffs(g) - 1) hist[dig] += __popc(g);
                 __syncwarp();
             }
-            {  // exclusive scan of the 256 counters, 8 per lane
+            {
                 int loc[8], sum = 0;
 #pragma unroll
                 for (int u = 0; u < 8; ++u) {
@@ -616,7 +695,13 @@ __global__ void __launch_bounds__(WPB * 32) k_num_warp(NumArgs a, const int32_t 
             cv = nv;
             nv = tv;
         }
-        // ---- write the row: strip diagonal, |c| > tol (+ fused cut)
+        // far keys below the window sort first
+        int nbelow = 0;
+        for (int rd = 0; rd < L; rd += 32) {
+            const int e2 = rd + l;
+            nbelow += __popc(__ballot_sync(kFull, e2 < L && (int64_t)ck[e2] < wbase));
+        }
+        // ---- write the row in ascending j: far-below, window, far-above
         const int64_t g0 = a.gptr[r], ub = a.gptr[r + 1] - g0;
         int32_t pi = 0;
         if (a.part) {
@@ -624,11 +709,7 @@ __global__ void __launch_bounds__(WPB * 32) k_num_warp(NumArgs a, const int32_t 
             badp |= (pi < 0) | (pi >= a.K);
         }
         int64_t o = 0;
-        for (int rd = 0; rd < L; rd += 32) {
-            const int e2 = rd + l;
-            const bool v = e2 < L;
-            const int key = v ? ck[e2] : -1;
-            const double c = v ? cv[e2] : 0.0;
+        auto emit = [&](bool v, int key, double c) {
             const bool isdiag = v && (int64_t)key == i;
             if (isdiag && a.diag) a.diag[r] = c;
             const bool keep = v && !isdiag && fabs(c) > a.tol;
@@ -644,7 +725,29 @@ __global__ void __launch_bounds__(WPB * 32) k_num_warp(NumArgs a, const int32_t 
                 }
             }
             o += __popc(bal);
+        };
+        for (int rd = 0; rd < nbelow; rd += 32) {
+            const int e2 = rd + l;
+            const bool v = e2 < nbelow;
+            emit(v, v ? ck[e2] : -1, v ? cv[e2] : 0.0);
         }
+        for (int rd = 0; rd < kWinWords; ++rd) {
+            const int slot = rd * 32 + l;
+            const bool v = (wbits[rd] >> l) & 1u;
+            emit(v, (int)(wbase + slot), v ? wv[slot] : 0.0);
+        }
+        for (int rd = nbelow; rd < L; rd += 32) {
+            const int e2 = rd + l;
+            const bool v = e2 < L;
+            emit(v, v ? ck[e2] : -1, v ? cv[e2] : 0.0);
+        }
+        __syncwarp();
+        // reset the far table (it also served as a radix buffer) and the bitmap
+        for (int s2 = l; s2 < T; s2 += 32) {
+            keys[s2] = -1;
+            vals[s2] = +0.0;
+        }
+        if (l < kWinWords) wbits[l] = 0u;
         if (o < ub) {
             for (int64_t t = o + l; t < ub; t += 32) a.gcol[g0 + t] = -1;
             if (l == 0) atomicOr(a.holes, 1);
@@ -652,7 +755,7 @@ __global__ void __launch_bounds__(WPB * 32) k_num_warp(NumArgs a, const int32_t 
         __syncwarp();
     }
     if (a.part) {
-        const double v = block_tree_sum<WPB * 32>(cut.value());
+        const double v = block_tree_sum<kWarpHashThreads>(cut.value());
         if (threadIdx.x == 0) {
             a.cutp[blockIdx.x] = v;
             if (blockIdx.x == 0) *a.cut_used = (int)gridDim.x;
@@ -663,16 +766,17 @@ __global__ void __launch_bounds__(WPB * 32) k_num_warp(NumArgs a, const int32_t 
 
 template <int LOGT>
 static void launch_num_warp_t(const NumArgs &a, const int32_t *list, const int64_t *count, cudaStream_t s) {
-    constexpr int WPB = LOGT >= 11 ? 4 : 8;
-    const size_t smem = (size_t)WPB * NumWarpSmem<LOGT>::bytes;
+    const size_t smem = (size_t)(kWarpHashThreads / 32) * NumWarpSmem<LOGT>::bytes;
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(k_num_warp<LOGT, WPB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(k_num_warp<LOGT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         attr = true;
     }
     int per_sm = (int)((220 * 1024) / smem);
-    per_sm = per_sm < 1 ? 1 : (per_sm > 4 ? 4 : per_sm);
-    k_num_warp<LOGT, WPB><<<sms() * per_sm, WPB * 32, smem, s>>>(a, list, count);
+    per_sm = per_sm < 1 ? 1 : (per_sm > 16 ? 16 : per_sm);
+    int g = sms() * per_sm;
+    if (g > kCutSlotsPerLaunch) g = kCutSlotsPerLaunch;
+    k_num_warp<LOGT><<<g, kWarpHashThreads, smem, s>>>(a, list, count);
     note_launch();
 }
 
@@ -704,11 +808,14 @@ constexpr int kHugeWarps = kHugeThreads / 32;
 
 static int64_t bitmap_words(int64_t nrows) { return (nrows + 31) / 32; }
 
+// Scratch layout: [slots bitmaps][slots dense accumulators]; only the bitmap
+// prefix (huge_bitmap_bytes) needs zeroing -- each row clears what it set.
+static size_t bitmap_stride(int64_t nrows) { return ((size_t)bitmap_words(nrows) * 4 + 255) & ~(size_t)255; }
+
+size_t huge_bitmap_bytes(int64_t nrows, int slots) { return bitmap_stride(nrows) * (size_t)slots; }
+
 size_t huge_scratch_bytes(int64_t nrows, int slots, bool numeric) {
-    size_t per = (size_t)bitmap_words(nrows) * 4;
-    per = (per + 255) & ~(size_t)255;
-    if (numeric) per += (size_t)nrows * 8;
-    return per * (size_t)slots;
+    return huge_bitmap_bytes(nrows, slots) + (numeric ? (size_t)nrows * 8 * (size_t)slots : 0);
 }
 
 int huge_slots(int64_t nrows, int64_t n_huge) {
@@ -810,7 +917,10 @@ __global__ void __launch_bounds__(kHugeThreads) k_sym_huge(SymArgs a, const int3
             }
         }
         cnt = block_sum(cnt);
-        if (threadIdx.x == 0) a.nnzc[i - a.rb] = cnt;
+        if (threadIdx.x == 0) {
+            a.nnzc[i - a.rb] = cnt;
+            a.farc[i - a.rb] = kFarHuge;
+        }
         __syncthreads();
     }
 }
@@ -821,9 +931,8 @@ __global__ void __launch_bounds__(kHugeThreads) k_num_huge(NumArgs a, const int3
     __shared__ int64_t s_incl[kHugeThreads], s_cs[kHugeThreads];
     __shared__ double s_a[kHugeThreads];
     __shared__ int64_t s_scan[kHugeWarps];
-    unsigned char *slot = scratch + slot_bytes * blockIdx.x;
-    unsigned *bm = reinterpret_cast<unsigned *>(slot);
-    double *acc_g = reinterpret_cast<double *>(slot + (((size_t)nwords * 4 + 255) & ~(size_t)255));
+    unsigned *bm = reinterpret_cast<unsigned *>(scratch + slot_bytes * blockIdx.x);
+    double *acc_g = reinterpret_cast<double *>(scratch + slot_bytes * gridDim.x) + (size_t)blockIdx.x * a.A.nrows;
     const int w = threadIdx.x >> 5, l = lane_id();
     const unsigned lt = lanemask_lt();
     const int64_t n = *count;
@@ -946,14 +1055,14 @@ __global__ void __launch_bounds__(kHugeThreads) k_num_huge(NumArgs a, const int3
 
 void launch_sym_huge(const SymArgs &a, const int32_t *list, const int64_t *count, int slots, void *scratch,
                      cudaStream_t s) {
-    const size_t slot_bytes = huge_scratch_bytes(a.A.nrows, 1, true);
+    const size_t slot_bytes = bitmap_stride(a.A.nrows);
     k_sym_huge<<<slots, kHugeThreads, 0, s>>>(a, list, count, static_cast<unsigned char *>(scratch), slot_bytes);
     note_launch();
 }
 
 void launch_num_huge(const NumArgs &a, const int32_t *list, const int64_t *count, int slots, void *scratch,
                      cudaStream_t s) {
-    const size_t slot_bytes = huge_scratch_bytes(a.A.nrows, 1, true);
+    const size_t slot_bytes = bitmap_stride(a.A.nrows);
     NumArgs b = a;
     if (a.cutp) {
         b.cutp = a.cutp + (int64_t)7 * kCutSlotsPerLaunch;

@@ -272,6 +272,7 @@ struct rig_plan {
     int32_t *sym_lists = nullptr, *num_lists = nullptr;
     int64_t list_cap = 0;
     int64_t *nnzc = nullptr, *gptr_ub = nullptr;
+    int32_t *farc = nullptr;
     void *huge_scratch = nullptr;
     int huge_slots_n = 0;
     int64_t nnz_upper = 0;
@@ -302,6 +303,7 @@ static void plan_build(rig_plan *p, const rig_csr_t *Ain, int64_t *gptr_out, boo
     const size_t o_vt = L.add(sizeof(double) * (size_t)(nnz + m));
     const size_t o_sym = L.add(sizeof(int32_t) * (size_t)kSymBins * (size_t)std::max<int64_t>(nloc, 1));
     const size_t o_nnzc = L.add(sizeof(int64_t) * (size_t)nloc);
+    const size_t o_farc = L.add(sizeof(int32_t) * (size_t)nloc);
     const size_t o_gptr = gptr_out ? 0 : L.add(sizeof(int64_t) * (size_t)(nloc + 1));
     unsigned char *ws = p->cached ? ws_get(0, L.bytes, s) : p->arena.raw(L.bytes);
     CK(cudaMemsetAsync(ws, 0, zero_bytes, s));
@@ -313,6 +315,7 @@ static void plan_build(rig_plan *p, const rig_csr_t *Ain, int64_t *gptr_out, boo
     double *vt = reinterpret_cast<double *>(ws + o_vt);
     p->sym_lists = reinterpret_cast<int32_t *>(ws + o_sym);
     p->nnzc = reinterpret_cast<int64_t *>(ws + o_nnzc);
+    p->farc = reinterpret_cast<int32_t *>(ws + o_farc);
     p->gptr_ub = gptr_out ? gptr_out : reinterpret_cast<int64_t *>(ws + o_gptr);
     p->list_cap = nloc;
     HostStage *hs = host_stage();
@@ -343,7 +346,7 @@ static void plan_build(rig_plan *p, const rig_csr_t *Ain, int64_t *gptr_out, boo
     p->A = Csr{n, m, nnz, Ain->row_ptr, Ain->col_idx, p->scale ? ahat : Ain->val};
     p->T = Csc{cp, ri, vt};
     // a3 + a4 (merge rows): products, structural nnz(C_i), bins for the rest
-    SymArgs sa{p->A, p->T, p->rb, p->re, p->nnzc};
+    SymArgs sa{p->A, p->T, p->rb, p->re, p->nnzc, p->farc};
     if (nloc > 0) {
         Prof pf(P_ANALYZE, s);
         launch_analyze_sym(sa, p->sym_lists, p->list_cap, p->ctr, s);
@@ -373,12 +376,12 @@ static void plan_build(rig_plan *p, const rig_csr_t *Ain, int64_t *gptr_out, boo
         p->num_lists = reinterpret_cast<int32_t *>(wb + o_num);
         if (n_big > 0) {
             p->huge_scratch = wb + o_huge;
-            CK(cudaMemsetAsync(p->huge_scratch, 0, huge_bytes, s));
+            CK(cudaMemsetAsync(p->huge_scratch, 0, huge_bitmap_bytes(n, p->huge_slots_n), s));
         }
         if (p->h.sym_count[kNumSymBins] > 0)
             launch_sym_huge(sa, p->sym_lists + (int64_t)kNumSymBins * p->list_cap, p->ctr->sym_count + kNumSymBins,
                             p->huge_slots_n, p->huge_scratch, s);
-        launch_bin_num(p->sym_lists, p->list_cap, p->ctr, p->nnzc, p->rb, p->num_lists, n_mid, p->ctr->num_count, s);
+        launch_bin_num(p->sym_lists, p->list_cap, p->ctr, p->farc, p->rb, p->num_lists, n_mid, p->ctr->num_count, s);
     }
     check_launch("symbolic");
     {
