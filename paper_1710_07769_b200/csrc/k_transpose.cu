@@ -23,8 +23,8 @@ namespace rig {
 // about kBucketTarget records (transpose_shift).
 constexpr int kMinShift = 3, kMaxShift = 9;
 constexpr int kMaxBucketCols = 1 << kMaxShift;
-constexpr int kBucketTarget = 1024;
-constexpr int kBucketCap = 2048;  // records per bucket sorted in shared memory (32 KB)
+constexpr int kBucketTarget = 512;
+constexpr int kBucketCap = 1024;  // records per bucket sorted in shared memory (16 KB)
 
 struct __align__(16) Rec {
     int32_t col, row;
@@ -127,7 +127,7 @@ __device__ void bitonic_sort_block(int64_t len, KeyAt key, Swap swap) {
     }
 }
 
-constexpr int kSortThreads = 256;
+constexpr int kSortThreads = 128;
 
 __global__ void __launch_bounds__(kSortThreads) k_bucket_sort(const Rec *__restrict__ rec,
                                                               const int64_t *__restrict__ cp, int64_t ncols,
@@ -241,7 +241,7 @@ void launch_transpose(const Csr &A, int scale, const int64_t *cp, double *ahat, 
     }
     if (A.ncols > 0) {
         const int64_t nb = (A.ncols + (1 << shift) - 1) >> shift;
-        const int64_t cap = (int64_t)num_sms() * 8;
+        const int64_t cap = (int64_t)num_sms() * 16;
         k_bucket_sort<<<(unsigned)(nb < cap ? nb : cap), kSortThreads, 0, s>>>(static_cast<const Rec *>(rec), cp,
                                                                                 A.ncols, gcur, ri, vt, shift);
         note_launch();
