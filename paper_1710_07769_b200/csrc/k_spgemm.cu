@@ -889,106 +889,165 @@ __device__ __forceinline__ int64_t block_sum(int64_t v) {
     return t;
 }
 
+// Second-level bitmap in shared memory: bit (w & 31) of word w >> 5 is set iff
+// the row's L1 bitmap word w (global) is non-zero, so output and clearing
+// touch only non-empty L1 words instead of all nrows/32.
+__host__ __device__ __forceinline__ int64_t l2_words(int64_t nwords) { return (nwords + 31) / 32; }
+
 __global__ void __launch_bounds__(kHugeThreads) k_sym_huge(SymArgs a, const int32_t *__restrict__ list,
                                                            const int64_t *count, unsigned char *scratch,
-                                                           size_t slot_bytes) {
+                                                           size_t slot_bytes, int64_t nwords) {
+    extern __shared__ unsigned l2[];
     __shared__ int64_t s_incl[kHugeThreads], s_cs[kHugeThreads];
+    const int64_t nw2 = l2_words(nwords);
     unsigned *bm = reinterpret_cast<unsigned *>(scratch + slot_bytes * blockIdx.x);
+    for (int64_t t = threadIdx.x; t < nw2; t += kHugeThreads) l2[t] = 0u;
+    __syncthreads();
     const int64_t n = *count;
     for (int64_t idx = blockIdx.x; idx < n; idx += gridDim.x) {
         const int64_t i = list[idx];
         const int64_t s = a.A.rp[i], e = a.A.rp[i + 1];
         int64_t cnt = 0;
-        for (int pass = 0; pass < 2; ++pass) {  // pass 0: set + count, pass 1: clear
-            for (int64_t base = s; base < e; base += kHugeThreads) {
-                const int64_t total = block_batch(a.A, a.T, base, e, s_incl, s_cs, nullptr);
-                for (int64_t pp = threadIdx.x; pp < total; pp += kHugeThreads) {
-                    const int t = block_find(s_incl, pp);
-                    const int64_t ex = t ? s_incl[t - 1] : 0;
-                    const int j = a.T.ri[s_cs[t] + pp - ex];
-                    if (pass == 0) {
-                        const unsigned bit = 1u << (j & 31);
-                        if (!(atomicOr(&bm[j >> 5], bit) & bit)) ++cnt;
-                    } else {
-                        bm[j >> 5] = 0u;
-                    }
+        for (int64_t base = s; base < e; base += kHugeThreads) {
+            const int64_t total = block_batch(a.A, a.T, base, e, s_incl, s_cs, nullptr);
+            for (int64_t pp = threadIdx.x; pp < total; pp += kHugeThreads) {
+                const int t = block_find(s_incl, pp);
+                const int64_t ex = t ? s_incl[t - 1] : 0;
+                const int j = a.T.ri[s_cs[t] + pp - ex];
+                const unsigned bit = 1u << (j & 31);
+                const unsigned old = atomicOr(&bm[j >> 5], bit);
+                if (!(old & bit)) {
+                    ++cnt;
+                    if (old == 0u) atomicOr(&l2[j >> 10], 1u << ((j >> 5) & 31));
                 }
-                __syncthreads();
             }
+            __syncthreads();
         }
         cnt = block_sum(cnt);
         if (threadIdx.x == 0) {
             a.nnzc[i - a.rb] = cnt;
             a.farc[i - a.rb] = kFarHuge;
         }
+        // clear the touched L1 words and the L2 bitmap
+        for (int64_t t = threadIdx.x; t < nw2; t += kHugeThreads) {
+            for (unsigned m = l2[t]; m; m &= m - 1) bm[t * 32 + __ffs(m) - 1] = 0u;
+            l2[t] = 0u;
+        }
         __syncthreads();
     }
 }
 
+// Numeric: the row's products are enumerated 512 at a time (one 32-product
+// sub-chunk per warp) and routed, in product order, into shared-memory queues
+// of their owner warp ((j >> 5) % 16).  Each owner then applies its queue in
+// order (ordered __match_any_sync chains) to the dense accumulator, so every
+// chain runs in ascending k and each product is handled once.
 __global__ void __launch_bounds__(kHugeThreads) k_num_huge(NumArgs a, const int32_t *__restrict__ list,
                                                            const int64_t *count, unsigned char *scratch,
                                                            size_t slot_bytes, int64_t nwords) {
+    extern __shared__ unsigned l2[];
     __shared__ int64_t s_incl[kHugeThreads], s_cs[kHugeThreads];
     __shared__ double s_a[kHugeThreads];
+    __shared__ int32_t q_j[kHugeThreads];
+    __shared__ double q_a[kHugeThreads], q_b[kHugeThreads];
+    __shared__ int cnt[kHugeWarps][kHugeWarps + 1];
+    __shared__ int otot[kHugeWarps], obase[kHugeWarps + 1];
     __shared__ int64_t s_scan[kHugeWarps];
+    const int64_t nw2 = l2_words(nwords);
     unsigned *bm = reinterpret_cast<unsigned *>(scratch + slot_bytes * blockIdx.x);
     double *acc_g = reinterpret_cast<double *>(scratch + slot_bytes * gridDim.x) + (size_t)blockIdx.x * a.A.nrows;
-    const int w = threadIdx.x >> 5, l = lane_id();
+    const int tid = threadIdx.x, w = tid >> 5, l = lane_id();
     const unsigned lt = lanemask_lt();
-    const int64_t n = *count;
+    for (int64_t t = tid; t < nw2; t += kHugeThreads) l2[t] = 0u;
+    __syncthreads();
     Comp cut;
     int badp = 0;
+    const int64_t n = *count;
     for (int64_t idx = blockIdx.x; idx < n; idx += gridDim.x) {
         const int64_t i = list[idx];
         const int64_t r = i - a.rb;
         const int64_t s = a.A.rp[i], e = a.A.rp[i + 1];
         for (int64_t base = s; base < e; base += kHugeThreads) {
             const int64_t total = block_batch(a.A, a.T, base, e, s_incl, s_cs, s_a);
-            // every warp walks every chunk in order; it only touches its keys
-            for (int64_t c0 = 0; c0 < total; c0 += 32) {
-                const int64_t pp = c0 + l;
-                const bool inr = pp < total;
-                int j = -2 - l;
-                bool own = false;
+            for (int64_t c0 = 0; c0 < total; c0 += kHugeThreads) {
+                // ---- enumerate: warp w takes products c0 + 32 w + l
+                const int64_t pp = c0 + tid;
+                const bool valid = pp < total;
+                int j = 0, o = 32 + l;
                 double aik = 0.0, bjk = 0.0;
-                if (inr) {
+                if (valid) {
                     const int t = block_find(s_incl, pp);
                     const int64_t ex = t ? s_incl[t - 1] : 0;
                     const int64_t q = s_cs[t] + pp - ex;
-                    const int jj = a.T.ri[q];
-                    if (((jj >> 5) % kHugeWarps) == w) {
-                        own = true;
-                        j = jj;
-                        aik = s_a[t];
-                        bjk = a.T.vt[q];
-                    }
+                    j = a.T.ri[q];
+                    bjk = a.T.vt[q];
+                    aik = s_a[t];
+                    o = (j >> 5) & (kHugeWarps - 1);
                 }
-                if (!__any_sync(kFull, own)) continue;
-                const unsigned g = __match_any_sync(kFull, j);
-                const int leader = __ffs(g) - 1;
+                const unsigned g = __match_any_sync(kFull, o);
                 const int rank = __popc(g & lt);
-                const int cnt = __popc(g);
-                double acc = 0.0;
-                if (own && rank == 0) {
-                    const unsigned bit = 1u << (j & 31);
-                    const unsigned old = atomicOr(&bm[j >> 5], bit);
-                    acc = (old & bit) ? acc_g[j] : +0.0;
-                }
-                (void)leader;
-                const int pred = rank ? 31 - __clz(g & lt) : l;
-                const int maxc = __reduce_max_sync(kFull, own ? cnt : 0);
-                for (int it = 0; it < maxc; ++it) {
-                    const double x = shfl_d(acc, pred);
-                    if (own && rank == it) acc = __fma_rn(aik, bjk, rank == 0 ? acc : x);
-                }
-                if (own && rank == cnt - 1) acc_g[j] = acc;
+                if (l < kHugeWarps) cnt[w][l] = 0;
                 __syncwarp();
+                if (valid && l == __ffs(g) - 1) cnt[w][o] = __popc(g);
+                __syncthreads();
+                if (tid < kHugeWarps) {  // owner tid: offsets of each sub-chunk in its queue
+                    int run = 0;
+                    for (int ww = 0; ww < kHugeWarps; ++ww) {
+                        const int c = cnt[ww][tid];
+                        cnt[ww][tid] = run;
+                        run += c;
+                    }
+                    otot[tid] = run;
+                }
+                __syncthreads();
+                if (tid == 0) {
+                    int sum = 0;
+                    for (int oo = 0; oo < kHugeWarps; ++oo) {
+                        obase[oo] = sum;
+                        sum += otot[oo];
+                    }
+                    obase[kHugeWarps] = sum;
+                }
+                __syncthreads();
+                if (valid) {
+                    const int pos = obase[o] + cnt[w][o] + rank;
+                    q_j[pos] = j;
+                    q_a[pos] = aik;
+                    q_b[pos] = bjk;
+                }
+                __syncthreads();
+                // ---- owner warp w applies its queue segment in order
+                const int qe = obase[w + 1];
+                for (int qs = obase[w]; qs < qe; qs += 32) {
+                    const int ee = qs + l;
+                    const bool v = ee < qe;
+                    const int jj = v ? q_j[ee] : -2 - l;
+                    const unsigned gg = __match_any_sync(kFull, jj);
+                    const int rk = __popc(gg & lt);
+                    const int cn = __popc(gg);
+                    double acc = 0.0;
+                    if (v && rk == 0) {
+                        const unsigned bit = 1u << (jj & 31);
+                        const unsigned old = atomicOr(&bm[jj >> 5], bit);
+                        if (old == 0u) atomicOr(&l2[jj >> 10], 1u << ((jj >> 5) & 31));
+                        acc = (old & bit) ? acc_g[jj] : +0.0;
+                    }
+                    const int pred = rk ? 31 - __clz(gg & lt) : l;
+                    const int maxc = __reduce_max_sync(kFull, v ? cn : 0);
+                    const double qa = v ? q_a[ee] : 0.0, qb = v ? q_b[ee] : 0.0;
+                    for (int it = 0; it < maxc; ++it) {
+                        const double x = shfl_d(acc, pred);
+                        if (v && rk == it) acc = __fma_rn(qa, qb, rk == 0 ? acc : x);
+                    }
+                    if (v && rk == cn - 1) acc_g[jj] = acc;
+                    __syncwarp();
+                }
+                __syncthreads();
             }
-            __syncthreads();
         }
         __threadfence_block();
         __syncthreads();
-        // ---- emit in ascending j by scanning the bitmap (+ fused cut)
+        // ---- emit in ascending j: walk the non-empty L1 words via the L2 bitmap
         const int64_t g0 = a.gptr[r], ub = a.gptr[r + 1] - g0;
         int32_t pi = 0;
         if (a.part) {
@@ -996,20 +1055,22 @@ __global__ void __launch_bounds__(kHugeThreads) k_num_huge(NumArgs a, const int3
             badp |= (pi < 0) | (pi >= a.K);
         }
         int64_t o = 0;
-        for (int64_t wb = 0; wb < nwords; wb += kHugeThreads) {
-            const int64_t wi = wb + threadIdx.x;
-            unsigned word = wi < nwords ? bm[wi] : 0u;
+        for (int64_t rb2 = 0; rb2 < nw2; rb2 += kHugeThreads) {
+            const int64_t t2 = rb2 + tid;
+            const unsigned m2 = t2 < nw2 ? l2[t2] : 0u;
             int keep = 0;
-            for (unsigned m = word; m; m &= m - 1) {
-                const int64_t j = wi * 32 + __ffs(m) - 1;
-                const double c = acc_g[j];
-                if (j == i) {
-                    if (a.diag) a.diag[r] = c;
-                } else if (fabs(c) > a.tol) {
-                    ++keep;
+            for (unsigned mm = m2; mm; mm &= mm - 1) {
+                const int64_t w1 = t2 * 32 + __ffs(mm) - 1;
+                for (unsigned m = bm[w1]; m; m &= m - 1) {
+                    const int64_t j = w1 * 32 + __ffs(m) - 1;
+                    const double c = acc_g[j];
+                    if (j == i) {
+                        if (a.diag) a.diag[r] = c;
+                    } else if (fabs(c) > a.tol) {
+                        ++keep;
+                    }
                 }
             }
-            // block exclusive scan of keep
             const int64_t inc = warp_incl_scan((int64_t)keep);
             if (l == 31) s_scan[w] = inc;
             __syncthreads();
@@ -1019,27 +1080,31 @@ __global__ void __launch_bounds__(kHugeThreads) k_num_huge(NumArgs a, const int3
                 tot += s_scan[k];
             }
             int64_t pos = g0 + o + wofs + inc - keep;
-            for (unsigned m = word; m; m &= m - 1) {
-                const int64_t j = wi * 32 + __ffs(m) - 1;
-                const double c = acc_g[j];
-                if (j != i && fabs(c) > a.tol) {
-                    a.gcol[pos] = (int32_t)j;
-                    a.gw[pos] = fabs(c);
-                    ++pos;
-                    if (a.part && j > i) {
-                        const int32_t pj = a.part[j];
-                        badp |= (pj < 0) | (pj >= a.K);
-                        if (pj != pi) cut.add(fabs(c));
+            for (unsigned mm = m2; mm; mm &= mm - 1) {
+                const int64_t w1 = t2 * 32 + __ffs(mm) - 1;
+                for (unsigned m = bm[w1]; m; m &= m - 1) {
+                    const int64_t j = w1 * 32 + __ffs(m) - 1;
+                    const double c = acc_g[j];
+                    if (j != i && fabs(c) > a.tol) {
+                        a.gcol[pos] = (int32_t)j;
+                        a.gw[pos] = fabs(c);
+                        ++pos;
+                        if (a.part && j > i) {
+                            const int32_t pj = a.part[j];
+                            badp |= (pj < 0) | (pj >= a.K);
+                            if (pj != pi) cut.add(fabs(c));
+                        }
                     }
                 }
+                bm[w1] = 0u;
             }
-            if (word) bm[wi] = 0u;
+            if (t2 < nw2) l2[t2] = 0u;
             o += tot;
             __syncthreads();
         }
         if (o < ub) {
-            for (int64_t t = o + threadIdx.x; t < ub; t += kHugeThreads) a.gcol[g0 + t] = -1;
-            if (threadIdx.x == 0) atomicOr(a.holes, 1);
+            for (int64_t t = o + tid; t < ub; t += kHugeThreads) a.gcol[g0 + t] = -1;
+            if (tid == 0) atomicOr(a.holes, 1);
         }
         __syncthreads();
     }
@@ -1056,20 +1121,27 @@ __global__ void __launch_bounds__(kHugeThreads) k_num_huge(NumArgs a, const int3
 void launch_sym_huge(const SymArgs &a, const int32_t *list, const int64_t *count, int slots, void *scratch,
                      cudaStream_t s) {
     const size_t slot_bytes = bitmap_stride(a.A.nrows);
-    k_sym_huge<<<slots, kHugeThreads, 0, s>>>(a, list, count, static_cast<unsigned char *>(scratch), slot_bytes);
+    const int64_t nw = bitmap_words(a.A.nrows);
+    const size_t smem = (size_t)l2_words(nw) * sizeof(unsigned);
+    cudaFuncSetAttribute(k_sym_huge, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_sym_huge<<<slots, kHugeThreads, smem, s>>>(a, list, count, static_cast<unsigned char *>(scratch), slot_bytes,
+                                                 nw);
     note_launch();
 }
 
 void launch_num_huge(const NumArgs &a, const int32_t *list, const int64_t *count, int slots, void *scratch,
                      cudaStream_t s) {
     const size_t slot_bytes = bitmap_stride(a.A.nrows);
+    const int64_t nw = bitmap_words(a.A.nrows);
+    const size_t smem = (size_t)l2_words(nw) * sizeof(unsigned);
+    cudaFuncSetAttribute(k_num_huge, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     NumArgs b = a;
     if (a.cutp) {
         b.cutp = a.cutp + (int64_t)7 * kCutSlotsPerLaunch;
         b.cut_used = a.cut_used + 7;
     }
-    k_num_huge<<<slots, kHugeThreads, 0, s>>>(b, list, count, static_cast<unsigned char *>(scratch), slot_bytes,
-                                              bitmap_words(a.A.nrows));
+    k_num_huge<<<slots, kHugeThreads, smem, s>>>(b, list, count, static_cast<unsigned char *>(scratch), slot_bytes,
+                                                 nw);
     note_launch();
 }
 
