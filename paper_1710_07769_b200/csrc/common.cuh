@@ -104,10 +104,17 @@ int64_t transpose_buckets(int64_t nnz, int64_t ncols);
 constexpr size_t kTransposeRecBytes = 16;
 void launch_transpose(const Csr &A, int scale, const int64_t *cp, double *ahat, unsigned long long *bcur,
                       void *rec, unsigned *gcur, int32_t *ri, double *vt, int *err, cudaStream_t s);
-void launch_analyze(const Csr &A, const int64_t *cp, int64_t rb, int64_t re, int64_t *f, int32_t *sym_lists,
-                    int64_t cap, DevCounters *ctr, cudaStream_t s);
-void launch_bin_num(const int32_t *sym_lists, int64_t sym_cap, const DevCounters *ctr, const int32_t *farc,
-                    int64_t rb, int32_t *num_lists, int64_t num_cap, int64_t *num_count, cudaStream_t s);
+void launch_analyze(const Csr &A, const int64_t *cp, int64_t rb, int64_t re, int64_t *f, DevCounters *ctr,
+                    cudaStream_t s);
+// Ordered row bins (k_prep.cu): mode 0 symbolic (from bin8), mode 1 numeric
+// (from farc); lists[b * cap ...] in ascending row order; counts[b] written
+// when non-null.  cnt: u32[bins_count_elems(nloc)], off: int64[that + 1],
+// scan_tmp: scan_tmp_bytes(that).
+constexpr int kMaxBins = 8;
+constexpr uint8_t kBinNone = 0xff;  // bin8 of a merge-path row
+size_t bins_count_elems(int64_t nloc);
+void launch_bins(int mode, const uint8_t *bin8, const int32_t *farc, int64_t rb, int64_t nloc, unsigned *cnt,
+                 int64_t *off, void *scan_tmp, int32_t *lists, int64_t cap, int64_t *counts, cudaStream_t s);
 
 // k_scan.cu: out[0..n] = exclusive prefix of in[0..n-1] (out[n] = total).
 enum class ScanOp { Identity, UbOffDiag };
@@ -195,7 +202,9 @@ inline int stage_cap_for(int64_t products, int64_t rows) {
 constexpr int kCutSlotsPerLaunch = 4096;
 constexpr int kCutLaunches = 8;  // merge + 6 warp bins + huge
 // a3 + a4(merge rows) fused: products, merge-row nnzC, bins for the others
-void launch_analyze_sym(const SymArgs &a, int32_t *sym_lists, int64_t cap, DevCounters *ctr, cudaStream_t s);
+// bin8[r]: symbolic bin of row r, or kBinNone on the merge path;
+// ctr->sym_count / n_mid: bin totals.
+void launch_analyze_sym(const SymArgs &a, uint8_t *bin8, DevCounters *ctr, cudaStream_t s);
 // maxlen: longest A row on the merge path in the shard (DevCounters::max_len)
 void launch_sym_merge(const SymArgs &a, int maxlen, cudaStream_t s);
 void launch_num_merge(const NumArgs &a, int maxlen, cudaStream_t s);

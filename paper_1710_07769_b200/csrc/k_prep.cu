@@ -1,6 +1,8 @@
 // k_prep.cu -- steps a0-a3 of the hot path:
 //   a0 validate (flag-gated), a1 row scaling fused into the a2 transpose
 //   scatter, a2 column access (CSC of A_hat), a3 flop count + binning.
+#include <algorithm>
+
 #include "common.cuh"
 
 namespace rig {
@@ -72,20 +74,18 @@ void launch_col_hist(const Csr &A, unsigned *cnt, unsigned *rank, cudaStream_t s
 // a1 + a2 (scaling, CSC): k_transpose.cu
 
 // ------------------------------------------------------------------ a3
-// f_i = sum over k in row i of nnz(column k) (Gustavson products).  Rows off
-// the merge path go to symbolic bin ceil(log2(2 f_i)) in [6, 12], or to the
-// huge bin (index 7) above that.
+// f_i = sum over k in row i of nnz(column k) (Gustavson products), for the
+// flop-balanced row split.  (The build path computes f_i in k_analyze_sym.)
 __device__ __forceinline__ int ceil_log2_2x(int64_t m) {
     const int64_t m2 = 2 * (m > 1 ? m : 1);
     return 64 - __clzll(m2 - 1);
 }
 
 __global__ void k_analyze(Csr A, const int64_t *__restrict__ cp, int64_t rb, int64_t re, int64_t *f,
-                          int32_t *sym_lists, int64_t cap, DevCounters *ctr) {
+                          DevCounters *ctr) {
     const int64_t nloc = re - rb;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     int64_t local = 0;
-    int maxlen = 0;
     for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < nloc; r += stride) {
         const int64_t i = rb + r;
         const int64_t s = A.rp[i], e = A.rp[i + 1];
@@ -94,21 +94,9 @@ __global__ void k_analyze(Csr A, const int64_t *__restrict__ cp, int64_t rb, int
             const int k = A.ci[p];
             fi += cp[k + 1] - cp[k];
         }
-        if (f) f[r] = fi;
+        f[r] = fi;
         local += fi;
-        const bool merge = e - s <= kMergeMaxLen && fi <= kMergeMaxF;
-        if (merge) maxlen = max(maxlen, (int)(e - s));
-        if (sym_lists && !merge) {
-            int lg = ceil_log2_2x(fi);
-            if (lg < kSymBinMinLog) lg = kSymBinMinLog;
-            const int b = lg > kSymBinMaxLog ? kNumSymBins : lg - kSymBinMinLog;
-            const unsigned long long pos = atomicAdd((unsigned long long *)&ctr->sym_count[b], 1ull);
-            sym_lists[b * cap + (int64_t)pos] = (int32_t)i;
-            atomicAdd((unsigned long long *)&ctr->n_mid, 1ull);
-        }
     }
-    maxlen = __reduce_max_sync(kFull, maxlen);
-    if (lane_id() == 0 && maxlen) atomicMax(&ctr->max_len, maxlen);
     local = warp_sum(local);
     __shared__ int64_t part[32];
     if (lane_id() == 0) part[threadIdx.x >> 5] = local;
@@ -120,35 +108,107 @@ __global__ void k_analyze(Csr A, const int64_t *__restrict__ cp, int64_t rb, int
     }
 }
 
-void launch_analyze(const Csr &A, const int64_t *cp, int64_t rb, int64_t re, int64_t *f, int32_t *sym_lists,
-                    int64_t cap, DevCounters *ctr, cudaStream_t s) {
-    k_analyze<<<grid_for(re - rb, 256), 256, 0, s>>>(A, cp, rb, re, f, sym_lists, cap, ctr);
+void launch_analyze(const Csr &A, const int64_t *cp, int64_t rb, int64_t re, int64_t *f, DevCounters *ctr,
+                    cudaStream_t s) {
+    k_analyze<<<grid_for(re - rb, 256), 256, 0, s>>>(A, cp, rb, re, f, ctr);
     note_launch();
 }
 
-// Numeric bins by nnzC_i: table T = 2^ceil(log2(2 nnzC_i)) in [64, 2048];
-// larger -> huge bin (index 6).
-__global__ void k_bin_num(const int32_t *__restrict__ sym_lists, int64_t sym_cap, const DevCounters *ctr,
-                          const int32_t *__restrict__ farc, int64_t rb, int32_t *num_lists, int64_t num_cap,
-                          int64_t *num_count) {
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int b = 0; b < kSymBins; ++b) {
-        const int64_t n = ctr->sym_count[b];
-        for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n; t += stride) {
-            const int32_t i = sym_lists[b * sym_cap + t];
-            int lg = ceil_log2_2x(farc[i - rb]);
-            if (lg < kNumBinMinLog) lg = kNumBinMinLog;
-            const int nb = lg > kNumBinMaxLog ? kNumNumBins : lg - kNumBinMinLog;
-            const unsigned long long pos = atomicAdd((unsigned long long *)&num_count[nb], 1ull);
-            num_lists[nb * num_cap + (int64_t)pos] = i;
+// ------------------------------------------------------------------ row bins
+// Rows off the merge path are listed per bin in ASCENDING row order, so the
+// warps that run at the same time work on neighbouring rows and share their
+// CSC columns in L2 (banded / stencil inputs).  Deterministic three-step
+// partition: per-tile bin counts -> exclusive scan -> ordered scatter.
+//   mode 0 (symbolic): bin = bin8[r] (k_analyze_sym: ceil(log2(2 f_i)) bins)
+//   mode 1 (numeric):  bin = ceil(log2(2 farc_r)) clamped to [6, 11] -> 0..5,
+//                      larger (or a huge symbolic row) -> huge bin 6
+// Merge-path rows (bin8 = kBinNone) are in no list.
+constexpr int kBinThreads = 256;
+constexpr int kBinRounds = 4;
+constexpr int64_t kBinTile = (int64_t)kBinThreads * kBinRounds;
+constexpr int kBinWarps = kBinThreads / 32;
+
+__device__ __forceinline__ int row_bin(int mode, const uint8_t *__restrict__ bin8, const int32_t *__restrict__ farc,
+                                       int64_t r) {
+    const int b = bin8[r];
+    if (b == kBinNone) return -1;
+    if (mode == 0) return b;
+    int lg = ceil_log2_2x(farc[r]);
+    if (lg < kNumBinMinLog) lg = kNumBinMinLog;
+    return lg > kNumBinMaxLog ? kNumNumBins : lg - kNumBinMinLog;
+}
+
+__global__ void __launch_bounds__(kBinThreads) k_bin_count(int mode, const uint8_t *__restrict__ bin8,
+                                                           const int32_t *__restrict__ farc, int64_t nloc, int nb,
+                                                           unsigned *cnt, int64_t nt) {
+    __shared__ unsigned sc[kMaxBins];
+    for (int64_t tile = blockIdx.x; tile < nt; tile += gridDim.x) {
+        if (threadIdx.x < kMaxBins) sc[threadIdx.x] = 0;
+        __syncthreads();
+#pragma unroll
+        for (int j = 0; j < kBinRounds; ++j) {
+            const int64_t r = tile * kBinTile + j * kBinThreads + threadIdx.x;
+            const int b = r < nloc ? row_bin(mode, bin8, farc, r) : -1;
+            const unsigned g = __match_any_sync(kFull, b);
+            if (b >= 0 && lane_id() == __ffs(g) - 1) atomicAdd(&sc[b], (unsigned)__popc(g));
+        }
+        __syncthreads();
+        if (threadIdx.x < nb) cnt[(int64_t)threadIdx.x * nt + tile] = sc[threadIdx.x];
+        __syncthreads();
+    }
+}
+
+__global__ void __launch_bounds__(kBinThreads) k_bin_scatter(int mode, const uint8_t *__restrict__ bin8,
+                                                             const int32_t *__restrict__ farc, int64_t rb,
+                                                             int64_t nloc, int nb, const int64_t *__restrict__ off,
+                                                             int64_t nt, int32_t *lists, int64_t cap,
+                                                             int64_t *counts) {
+    __shared__ unsigned wc[kBinWarps][kMaxBins];
+    __shared__ int64_t run[kMaxBins];
+    const int w = threadIdx.x >> 5, l = lane_id();
+    if (counts && blockIdx.x == 0 && threadIdx.x < nb)
+        counts[threadIdx.x] = off[(int64_t)(threadIdx.x + 1) * nt] - off[(int64_t)threadIdx.x * nt];
+    for (int64_t tile = blockIdx.x; tile < nt; tile += gridDim.x) {
+        if (threadIdx.x < nb) run[threadIdx.x] = off[(int64_t)threadIdx.x * nt + tile] - off[(int64_t)threadIdx.x * nt];
+        for (int t = threadIdx.x; t < kBinWarps * kMaxBins; t += kBinThreads) (&wc[0][0])[t] = 0;
+        __syncthreads();
+        for (int j = 0; j < kBinRounds; ++j) {
+            const int64_t r = tile * kBinTile + j * kBinThreads + threadIdx.x;
+            const int b = r < nloc ? row_bin(mode, bin8, farc, r) : -1;
+            const unsigned g = __match_any_sync(kFull, b);
+            if (b >= 0 && l == __ffs(g) - 1) wc[w][b] = (unsigned)__popc(g);
+            __syncthreads();
+            if (b >= 0) {
+                int64_t pos = run[b] + __popc(g & lanemask_lt());
+                for (int v = 0; v < w; ++v) pos += wc[v][b];
+                lists[(int64_t)b * cap + pos] = (int32_t)(rb + r);
+            }
+            __syncthreads();
+            if (threadIdx.x < nb) {
+                unsigned t = 0;
+                for (int v = 0; v < kBinWarps; ++v) {
+                    t += wc[v][threadIdx.x];
+                    wc[v][threadIdx.x] = 0;
+                }
+                run[threadIdx.x] += t;
+            }
+            __syncthreads();
         }
     }
 }
 
-void launch_bin_num(const int32_t *sym_lists, int64_t sym_cap, const DevCounters *ctr, const int32_t *farc,
-                    int64_t rb, int32_t *num_lists, int64_t num_cap, int64_t *num_count, cudaStream_t s) {
-    k_bin_num<<<grid_for(num_cap, 256), 256, 0, s>>>(sym_lists, sym_cap, ctr, farc, rb, num_lists, num_cap,
-                                                      num_count);
+size_t bins_count_elems(int64_t nloc) { return (size_t)kMaxBins * (size_t)((nloc + kBinTile - 1) / kBinTile); }
+
+void launch_bins(int mode, const uint8_t *bin8, const int32_t *farc, int64_t rb, int64_t nloc, unsigned *cnt,
+                 int64_t *off, void *scan_tmp, int32_t *lists, int64_t cap, int64_t *counts, cudaStream_t s) {
+    const int nb = mode == 0 ? kSymBins : kNumBins;
+    const int64_t nt = (nloc + kBinTile - 1) / kBinTile;
+    if (nt == 0) return;
+    const unsigned g = (unsigned)std::min<int64_t>(nt, (int64_t)num_sms() * 8);
+    k_bin_count<<<g, kBinThreads, 0, s>>>(mode, bin8, farc, nloc, nb, cnt, nt);
+    note_launch();
+    scan_u32(cnt, (int64_t)nb * nt, off, scan_tmp, 0, s);
+    k_bin_scatter<<<g, kBinThreads, 0, s>>>(mode, bin8, farc, rb, nloc, nb, off, nt, lists, cap, counts);
     note_launch();
 }
 

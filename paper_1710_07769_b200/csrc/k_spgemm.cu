@@ -226,12 +226,14 @@ static int sms() {
 // merge-path rows get their structural nnz(C_i) right away, the others are
 // binned for the warp-hash / huge symbolic kernels by ceil(log2(2 f_i)).
 template <typename IdxT>
-__global__ void __launch_bounds__(kMergeThreads) k_analyze_sym(SymArgs a, int32_t *sym_lists, int64_t cap,
-                                                               DevCounters *ctr) {
+__global__ void __launch_bounds__(kMergeThreads) k_analyze_sym(SymArgs a, uint8_t *bin8, DevCounters *ctr) {
     const int64_t nloc = a.re - a.rb;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     int64_t local = 0;
     int maxlen = 0;
+    // per-thread bin counts, two 32-bit counters per register (bins 0..7;
+    // a thread sees at most nloc / stride rows, far below 2^32)
+    unsigned long long pc0 = 0, pc1 = 0, pc2 = 0, pc3 = 0;
     for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < nloc; r += stride) {
         const int64_t i = a.rb + r;
         const int64_t s = a.A.rp[i], e = a.A.rp[i + 1];
@@ -261,15 +263,35 @@ __global__ void __launch_bounds__(kMergeThreads) k_analyze_sym(SymArgs a, int32_
                 default: break;
             }
             a.nnzc[r] = c;
+            bin8[r] = kBinNone;
         } else {
             const int64_t m2 = 2 * (fi > 1 ? fi : 1);
             int lg = 64 - __clzll(m2 - 1);
             if (lg < kSymBinMinLog) lg = kSymBinMinLog;
             const int b = lg > kSymBinMaxLog ? kNumSymBins : lg - kSymBinMinLog;
-            const unsigned long long pos = atomicAdd((unsigned long long *)&ctr->sym_count[b], 1ull);
-            sym_lists[b * cap + (int64_t)pos] = (int32_t)i;
-            atomicAdd((unsigned long long *)&ctr->n_mid, 1ull);
+            bin8[r] = (uint8_t)b;
+            const unsigned long long inc = 1ull << (32 * (b & 1));
+            pc0 += (b >> 1) == 0 ? inc : 0ull;
+            pc1 += (b >> 1) == 1 ? inc : 0ull;
+            pc2 += (b >> 1) == 2 ? inc : 0ull;
+            pc3 += (b >> 1) == 3 ? inc : 0ull;
         }
+    }
+    pc0 = warp_sum(pc0);
+    pc1 = warp_sum(pc1);
+    pc2 = warp_sum(pc2);
+    pc3 = warp_sum(pc3);
+    if (lane_id() == 0 && (pc0 | pc1 | pc2 | pc3)) {
+        const unsigned long long pcs[4] = {pc0, pc1, pc2, pc3};
+        unsigned long long mid = 0;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const unsigned long long lo = pcs[q] & 0xffffffffull, hi = pcs[q] >> 32;
+            if (lo) atomicAdd((unsigned long long *)&ctr->sym_count[2 * q], lo);
+            if (hi) atomicAdd((unsigned long long *)&ctr->sym_count[2 * q + 1], hi);
+            mid += lo + hi;
+        }
+        atomicAdd((unsigned long long *)&ctr->n_mid, mid);
     }
     maxlen = __reduce_max_sync(kFull, maxlen);
     if (lane_id() == 0 && maxlen) atomicMax(&ctr->max_len, maxlen);
@@ -277,14 +299,14 @@ __global__ void __launch_bounds__(kMergeThreads) k_analyze_sym(SymArgs a, int32_
     if (lane_id() == 0 && local) atomicAdd((unsigned long long *)&ctr->products, (unsigned long long)local);
 }
 
-void launch_analyze_sym(const SymArgs &a, int32_t *sym_lists, int64_t cap, DevCounters *ctr, cudaStream_t s) {
+void launch_analyze_sym(const SymArgs &a, uint8_t *bin8, DevCounters *ctr, cudaStream_t s) {
     const int64_t nloc = a.re - a.rb;
     int64_t g = (nloc + kMergeThreads - 1) / kMergeThreads;
     g = g < 1 ? 1 : (g > (int64_t)sms() * 16 ? (int64_t)sms() * 16 : g);
     if (a.A.nnz <= INT32_MAX)
-        k_analyze_sym<int32_t><<<(unsigned)g, kMergeThreads, 0, s>>>(a, sym_lists, cap, ctr);
+        k_analyze_sym<int32_t><<<(unsigned)g, kMergeThreads, 0, s>>>(a, bin8, ctr);
     else
-        k_analyze_sym<int64_t><<<(unsigned)g, kMergeThreads, 0, s>>>(a, sym_lists, cap, ctr);
+        k_analyze_sym<int64_t><<<(unsigned)g, kMergeThreads, 0, s>>>(a, bin8, ctr);
     note_launch();
 }
 
@@ -383,9 +405,9 @@ __device__ __forceinline__ int find_seg(const Batch &b, int64_t pp) {
 
 // One product per lane for the chunk [c0, c0+32) of a batch.  The lane's
 // segment (row entry) comes from an OR-reduced bitmask of the segment starts
-// that fall inside the chunk -- no shuffle search.
+// that fall inside the chunk -- no shuffle search.  Lanes past the batch get
+// j = -2 - lane (negative and pairwise distinct).
 struct Chunk {
-    bool valid;
     int j;
     double b;  // a_hat_jk
     double a;  // a_hat_ik
@@ -400,12 +422,36 @@ __device__ __forceinline__ Chunk fetch_chunk(const Csc &T, const Batch &b, int64
     const int seg = (seg0 + __popc(starts & ((2u << l) - 1u))) & 31;
     const int64_t pp = c0 + l;
     Chunk c;
-    c.valid = pp < b.total;
+    const bool valid = pp < b.total;
     const int64_t q = __shfl_sync(kFull, b.cs - b.excl, seg) + pp;
     c.a = NEED_VAL ? shfl_d(b.a, seg) : 0.0;
-    c.j = c.valid ? T.ri[q] : -2 - l;
-    c.b = (NEED_VAL && c.valid) ? T.vt[q] : 0.0;
+    c.j = valid ? T.ri[q] : -2 - l;
+    c.b = (NEED_VAL && valid) ? T.vt[q] : 0.0;
     return c;
+}
+
+// One column segment (or a 32-entry piece of a longer one) of row entry t of
+// a batch: lane l takes entry off + l of column k_t.  Keys inside a piece are
+// distinct (rows of one column), so a piece updates its accumulators with no
+// conflicts and no chains -- the segment mode of the numeric warp kernel.
+struct Piece {
+    int j;      // -1: lane idle
+    double b;   // a_hat_jk
+    double a;   // a_hat_ik (uniform)
+    int64_t len;  // column length (uniform)
+};
+
+__device__ __forceinline__ Piece fetch_piece(const Csc &T, const Batch &b, int t, int64_t off) {
+    const int l = lane_id();
+    Piece p;
+    const int64_t cs = __shfl_sync(kFull, b.cs, t);
+    p.len = __shfl_sync(kFull, b.incl - b.excl, t);
+    p.a = shfl_d(b.a, t);
+    const bool valid = off + l < p.len;
+    const int64_t q = cs + off + l;
+    p.j = valid ? T.ri[q] : -1;
+    p.b = valid ? T.vt[q] : 0.0;
+    return p;
 }
 
 __device__ __forceinline__ unsigned hash_key(int j, int logt) {
@@ -423,7 +469,7 @@ __device__ __forceinline__ unsigned hash_key(int j, int logt) {
 constexpr int kWarpHashThreads = 128;  // 4 warps per CTA, many CTAs per SM
 constexpr int kWinHalf = 128;
 constexpr int kWin = 2 * kWinHalf;
-constexpr int kWinWords = kWin / 32;
+constexpr int kWinSeenWords = kWin / 4;  // symbolic: one byte per window slot
 constexpr int kFarHuge = 1 << 30;  // farc marker: route the numeric pass to the huge path
 
 template <int LOGT>
@@ -432,18 +478,19 @@ __global__ void __launch_bounds__(kWarpHashThreads) k_sym_warp(SymArgs a, const 
     constexpr int T = 1 << LOGT;
     extern __shared__ int32_t sym_tab[];
     const int w = threadIdx.x >> 5, l = lane_id();
-    int32_t *keys = sym_tab + w * (T + kWinWords);
-    unsigned *wbits = reinterpret_cast<unsigned *>(keys + T);
+    int32_t *keys = sym_tab + w * (T + kWinSeenWords);
+    unsigned *seenw = reinterpret_cast<unsigned *>(keys + T);  // one byte per window slot
+    unsigned char *seen = reinterpret_cast<unsigned char *>(seenw);
     const int64_t n = *count;
     for (int s = l; s < T; s += 32) keys[s] = -1;
-    if (l < kWinWords) wbits[l] = 0u;
+    for (int s = l; s < kWinSeenWords; s += 32) seenw[s] = 0u;
     __syncwarp();
     const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
     for (int64_t idx = blockIdx.x * (int64_t)(blockDim.x >> 5) + w; idx < n; idx += nw) {
         const int64_t i = list[idx];
         const int64_t s = a.A.rp[i], e = a.A.rp[i + 1];
         const int64_t wbase = i - kWinHalf;
-        int nnear = 0, nfar = 0;
+        int nfar = 0;
         for (int64_t base = s; base < e; base += 32) {
             const Batch b = load_batch(a.A, a.T, base, e, false);
             Chunk cur = fetch_chunk<false>(a.T, b, 0);
@@ -451,35 +498,28 @@ __global__ void __launch_bounds__(kWarpHashThreads) k_sym_warp(SymArgs a, const 
                 Chunk nxt = cur;
                 if (c0 + 32 < b.total) nxt = fetch_chunk<false>(a.T, b, c0 + 32);
                 const int64_t d = (int64_t)cur.j - wbase;
-                const bool near = cur.valid && d >= 0 && d < kWin;
-                // window: one OR per touched bitmap word (no same-word atomics)
-                unsigned touched = __reduce_or_sync(kFull, near ? (1u << (int)(d >> 5)) : 0u);
-                while (touched) {
-                    const int wd = __ffs(touched) - 1;
-                    touched &= touched - 1;
-                    const unsigned m = __reduce_or_sync(kFull, (near && (d >> 5) == wd) ? (1u << (int)(d & 31)) : 0u);
-                    if (l == 0) {
-                        const unsigned old = wbits[wd];
-                        nnear += __popc(m & ~old);
-                        wbits[wd] = old | m;
-                    }
-                }
-                if (cur.valid && !near) {
-                    unsigned sl = hash_key(cur.j, LOGT);
-                    while (true) {
-                        const int prev = atomicCAS(&keys[sl], -1, cur.j);
-                        if (prev == -1) {
-                            ++nfar;
-                            break;
+                if (cur.j >= 0) {
+                    if (d >= 0 && d < kWin) {
+                        seen[d] = 1;  // idempotent: no atomics, duplicates harmless
+                    } else {
+                        unsigned sl = hash_key(cur.j, LOGT);
+                        while (true) {
+                            const int prev = atomicCAS(&keys[sl], -1, cur.j);
+                            if (prev == -1) {
+                                ++nfar;
+                                break;
+                            }
+                            if (prev == cur.j) break;
+                            sl = (sl + 1) & (T - 1);
                         }
-                        if (prev == cur.j) break;
-                        sl = (sl + 1) & (T - 1);
                     }
                 }
-                __syncwarp();
                 cur = nxt;
             }
         }
+        __syncwarp();
+        int nnear = 0;
+        for (int s2 = l; s2 < kWinSeenWords; s2 += 32) nnear += __popc(seenw[s2]);  // bytes are 0 / 1
         nnear = warp_sum(nnear);
         nfar = warp_sum(nfar);
         if (l == 0) {
@@ -488,7 +528,7 @@ __global__ void __launch_bounds__(kWarpHashThreads) k_sym_warp(SymArgs a, const 
         }
         __syncwarp();
         for (int s2 = l; s2 < T; s2 += 32) keys[s2] = -1;
-        if (l < kWinWords) wbits[l] = 0u;
+        for (int s2 = l; s2 < kWinSeenWords; s2 += 32) seenw[s2] = 0u;
         __syncwarp();
     }
 }
@@ -496,7 +536,7 @@ __global__ void __launch_bounds__(kWarpHashThreads) k_sym_warp(SymArgs a, const 
 template <int LOGT>
 static void launch_sym_warp_t(const SymArgs &a, const int32_t *list, const int64_t *count, cudaStream_t s) {
     constexpr int T = 1 << LOGT;
-    const size_t smem = (size_t)(kWarpHashThreads / 32) * (T + kWinWords) * sizeof(int32_t);
+    const size_t smem = (size_t)(kWarpHashThreads / 32) * (T + kWinSeenWords) * sizeof(int32_t);
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(k_sym_warp<LOGT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -522,16 +562,32 @@ void launch_sym_warp(const SymArgs &a, const int32_t *lists, int64_t cap, const 
 // Numeric, per warp (T = 2^LOGT far-table slots >= 2 * far keys):
 //   wv[kWin] window values, vals[T] / keys[T] far table (+0.0 / -1 when
 //   empty; reused as the second radix buffer), radix buffer of T/2
-//   (key, value), window bitmap, hist[256].
+//   (key, value), hist[256].  Every accumulator starts at +0.0, so the first
+//   fma of a chain sees +0.0 exactly as in the ordering contract; an
+//   untouched window slot reads +0.0 and is never emitted (|c| > tol >= 0).
 template <int LOGT>
 struct NumWarpSmem {
     static constexpr int T = 1 << LOGT;
-    static constexpr size_t bytes =
-        (size_t)kWin * 8 + (size_t)T * 8 + (size_t)T * 4 + (size_t)(T / 2) * 12 + kWinWords * 4 + 256 * 4;
+    static constexpr size_t bytes = (size_t)kWin * 8 + (size_t)T * 8 + (size_t)T * 4 + (size_t)(T / 2) * 12 + 256 * 4;
 };
 
+// Segment mode when the batch's mean column length is at least this.
+constexpr int kSegMinMean = 12;
+
 template <int LOGT>
-__global__ void __launch_bounds__(kWarpHashThreads) k_num_warp(NumArgs a, const int32_t *__restrict__ list,
+__device__ __forceinline__ double *far_slot(int32_t *keys, double *vals, int j) {
+    constexpr int T = 1 << LOGT;
+    unsigned sl = hash_key(j, LOGT);
+    while (true) {
+        const int prev = atomicCAS(&keys[sl], -1, j);
+        if (prev == -1 || prev == j) break;
+        sl = (sl + 1) & (T - 1);
+    }
+    return vals + sl;
+}
+
+template <int LOGT>
+__global__ void __launch_bounds__(kWarpHashThreads, 1) k_num_warp(NumArgs a, const int32_t *__restrict__ list,
                                                                const int64_t *count) {
     constexpr int T = 1 << LOGT;
     constexpr int H = T / 2;
@@ -544,8 +600,7 @@ __global__ void __launch_bounds__(kWarpHashThreads) k_num_warp(NumArgs a, const 
     double *av = vals + T;
     int32_t *keys = reinterpret_cast<int32_t *>(av + H);
     int32_t *ak = keys + T;
-    unsigned *wbits = reinterpret_cast<unsigned *>(ak + H);
-    int32_t *hist = reinterpret_cast<int32_t *>(wbits + kWinWords);
+    int32_t *hist = ak + H;
     const unsigned lt = lanemask_lt();
     Comp cut;
     int badp = 0;
@@ -554,7 +609,7 @@ __global__ void __launch_bounds__(kWarpHashThreads) k_num_warp(NumArgs a, const 
         keys[s] = -1;
         vals[s] = +0.0;
     }
-    if (l < kWinWords) wbits[l] = 0u;
+    for (int s = l; s < kWin; s += 32) wv[s] = +0.0;
     __syncwarp();
     const int64_t n = *count;
     const int64_t nw = (int64_t)gridDim.x * WPB;
@@ -563,59 +618,68 @@ __global__ void __launch_bounds__(kWarpHashThreads) k_num_warp(NumArgs a, const 
         const int64_t r = i - a.rb;
         const int64_t s = a.A.rp[i], e = a.A.rp[i + 1];
         const int64_t wbase = i - kWinHalf;
-        // ---- accumulate (ordered chains)
+        // ---- accumulate (ordered chains: products applied in ascending k)
         for (int64_t bb = s; bb < e; bb += 32) {
             const Batch b = load_batch(a.A, a.T, bb, e, true);
+            const int nent = (int)min((int64_t)32, e - bb);
+            if (b.total >= (int64_t)kSegMinMean * nent) {
+                // segment mode: one column (piece) per round, keys distinct
+                int t = 0;
+                int64_t off = 0;
+                Piece cur = fetch_piece(a.T, b, 0, 0);
+                while (true) {
+                    int tn = t;
+                    int64_t offn = off + 32;
+                    if (offn >= cur.len) {
+                        tn = t + 1;
+                        offn = 0;
+                    }
+                    const bool more = tn < nent;
+                    Piece nxt = cur;
+                    if (more) nxt = fetch_piece(a.T, b, tn, offn);
+                    if (cur.j >= 0) {
+                        const int64_t d = (int64_t)cur.j - wbase;
+                        double *acc = (d >= 0 && d < kWin) ? wv + d : far_slot<LOGT>(keys, vals, cur.j);
+                        *acc = __fma_rn(cur.a, cur.b, *acc);
+                    }
+                    __syncwarp();
+                    if (!more) break;
+                    cur = nxt;
+                    t = tn;
+                    off = offn;
+                }
+                continue;
+            }
+            // chunk mode: 32 products per round; a key repeated inside the
+            // chunk (several columns) is chained through its lanes in order
             Chunk cur = fetch_chunk<true>(a.T, b, 0);
             for (int64_t c0 = 0; c0 < b.total; c0 += 32) {
                 Chunk nxt = cur;
                 if (c0 + 32 < b.total) nxt = fetch_chunk<true>(a.T, b, c0 + 32);
-                const bool valid = cur.valid;
                 const int j = cur.j;
+                const bool valid = j >= 0;
                 const int64_t d = (int64_t)j - wbase;
                 const bool near = valid && d >= 0 && d < kWin;
                 const unsigned g = __match_any_sync(kFull, j);
                 const int leader = __ffs(g) - 1;
                 const int rank = __popc(g & lt);
                 const int cnt = __popc(g);
-                const bool lead = valid && l == leader;
-                int slot = near ? (int)d : 0;
+                double *accp = wv;
                 double acc = 0.0;
-                if (lead && near) {  // first touch of a window key starts its chain at +0.0
-                    acc = ((wbits[slot >> 5] >> (slot & 31)) & 1u) ? wv[slot] : +0.0;
+                if (valid && l == leader) {
+                    accp = near ? wv + d : far_slot<LOGT>(keys, vals, j);
+                    acc = *accp;
                 }
-                __syncwarp();  // old bits read before the bitmap update
-                unsigned touched = __reduce_or_sync(kFull, (lead && near) ? (1u << (slot >> 5)) : 0u);
-                while (touched) {
-                    const int wd = __ffs(touched) - 1;
-                    touched &= touched - 1;
-                    const unsigned m =
-                        __reduce_or_sync(kFull, (lead && near && (slot >> 5) == wd) ? (1u << (slot & 31)) : 0u);
-                    if (l == 0) wbits[wd] |= m;
-                }
-                if (lead && !near) {
-                    unsigned sl = hash_key(j, LOGT);
-                    while (true) {
-                        const int prev = atomicCAS(&keys[sl], -1, j);
-                        if (prev == -1 || prev == j) break;
-                        sl = (sl + 1) & (T - 1);
-                    }
-                    slot = (int)sl;
-                    acc = vals[slot];
-                }
-                slot = __shfl_sync(kFull, slot, leader);
                 const int pred = rank ? 31 - __clz(g & lt) : l;
                 const int maxc = __reduce_max_sync(kFull, valid ? cnt : 0);
                 for (int it = 0; it < maxc; ++it) {
                     const double x = shfl_d(acc, pred);
                     if (valid && rank == it) acc = __fma_rn(cur.a, cur.b, rank == 0 ? acc : x);
                 }
-                if (valid && rank == cnt - 1) {
-                    if (near)
-                        wv[slot] = acc;
-                    else
-                        vals[slot] = acc;
-                }
+                // the last lane of each key's group stores the chain's value
+                const int last = 31 - __clz(g);
+                const unsigned long long pa = __shfl_sync(kFull, (unsigned long long)accp, leader);
+                if (valid && l == last) *reinterpret_cast<double *>(pa) = acc;
                 __syncwarp();
                 cur = nxt;
             }
@@ -731,10 +795,10 @@ __global__ void __launch_bounds__(kWarpHashThreads) k_num_warp(NumArgs a, const 
             const bool v = e2 < nbelow;
             emit(v, v ? ck[e2] : -1, v ? cv[e2] : 0.0);
         }
-        for (int rd = 0; rd < kWinWords; ++rd) {
-            const int slot = rd * 32 + l;
-            const bool v = (wbits[rd] >> l) & 1u;
-            emit(v, (int)(wbase + slot), v ? wv[slot] : 0.0);
+        for (int slot = l; slot < kWin; slot += 32) {  // untouched slots hold +0.0: never kept
+            const int64_t key = wbase + slot;
+            emit(key >= 0, (int)key, wv[slot]);
+            wv[slot] = +0.0;
         }
         for (int rd = nbelow; rd < L; rd += 32) {
             const int e2 = rd + l;
@@ -747,7 +811,6 @@ __global__ void __launch_bounds__(kWarpHashThreads) k_num_warp(NumArgs a, const 
             keys[s2] = -1;
             vals[s2] = +0.0;
         }
-        if (l < kWinWords) wbits[l] = 0u;
         if (o < ub) {
             for (int64_t t = o + l; t < ub; t += 32) a.gcol[g0 + t] = -1;
             if (l == 0) atomicOr(a.holes, 1);

@@ -304,6 +304,11 @@ static void plan_build(rig_plan *p, const rig_csr_t *Ain, int64_t *gptr_out, boo
     const size_t o_sym = L.add(sizeof(int32_t) * (size_t)kSymBins * (size_t)std::max<int64_t>(nloc, 1));
     const size_t o_nnzc = L.add(sizeof(int64_t) * (size_t)nloc);
     const size_t o_farc = L.add(sizeof(int32_t) * (size_t)nloc);
+    const size_t o_bin8 = L.add((size_t)nloc);
+    const size_t nbc = bins_count_elems(nloc);
+    const size_t o_bcnt = L.add(sizeof(unsigned) * nbc);
+    const size_t o_boff = L.add(sizeof(int64_t) * (nbc + 1));
+    const size_t o_bst = L.add(scan_tmp_bytes((int64_t)nbc));
     const size_t o_gptr = gptr_out ? 0 : L.add(sizeof(int64_t) * (size_t)(nloc + 1));
     unsigned char *ws = p->cached ? ws_get(0, L.bytes, s) : p->arena.raw(L.bytes);
     CK(cudaMemsetAsync(ws, 0, zero_bytes, s));
@@ -318,6 +323,9 @@ static void plan_build(rig_plan *p, const rig_csr_t *Ain, int64_t *gptr_out, boo
     p->farc = reinterpret_cast<int32_t *>(ws + o_farc);
     p->gptr_ub = gptr_out ? gptr_out : reinterpret_cast<int64_t *>(ws + o_gptr);
     p->list_cap = nloc;
+    uint8_t *bin8 = reinterpret_cast<uint8_t *>(ws + o_bin8);
+    unsigned *bcnt = reinterpret_cast<unsigned *>(ws + o_bcnt);
+    int64_t *boff = reinterpret_cast<int64_t *>(ws + o_boff);
     HostStage *hs = host_stage();
 
     // a0: validation must finish before anything indexes with the input
@@ -349,7 +357,7 @@ static void plan_build(rig_plan *p, const rig_csr_t *Ain, int64_t *gptr_out, boo
     SymArgs sa{p->A, p->T, p->rb, p->re, p->nnzc, p->farc};
     if (nloc > 0) {
         Prof pf(P_ANALYZE, s);
-        launch_analyze_sym(sa, p->sym_lists, p->list_cap, p->ctr, s);
+        launch_analyze_sym(sa, bin8, p->ctr, s);
     }
     check_launch("analyze");
     // sync 1: errors, products, bin sizes
@@ -361,6 +369,7 @@ static void plan_build(rig_plan *p, const rig_csr_t *Ain, int64_t *gptr_out, boo
     const int64_t n_mid = p->h.n_mid;
     if (n_mid > 0) {
         Prof pf(P_SYMBOLIC, s);
+        launch_bins(0, bin8, nullptr, p->rb, nloc, bcnt, boff, ws + o_bst, p->sym_lists, p->list_cap, nullptr, s);
         launch_sym_warp(sa, p->sym_lists, p->list_cap, p->ctr->sym_count, p->h.sym_count, s);
         // rows with f > 1024 may need the huge numeric path too (nnzC <= f)
         const int64_t n_big = p->h.sym_count[kNumSymBins] + p->h.sym_count[kNumSymBins - 1];
@@ -381,7 +390,7 @@ static void plan_build(rig_plan *p, const rig_csr_t *Ain, int64_t *gptr_out, boo
         if (p->h.sym_count[kNumSymBins] > 0)
             launch_sym_huge(sa, p->sym_lists + (int64_t)kNumSymBins * p->list_cap, p->ctr->sym_count + kNumSymBins,
                             p->huge_slots_n, p->huge_scratch, s);
-        launch_bin_num(p->sym_lists, p->list_cap, p->ctr, p->farc, p->rb, p->num_lists, n_mid, p->ctr->num_count, s);
+        launch_bins(1, bin8, p->farc, p->rb, nloc, bcnt, boff, ws + o_bst, p->num_lists, n_mid, p->ctr->num_count, s);
     }
     check_launch("symbolic");
     {
@@ -772,7 +781,7 @@ int rig_row_split(const rig_csr_t *A, int32_t parts, int64_t *split, rig_stream_
     Prof pf(P_SPLIT, s);
     if (A->nnz > 0) launch_col_hist(A0, cnt, nullptr, s);
     scan_u32(cnt, m, cp, ws + o_st1, 0, s);
-    if (n > 0) launch_analyze(A0, cp, 0, n, f, nullptr, 0, ctr, s);
+    if (n > 0) launch_analyze(A0, cp, 0, n, f, ctr, s);
     scan_i64(f, n, fp, ScanOp::Identity, ws + o_st2, 0, s);
     launch_split(fp, n, parts, sp, s);
     check_launch("split");
