@@ -24,12 +24,10 @@ enum : int {
 // <= kMergeMaxF take the thread-per-row k-way merge path (k_spgemm.cu).
 constexpr int kMergeMaxLen = 8;
 constexpr int64_t kMergeMaxF = 4096;
-// Warp-hash bins: symbolic table T = next_pow2(2 f) in [64, 4096] (keys only);
-// numeric table T = next_pow2(2 nnzC) in [64, 2048] (key + value).
+// Rows off the merge path are binned by ceil(log2(2 f_i)) in [6, 12]
+// (bins 0..6: the mid-row kernels); beyond that the huge bin kNumSymBins.
 constexpr int kSymBinMinLog = 6, kSymBinMaxLog = 12;
-constexpr int kNumBinMinLog = 6, kNumBinMaxLog = 11;
 constexpr int kNumSymBins = kSymBinMaxLog - kSymBinMinLog + 1;  // 7
-constexpr int kNumNumBins = kNumBinMaxLog - kNumBinMinLog + 1;  // 6
 
 struct Csr {
     int64_t nrows, ncols, nnz;
@@ -49,7 +47,6 @@ __device__ __forceinline__ int64_t csc_begin(const Csc &T, int k) { return T.cp[
 
 // Counters written by the device and read back by the host at a sync.
 constexpr int kSymBins = kNumSymBins + 1;  // + huge
-constexpr int kNumBins = kNumNumBins + 1;  // + huge
 struct DevCounters {
     int err;
     int holes;          // numeric pass dropped an entry (|c| <= tol or exact 0)
@@ -57,8 +54,12 @@ struct DevCounters {
     int max_len;        // longest A row (in the shard) on the merge path
     int64_t products;   // sum f_i over the shard
     int64_t n_mid;      // rows not on the merge path
+    int64_t nnz_rows;      // sum of A-row lengths over the shard
+    int64_t max_f;         // largest f_i off the merge path
+    int64_t mid_slots;     // sum (f_i - len_i) off the merge path: temporary entries
     int64_t sym_count[8];
-    int64_t num_count[8];
+    int64_t list_count[2]; // mid / huge list lengths (device side)
+    int64_t defer_count[2];// rows deferred by the small / big mid kernels
 };
 
 __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
@@ -102,19 +103,20 @@ void launch_col_hist(const Csr &A, unsigned *cnt, unsigned *rank /*nullable*/, c
 // k_transpose.cu: bucketed a1 + a2 (see there for the CSC layout with sentinels)
 int64_t transpose_buckets(int64_t nnz, int64_t ncols);
 constexpr size_t kTransposeRecBytes = 16;
+// bcur: u64[transpose_buckets] zeroed; gcur: u32[ncols] zeroed; big: int[1 + transpose_buckets]
+// with big[0] zeroed (list of buckets too large for the warp sort).
 void launch_transpose(const Csr &A, int scale, const int64_t *cp, double *ahat, unsigned long long *bcur,
-                      void *rec, unsigned *gcur, int32_t *ri, double *vt, int *err, cudaStream_t s);
+                      void *rec, unsigned *gcur, int *big, int32_t *ri, double *vt, int *err, cudaStream_t s);
 void launch_analyze(const Csr &A, const int64_t *cp, int64_t rb, int64_t re, int64_t *f, DevCounters *ctr,
                     cudaStream_t s);
-// Ordered row bins (k_prep.cu): mode 0 symbolic (from bin8), mode 1 numeric
-// (from farc); lists[b * cap ...] in ascending row order; counts[b] written
-// when non-null.  cnt: u32[bins_count_elems(nloc)], off: int64[that + 1],
+// Ordered row lists (k_prep.cu): list 0 = mid rows (bin8 < kNumSymBins),
+// list 1 = huge rows; lists[b * cap ...] in ascending row order; counts[b]
+// written when non-null.  cnt: u32[bins_count_elems(nloc)], off: int64[that + 1],
 // scan_tmp: scan_tmp_bytes(that).
-constexpr int kMaxBins = 8;
 constexpr uint8_t kBinNone = 0xff;  // bin8 of a merge-path row
 size_t bins_count_elems(int64_t nloc);
-void launch_bins(int mode, const uint8_t *bin8, const int32_t *farc, int64_t rb, int64_t nloc, unsigned *cnt,
-                 int64_t *off, void *scan_tmp, int32_t *lists, int64_t cap, int64_t *counts, cudaStream_t s);
+void launch_bins(const uint8_t *bin8, int64_t rb, int64_t nloc, unsigned *cnt, int64_t *off, void *scan_tmp,
+                 int32_t *lists, int64_t cap, int64_t *counts, cudaStream_t s);
 
 // k_scan.cu: out[0..n] = exclusive prefix of in[0..n-1] (out[n] = total).
 enum class ScanOp { Identity, UbOffDiag };
@@ -128,8 +130,8 @@ struct SymArgs {
     Csr A;
     Csc T;
     int64_t rb, re;
-    int64_t *nnzc;  // [re-rb]
-    int32_t *farc;  // [re-rb] distinct far keys (warp path; numeric binning)
+    int64_t *nnzc;  // [re-rb] merge rows: structural nnz(C_i) incl. the diagonal
+    int64_t *fnm;   // [re-rb] rows off the merge path: f_i - len_i (temporary slots), else 0
 };
 struct NumArgs {
     Csr A;
@@ -200,7 +202,7 @@ inline int stage_cap_for(int64_t products, int64_t rows) {
 
 // Cut slots reserved per numeric launch in the fused-cut partials array.
 constexpr int kCutSlotsPerLaunch = 4096;
-constexpr int kCutLaunches = 8;  // merge + 6 warp bins + huge
+constexpr int kCutLaunches = 8;  // merge, mid small, mid big, huge (+ spare slots)
 // a3 + a4(merge rows) fused: products, merge-row nnzC, bins for the others
 // bin8[r]: symbolic bin of row r, or kBinNone on the merge path;
 // ctr->sym_count / n_mid: bin totals.
@@ -208,19 +210,39 @@ void launch_analyze_sym(const SymArgs &a, uint8_t *bin8, DevCounters *ctr, cudaS
 // maxlen: longest A row on the merge path in the shard (DevCounters::max_len)
 void launch_sym_merge(const SymArgs &a, int maxlen, cudaStream_t s);
 void launch_num_merge(const NumArgs &a, int maxlen, cudaStream_t s);
-// counts: device bin sizes (loop bounds); hcounts: host copy (skip empty bins)
-void launch_sym_warp(const SymArgs &a, const int32_t *lists, int64_t list_cap, const int64_t *counts,
-                     const int64_t *hcounts, cudaStream_t s);
-void launch_num_warp(const NumArgs &a, const int32_t *lists, int64_t list_cap, const int64_t *counts,
-                     const int64_t *hcounts, cudaStream_t s);
+// Rows off the merge path (k_midrow.cu, k_spgemm.cu huge path): each row is
+// written with its exact kept entries to a temporary at toff[r] and
+// cnt[r] = kept + 1 (the graph scan subtracts the diagonal slot); k_copy_rows
+// places it after the scan.
+struct MidArgs {
+    Csr A;
+    Csc T;
+    int64_t rb;
+    const int32_t *list;    // rows (global ids) to process
+    const int64_t *count;   // device: number of rows in list
+    const int64_t *toff;    // [nloc] temporary offsets
+    int32_t *tcol;
+    double *tw;
+    int64_t *cnt;           // [nloc] out
+    int32_t *defer_list;    // rows whose far list overflowed this kernel's capacity
+    int64_t *defer_count;
+    double *diag;           // may be null
+    double tol;
+    const int32_t *part;    // fused a7 (optional), as in NumArgs
+    int32_t K;
+    double *cutp;
+    int *bad_part;
+    int *cut_used;
+};
+constexpr int kMidSmallCap = 256, kMidBigCap = 2048;  // far-list capacities of the two mid kernels
+void launch_num_mid(const MidArgs &a, int fcap, cudaStream_t s);
+void launch_copy_rows(const int32_t *list, const int64_t *count, int64_t rb, const int64_t *toff, const int64_t *gptr,
+                      const int32_t *tcol, const double *tw, int32_t *gcol, double *gw, cudaStream_t s);
 // huge rows: CTA per row, dense accumulator + bitmap in global scratch
 size_t huge_scratch_bytes(int64_t nrows, int slots, bool numeric);
 size_t huge_bitmap_bytes(int64_t nrows, int slots);  // zeroed prefix of the scratch
 int huge_slots(int64_t nrows, int64_t n_huge);
-void launch_sym_huge(const SymArgs &a, const int32_t *list, const int64_t *count, int slots, void *scratch,
-                     cudaStream_t s);
-void launch_num_huge(const NumArgs &a, const int32_t *list, const int64_t *count, int slots, void *scratch,
-                     cudaStream_t s);
+void launch_num_huge(const MidArgs &a, int slots, void *scratch, cudaStream_t s);
 
 // k_post.cu
 void launch_count_kept(const int64_t *gptr_ub, int64_t nloc, const int32_t *gcol, int64_t *kept, cudaStream_t s);

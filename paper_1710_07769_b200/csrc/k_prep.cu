@@ -76,10 +76,6 @@ void launch_col_hist(const Csr &A, unsigned *cnt, unsigned *rank, cudaStream_t s
 // ------------------------------------------------------------------ a3
 // f_i = sum over k in row i of nnz(column k) (Gustavson products), for the
 // flop-balanced row split.  (The build path computes f_i in k_analyze_sym.)
-__device__ __forceinline__ int ceil_log2_2x(int64_t m) {
-    const int64_t m2 = 2 * (m > 1 ? m : 1);
-    return 64 - __clzll(m2 - 1);
-}
 
 __global__ void k_analyze(Csr A, const int64_t *__restrict__ cp, int64_t rb, int64_t re, int64_t *f,
                           DevCounters *ctr) {
@@ -114,82 +110,77 @@ void launch_analyze(const Csr &A, const int64_t *cp, int64_t rb, int64_t re, int
     note_launch();
 }
 
-// ------------------------------------------------------------------ row bins
-// Rows off the merge path are listed per bin in ASCENDING row order, so the
-// warps that run at the same time work on neighbouring rows and share their
-// CSC columns in L2 (banded / stencil inputs).  Deterministic three-step
-// partition: per-tile bin counts -> exclusive scan -> ordered scatter.
-//   mode 0 (symbolic): bin = bin8[r] (k_analyze_sym: ceil(log2(2 f_i)) bins)
-//   mode 1 (numeric):  bin = ceil(log2(2 farc_r)) clamped to [6, 11] -> 0..5,
-//                      larger (or a huge symbolic row) -> huge bin 6
-// Merge-path rows (bin8 = kBinNone) are in no list.
+// ------------------------------------------------------------------ row lists
+// Rows off the merge path are listed in ASCENDING row order (list 0: mid
+// rows, list 1: huge rows), so the warps that run at the same time work on
+// neighbouring rows and share their CSC columns in L2 (banded / stencil
+// inputs).  Deterministic three-step partition: per-tile counts -> exclusive
+// scan -> ordered scatter.  Merge-path rows (bin8 = kBinNone) are in no list.
 constexpr int kBinThreads = 256;
 constexpr int kBinRounds = 4;
 constexpr int64_t kBinTile = (int64_t)kBinThreads * kBinRounds;
 constexpr int kBinWarps = kBinThreads / 32;
+constexpr int kLists = 2;
 
-__device__ __forceinline__ int row_bin(int mode, const uint8_t *__restrict__ bin8, const int32_t *__restrict__ farc,
-                                       int64_t r) {
+__device__ __forceinline__ int row_list(const uint8_t *__restrict__ bin8, int64_t r) {
     const int b = bin8[r];
     if (b == kBinNone) return -1;
-    if (mode == 0) return b;
-    int lg = ceil_log2_2x(farc[r]);
-    if (lg < kNumBinMinLog) lg = kNumBinMinLog;
-    return lg > kNumBinMaxLog ? kNumNumBins : lg - kNumBinMinLog;
+    return b == kNumSymBins ? 1 : 0;
 }
 
-__global__ void __launch_bounds__(kBinThreads) k_bin_count(int mode, const uint8_t *__restrict__ bin8,
-                                                           const int32_t *__restrict__ farc, int64_t nloc, int nb,
+__global__ void __launch_bounds__(kBinThreads) k_bin_count(const uint8_t *__restrict__ bin8, int64_t nloc,
                                                            unsigned *cnt, int64_t nt) {
-    __shared__ unsigned sc[kMaxBins];
+    __shared__ unsigned sc[kLists];
     for (int64_t tile = blockIdx.x; tile < nt; tile += gridDim.x) {
-        if (threadIdx.x < kMaxBins) sc[threadIdx.x] = 0;
+        if (threadIdx.x < kLists) sc[threadIdx.x] = 0;
         __syncthreads();
 #pragma unroll
         for (int j = 0; j < kBinRounds; ++j) {
             const int64_t r = tile * kBinTile + j * kBinThreads + threadIdx.x;
-            const int b = r < nloc ? row_bin(mode, bin8, farc, r) : -1;
-            const unsigned g = __match_any_sync(kFull, b);
-            if (b >= 0 && lane_id() == __ffs(g) - 1) atomicAdd(&sc[b], (unsigned)__popc(g));
+            const int b = r < nloc ? row_list(bin8, r) : -1;
+#pragma unroll
+            for (int q = 0; q < kLists; ++q) {
+                const unsigned m = __ballot_sync(kFull, b == q);
+                if (lane_id() == 0 && m) atomicAdd(&sc[q], (unsigned)__popc(m));
+            }
         }
         __syncthreads();
-        if (threadIdx.x < nb) cnt[(int64_t)threadIdx.x * nt + tile] = sc[threadIdx.x];
+        if (threadIdx.x < kLists) cnt[(int64_t)threadIdx.x * nt + tile] = sc[threadIdx.x];
         __syncthreads();
     }
 }
 
-__global__ void __launch_bounds__(kBinThreads) k_bin_scatter(int mode, const uint8_t *__restrict__ bin8,
-                                                             const int32_t *__restrict__ farc, int64_t rb,
-                                                             int64_t nloc, int nb, const int64_t *__restrict__ off,
-                                                             int64_t nt, int32_t *lists, int64_t cap,
-                                                             int64_t *counts) {
-    __shared__ unsigned wc[kBinWarps][kMaxBins];
-    __shared__ int64_t run[kMaxBins];
+__global__ void __launch_bounds__(kBinThreads) k_bin_scatter(const uint8_t *__restrict__ bin8, int64_t rb,
+                                                             int64_t nloc, const int64_t *__restrict__ off, int64_t nt,
+                                                             int32_t *lists, int64_t cap, int64_t *counts) {
+    __shared__ unsigned wc[kBinWarps][kLists];
+    __shared__ int64_t run[kLists];
     const int w = threadIdx.x >> 5, l = lane_id();
-    if (counts && blockIdx.x == 0 && threadIdx.x < nb)
+    if (counts && blockIdx.x == 0 && threadIdx.x < kLists)
         counts[threadIdx.x] = off[(int64_t)(threadIdx.x + 1) * nt] - off[(int64_t)threadIdx.x * nt];
     for (int64_t tile = blockIdx.x; tile < nt; tile += gridDim.x) {
-        if (threadIdx.x < nb) run[threadIdx.x] = off[(int64_t)threadIdx.x * nt + tile] - off[(int64_t)threadIdx.x * nt];
-        for (int t = threadIdx.x; t < kBinWarps * kMaxBins; t += kBinThreads) (&wc[0][0])[t] = 0;
+        if (threadIdx.x < kLists)
+            run[threadIdx.x] = off[(int64_t)threadIdx.x * nt + tile] - off[(int64_t)threadIdx.x * nt];
         __syncthreads();
         for (int j = 0; j < kBinRounds; ++j) {
             const int64_t r = tile * kBinTile + j * kBinThreads + threadIdx.x;
-            const int b = r < nloc ? row_bin(mode, bin8, farc, r) : -1;
-            const unsigned g = __match_any_sync(kFull, b);
-            if (b >= 0 && l == __ffs(g) - 1) wc[w][b] = (unsigned)__popc(g);
+            const int b = r < nloc ? row_list(bin8, r) : -1;
+            unsigned m[kLists];
+#pragma unroll
+            for (int q = 0; q < kLists; ++q) {
+                m[q] = __ballot_sync(kFull, b == q);
+                if (l == 0) wc[w][q] = (unsigned)__popc(m[q]);
+            }
             __syncthreads();
             if (b >= 0) {
-                int64_t pos = run[b] + __popc(g & lanemask_lt());
+                int64_t pos = run[b] + __popc(m[b] & lanemask_lt());
                 for (int v = 0; v < w; ++v) pos += wc[v][b];
                 lists[(int64_t)b * cap + pos] = (int32_t)(rb + r);
             }
             __syncthreads();
-            if (threadIdx.x < nb) {
+            if (threadIdx.x < kLists) {
                 unsigned t = 0;
-                for (int v = 0; v < kBinWarps; ++v) {
-                    t += wc[v][threadIdx.x];
-                    wc[v][threadIdx.x] = 0;
-                }
+                for (int v = 0; v < kBinWarps; ++v) t += wc[v][threadIdx.x];
                 run[threadIdx.x] += t;
             }
             __syncthreads();
@@ -197,18 +188,17 @@ __global__ void __launch_bounds__(kBinThreads) k_bin_scatter(int mode, const uin
     }
 }
 
-size_t bins_count_elems(int64_t nloc) { return (size_t)kMaxBins * (size_t)((nloc + kBinTile - 1) / kBinTile); }
+size_t bins_count_elems(int64_t nloc) { return (size_t)kLists * (size_t)((nloc + kBinTile - 1) / kBinTile); }
 
-void launch_bins(int mode, const uint8_t *bin8, const int32_t *farc, int64_t rb, int64_t nloc, unsigned *cnt,
-                 int64_t *off, void *scan_tmp, int32_t *lists, int64_t cap, int64_t *counts, cudaStream_t s) {
-    const int nb = mode == 0 ? kSymBins : kNumBins;
+void launch_bins(const uint8_t *bin8, int64_t rb, int64_t nloc, unsigned *cnt, int64_t *off, void *scan_tmp,
+                 int32_t *lists, int64_t cap, int64_t *counts, cudaStream_t s) {
     const int64_t nt = (nloc + kBinTile - 1) / kBinTile;
     if (nt == 0) return;
     const unsigned g = (unsigned)std::min<int64_t>(nt, (int64_t)num_sms() * 8);
-    k_bin_count<<<g, kBinThreads, 0, s>>>(mode, bin8, farc, nloc, nb, cnt, nt);
+    k_bin_count<<<g, kBinThreads, 0, s>>>(bin8, nloc, cnt, nt);
     note_launch();
-    scan_u32(cnt, (int64_t)nb * nt, off, scan_tmp, 0, s);
-    k_bin_scatter<<<g, kBinThreads, 0, s>>>(mode, bin8, farc, rb, nloc, nb, off, nt, lists, cap, counts);
+    scan_u32(cnt, (int64_t)kLists * nt, off, scan_tmp, 0, s);
+    k_bin_scatter<<<g, kBinThreads, 0, s>>>(bin8, rb, nloc, off, nt, lists, cap, counts);
     note_launch();
 }
 

@@ -8,11 +8,7 @@
 //  * merge path (row length <= 8): one thread per row performs a k-way merge
 //    of the row's column runs (sorted by j); for the current minimum j it
 //    folds the runs in ascending k -- exactly the chain.
-//  * warp-hash path: products are enumerated in (k ascending, column order)
-//    and processed in chunks of 32 lanes in that order; lanes with the same j
-//    (__match_any_sync) pass the accumulator down the group in lane order, so
-//    each key's chain is applied in ascending k.  Then an LSD radix sort
-//    orders the row by j.
+//  * mid rows (k_midrow.cu): window + sorted far runs, see there.
 //  * huge path (one CTA per row): warp w owns the keys with (j/32) % W == w
 //    and walks the whole product stream in order, so again every chain runs in
 //    ascending k; the dense accumulator's bitmap yields j-sorted output.
@@ -229,7 +225,7 @@ template <typename IdxT>
 __global__ void __launch_bounds__(kMergeThreads) k_analyze_sym(SymArgs a, uint8_t *bin8, DevCounters *ctr) {
     const int64_t nloc = a.re - a.rb;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    int64_t local = 0;
+    int64_t local = 0, nnzr = 0, maxf = 0, slots = 0;
     int maxlen = 0;
     // per-thread bin counts, two 32-bit counters per register (bins 0..7;
     // a thread sees at most nloc / stride rows, far below 2^32)
@@ -247,6 +243,7 @@ __global__ void __launch_bounds__(kMergeThreads) k_analyze_sym(SymArgs a, uint8_
                 if (k[u] >= 0) fi += a.T.cp[k[u] + 1] - a.T.cp[k[u]];
         }
         local += fi;
+        nnzr += e - s;
         const int len = (int)min(e - s, (int64_t)kMergeMaxLen + 1);
         if (len <= kMergeMaxLen && fi <= kMergeMaxF) {
             maxlen = max(maxlen, len);
@@ -263,6 +260,7 @@ __global__ void __launch_bounds__(kMergeThreads) k_analyze_sym(SymArgs a, uint8_
                 default: break;
             }
             a.nnzc[r] = c;
+            a.fnm[r] = 0;
             bin8[r] = kBinNone;
         } else {
             const int64_t m2 = 2 * (fi > 1 ? fi : 1);
@@ -270,6 +268,9 @@ __global__ void __launch_bounds__(kMergeThreads) k_analyze_sym(SymArgs a, uint8_
             if (lg < kSymBinMinLog) lg = kSymBinMinLog;
             const int b = lg > kSymBinMaxLog ? kNumSymBins : lg - kSymBinMinLog;
             bin8[r] = (uint8_t)b;
+            a.fnm[r] = fi - (e - s);  // >= its off-diagonal entries: temporary slots
+            slots += fi - (e - s);
+            maxf = max(maxf, fi);
             const unsigned long long inc = 1ull << (32 * (b & 1));
             pc0 += (b >> 1) == 0 ? inc : 0ull;
             pc1 += (b >> 1) == 1 ? inc : 0ull;
@@ -277,26 +278,48 @@ __global__ void __launch_bounds__(kMergeThreads) k_analyze_sym(SymArgs a, uint8_
             pc3 += (b >> 1) == 3 ? inc : 0ull;
         }
     }
-    pc0 = warp_sum(pc0);
-    pc1 = warp_sum(pc1);
-    pc2 = warp_sum(pc2);
-    pc3 = warp_sum(pc3);
-    if (lane_id() == 0 && (pc0 | pc1 | pc2 | pc3)) {
-        const unsigned long long pcs[4] = {pc0, pc1, pc2, pc3};
-        unsigned long long mid = 0;
+    // CTA reduction, then one atomic per counter per CTA
+    constexpr int W = kMergeThreads / 32;
+    __shared__ unsigned long long red[W][8];
+    __shared__ int redmax[W];
+    const unsigned long long vals[8] = {warp_sum(pc0), warp_sum(pc1), warp_sum(pc2), warp_sum(pc3),
+                                        (unsigned long long)warp_sum(local), (unsigned long long)warp_sum(nnzr),
+                                        (unsigned long long)__reduce_max_sync(kFull, (unsigned)min(maxf, (int64_t)UINT_MAX)),
+                                        (unsigned long long)warp_sum(slots)};
+    maxlen = __reduce_max_sync(kFull, maxlen);
+    const int w = threadIdx.x >> 5;
+    if (lane_id() == 0) {
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const unsigned long long lo = pcs[q] & 0xffffffffull, hi = pcs[q] >> 32;
+        for (int q = 0; q < 8; ++q) red[w][q] = vals[q];
+        redmax[w] = maxlen;
+    }
+    __syncthreads();
+    if (threadIdx.x < 9) {
+        const int q = threadIdx.x;
+        unsigned long long t = 0;
+        int mx = 0;
+        for (int k = 0; k < W; ++k) {
+            if (q < 6 || q == 7) t += red[k][q];
+            if (q == 6) t = max(t, red[k][q]);
+            mx = max(mx, redmax[k]);
+        }
+        if (q < 4) {  // bin counts: two 32-bit halves per word
+            const unsigned long long lo = t & 0xffffffffull, hi = t >> 32;
             if (lo) atomicAdd((unsigned long long *)&ctr->sym_count[2 * q], lo);
             if (hi) atomicAdd((unsigned long long *)&ctr->sym_count[2 * q + 1], hi);
-            mid += lo + hi;
+            if (lo + hi) atomicAdd((unsigned long long *)&ctr->n_mid, lo + hi);
+        } else if (q == 4) {
+            if (t) atomicAdd((unsigned long long *)&ctr->products, t);
+        } else if (q == 5) {
+            if (t) atomicAdd((unsigned long long *)&ctr->nnz_rows, t);
+        } else if (q == 6) {
+            if (t) atomicMax((unsigned long long *)&ctr->max_f, t);
+        } else if (q == 7) {
+            if (t) atomicAdd((unsigned long long *)&ctr->mid_slots, t);
+        } else if (mx) {
+            atomicMax(&ctr->max_len, mx);
         }
-        atomicAdd((unsigned long long *)&ctr->n_mid, mid);
     }
-    maxlen = __reduce_max_sync(kFull, maxlen);
-    if (lane_id() == 0 && maxlen) atomicMax(&ctr->max_len, maxlen);
-    local = warp_sum(local);
-    if (lane_id() == 0 && local) atomicAdd((unsigned long long *)&ctr->products, (unsigned long long)local);
 }
 
 void launch_analyze_sym(const SymArgs &a, uint8_t *bin8, DevCounters *ctr, cudaStream_t s) {
@@ -359,507 +382,6 @@ void launch_num_merge(const NumArgs &a, int maxlen, cudaStream_t s) {
         launch_merge_r<int32_t>(maxlen, nullptr, &a, s);
     else
         launch_merge_r<int64_t>(maxlen, nullptr, &a, s);
-}
-
-// ======================================================== product enumeration
-// Row entries of row i are taken 32 at a time; for each, the column segment
-// [cp[k], cp[k+1]) of the CSC.  Products of the batch are numbered 0..total-1
-// in (k ascending, column order); lane L of a chunk handles product c0+L.
-struct Batch {
-    int64_t incl;  // inclusive prefix of column lengths (this lane's entry)
-    int64_t excl;
-    int64_t cs;    // column start
-    double a;      // a_hat_ik of this lane's entry
-    int64_t total;
-};
-
-__device__ __forceinline__ Batch load_batch(const Csr &A, const Csc &T, int64_t base, int64_t e, bool need_a) {
-    Batch b;
-    const int64_t p = base + lane_id();
-    int64_t cl = 0;
-    b.cs = 0;
-    b.a = 0.0;
-    if (p < e) {
-        const int k = A.ci[p];
-        const int64_t c0 = T.cp[k];
-        cl = T.cp[k + 1] - c0;
-        b.cs = c0 + k;  // sentinel layout (csc_begin)
-        if (need_a) b.a = A.v[p];
-    }
-    b.incl = warp_incl_scan(cl);
-    b.excl = b.incl - cl;
-    b.total = __shfl_sync(kFull, b.incl, 31);
-    return b;
-}
-
-// Segment (lane index) holding product pp: number of lanes with incl <= pp.
-__device__ __forceinline__ int find_seg(const Batch &b, int64_t pp) {
-    int t = 0;
-#pragma unroll
-    for (int step = 16; step >= 1; step >>= 1) {
-        const int64_t v = __shfl_sync(kFull, b.incl, t + step - 1);
-        if (v <= pp) t += step;
-    }
-    return t;
-}
-
-// One product per lane for the chunk [c0, c0+32) of a batch.  The lane's
-// segment (row entry) comes from an OR-reduced bitmask of the segment starts
-// that fall inside the chunk -- no shuffle search.  Lanes past the batch get
-// j = -2 - lane (negative and pairwise distinct).
-struct Chunk {
-    int j;
-    double b;  // a_hat_jk
-    double a;  // a_hat_ik
-};
-
-template <bool NEED_VAL>
-__device__ __forceinline__ Chunk fetch_chunk(const Csc &T, const Batch &b, int64_t c0) {
-    const int l = lane_id();
-    const int64_t rel = b.excl - c0;
-    const unsigned starts = __reduce_or_sync(kFull, (rel > 0 && rel < 32) ? (1u << (int)rel) : 0u);
-    const int seg0 = __popc(__ballot_sync(kFull, b.incl <= c0));
-    const int seg = (seg0 + __popc(starts & ((2u << l) - 1u))) & 31;
-    const int64_t pp = c0 + l;
-    Chunk c;
-    const bool valid = pp < b.total;
-    const int64_t q = __shfl_sync(kFull, b.cs - b.excl, seg) + pp;
-    c.a = NEED_VAL ? shfl_d(b.a, seg) : 0.0;
-    c.j = valid ? T.ri[q] : -2 - l;
-    c.b = (NEED_VAL && valid) ? T.vt[q] : 0.0;
-    return c;
-}
-
-// One column segment (or a 32-entry piece of a longer one) of row entry t of
-// a batch: lane l takes entry off + l of column k_t.  Keys inside a piece are
-// distinct (rows of one column), so a piece updates its accumulators with no
-// conflicts and no chains -- the segment mode of the numeric warp kernel.
-struct Piece {
-    int j;      // -1: lane idle
-    double b;   // a_hat_jk
-    double a;   // a_hat_ik (uniform)
-    int64_t len;  // column length (uniform)
-};
-
-__device__ __forceinline__ Piece fetch_piece(const Csc &T, const Batch &b, int t, int64_t off) {
-    const int l = lane_id();
-    Piece p;
-    const int64_t cs = __shfl_sync(kFull, b.cs, t);
-    p.len = __shfl_sync(kFull, b.incl - b.excl, t);
-    p.a = shfl_d(b.a, t);
-    const bool valid = off + l < p.len;
-    const int64_t q = cs + off + l;
-    p.j = valid ? T.ri[q] : -1;
-    p.b = valid ? T.vt[q] : 0.0;
-    return p;
-}
-
-__device__ __forceinline__ unsigned hash_key(int j, int logt) {
-    return ((unsigned)j * 0x9E3779B1u) >> (32 - logt);
-}
-
-// ======================================================== warp paths
-// Rows off the merge path.  Keys j inside the row's window
-// [i - kWinHalf, i + kWinHalf) go to a direct-mapped window (occupancy bitmap
-// + values): no hashing, and already in order for the output.  Other ("far")
-// keys use an open-addressing table in shared memory.  Banded rows (config 5)
-// keep most keys in the window; random rows (config 4) keep most in the table.
-// Chunks are software-pipelined: the next chunk's gathers are issued before
-// the current chunk is accumulated.
-constexpr int kWarpHashThreads = 128;  // 4 warps per CTA, many CTAs per SM
-constexpr int kWinHalf = 128;
-constexpr int kWin = 2 * kWinHalf;
-constexpr int kWinSeenWords = kWin / 4;  // symbolic: one byte per window slot
-constexpr int kFarHuge = 1 << 30;  // farc marker: route the numeric pass to the huge path
-
-template <int LOGT>
-__global__ void __launch_bounds__(kWarpHashThreads) k_sym_warp(SymArgs a, const int32_t *__restrict__ list,
-                                                               const int64_t *count) {
-    constexpr int T = 1 << LOGT;
-    extern __shared__ int32_t sym_tab[];
-    const int w = threadIdx.x >> 5, l = lane_id();
-    int32_t *keys = sym_tab + w * (T + kWinSeenWords);
-    unsigned *seenw = reinterpret_cast<unsigned *>(keys + T);  // one byte per window slot
-    unsigned char *seen = reinterpret_cast<unsigned char *>(seenw);
-    const int64_t n = *count;
-    for (int s = l; s < T; s += 32) keys[s] = -1;
-    for (int s = l; s < kWinSeenWords; s += 32) seenw[s] = 0u;
-    __syncwarp();
-    const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
-    for (int64_t idx = blockIdx.x * (int64_t)(blockDim.x >> 5) + w; idx < n; idx += nw) {
-        const int64_t i = list[idx];
-        const int64_t s = a.A.rp[i], e = a.A.rp[i + 1];
-        const int64_t wbase = i - kWinHalf;
-        int nfar = 0;
-        for (int64_t base = s; base < e; base += 32) {
-            const Batch b = load_batch(a.A, a.T, base, e, false);
-            Chunk cur = fetch_chunk<false>(a.T, b, 0);
-            for (int64_t c0 = 0; c0 < b.total; c0 += 32) {
-                Chunk nxt = cur;
-                if (c0 + 32 < b.total) nxt = fetch_chunk<false>(a.T, b, c0 + 32);
-                const int64_t d = (int64_t)cur.j - wbase;
-                if (cur.j >= 0) {
-                    if (d >= 0 && d < kWin) {
-                        seen[d] = 1;  // idempotent: no atomics, duplicates harmless
-                    } else {
-                        unsigned sl = hash_key(cur.j, LOGT);
-                        while (true) {
-                            const int prev = atomicCAS(&keys[sl], -1, cur.j);
-                            if (prev == -1) {
-                                ++nfar;
-                                break;
-                            }
-                            if (prev == cur.j) break;
-                            sl = (sl + 1) & (T - 1);
-                        }
-                    }
-                }
-                cur = nxt;
-            }
-        }
-        __syncwarp();
-        int nnear = 0;
-        for (int s2 = l; s2 < kWinSeenWords; s2 += 32) nnear += __popc(seenw[s2]);  // bytes are 0 / 1
-        nnear = warp_sum(nnear);
-        nfar = warp_sum(nfar);
-        if (l == 0) {
-            a.nnzc[i - a.rb] = nnear + nfar;
-            a.farc[i - a.rb] = nfar;
-        }
-        __syncwarp();
-        for (int s2 = l; s2 < T; s2 += 32) keys[s2] = -1;
-        for (int s2 = l; s2 < kWinSeenWords; s2 += 32) seenw[s2] = 0u;
-        __syncwarp();
-    }
-}
-
-template <int LOGT>
-static void launch_sym_warp_t(const SymArgs &a, const int32_t *list, const int64_t *count, cudaStream_t s) {
-    constexpr int T = 1 << LOGT;
-    const size_t smem = (size_t)(kWarpHashThreads / 32) * (T + kWinSeenWords) * sizeof(int32_t);
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(k_sym_warp<LOGT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        attr = true;
-    }
-    int per_sm = (int)((200 * 1024) / smem);
-    per_sm = per_sm < 1 ? 1 : (per_sm > 16 ? 16 : per_sm);
-    k_sym_warp<LOGT><<<sms() * per_sm, kWarpHashThreads, smem, s>>>(a, list, count);
-    note_launch();
-}
-
-void launch_sym_warp(const SymArgs &a, const int32_t *lists, int64_t cap, const int64_t *counts,
-                     const int64_t *hcounts, cudaStream_t s) {
-    if (hcounts[0]) launch_sym_warp_t<6>(a, lists + 0 * cap, counts + 0, s);
-    if (hcounts[1]) launch_sym_warp_t<7>(a, lists + 1 * cap, counts + 1, s);
-    if (hcounts[2]) launch_sym_warp_t<8>(a, lists + 2 * cap, counts + 2, s);
-    if (hcounts[3]) launch_sym_warp_t<9>(a, lists + 3 * cap, counts + 3, s);
-    if (hcounts[4]) launch_sym_warp_t<10>(a, lists + 4 * cap, counts + 4, s);
-    if (hcounts[5]) launch_sym_warp_t<11>(a, lists + 5 * cap, counts + 5, s);
-    if (hcounts[6]) launch_sym_warp_t<12>(a, lists + 6 * cap, counts + 6, s);
-}
-
-// Numeric, per warp (T = 2^LOGT far-table slots >= 2 * far keys):
-//   wv[kWin] window values, vals[T] / keys[T] far table (+0.0 / -1 when
-//   empty; reused as the second radix buffer), radix buffer of T/2
-//   (key, value), hist[256].  Every accumulator starts at +0.0, so the first
-//   fma of a chain sees +0.0 exactly as in the ordering contract; an
-//   untouched window slot reads +0.0 and is never emitted (|c| > tol >= 0).
-template <int LOGT>
-struct NumWarpSmem {
-    static constexpr int T = 1 << LOGT;
-    static constexpr size_t bytes = (size_t)kWin * 8 + (size_t)T * 8 + (size_t)T * 4 + (size_t)(T / 2) * 12 + 256 * 4;
-};
-
-// Segment mode when the batch's mean column length is at least this.
-constexpr int kSegMinMean = 12;
-
-template <int LOGT>
-__device__ __forceinline__ double *far_slot(int32_t *keys, double *vals, int j) {
-    constexpr int T = 1 << LOGT;
-    unsigned sl = hash_key(j, LOGT);
-    while (true) {
-        const int prev = atomicCAS(&keys[sl], -1, j);
-        if (prev == -1 || prev == j) break;
-        sl = (sl + 1) & (T - 1);
-    }
-    return vals + sl;
-}
-
-template <int LOGT>
-__global__ void __launch_bounds__(kWarpHashThreads, 1) k_num_warp(NumArgs a, const int32_t *__restrict__ list,
-                                                               const int64_t *count) {
-    constexpr int T = 1 << LOGT;
-    constexpr int H = T / 2;
-    constexpr int WPB = kWarpHashThreads / 32;
-    extern __shared__ __align__(16) unsigned char num_smem[];
-    const int w = threadIdx.x >> 5, l = lane_id();
-    unsigned char *base = num_smem + (size_t)w * NumWarpSmem<LOGT>::bytes;
-    double *wv = reinterpret_cast<double *>(base);
-    double *vals = wv + kWin;
-    double *av = vals + T;
-    int32_t *keys = reinterpret_cast<int32_t *>(av + H);
-    int32_t *ak = keys + T;
-    int32_t *hist = ak + H;
-    const unsigned lt = lanemask_lt();
-    Comp cut;
-    int badp = 0;
-
-    for (int s = l; s < T; s += 32) {
-        keys[s] = -1;
-        vals[s] = +0.0;
-    }
-    for (int s = l; s < kWin; s += 32) wv[s] = +0.0;
-    __syncwarp();
-    const int64_t n = *count;
-    const int64_t nw = (int64_t)gridDim.x * WPB;
-    for (int64_t idx = blockIdx.x * (int64_t)WPB + w; idx < n; idx += nw) {
-        const int64_t i = list[idx];
-        const int64_t r = i - a.rb;
-        const int64_t s = a.A.rp[i], e = a.A.rp[i + 1];
-        const int64_t wbase = i - kWinHalf;
-        // ---- accumulate (ordered chains: products applied in ascending k)
-        for (int64_t bb = s; bb < e; bb += 32) {
-            const Batch b = load_batch(a.A, a.T, bb, e, true);
-            const int nent = (int)min((int64_t)32, e - bb);
-            if (b.total >= (int64_t)kSegMinMean * nent) {
-                // segment mode: one column (piece) per round, keys distinct
-                int t = 0;
-                int64_t off = 0;
-                Piece cur = fetch_piece(a.T, b, 0, 0);
-                while (true) {
-                    int tn = t;
-                    int64_t offn = off + 32;
-                    if (offn >= cur.len) {
-                        tn = t + 1;
-                        offn = 0;
-                    }
-                    const bool more = tn < nent;
-                    Piece nxt = cur;
-                    if (more) nxt = fetch_piece(a.T, b, tn, offn);
-                    if (cur.j >= 0) {
-                        const int64_t d = (int64_t)cur.j - wbase;
-                        double *acc = (d >= 0 && d < kWin) ? wv + d : far_slot<LOGT>(keys, vals, cur.j);
-                        *acc = __fma_rn(cur.a, cur.b, *acc);
-                    }
-                    __syncwarp();
-                    if (!more) break;
-                    cur = nxt;
-                    t = tn;
-                    off = offn;
-                }
-                continue;
-            }
-            // chunk mode: 32 products per round; a key repeated inside the
-            // chunk (several columns) is chained through its lanes in order
-            Chunk cur = fetch_chunk<true>(a.T, b, 0);
-            for (int64_t c0 = 0; c0 < b.total; c0 += 32) {
-                Chunk nxt = cur;
-                if (c0 + 32 < b.total) nxt = fetch_chunk<true>(a.T, b, c0 + 32);
-                const int j = cur.j;
-                const bool valid = j >= 0;
-                const int64_t d = (int64_t)j - wbase;
-                const bool near = valid && d >= 0 && d < kWin;
-                const unsigned g = __match_any_sync(kFull, j);
-                const int leader = __ffs(g) - 1;
-                const int rank = __popc(g & lt);
-                const int cnt = __popc(g);
-                double *accp = wv;
-                double acc = 0.0;
-                if (valid && l == leader) {
-                    accp = near ? wv + d : far_slot<LOGT>(keys, vals, j);
-                    acc = *accp;
-                }
-                const int pred = rank ? 31 - __clz(g & lt) : l;
-                const int maxc = __reduce_max_sync(kFull, valid ? cnt : 0);
-                for (int it = 0; it < maxc; ++it) {
-                    const double x = shfl_d(acc, pred);
-                    if (valid && rank == it) acc = __fma_rn(cur.a, cur.b, rank == 0 ? acc : x);
-                }
-                // the last lane of each key's group stores the chain's value
-                const int last = 31 - __clz(g);
-                const unsigned long long pa = __shfl_sync(kFull, (unsigned long long)accp, leader);
-                if (valid && l == last) *reinterpret_cast<double *>(pa) = acc;
-                __syncwarp();
-                cur = nxt;
-            }
-        }
-        // ---- far keys: compact the table into (ak, av)
-        int L = 0;
-        int jmin = INT_MAX, jmax = -1;
-        for (int b0 = 0; b0 < T; b0 += 32) {
-            const int sidx = b0 + l;
-            const int k = keys[sidx];
-            const bool occ = k >= 0;
-            const unsigned bal = __ballot_sync(kFull, occ);
-            if (occ) {
-                const int pos = L + __popc(bal & lt);
-                ak[pos] = k;
-                av[pos] = vals[sidx];
-                jmin = min(jmin, k);
-                jmax = max(jmax, k);
-            }
-            L += __popc(bal);
-        }
-        jmin = __reduce_min_sync(kFull, jmin);
-        jmax = __reduce_max_sync(kFull, jmax);
-        __syncwarp();
-        // ---- LSD radix sort of the far keys on (key - jmin), 8-bit digits,
-        // stable; the (now copied-out) table region is the second buffer
-        const unsigned span = L > 1 ? (unsigned)(jmax - jmin) : 0u;
-        const int bits = span ? 32 - __clz(span) : 0;
-        int32_t *ck = ak, *nk = keys;
-        double *cv = av, *nv = vals;
-        for (int sh = 0; sh < bits; sh += 8) {
-            for (int h = l; h < 256; h += 32) hist[h] = 0;
-            __syncwarp();
-            for (int rd = 0; rd < L; rd += 32) {
-                const int e2 = rd + l;
-                const bool v = e2 < L;
-                const int dig = v ? (int)(((unsigned)(ck[e2] - jmin) >> sh) & 255u) : 256 + l;
-                const unsigned g = __match_any_sync(kFull, dig);
-                if (v && l == __ffs(g) - 1) hist[dig] += __popc(g);
-                __syncwarp();
-            }
-            {
-                int loc[8], sum = 0;
-#pragma unroll
-                for (int u = 0; u < 8; ++u) {
-                    loc[u] = hist[l * 8 + u];
-                    sum += loc[u];
-                }
-                const int inc = warp_incl_scan(sum);
-                int run = inc - sum;
-#pragma unroll
-                for (int u = 0; u < 8; ++u) {
-                    hist[l * 8 + u] = run;
-                    run += loc[u];
-                }
-            }
-            __syncwarp();
-            for (int rd = 0; rd < L; rd += 32) {
-                const int e2 = rd + l;
-                const bool v = e2 < L;
-                const int key = v ? ck[e2] : 0;
-                const int dig = v ? (int)(((unsigned)(key - jmin) >> sh) & 255u) : 256 + l;
-                const unsigned g = __match_any_sync(kFull, dig);
-                if (v) {
-                    const int pos = hist[dig] + __popc(g & lt);
-                    nk[pos] = key;
-                    nv[pos] = cv[e2];
-                }
-                __syncwarp();
-                if (v && l == 31 - __clz(g)) hist[dig] += __popc(g);
-                __syncwarp();
-            }
-            int32_t *tk = ck;
-            ck = nk;
-            nk = tk;
-            double *tv = cv;
-            cv = nv;
-            nv = tv;
-        }
-        // far keys below the window sort first
-        int nbelow = 0;
-        for (int rd = 0; rd < L; rd += 32) {
-            const int e2 = rd + l;
-            nbelow += __popc(__ballot_sync(kFull, e2 < L && (int64_t)ck[e2] < wbase));
-        }
-        // ---- write the row in ascending j: far-below, window, far-above
-        const int64_t g0 = a.gptr[r], ub = a.gptr[r + 1] - g0;
-        int32_t pi = 0;
-        if (a.part) {
-            pi = a.part[i];
-            badp |= (pi < 0) | (pi >= a.K);
-        }
-        int64_t o = 0;
-        auto emit = [&](bool v, int key, double c) {
-            const bool isdiag = v && (int64_t)key == i;
-            if (isdiag && a.diag) a.diag[r] = c;
-            const bool keep = v && !isdiag && fabs(c) > a.tol;
-            const unsigned bal = __ballot_sync(kFull, keep);
-            if (keep) {
-                const int64_t pos = g0 + o + __popc(bal & lt);
-                a.gcol[pos] = key;
-                a.gw[pos] = fabs(c);
-                if (a.part && (int64_t)key > i) {
-                    const int32_t pj = a.part[key];
-                    badp |= (pj < 0) | (pj >= a.K);
-                    if (pj != pi) cut.add(fabs(c));
-                }
-            }
-            o += __popc(bal);
-        };
-        for (int rd = 0; rd < nbelow; rd += 32) {
-            const int e2 = rd + l;
-            const bool v = e2 < nbelow;
-            emit(v, v ? ck[e2] : -1, v ? cv[e2] : 0.0);
-        }
-        for (int slot = l; slot < kWin; slot += 32) {  // untouched slots hold +0.0: never kept
-            const int64_t key = wbase + slot;
-            emit(key >= 0, (int)key, wv[slot]);
-            wv[slot] = +0.0;
-        }
-        for (int rd = nbelow; rd < L; rd += 32) {
-            const int e2 = rd + l;
-            const bool v = e2 < L;
-            emit(v, v ? ck[e2] : -1, v ? cv[e2] : 0.0);
-        }
-        __syncwarp();
-        // reset the far table (it also served as a radix buffer) and the bitmap
-        for (int s2 = l; s2 < T; s2 += 32) {
-            keys[s2] = -1;
-            vals[s2] = +0.0;
-        }
-        if (o < ub) {
-            for (int64_t t = o + l; t < ub; t += 32) a.gcol[g0 + t] = -1;
-            if (l == 0) atomicOr(a.holes, 1);
-        }
-        __syncwarp();
-    }
-    if (a.part) {
-        const double v = block_tree_sum<kWarpHashThreads>(cut.value());
-        if (threadIdx.x == 0) {
-            a.cutp[blockIdx.x] = v;
-            if (blockIdx.x == 0) *a.cut_used = (int)gridDim.x;
-        }
-        if (__syncthreads_or(badp) && threadIdx.x == 0) atomicOr(a.bad_part, 1);
-    }
-}
-
-template <int LOGT>
-static void launch_num_warp_t(const NumArgs &a, const int32_t *list, const int64_t *count, cudaStream_t s) {
-    const size_t smem = (size_t)(kWarpHashThreads / 32) * NumWarpSmem<LOGT>::bytes;
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(k_num_warp<LOGT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        attr = true;
-    }
-    int per_sm = (int)((220 * 1024) / smem);
-    per_sm = per_sm < 1 ? 1 : (per_sm > 16 ? 16 : per_sm);
-    int g = sms() * per_sm;
-    if (g > kCutSlotsPerLaunch) g = kCutSlotsPerLaunch;
-    k_num_warp<LOGT><<<g, kWarpHashThreads, smem, s>>>(a, list, count);
-    note_launch();
-}
-
-void launch_num_warp(const NumArgs &a, const int32_t *lists, int64_t cap, const int64_t *counts,
-                     const int64_t *hcounts, cudaStream_t s) {
-    // fused-cut partial slots: launch slot 0 = merge, 1..6 = these bins, 7 = huge
-    NumArgs b[6];
-    for (int k = 0; k < 6; ++k) {
-        b[k] = a;
-        if (a.cutp) {
-            b[k].cutp = a.cutp + (int64_t)(1 + k) * kCutSlotsPerLaunch;
-            b[k].cut_used = a.cut_used + 1 + k;
-        }
-    }
-    if (hcounts[0]) launch_num_warp_t<6>(b[0], lists + 0 * cap, counts + 0, s);
-    if (hcounts[1]) launch_num_warp_t<7>(b[1], lists + 1 * cap, counts + 1, s);
-    if (hcounts[2]) launch_num_warp_t<8>(b[2], lists + 2 * cap, counts + 2, s);
-    if (hcounts[3]) launch_num_warp_t<9>(b[3], lists + 3 * cap, counts + 3, s);
-    if (hcounts[4]) launch_num_warp_t<10>(b[4], lists + 4 * cap, counts + 4, s);
-    if (hcounts[5]) launch_num_warp_t<11>(b[5], lists + 5 * cap, counts + 5, s);
 }
 
 // ======================================================== huge rows
@@ -957,57 +479,13 @@ __device__ __forceinline__ int64_t block_sum(int64_t v) {
 // touch only non-empty L1 words instead of all nrows/32.
 __host__ __device__ __forceinline__ int64_t l2_words(int64_t nwords) { return (nwords + 31) / 32; }
 
-__global__ void __launch_bounds__(kHugeThreads) k_sym_huge(SymArgs a, const int32_t *__restrict__ list,
-                                                           const int64_t *count, unsigned char *scratch,
-                                                           size_t slot_bytes, int64_t nwords) {
-    extern __shared__ unsigned l2[];
-    __shared__ int64_t s_incl[kHugeThreads], s_cs[kHugeThreads];
-    const int64_t nw2 = l2_words(nwords);
-    unsigned *bm = reinterpret_cast<unsigned *>(scratch + slot_bytes * blockIdx.x);
-    for (int64_t t = threadIdx.x; t < nw2; t += kHugeThreads) l2[t] = 0u;
-    __syncthreads();
-    const int64_t n = *count;
-    for (int64_t idx = blockIdx.x; idx < n; idx += gridDim.x) {
-        const int64_t i = list[idx];
-        const int64_t s = a.A.rp[i], e = a.A.rp[i + 1];
-        int64_t cnt = 0;
-        for (int64_t base = s; base < e; base += kHugeThreads) {
-            const int64_t total = block_batch(a.A, a.T, base, e, s_incl, s_cs, nullptr);
-            for (int64_t pp = threadIdx.x; pp < total; pp += kHugeThreads) {
-                const int t = block_find(s_incl, pp);
-                const int64_t ex = t ? s_incl[t - 1] : 0;
-                const int j = a.T.ri[s_cs[t] + pp - ex];
-                const unsigned bit = 1u << (j & 31);
-                const unsigned old = atomicOr(&bm[j >> 5], bit);
-                if (!(old & bit)) {
-                    ++cnt;
-                    if (old == 0u) atomicOr(&l2[j >> 10], 1u << ((j >> 5) & 31));
-                }
-            }
-            __syncthreads();
-        }
-        cnt = block_sum(cnt);
-        if (threadIdx.x == 0) {
-            a.nnzc[i - a.rb] = cnt;
-            a.farc[i - a.rb] = kFarHuge;
-        }
-        // clear the touched L1 words and the L2 bitmap
-        for (int64_t t = threadIdx.x; t < nw2; t += kHugeThreads) {
-            for (unsigned m = l2[t]; m; m &= m - 1) bm[t * 32 + __ffs(m) - 1] = 0u;
-            l2[t] = 0u;
-        }
-        __syncthreads();
-    }
-}
-
 // Numeric: the row's products are enumerated 512 at a time (one 32-product
 // sub-chunk per warp) and routed, in product order, into shared-memory queues
 // of their owner warp ((j >> 5) % 16).  Each owner then applies its queue in
 // order (ordered __match_any_sync chains) to the dense accumulator, so every
 // chain runs in ascending k and each product is handled once.
-__global__ void __launch_bounds__(kHugeThreads) k_num_huge(NumArgs a, const int32_t *__restrict__ list,
-                                                           const int64_t *count, unsigned char *scratch,
-                                                           size_t slot_bytes, int64_t nwords) {
+__global__ void __launch_bounds__(kHugeThreads) k_num_huge(MidArgs a, unsigned char *scratch, size_t slot_bytes,
+                                                           int64_t nwords) {
     extern __shared__ unsigned l2[];
     __shared__ int64_t s_incl[kHugeThreads], s_cs[kHugeThreads];
     __shared__ double s_a[kHugeThreads];
@@ -1025,9 +503,9 @@ __global__ void __launch_bounds__(kHugeThreads) k_num_huge(NumArgs a, const int3
     __syncthreads();
     Comp cut;
     int badp = 0;
-    const int64_t n = *count;
+    const int64_t n = *a.count;
     for (int64_t idx = blockIdx.x; idx < n; idx += gridDim.x) {
-        const int64_t i = list[idx];
+        const int64_t i = a.list[idx];
         const int64_t r = i - a.rb;
         const int64_t s = a.A.rp[i], e = a.A.rp[i + 1];
         for (int64_t base = s; base < e; base += kHugeThreads) {
@@ -1111,7 +589,7 @@ __global__ void __launch_bounds__(kHugeThreads) k_num_huge(NumArgs a, const int3
         __threadfence_block();
         __syncthreads();
         // ---- emit in ascending j: walk the non-empty L1 words via the L2 bitmap
-        const int64_t g0 = a.gptr[r], ub = a.gptr[r + 1] - g0;
+        const int64_t g0 = a.toff[r];  // temporary slot of the row
         int32_t pi = 0;
         if (a.part) {
             pi = a.part[i];
@@ -1149,8 +627,8 @@ __global__ void __launch_bounds__(kHugeThreads) k_num_huge(NumArgs a, const int3
                     const int64_t j = w1 * 32 + __ffs(m) - 1;
                     const double c = acc_g[j];
                     if (j != i && fabs(c) > a.tol) {
-                        a.gcol[pos] = (int32_t)j;
-                        a.gw[pos] = fabs(c);
+                        a.tcol[pos] = (int32_t)j;
+                        a.tw[pos] = fabs(c);
                         ++pos;
                         if (a.part && j > i) {
                             const int32_t pj = a.part[j];
@@ -1165,10 +643,7 @@ __global__ void __launch_bounds__(kHugeThreads) k_num_huge(NumArgs a, const int3
             o += tot;
             __syncthreads();
         }
-        if (o < ub) {
-            for (int64_t t = o + tid; t < ub; t += kHugeThreads) a.gcol[g0 + t] = -1;
-            if (tid == 0) atomicOr(a.holes, 1);
-        }
+        if (tid == 0) a.cnt[r] = o + 1;  // exact kept count (+1: the scan subtracts the diagonal)
         __syncthreads();
     }
     if (a.part) {
@@ -1181,30 +656,12 @@ __global__ void __launch_bounds__(kHugeThreads) k_num_huge(NumArgs a, const int3
     }
 }
 
-void launch_sym_huge(const SymArgs &a, const int32_t *list, const int64_t *count, int slots, void *scratch,
-                     cudaStream_t s) {
-    const size_t slot_bytes = bitmap_stride(a.A.nrows);
-    const int64_t nw = bitmap_words(a.A.nrows);
-    const size_t smem = (size_t)l2_words(nw) * sizeof(unsigned);
-    cudaFuncSetAttribute(k_sym_huge, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_sym_huge<<<slots, kHugeThreads, smem, s>>>(a, list, count, static_cast<unsigned char *>(scratch), slot_bytes,
-                                                 nw);
-    note_launch();
-}
-
-void launch_num_huge(const NumArgs &a, const int32_t *list, const int64_t *count, int slots, void *scratch,
-                     cudaStream_t s) {
+void launch_num_huge(const MidArgs &a, int slots, void *scratch, cudaStream_t s) {
     const size_t slot_bytes = bitmap_stride(a.A.nrows);
     const int64_t nw = bitmap_words(a.A.nrows);
     const size_t smem = (size_t)l2_words(nw) * sizeof(unsigned);
     cudaFuncSetAttribute(k_num_huge, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    NumArgs b = a;
-    if (a.cutp) {
-        b.cutp = a.cutp + (int64_t)7 * kCutSlotsPerLaunch;
-        b.cut_used = a.cut_used + 7;
-    }
-    k_num_huge<<<slots, kHugeThreads, smem, s>>>(b, list, count, static_cast<unsigned char *>(scratch), slot_bytes,
-                                                 nw);
+    k_num_huge<<<slots, kHugeThreads, smem, s>>>(a, static_cast<unsigned char *>(scratch), slot_bytes, nw);
     note_launch();
 }
 

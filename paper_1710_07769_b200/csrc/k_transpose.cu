@@ -20,21 +20,54 @@
 namespace rig {
 
 // Bucket width 2^shift columns, chosen per matrix so an average bucket holds
-// about kBucketTarget records (transpose_shift).
+// about kBucketTarget records; a warp sorts a bucket whose records plus one
+// sentinel per column fit kBucketSlots, larger buckets go to a CTA-wide pass.
 constexpr int kMinShift = 3, kMaxShift = 9;
 constexpr int kMaxBucketCols = 1 << kMaxShift;
-constexpr int kBucketTarget = 512;
-constexpr int kBucketCap = 1024;  // records per bucket sorted in shared memory (16 KB)
+constexpr int kBucketTarget = 384;
+constexpr int kBucketSlots = 1024;
 
 struct __align__(16) Rec {
     int32_t col, row;
     double x;
 };
 
-__global__ void __launch_bounds__(256) k_bucket_scatter(Csr A, int scale, double *__restrict__ ahat,
-                                                        const int64_t *__restrict__ cp, unsigned long long *bcur,
-                                                        Rec *__restrict__ rec, int *err, int shift) {
-    const int l = lane_id();
+// a /_rn b for b > 0 normal, given y = RN(1/b) (one reciprocal per row).
+// Markstein: q0 = a*y, r = a - q0*b (exact by fma), q1 = q0 + r*y.  q1 is
+// returned only if it is PROVEN to be RN(a/b): q1 normal and not a power of
+// two (symmetric rounding interval) and the exact remainder a - q1*b, which
+// the fma gives rounded monotonically, strictly inside b*ulp(q1)/2 (h is a
+// power-of-two multiple of b, exact while normal).  Anything else falls back
+// to __ddiv_rn, so the result is bit-identical to the IEEE division
+// (R5) -- the fast path only skips work.
+__device__ __forceinline__ double div_rn_fast(double a, double b, double y) {
+    const double q0 = __dmul_rn(a, y);
+    const double r = __fma_rn(-q0, b, a);
+    const double q1 = __fma_rn(r, y, q0);
+    const double r1 = __fma_rn(-q1, b, a);
+    const long long bits = __double_as_longlong(q1);
+    const int e = (int)((bits >> 52) & 0x7ff);
+    if (e > 54 && e < 2046 && (bits & 0xfffffffffffffll) != 0) {
+        const double h = __dmul_rn(b, __longlong_as_double((long long)(e - 53) << 52));  // b * ulp(q1) / 2
+        if (h >= 0x1p-1000 && fabs(r1) < h) return q1;
+    }
+    return __ddiv_rn(a, b);
+}
+
+constexpr int kScatterThreads = 256;
+
+// One warp per tile of 32 consecutive rows.  Lane l computes the norm of row
+// r0 + l (ordered fma chain) and its reciprocal; the
+// warp then walks the tile's entries 32 at a time (coalesced), finds each
+// entry's row from the bitmask of row starts inside the chunk (no search),
+// scales it, writes a_hat and appends a 16-byte record (col, row, a_hat) to
+// the column's bucket; lanes hitting the same bucket share one atomic.
+__global__ void __launch_bounds__(kScatterThreads) k_bucket_scatter(Csr A, int scale, double *__restrict__ ahat,
+                                                                    const int64_t *__restrict__ cp,
+                                                                    unsigned long long *bcur, Rec *__restrict__ rec,
+                                                                    int *err, int shift) {
+    __shared__ int s_nz[kScatterThreads / 32][32];  // lane of the k-th nonempty row of the tile
+    const int l = lane_id(), w = threadIdx.x >> 5;
     const unsigned lt = lanemask_lt();
     const int64_t ntiles = (A.nrows + 31) / 32;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -44,62 +77,79 @@ __global__ void __launch_bounds__(256) k_bucket_scatter(Csr A, int scale, double
         const int64_t hi = A.rp[r0 + rows];
         const int64_t my_s = l < rows ? A.rp[r0 + l] : hi;
         const int64_t my_e = l < rows ? A.rp[r0 + l + 1] : hi;
-        double nrm = 1.0;
+        double nrm = 1.0, y = 1.0;
         int bad = 0;
         if (scale && l < rows) {
             double ss = +0.0;
             for (int64_t p0 = my_s; p0 < my_e; p0 += 8) {  // 8 loads in flight, chain in order
-                double a[8];
+                double av[8];
 #pragma unroll
-                for (int u = 0; u < 8; ++u) a[u] = p0 + u < my_e ? A.v[p0 + u] : 0.0;
+                for (int u = 0; u < 8; ++u) av[u] = p0 + u < my_e ? A.v[p0 + u] : 0.0;
 #pragma unroll
                 for (int u = 0; u < 8; ++u)
-                    if (p0 + u < my_e) ss = __fma_rn(a[u], a[u], ss);
+                    if (p0 + u < my_e) ss = __fma_rn(av[u], av[u], ss);
             }
-            if (!isfinite(ss))
+            if (!isfinite(ss)) {
                 bad = kErrNonFinite;
-            else if (ss == 0.0)
+            } else if (ss == 0.0) {
                 bad = kErrZeroRow;
-            else
+            } else {
                 nrm = __dsqrt_rn(ss);
+                y = __drcp_rn(nrm);
+            }
         }
         if (bad) atomicOr(err, bad);
+        const bool ne = my_e > my_s;
+        const unsigned NE = __ballot_sync(kFull, ne);
+        if (ne) s_nz[w][__popc(NE & lt)] = l;
+        __syncwarp();
         const int64_t lo = __shfl_sync(kFull, my_s, 0);
-        const int64_t last = __shfl_sync(kFull, my_s, 31);
-        for (int64_t base = lo; base < hi; base += 32) {
-            const int64_t p = base + l;
-            int t = 0;  // row of entry p: (number of lanes with start <= p) - 1
+        int cnt = NE ? 1 : 0;  // nonempty rows starting at or before c0
+        constexpr int U = 4;  // chunks per group: their bucket atomics are in flight together
+        for (int64_t g0 = lo; g0 < hi; g0 += 32 * U) {
+            int kk[U], row[U], bb[U];
+            double xx[U];
+            unsigned gg[U];
+            unsigned long long off[U];
 #pragma unroll
-            for (int step = 16; step >= 1; step >>= 1) {
-                const int64_t v = __shfl_sync(kFull, my_s, t + step - 1);
-                if (v <= p) t += step;
+            for (int u = 0; u < U; ++u) {
+                const int64_t c0 = g0 + 32 * u;
+                // bit (rel - 1) for nonempty rows starting at c0 + rel, 1 <= rel <= 32
+                const int64_t rel = my_s - c0;
+                const unsigned S = __reduce_or_sync(kFull, (ne && rel >= 1 && rel <= 32) ? (1u << (rel - 1)) : 0u);
+                const int k_row = cnt + __popc(S & ((1u << l) - 1u));  // nonempty starts <= c0 + l
+                cnt += __popc(S);
+                row[u] = s_nz[w][(k_row > 0 ? k_row : 1) - 1];
+                const double rn = shfl_d(nrm, row[u]), ry = shfl_d(y, row[u]);
+                const int64_t p = c0 + l;
+                const bool valid = p < hi;
+                kk[u] = 0;
+                xx[u] = 0.0;
+                if (valid) {
+                    kk[u] = A.ci[p];
+                    const double av = A.v[p];
+                    xx[u] = scale ? div_rn_fast(av, rn, ry) : av;
+                    if (scale) ahat[p] = xx[u];
+                }
+                bb[u] = valid ? (kk[u] >> shift) : -1 - l;
+                gg[u] = __match_any_sync(kFull, bb[u]);
+                off[u] = 0;
+                if (valid && l == __ffs(gg[u]) - 1) off[u] = atomicAdd(&bcur[bb[u]], (unsigned long long)__popc(gg[u]));
             }
-            if (t == 31 && last <= p) t = 32;
-            const int row = t > 0 ? t - 1 : 0;
-            const double rn = __shfl_sync(kFull, nrm, row);
-            const bool valid = p < hi;
-            int k = 0;
-            double x = 0.0;
-            if (valid) {
-                k = A.ci[p];
-                x = scale ? __ddiv_rn(A.v[p], rn) : A.v[p];
-                if (scale) ahat[p] = x;
-            }
-            const int b = valid ? (k >> shift) : -1 - l;
-            const unsigned g = __match_any_sync(kFull, b);
-            const int leader = __ffs(g) - 1;
-            unsigned long long off = 0;
-            if (valid && l == leader) off = atomicAdd(&bcur[b], (unsigned long long)__popc(g));
-            off = __shfl_sync(kFull, off, leader);
-            if (valid) {
-                const int64_t pos = cp[(int64_t)b << shift] + (int64_t)off + __popc(g & lt);
-                Rec r;
-                r.col = k;
-                r.row = (int32_t)(r0 + row);
-                r.x = x;
-                rec[pos] = r;
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const unsigned long long o = __shfl_sync(kFull, off[u], __ffs(gg[u]) - 1);
+                if (bb[u] >= 0) {
+                    const int64_t pos = cp[(int64_t)bb[u] << shift] + (int64_t)o + __popc(gg[u] & lt);
+                    Rec r;
+                    r.col = kk[u];
+                    r.row = (int32_t)(r0 + row[u]);
+                    r.x = xx[u];
+                    rec[pos] = r;
+                }
             }
         }
+        __syncwarp();
     }
 }
 
@@ -127,100 +177,139 @@ __device__ void bitonic_sort_block(int64_t len, KeyAt key, Swap swap) {
     }
 }
 
-constexpr int kSortThreads = 128;
+constexpr int kSortThreads = 64;  // 2 warps: one bucket per warp
+constexpr int kSortWarps = kSortThreads / 32;
 
+// One warp per bucket: records are placed by column straight into their CSC
+// slots (column c of the bucket occupies [loff[c] + c, loff[c+1] + c), then
+// its sentinel), each column is ordered by row (columns are short: insertion
+// sort by one lane), and the slice -- entries and sentinels -- is written
+// with fully coalesced stores.  Buckets that do not fit are listed for
+// k_bucket_sort_big.
 __global__ void __launch_bounds__(kSortThreads) k_bucket_sort(const Rec *__restrict__ rec,
                                                               const int64_t *__restrict__ cp, int64_t ncols,
-                                                              unsigned *gcur, int32_t *ri, double *vt, int shift) {
-    __shared__ Rec srec[kBucketCap];
-    __shared__ int loff[kMaxBucketCols + 1];
-    __shared__ int cur[kMaxBucketCols];
+                                                              int32_t *ri, double *vt, int shift, int *big_list,
+                                                              int *big_count) {
+    __shared__ int32_t s_ri[kSortWarps][kBucketSlots];
+    __shared__ double s_vt[kSortWarps][kBucketSlots];
+    __shared__ uint16_t s_off[kSortWarps][kMaxBucketCols + 1];
+    __shared__ unsigned s_cur[kSortWarps][kMaxBucketCols];
+    const int w = threadIdx.x >> 5, l = lane_id();
+    int32_t *sr = s_ri[w];
+    double *sv = s_vt[w];
+    uint16_t *loff = s_off[w];
+    unsigned *cur = s_cur[w];
     const int bcols = 1 << shift;
     const int64_t nb = (ncols + bcols - 1) / bcols;
-    for (int64_t b = blockIdx.x; b < nb; b += gridDim.x) {
+    for (int64_t b = (int64_t)blockIdx.x * kSortWarps + w; b < nb; b += (int64_t)gridDim.x * kSortWarps) {
         const int64_t c0 = b << shift;
         const int ncb = (int)min((int64_t)bcols, ncols - c0);
-        const int64_t e0 = cp[c0], e1 = cp[c0 + ncb];
-        const int64_t E = e1 - e0;
-        const int64_t out0 = e0 + c0;  // CSC slot of the bucket's first entry
-        if (E <= kBucketCap) {
-            for (int c = threadIdx.x; c <= ncb; c += kSortThreads) loff[c] = (int)(cp[c0 + c] - e0);
-            for (int c = threadIdx.x; c < ncb; c += kSortThreads) cur[c] = 0;
-            __syncthreads();
-            // counting placement by column (order within a column fixed below)
-            for (int64_t t = threadIdx.x; t < E; t += kSortThreads) {
-                const Rec r = rec[e0 + t];
-                const int lc = r.col - (int)c0;
-                srec[loff[lc] + atomicAdd(&cur[lc], 1)] = r;
+        const int64_t e0 = cp[c0];
+        const int64_t E = cp[c0 + ncb] - e0;
+        if (E + ncb > kBucketSlots) {
+            if (l == 0) big_list[atomicAdd(big_count, 1)] = (int)b;
+            continue;
+        }
+        // slot offsets include one sentinel per earlier column
+        for (int c = l; c <= ncb; c += 32) {
+            const int o = (int)(cp[c0 + c] - e0) + c;
+            loff[c] = (uint16_t)o;
+            if (c < ncb) cur[c] = (unsigned)o;
+        }
+        __syncwarp();
+        for (int t0 = 0; t0 < (int)E; t0 += 128) {  // 4 record loads in flight per lane
+            Rec rr[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int t = t0 + 32 * u + l;
+                if (t < (int)E) rr[u] = rec[e0 + t];
             }
-            __syncthreads();
-            // each column ascending by row (columns are short: insertion sort)
-            for (int c = threadIdx.x; c < ncb; c += kSortThreads) {
-                const int s = loff[c], e = loff[c + 1];
-                for (int a2 = s + 1; a2 < e; ++a2) {
-                    const Rec key = srec[a2];
-                    int q = a2 - 1;
-                    while (q >= s && srec[q].row > key.row) {
-                        srec[q + 1] = srec[q];
-                        --q;
-                    }
-                    srec[q + 1] = key;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                if (t0 + 32 * u + l < (int)E) {
+                    const int pos = (int)atomicAdd(&cur[rr[u].col - (int)c0], 1u);
+                    sr[pos] = rr[u].row;
+                    sv[pos] = rr[u].x;
                 }
             }
-            __syncthreads();
-            // coalesced write-out: entry j of column lc goes to out0 + j + lc
-            for (int64_t j = threadIdx.x; j < E; j += kSortThreads) {
-                const Rec r = srec[j];
-                const int64_t o = out0 + j + (r.col - c0);
-                ri[o] = r.row;
-                vt[o] = r.x;
-            }
-            for (int c = threadIdx.x; c < ncb; c += kSortThreads) {
-                const int64_t o = out0 + loff[c + 1] + c;
-                ri[o] = INT_MAX;
-                vt[o] = 0.0;
-            }
-            __syncthreads();
-        } else {
-            // large bucket: place with global per-column cursors, then sort each
-            // column in global memory (correct for any skew, slower)
-            for (int64_t t = threadIdx.x; t < E; t += kSortThreads) {
-                const Rec r = rec[e0 + t];
-                const int64_t o = cp[r.col] + r.col + atomicAdd(&gcur[r.col], 1u);
-                ri[o] = r.row;
-                vt[o] = r.x;
-            }
-            for (int c = threadIdx.x; c < ncb; c += kSortThreads) {
-                const int64_t o = cp[c0 + c + 1] + c0 + c;
-                ri[o] = INT_MAX;
-                vt[o] = 0.0;
-            }
-            __threadfence_block();
-            __syncthreads();
-            for (int c = 0; c < ncb; ++c) {
-                const int64_t s = cp[c0 + c] + c0 + c, len = cp[c0 + c + 1] - cp[c0 + c];
-                int32_t *gk = ri + s;
-                double *gv = vt + s;
-                bitonic_sort_block(
-                    len, [&](int64_t i) { return gk[i]; },
-                    [&](int64_t i, int64_t j) {
-                        const int32_t tk = gk[i];
-                        gk[i] = gk[j];
-                        gk[j] = tk;
-                        const double tv = gv[i];
-                        gv[i] = gv[j];
-                        gv[j] = tv;
-                    });
-            }
-            __syncthreads();
         }
+        __syncwarp();
+        for (int c = l; c < ncb; c += 32) {
+            const int s = loff[c], e = loff[c + 1] - 1;  // [s, e) entries, e = sentinel slot
+            for (int q = s + 1; q < e; ++q) {
+                const int kr = sr[q];
+                const double kv = sv[q];
+                int t = q - 1;
+                while (t >= s && sr[t] > kr) {
+                    sr[t + 1] = sr[t];
+                    sv[t + 1] = sv[t];
+                    --t;
+                }
+                sr[t + 1] = kr;
+                sv[t + 1] = kv;
+            }
+            sr[e] = INT_MAX;
+            sv[e] = 0.0;
+        }
+        __syncwarp();
+        const int64_t out0 = e0 + c0;
+        const int n = (int)E + ncb;
+        for (int t = l; t < n; t += 32) {
+            ri[out0 + t] = sr[t];
+            vt[out0 + t] = sv[t];
+        }
+        __syncwarp();
+    }
+}
+
+// Buckets too large for one warp: place with global per-column cursors, then
+// sort each column in global memory (correct for any skew, slower).
+__global__ void __launch_bounds__(128) k_bucket_sort_big(const Rec *__restrict__ rec, const int64_t *__restrict__ cp,
+                                                         int64_t ncols, unsigned *gcur, int32_t *ri, double *vt,
+                                                         int shift, const int *big_list, const int *big_count) {
+    const int bcols = 1 << shift;
+    const int nbig = *big_count;
+    for (int q = blockIdx.x; q < nbig; q += gridDim.x) {
+        const int64_t b = big_list[q];
+        const int64_t c0 = b << shift;
+        const int ncb = (int)min((int64_t)bcols, ncols - c0);
+        const int64_t e0 = cp[c0], E = cp[c0 + ncb] - e0;
+        for (int64_t t = threadIdx.x; t < E; t += blockDim.x) {
+            const Rec r = rec[e0 + t];
+            const int64_t o = cp[r.col] + r.col + atomicAdd(&gcur[r.col], 1u);
+            ri[o] = r.row;
+            vt[o] = r.x;
+        }
+        for (int c = threadIdx.x; c < ncb; c += blockDim.x) {
+            const int64_t o = cp[c0 + c + 1] + c0 + c;
+            ri[o] = INT_MAX;
+            vt[o] = 0.0;
+        }
+        __threadfence_block();
+        __syncthreads();
+        for (int c = 0; c < ncb; ++c) {
+            const int64_t s = cp[c0 + c] + c0 + c, len = cp[c0 + c + 1] - cp[c0 + c];
+            int32_t *gk = ri + s;
+            double *gv = vt + s;
+            bitonic_sort_block(
+                len, [&](int64_t i) { return gk[i]; },
+                [&](int64_t i, int64_t j) {
+                    const int32_t tk = gk[i];
+                    gk[i] = gk[j];
+                    gk[j] = tk;
+                    const double tv = gv[i];
+                    gv[i] = gv[j];
+                    gv[j] = tv;
+                });
+        }
+        __syncthreads();
     }
 }
 
 int transpose_shift(int64_t nnz, int64_t ncols) {
     const double avg = ncols > 0 ? (double)nnz / (double)ncols : 1.0;
     int sh = kMinShift;
-    while (sh < kMaxShift && (double)(1 << (sh + 1)) * avg <= kBucketTarget) ++sh;
+    while (sh < kMaxShift && (double)(1 << (sh + 1)) * (avg + 1.0) <= kBucketTarget) ++sh;
     return sh;
 }
 
@@ -230,21 +319,27 @@ int64_t transpose_buckets(int64_t nnz, int64_t ncols) {
 }
 
 void launch_transpose(const Csr &A, int scale, const int64_t *cp, double *ahat, unsigned long long *bcur,
-                      void *rec, unsigned *gcur, int32_t *ri, double *vt, int *err, cudaStream_t s) {
+                      void *rec, unsigned *gcur, int *big, int32_t *ri, double *vt, int *err, cudaStream_t s) {
     const int shift = transpose_shift(A.nnz, A.ncols);
     if (A.nrows > 0) {
-        int64_t g = (A.nrows + 255) / 256;
+        int64_t g = (A.nrows + kScatterThreads - 1) / kScatterThreads;
         const int64_t cap = (int64_t)num_sms() * 8;
         g = g < 1 ? 1 : (g > cap ? cap : g);
-        k_bucket_scatter<<<(unsigned)g, 256, 0, s>>>(A, scale, ahat, cp, bcur, static_cast<Rec *>(rec), err, shift);
+        k_bucket_scatter<<<(unsigned)g, kScatterThreads, 0, s>>>(A, scale, ahat, cp, bcur, static_cast<Rec *>(rec),
+                                                                 err, shift);
         note_launch();
     }
     if (A.ncols > 0) {
         const int64_t nb = (A.ncols + (1 << shift) - 1) >> shift;
         const int64_t cap = (int64_t)num_sms() * 16;
-        k_bucket_sort<<<(unsigned)(nb < cap ? nb : cap), kSortThreads, 0, s>>>(static_cast<const Rec *>(rec), cp,
-                                                                                A.ncols, gcur, ri, vt, shift);
-        note_launch();
+        int64_t g = (nb + kSortWarps - 1) / kSortWarps;
+        g = g < cap ? g : cap;
+        // big[0] = count of big buckets, big[1..] = their ids
+        k_bucket_sort<<<(unsigned)g, kSortThreads, 0, s>>>(static_cast<const Rec *>(rec), cp, A.ncols, ri, vt, shift,
+                                                           big + 1, big);
+        k_bucket_sort_big<<<(unsigned)num_sms(), 128, 0, s>>>(static_cast<const Rec *>(rec), cp, A.ncols, gcur, ri,
+                                                              vt, shift, big + 1, big);
+        note_launch(2);
     }
 }
 

@@ -269,21 +269,25 @@ struct rig_plan {
     int64_t rb = 0, re = 0, nloc = 0;
     DevCounters *ctr = nullptr;  // device
     DevCounters h{};             // host copy (after sync 1)
-    int32_t *sym_lists = nullptr, *num_lists = nullptr;
-    int64_t list_cap = 0;
-    int64_t *nnzc = nullptr, *gptr_ub = nullptr;
-    int32_t *farc = nullptr;
+    int64_t *nnzc = nullptr;     // [nloc] merge rows: structural nnz(C_i); others: kept + 1 (numeric)
+    // rows off the merge path (h.n_mid > 0): exact rows in the temporary
+    int32_t *lists = nullptr;    // [2 * n_mid]: mid rows, huge rows (ascending)
+    int32_t *defer = nullptr;    // [2 * n_mid]: deferred by the small / big mid kernel
+    int64_t *toff = nullptr;     // [nloc + 1]
+    int32_t *tcol = nullptr;
+    double *tw = nullptr;
     void *huge_scratch = nullptr;
     int huge_slots_n = 0;
-    int64_t nnz_upper = 0;
-    bool cached = false;  // simple API: internal buffers from the per-thread cache
+    int64_t nnz_upper = 0;  // >= graph nnz: sum (f_i - len_i)
+    bool cached = false;    // simple API: internal buffers from the per-thread cache
     explicit rig_plan(cudaStream_t st) : s(st), arena(st) {}
 };
 
-// Steps a0-a4 for rows [rb, re).  The graph row pointers (structural
-// upper-bound offsets) go to gptr_out when given.  exact: also read back
-// nnz_upper (staged API; one more sync).
-static void plan_build(rig_plan *p, const rig_csr_t *Ain, int64_t *gptr_out, bool exact) {
+// Steps a0-a4 for rows [rb, re): validation, column pointers, scaling +
+// transpose, products / paths / merge-row structure (analyze), and the
+// ordered lists and temporary of the rows off the merge path.  One host
+// synchronisation (sync 1: errors, products, list sizes).
+static void plan_build(rig_plan *p, const rig_csr_t *Ain) {
     cudaStream_t s = p->s;
     const int64_t n = Ain->nrows, m = Ain->ncols, nnz = Ain->nnz, nloc = p->nloc;
     Csr A0{n, m, nnz, Ain->row_ptr, Ain->col_idx, Ain->val};
@@ -292,24 +296,18 @@ static void plan_build(rig_plan *p, const rig_csr_t *Ain, int64_t *gptr_out, boo
     const size_t o_ctr = L.add(sizeof(DevCounters));
     const size_t o_cnt = L.add(sizeof(unsigned) * (size_t)m);
     const size_t o_st1 = L.add(scan_tmp_bytes(m));
-    const size_t o_st2 = L.add(scan_tmp_bytes(nloc));
     const size_t o_bcur = L.add(sizeof(unsigned long long) * (size_t)transpose_buckets(nnz, m));
     const size_t o_gcur = L.add(sizeof(unsigned) * (size_t)m);
+    const size_t o_big = L.add(sizeof(int) * (size_t)(1 + transpose_buckets(nnz, m)));
     const size_t zero_bytes = L.bytes;
     const size_t o_cp = L.add(sizeof(int64_t) * (size_t)(m + 1));
     const size_t o_rec = L.add(kTransposeRecBytes * (size_t)nnz);
     const size_t o_ahat = p->scale ? L.add(sizeof(double) * (size_t)nnz) : 0;
     const size_t o_ri = L.add(sizeof(int32_t) * (size_t)(nnz + m));  // + one sentinel per column
     const size_t o_vt = L.add(sizeof(double) * (size_t)(nnz + m));
-    const size_t o_sym = L.add(sizeof(int32_t) * (size_t)kSymBins * (size_t)std::max<int64_t>(nloc, 1));
     const size_t o_nnzc = L.add(sizeof(int64_t) * (size_t)nloc);
-    const size_t o_farc = L.add(sizeof(int32_t) * (size_t)nloc);
+    const size_t o_fnm = L.add(sizeof(int64_t) * (size_t)nloc);
     const size_t o_bin8 = L.add((size_t)nloc);
-    const size_t nbc = bins_count_elems(nloc);
-    const size_t o_bcnt = L.add(sizeof(unsigned) * nbc);
-    const size_t o_boff = L.add(sizeof(int64_t) * (nbc + 1));
-    const size_t o_bst = L.add(scan_tmp_bytes((int64_t)nbc));
-    const size_t o_gptr = gptr_out ? 0 : L.add(sizeof(int64_t) * (size_t)(nloc + 1));
     unsigned char *ws = p->cached ? ws_get(0, L.bytes, s) : p->arena.raw(L.bytes);
     CK(cudaMemsetAsync(ws, 0, zero_bytes, s));
     p->ctr = reinterpret_cast<DevCounters *>(ws + o_ctr);
@@ -318,14 +316,9 @@ static void plan_build(rig_plan *p, const rig_csr_t *Ain, int64_t *gptr_out, boo
     double *ahat = p->scale ? reinterpret_cast<double *>(ws + o_ahat) : nullptr;
     int32_t *ri = reinterpret_cast<int32_t *>(ws + o_ri);
     double *vt = reinterpret_cast<double *>(ws + o_vt);
-    p->sym_lists = reinterpret_cast<int32_t *>(ws + o_sym);
     p->nnzc = reinterpret_cast<int64_t *>(ws + o_nnzc);
-    p->farc = reinterpret_cast<int32_t *>(ws + o_farc);
-    p->gptr_ub = gptr_out ? gptr_out : reinterpret_cast<int64_t *>(ws + o_gptr);
-    p->list_cap = nloc;
+    int64_t *fnm = reinterpret_cast<int64_t *>(ws + o_fnm);
     uint8_t *bin8 = reinterpret_cast<uint8_t *>(ws + o_bin8);
-    unsigned *bcnt = reinterpret_cast<unsigned *>(ws + o_bcnt);
-    int64_t *boff = reinterpret_cast<int64_t *>(ws + o_boff);
     HostStage *hs = host_stage();
 
     // a0: validation must finish before anything indexes with the input
@@ -348,62 +341,60 @@ static void plan_build(rig_plan *p, const rig_csr_t *Ain, int64_t *gptr_out, boo
     {
         Prof pf(P_SCATTER, s);
         launch_transpose(A0, p->scale, cp, ahat, reinterpret_cast<unsigned long long *>(ws + o_bcur), ws + o_rec,
-                         reinterpret_cast<unsigned *>(ws + o_gcur), ri, vt, &p->ctr->err, s);
+                         reinterpret_cast<unsigned *>(ws + o_gcur), reinterpret_cast<int *>(ws + o_big), ri, vt,
+                         &p->ctr->err, s);
     }
     check_launch("prep");
     p->A = Csr{n, m, nnz, Ain->row_ptr, Ain->col_idx, p->scale ? ahat : Ain->val};
     p->T = Csc{cp, ri, vt};
-    // a3 + a4 (merge rows): products, structural nnz(C_i), bins for the rest
-    SymArgs sa{p->A, p->T, p->rb, p->re, p->nnzc, p->farc};
+    // a3 + a4 (merge rows): products, merge-row nnzC, paths of the others
+    SymArgs sa{p->A, p->T, p->rb, p->re, p->nnzc, fnm};
     if (nloc > 0) {
         Prof pf(P_ANALYZE, s);
         launch_analyze_sym(sa, bin8, p->ctr, s);
     }
     check_launch("analyze");
-    // sync 1: errors, products, bin sizes
+    // sync 1: errors, products, path sizes
     CK(cudaMemcpyAsync(&hs->ctr, p->ctr, sizeof(DevCounters), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     p->h = hs->ctr;
     if (p->h.err) throw Error(err_to_code(p->h.err), err_msg(err_to_code(p->h.err)));
-    // a4 for rows off the merge path
+    p->nnz_upper = p->h.products - p->h.nnz_rows;
     const int64_t n_mid = p->h.n_mid;
-    if (n_mid > 0) {
-        Prof pf(P_SYMBOLIC, s);
-        launch_bins(0, bin8, nullptr, p->rb, nloc, bcnt, boff, ws + o_bst, p->sym_lists, p->list_cap, nullptr, s);
-        launch_sym_warp(sa, p->sym_lists, p->list_cap, p->ctr->sym_count, p->h.sym_count, s);
-        // rows with f > 1024 may need the huge numeric path too (nnzC <= f)
-        const int64_t n_big = p->h.sym_count[kNumSymBins] + p->h.sym_count[kNumSymBins - 1];
-        Layout LB;
-        const size_t o_num = LB.add(sizeof(int32_t) * (size_t)kNumBins * (size_t)n_mid);
-        size_t o_huge = 0, huge_bytes = 0;
-        if (n_big > 0) {
-            p->huge_slots_n = huge_slots(n, n_big);
-            huge_bytes = huge_scratch_bytes(n, p->huge_slots_n, true);
-            o_huge = LB.add(huge_bytes);
-        }
-        unsigned char *wb = p->cached ? ws_get(1, LB.bytes, s) : p->arena.raw(LB.bytes);
-        p->num_lists = reinterpret_cast<int32_t *>(wb + o_num);
-        if (n_big > 0) {
-            p->huge_scratch = wb + o_huge;
-            CK(cudaMemsetAsync(p->huge_scratch, 0, huge_bitmap_bytes(n, p->huge_slots_n), s));
-        }
-        if (p->h.sym_count[kNumSymBins] > 0)
-            launch_sym_huge(sa, p->sym_lists + (int64_t)kNumSymBins * p->list_cap, p->ctr->sym_count + kNumSymBins,
-                            p->huge_slots_n, p->huge_scratch, s);
-        launch_bins(1, bin8, p->farc, p->rb, nloc, bcnt, boff, ws + o_bst, p->num_lists, n_mid, p->ctr->num_count, s);
+    if (n_mid == 0) return;
+    // ---- rows off the merge path: ordered lists, temporary layout
+    Prof pf(P_SYMBOLIC, s);
+    const bool need_huge = p->h.max_f > kMidBigCap;
+    const size_t nbc = bins_count_elems(nloc);
+    Layout LB;
+    const size_t o_toff = LB.add(sizeof(int64_t) * (size_t)(nloc + 1));
+    const size_t o_st2 = LB.add(scan_tmp_bytes(nloc));
+    const size_t o_lists = LB.add(sizeof(int32_t) * 2 * (size_t)n_mid);
+    const size_t o_defer = LB.add(sizeof(int32_t) * 2 * (size_t)n_mid);
+    const size_t o_bcnt = LB.add(sizeof(unsigned) * nbc);
+    const size_t o_boff = LB.add(sizeof(int64_t) * (nbc + 1));
+    const size_t o_bst = LB.add(scan_tmp_bytes((int64_t)nbc));
+    const size_t o_tcol = LB.add(sizeof(int32_t) * (size_t)p->h.mid_slots);
+    const size_t o_tw = LB.add(sizeof(double) * (size_t)p->h.mid_slots);
+    size_t o_huge = 0;
+    if (need_huge) {
+        p->huge_slots_n = huge_slots(n, n_mid);
+        o_huge = LB.add(huge_scratch_bytes(n, p->huge_slots_n, true));
     }
-    check_launch("symbolic");
-    {
-        Prof pf(P_UBSCAN, s);
-        scan_i64(p->nnzc, nloc, p->gptr_ub, ScanOp::UbOffDiag, ws + o_st2, 0, s);
+    unsigned char *wb = p->cached ? ws_get(1, LB.bytes, s) : p->arena.raw(LB.bytes);
+    p->toff = reinterpret_cast<int64_t *>(wb + o_toff);
+    p->lists = reinterpret_cast<int32_t *>(wb + o_lists);
+    p->defer = reinterpret_cast<int32_t *>(wb + o_defer);
+    p->tcol = reinterpret_cast<int32_t *>(wb + o_tcol);
+    p->tw = reinterpret_cast<double *>(wb + o_tw);
+    if (need_huge) {
+        p->huge_scratch = wb + o_huge;
+        CK(cudaMemsetAsync(p->huge_scratch, 0, huge_bitmap_bytes(n, p->huge_slots_n), s));
     }
-    check_launch("scan");
-    p->nnz_upper = -1;
-    if (exact) {  // sync 2 (staged API): exact capacity for the caller
-        CK(cudaMemcpyAsync(&hs->v[0], p->gptr_ub + nloc, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
-        CK(cudaStreamSynchronize(s));
-        p->nnz_upper = hs->v[0];
-    }
+    scan_i64(fnm, nloc, p->toff, ScanOp::Identity, wb + o_st2, 0, s);
+    launch_bins(bin8, p->rb, nloc, reinterpret_cast<unsigned *>(wb + o_bcnt), reinterpret_cast<int64_t *>(wb + o_boff),
+                wb + o_bst, p->lists, n_mid, p->ctr->list_count, s);
+    check_launch("lists");
 }
 
 struct CutReq {
@@ -412,35 +403,77 @@ struct CutReq {
     double *cut_dev = nullptr;
 };
 
-// a5 + a6 into caller arrays (capacity >= structural off-diagonal nnz); the
-// optional cutsize (a7) is fused into the numeric kernels and reduced right
-// behind them, so it costs no extra synchronisation.
-// Returns the final nnz.  Synchronises once (twice if entries were dropped).
+// a5 + a6 (+ fused a7) into caller arrays of capacity >= p->nnz_upper:
+// rows off the merge path into the temporary (exact counts), the scan of all
+// rows' counts into the graph row pointers, merge rows in place, the others
+// copied into place.  Returns the graph nnz.  Synchronises once (twice if a
+// merge row dropped an entry by value: compaction).
 static int64_t plan_numeric(rig_plan *p, int32_t *gcol, double *gw, double *diag, int64_t *row_ptr_out,
                             Arena &tmp_arena, const CutReq *cut) {
     cudaStream_t s = p->s;
-    // zeroed: holes flag, fused-cut used counts + bad flag; then the partials
+    // zeroed: holes flag, fused-cut used counts + bad flag
     Layout L;
     const size_t o_holes = L.add(sizeof(int));
     const size_t o_used = L.add(sizeof(int) * (kCutLaunches + 1));
     const size_t zero_bytes = L.bytes;
     const size_t o_cutp = cut ? L.add(sizeof(double) * (size_t)kCutLaunches * kCutSlotsPerLaunch) : 0;
+    const size_t o_st = L.add(scan_tmp_bytes(p->nloc));
     unsigned char *wn = p->cached ? ws_get(2, L.bytes, s) : tmp_arena.raw(L.bytes);
     CK(cudaMemsetAsync(wn, 0, zero_bytes, s));
     int *holes_d = reinterpret_cast<int *>(wn + o_holes);
     int *used = reinterpret_cast<int *>(wn + o_used);
     int *badp = used + kCutLaunches;
     double *cutp = cut ? reinterpret_cast<double *>(wn + o_cutp) : nullptr;
+    double *dg = (p->flags & RIG_FLAG_DIAG) ? diag : nullptr;
+    const int64_t n_mid = p->h.n_mid;
     {
         Prof pf(P_NUMERIC, s);
+        if (n_mid > 0) {
+            // slot segments of the fused-cut partials: 0 merge, 1 mid small, 2 mid big, 3 / 4 huge
+            auto seg = [&](MidArgs &x, int g) {
+                if (cut) {
+                    x.cutp = cutp + (int64_t)g * kCutSlotsPerLaunch;
+                    x.cut_used = used + g;
+                }
+            };
+            MidArgs ma{p->A,   p->T,  p->rb,   p->lists, p->ctr->list_count, p->toff, p->tcol, p->tw, p->nnzc,
+                       p->defer, p->ctr->defer_count, dg, p->tol, cut ? cut->part : nullptr, cut ? cut->K : 0,
+                       nullptr, badp, nullptr};
+            seg(ma, 1);
+            launch_num_mid(ma, kMidSmallCap, s);
+            if (p->h.max_f > kMidSmallCap) {  // rows whose far list may exceed the small capacity
+                MidArgs mb = ma;
+                mb.list = p->defer;
+                mb.count = p->ctr->defer_count;
+                mb.defer_list = p->defer + n_mid;
+                mb.defer_count = p->ctr->defer_count + 1;
+                seg(mb, 2);
+                launch_num_mid(mb, kMidBigCap, s);
+            }
+            if (p->huge_scratch) {
+                MidArgs hu = ma;
+                hu.list = p->lists + n_mid;  // f_i beyond the mid bins
+                hu.count = p->ctr->list_count + 1;
+                seg(hu, 3);
+                launch_num_huge(hu, p->huge_slots_n, p->huge_scratch, s);
+                hu.list = p->defer + n_mid;  // deferred by the big mid kernel
+                hu.count = p->ctr->defer_count + 1;
+                seg(hu, 4);
+                launch_num_huge(hu, p->huge_slots_n, p->huge_scratch, s);
+            }
+        }
+        {
+            Prof pfs(P_UBSCAN, s);
+            scan_i64(p->nnzc, p->nloc, row_ptr_out, ScanOp::UbOffDiag, wn + o_st, 0, s);
+        }
         NumArgs na{p->A,
                    p->T,
                    p->rb,
                    p->re,
-                   p->gptr_ub,
+                   row_ptr_out,
                    gcol,
                    gw,
-                   (p->flags & RIG_FLAG_DIAG) ? diag : nullptr,
+                   dg,
                    p->tol,
                    holes_d,
                    cut ? cut->part : nullptr,
@@ -450,13 +483,11 @@ static int64_t plan_numeric(rig_plan *p, int32_t *gcol, double *gw, double *diag
                    used,
                    stage_cap_for(p->h.products, p->nloc)};
         if (p->nloc > 0) launch_num_merge(na, p->h.max_len, s);
-        if (p->h.n_mid > 0) {
-            // numeric bin sizes are device-side; empty bins exit immediately
-            const int64_t all[8] = {1, 1, 1, 1, 1, 1, 1, 1};
-            launch_num_warp(na, p->num_lists, p->h.n_mid, p->ctr->num_count, all, s);
+        if (n_mid > 0) {
+            launch_copy_rows(p->lists, p->ctr->list_count, p->rb, p->toff, row_ptr_out, p->tcol, p->tw, gcol, gw, s);
             if (p->huge_scratch)
-                launch_num_huge(na, p->num_lists + (int64_t)kNumNumBins * p->h.n_mid,
-                                p->ctr->num_count + kNumNumBins, p->huge_slots_n, p->huge_scratch, s);
+                launch_copy_rows(p->lists + n_mid, p->ctr->list_count + 1, p->rb, p->toff, row_ptr_out, p->tcol, p->tw,
+                                 gcol, gw, s);
         }
         check_launch("numeric");
     }
@@ -467,37 +498,28 @@ static int64_t plan_numeric(rig_plan *p, int32_t *gcol, double *gw, double *diag
     }
     HostStage *hs = host_stage();
     CK(cudaMemcpyAsync(&hs->holes, holes_d, sizeof(int), cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpyAsync(&hs->v[0], p->gptr_ub + p->nloc, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(&hs->v[0], row_ptr_out + p->nloc, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     const int holes = hs->holes;
     const int64_t ub = hs->v[0];
-    p->nnz_upper = ub;
-    if (!holes) {
-        if (row_ptr_out != p->gptr_ub)
-            CK(cudaMemcpyAsync(row_ptr_out, p->gptr_ub, sizeof(int64_t) * (size_t)(p->nloc + 1),
-                               cudaMemcpyDeviceToDevice, s));
-        return ub;
-    }
-    // holes: count kept entries per row, scan, move into a temporary, copy back
+    if (!holes) return ub;
+    // holes (merge-row entries dropped by value): count kept entries per row,
+    // scan, move into a temporary, copy back
     Prof pf_c(P_COMPACT, s);
     Layout LC;
     const size_t o_copy = LC.add(sizeof(int64_t) * (size_t)(p->nloc + 1));
     const size_t o_kept = LC.add(sizeof(int64_t) * (size_t)p->nloc);
-    const size_t o_st = LC.add(scan_tmp_bytes(p->nloc));
+    const size_t o_st2 = LC.add(scan_tmp_bytes(p->nloc));
     const size_t o_c2 = LC.add(sizeof(int32_t) * (size_t)ub);
     const size_t o_w2 = LC.add(sizeof(double) * (size_t)ub);
     unsigned char *wc = tmp_arena.raw(LC.bytes);
-    const int64_t *ubp = p->gptr_ub;
-    if (row_ptr_out == p->gptr_ub) {  // keep the structural offsets for the move
-        int64_t *copy = reinterpret_cast<int64_t *>(wc + o_copy);
-        CK(cudaMemcpyAsync(copy, p->gptr_ub, sizeof(int64_t) * (size_t)(p->nloc + 1), cudaMemcpyDeviceToDevice, s));
-        ubp = copy;
-    }
+    int64_t *ubp = reinterpret_cast<int64_t *>(wc + o_copy);  // structural offsets
+    CK(cudaMemcpyAsync(ubp, row_ptr_out, sizeof(int64_t) * (size_t)(p->nloc + 1), cudaMemcpyDeviceToDevice, s));
     int64_t *kept = reinterpret_cast<int64_t *>(wc + o_kept);
     int32_t *c2 = reinterpret_cast<int32_t *>(wc + o_c2);
     double *w2 = reinterpret_cast<double *>(wc + o_w2);
     launch_count_kept(ubp, p->nloc, gcol, kept, s);
-    scan_i64(kept, p->nloc, row_ptr_out, ScanOp::Identity, wc + o_st, 0, s);
+    scan_i64(kept, p->nloc, row_ptr_out, ScanOp::Identity, wc + o_st2, 0, s);
     CK(cudaMemcpyAsync(&hs->v[1], row_ptr_out + p->nloc, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
     launch_compact_move(ubp, row_ptr_out, p->nloc, gcol, gw, c2, w2, s);
     check_launch("compact");
@@ -530,7 +552,7 @@ static rig_plan *make_plan(const rig_csr_t *A, int scale_rows, double drop_tol, 
                            int64_t re, cudaStream_t s) {
     rig_plan *p = new_plan(A, scale_rows, drop_tol, flags, rb, re, s);
     try {
-        plan_build(p, A, nullptr, true);
+        plan_build(p, A);
     } catch (...) {
         delete p;
         throw;
@@ -572,9 +594,9 @@ static void free_owned(rig_graph_t *g, cudaStream_t s) {
     std::memset(g, 0, sizeof(*g));
 }
 
-// Library-owned output.  The (col, w, diag) block is sized from the product
-// count P (known at the first sync; P >= nnz(C) >= graph nnz), so the numeric
-// pass follows the symbolic scan without a host round trip.
+// Library-owned output.  The (col, w, diag) block is sized from the bound
+// sum (f_i - len_i) >= graph nnz (known at the first sync), so the numeric
+// passes follow without another host round trip.
 static void build_owned(const rig_csr_t *A, int scale_rows, double drop_tol, uint32_t flags, int64_t rb, int64_t re,
                         rig_graph_t *out, cudaStream_t s, const CutReq *cut) {
     if (!out) throw Error(RIG_ERR_INVALID, "out is NULL");
@@ -586,8 +608,8 @@ static void build_owned(const rig_csr_t *A, int scale_rows, double drop_tol, uin
     unsigned char *block = nullptr;
     try {
         CK(cudaMallocAsync((void **)&rp, sizeof(int64_t) * (size_t)(p->nloc + 1), s));
-        plan_build(p, A, rp, false);
-        const int64_t cap = std::max<int64_t>(p->h.products, 1);
+        plan_build(p, A);
+        const int64_t cap = std::max<int64_t>(p->nnz_upper, 1);
         Layout L;
         const size_t o_col = L.add(sizeof(int32_t) * (size_t)cap);
         const size_t o_w = L.add(sizeof(double) * (size_t)cap);
