@@ -213,7 +213,7 @@ void launch_num_merge(const NumArgs &a, int maxlen, cudaStream_t s);
 // Rows off the merge path (k_midrow.cu, k_spgemm.cu huge path): each row is
 // written with its exact kept entries to a temporary at toff[r] and
 // cnt[r] = kept + 1 (the graph scan subtracts the diagonal slot); k_copy_rows
-// places it after the scan.
+// places it after the scan and takes its share of the fused cut.
 struct MidArgs {
     Csr A;
     Csc T;
@@ -228,16 +228,23 @@ struct MidArgs {
     int64_t *defer_count;
     double *diag;           // may be null
     double tol;
-    const int32_t *part;    // fused a7 (optional), as in NumArgs
+    int dbg;  // experiment switches (RIG_DEBUG_MASK); 0 in normal operation
+};
+// Fused a7 partials of one launch (part == nullptr: off): each CTA writes the
+// Neumaier sum of its cut edges to cutp[blockIdx.x], *used = gridDim.x.
+struct CutOut {
+    const int32_t *part;
     int32_t K;
     double *cutp;
-    int *bad_part;
-    int *cut_used;
+    int *bad;
+    int *used;
 };
+int debug_mask();  // RIG_DEBUG_MASK environment variable (performance experiments only)
 constexpr int kMidSmallCap = 256, kMidBigCap = 2048;  // far-list capacities of the two mid kernels
 void launch_num_mid(const MidArgs &a, int fcap, cudaStream_t s);
 void launch_copy_rows(const int32_t *list, const int64_t *count, int64_t rb, const int64_t *toff, const int64_t *gptr,
-                      const int32_t *tcol, const double *tw, int32_t *gcol, double *gw, cudaStream_t s);
+                      const int32_t *tcol, const double *tw, int32_t *gcol, double *gw, const CutOut &cut,
+                      cudaStream_t s);
 // huge rows: CTA per row, dense accumulator + bitmap in global scratch
 size_t huge_scratch_bytes(int64_t nrows, int slots, bool numeric);
 size_t huge_bitmap_bytes(int64_t nrows, int slots);  // zeroed prefix of the scratch

@@ -501,8 +501,6 @@ __global__ void __launch_bounds__(kHugeThreads) k_num_huge(MidArgs a, unsigned c
     const unsigned lt = lanemask_lt();
     for (int64_t t = tid; t < nw2; t += kHugeThreads) l2[t] = 0u;
     __syncthreads();
-    Comp cut;
-    int badp = 0;
     const int64_t n = *a.count;
     for (int64_t idx = blockIdx.x; idx < n; idx += gridDim.x) {
         const int64_t i = a.list[idx];
@@ -590,11 +588,6 @@ __global__ void __launch_bounds__(kHugeThreads) k_num_huge(MidArgs a, unsigned c
         __syncthreads();
         // ---- emit in ascending j: walk the non-empty L1 words via the L2 bitmap
         const int64_t g0 = a.toff[r];  // temporary slot of the row
-        int32_t pi = 0;
-        if (a.part) {
-            pi = a.part[i];
-            badp |= (pi < 0) | (pi >= a.K);
-        }
         int64_t o = 0;
         for (int64_t rb2 = 0; rb2 < nw2; rb2 += kHugeThreads) {
             const int64_t t2 = rb2 + tid;
@@ -630,11 +623,6 @@ __global__ void __launch_bounds__(kHugeThreads) k_num_huge(MidArgs a, unsigned c
                         a.tcol[pos] = (int32_t)j;
                         a.tw[pos] = fabs(c);
                         ++pos;
-                        if (a.part && j > i) {
-                            const int32_t pj = a.part[j];
-                            badp |= (pj < 0) | (pj >= a.K);
-                            if (pj != pi) cut.add(fabs(c));
-                        }
                     }
                 }
                 bm[w1] = 0u;
@@ -645,14 +633,6 @@ __global__ void __launch_bounds__(kHugeThreads) k_num_huge(MidArgs a, unsigned c
         }
         if (tid == 0) a.cnt[r] = o + 1;  // exact kept count (+1: the scan subtracts the diagonal)
         __syncthreads();
-    }
-    if (a.part) {
-        const double v = block_tree_sum<kHugeThreads>(cut.value());
-        if (threadIdx.x == 0) {
-            a.cutp[blockIdx.x] = v;
-            if (blockIdx.x == 0) *a.cut_used = (int)gridDim.x;
-        }
-        if (__syncthreads_or(badp) && threadIdx.x == 0) atomicOr(a.bad_part, 1);
     }
 }
 

@@ -180,23 +180,30 @@ __device__ void bitonic_sort_block(int64_t len, KeyAt key, Swap swap) {
 constexpr int kSortThreads = 64;  // 2 warps: one bucket per warp
 constexpr int kSortWarps = kSortThreads / 32;
 
-// One warp per bucket: records are placed by column straight into their CSC
-// slots (column c of the bucket occupies [loff[c] + c, loff[c+1] + c), then
-// its sentinel), each column is ordered by row (columns are short: insertion
-// sort by one lane), and the slice -- entries and sentinels -- is written
-// with fully coalesced stores.  Buckets that do not fit are listed for
+// One warp per bucket: records are placed by column into their CSC slots
+// (column c of the bucket occupies [loff[c], loff[c+1] - 1), then its
+// sentinel), each entry is ranked by row within its column, and the slice --
+// entries and sentinels, in rank order -- is written with fully coalesced
+// stores.  Buckets that do not fit are listed for
 // k_bucket_sort_big.
+template <bool RANK>
 __global__ void __launch_bounds__(kSortThreads) k_bucket_sort(const Rec *__restrict__ rec,
                                                               const int64_t *__restrict__ cp, int64_t ncols,
                                                               int32_t *ri, double *vt, int shift, int *big_list,
                                                               int *big_count) {
     __shared__ int32_t s_ri[kSortWarps][kBucketSlots];
     __shared__ double s_vt[kSortWarps][kBucketSlots];
+    constexpr int RS = RANK ? kBucketSlots : 1;
+    __shared__ uint16_t s_col[kSortWarps][RS];  // local column of a slot (0xffff: sentinel)
+    __shared__ uint16_t s_inv[kSortWarps][RS];  // sorted position -> slot
     __shared__ uint16_t s_off[kSortWarps][kMaxBucketCols + 1];
     __shared__ unsigned s_cur[kSortWarps][kMaxBucketCols];
     const int w = threadIdx.x >> 5, l = lane_id();
     int32_t *sr = s_ri[w];
     double *sv = s_vt[w];
+    uint16_t *scol = s_col[w], *inv = s_inv[w];
+    (void)scol;
+    (void)inv;
     uint16_t *loff = s_off[w];
     unsigned *cur = s_cur[w];
     const int bcols = 1 << shift;
@@ -215,6 +222,7 @@ __global__ void __launch_bounds__(kSortThreads) k_bucket_sort(const Rec *__restr
             const int o = (int)(cp[c0 + c] - e0) + c;
             loff[c] = (uint16_t)o;
             if (c < ncb) cur[c] = (unsigned)o;
+            if (RANK && c > 0) scol[o - 1] = 0xffff;  // sentinel slot of column c - 1
         }
         __syncwarp();
         for (int t0 = 0; t0 < (int)E; t0 += 128) {  // 4 record loads in flight per lane
@@ -227,36 +235,59 @@ __global__ void __launch_bounds__(kSortThreads) k_bucket_sort(const Rec *__restr
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
                 if (t0 + 32 * u + l < (int)E) {
-                    const int pos = (int)atomicAdd(&cur[rr[u].col - (int)c0], 1u);
+                    const int lc = rr[u].col - (int)c0;
+                    const int pos = (int)atomicAdd(&cur[lc], 1u);
                     sr[pos] = rr[u].row;
                     sv[pos] = rr[u].x;
+                    if (RANK) scol[pos] = (uint16_t)lc;
                 }
             }
         }
         __syncwarp();
-        for (int c = l; c < ncb; c += 32) {
-            const int s = loff[c], e = loff[c + 1] - 1;  // [s, e) entries, e = sentinel slot
-            for (int q = s + 1; q < e; ++q) {
-                const int kr = sr[q];
-                const double kv = sv[q];
-                int t = q - 1;
-                while (t >= s && sr[t] > kr) {
-                    sr[t + 1] = sr[t];
-                    sv[t + 1] = sv[t];
-                    --t;
+        const int n = (int)E + ncb;
+        if (RANK) {
+            // order each column by row: an entry's rank in its column is the
+            // number of entries of that column with a smaller row (rows are
+            // distinct), so every slot is ranked independently -- no serial
+            // insertion chains on long columns
+            for (int q = l; q < n; q += 32) {
+                const int c = scol[q];
+                if (c == 0xffff) {
+                    inv[q] = 0xffff;  // a sentinel stays at the end of its column
+                    continue;
                 }
-                sr[t + 1] = kr;
-                sv[t + 1] = kv;
+                const int s0 = loff[c], e1 = loff[c + 1] - 1;
+                const int rq = sr[q];
+                int rank = 0;
+                for (int t = s0; t < e1; ++t) rank += sr[t] < rq;
+                inv[s0 + rank] = (uint16_t)q;
             }
-            sr[e] = INT_MAX;
-            sv[e] = 0.0;
+        } else {
+            // short columns: insertion sort by one lane per column
+            for (int c = l; c < ncb; c += 32) {
+                const int s0 = loff[c], e1 = loff[c + 1] - 1;  // [s0, e1) entries, e1 = sentinel slot
+                for (int q = s0 + 1; q < e1; ++q) {
+                    const int kr = sr[q];
+                    const double kv = sv[q];
+                    int t = q - 1;
+                    while (t >= s0 && sr[t] > kr) {
+                        sr[t + 1] = sr[t];
+                        sv[t + 1] = sv[t];
+                        --t;
+                    }
+                    sr[t + 1] = kr;
+                    sv[t + 1] = kv;
+                }
+                sr[e1] = INT_MAX;
+                sv[e1] = 0.0;
+            }
         }
         __syncwarp();
         const int64_t out0 = e0 + c0;
-        const int n = (int)E + ncb;
         for (int t = l; t < n; t += 32) {
-            ri[out0 + t] = sr[t];
-            vt[out0 + t] = sv[t];
+            const int q = RANK ? (int)inv[t] : t;
+            ri[out0 + t] = q == 0xffff ? INT_MAX : sr[q];
+            vt[out0 + t] = q == 0xffff ? 0.0 : sv[q];
         }
         __syncwarp();
     }
@@ -335,8 +366,13 @@ void launch_transpose(const Csr &A, int scale, const int64_t *cp, double *ahat, 
         int64_t g = (nb + kSortWarps - 1) / kSortWarps;
         g = g < cap ? g : cap;
         // big[0] = count of big buckets, big[1..] = their ids
-        k_bucket_sort<<<(unsigned)g, kSortThreads, 0, s>>>(static_cast<const Rec *>(rec), cp, A.ncols, ri, vt, shift,
-                                                           big + 1, big);
+        // long columns: parallel ranking; short ones: per-lane insertion sorts
+        if (A.nnz > (int64_t)12 * A.ncols)
+            k_bucket_sort<true><<<(unsigned)g, kSortThreads, 0, s>>>(static_cast<const Rec *>(rec), cp, A.ncols, ri,
+                                                                     vt, shift, big + 1, big);
+        else
+            k_bucket_sort<false><<<(unsigned)g, kSortThreads, 0, s>>>(static_cast<const Rec *>(rec), cp, A.ncols, ri,
+                                                                      vt, shift, big + 1, big);
         k_bucket_sort_big<<<(unsigned)num_sms(), 128, 0, s>>>(static_cast<const Rec *>(rec), cp, A.ncols, gcur, ri,
                                                               vt, shift, big + 1, big);
         note_launch(2);

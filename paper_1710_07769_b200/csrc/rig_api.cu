@@ -24,6 +24,15 @@ namespace rig {
 static std::atomic<uint64_t> g_launches{0};
 void note_launch(int n) { g_launches.fetch_add((uint64_t)n, std::memory_order_relaxed); }
 
+int debug_mask() {
+    static int m = -1;
+    if (m < 0) {
+        const char *e = getenv("RIG_DEBUG_MASK");
+        m = e ? atoi(e) : 0;
+    }
+    return m;
+}
+
 int num_sms() {
     static int cache[64] = {0};
     int dev = 0;
@@ -364,7 +373,7 @@ static void plan_build(rig_plan *p, const rig_csr_t *Ain) {
     if (n_mid == 0) return;
     // ---- rows off the merge path: ordered lists, temporary layout
     Prof pf(P_SYMBOLIC, s);
-    const bool need_huge = p->h.max_f > kMidBigCap;
+    const bool need_huge = p->h.max_f > kMidSmallCap;  // far lists beyond the mid kernel go to the huge path
     const size_t nbc = bins_count_elems(nloc);
     Layout LB;
     const size_t o_toff = LB.add(sizeof(int64_t) * (size_t)(nloc + 1));
@@ -429,36 +438,16 @@ static int64_t plan_numeric(rig_plan *p, int32_t *gcol, double *gw, double *diag
     {
         Prof pf(P_NUMERIC, s);
         if (n_mid > 0) {
-            // slot segments of the fused-cut partials: 0 merge, 1 mid small, 2 mid big, 3 / 4 huge
-            auto seg = [&](MidArgs &x, int g) {
-                if (cut) {
-                    x.cutp = cutp + (int64_t)g * kCutSlotsPerLaunch;
-                    x.cut_used = used + g;
-                }
-            };
-            MidArgs ma{p->A,   p->T,  p->rb,   p->lists, p->ctr->list_count, p->toff, p->tcol, p->tw, p->nnzc,
-                       p->defer, p->ctr->defer_count, dg, p->tol, cut ? cut->part : nullptr, cut ? cut->K : 0,
-                       nullptr, badp, nullptr};
-            seg(ma, 1);
+            MidArgs ma{p->A,     p->T,     p->rb,  p->lists, p->ctr->list_count, p->toff, p->tcol, p->tw,
+                       p->nnzc,  p->defer, p->ctr->defer_count, dg, p->tol, debug_mask()};
             launch_num_mid(ma, kMidSmallCap, s);
-            if (p->h.max_f > kMidSmallCap) {  // rows whose far list may exceed the small capacity
-                MidArgs mb = ma;
-                mb.list = p->defer;
-                mb.count = p->ctr->defer_count;
-                mb.defer_list = p->defer + n_mid;
-                mb.defer_count = p->ctr->defer_count + 1;
-                seg(mb, 2);
-                launch_num_mid(mb, kMidBigCap, s);
-            }
             if (p->huge_scratch) {
                 MidArgs hu = ma;
                 hu.list = p->lists + n_mid;  // f_i beyond the mid bins
                 hu.count = p->ctr->list_count + 1;
-                seg(hu, 3);
                 launch_num_huge(hu, p->huge_slots_n, p->huge_scratch, s);
-                hu.list = p->defer + n_mid;  // deferred by the big mid kernel
-                hu.count = p->ctr->defer_count + 1;
-                seg(hu, 4);
+                hu.list = p->defer;  // far list beyond the mid kernel's capacity
+                hu.count = p->ctr->defer_count;
                 launch_num_huge(hu, p->huge_slots_n, p->huge_scratch, s);
             }
         }
@@ -476,18 +465,24 @@ static int64_t plan_numeric(rig_plan *p, int32_t *gcol, double *gw, double *diag
                    dg,
                    p->tol,
                    holes_d,
-                   cut ? cut->part : nullptr,
+                   (cut && !(debug_mask() & 256)) ? cut->part : nullptr,
                    cut ? cut->K : 0,
                    cutp,
                    badp,
                    used,
                    stage_cap_for(p->h.products, p->nloc)};
         if (p->nloc > 0) launch_num_merge(na, p->h.max_len, s);
-        if (n_mid > 0) {
-            launch_copy_rows(p->lists, p->ctr->list_count, p->rb, p->toff, row_ptr_out, p->tcol, p->tw, gcol, gw, s);
+        if (n_mid > 0) {  // cut-partial segments: 0 merge rows, 1 mid rows, 2 huge rows
+            auto co = [&](int g) {
+                CutOut c{nullptr, 0, nullptr, nullptr, nullptr};
+                if (cut) c = CutOut{cut->part, cut->K, cutp + (int64_t)g * kCutSlotsPerLaunch, badp, used + g};
+                return c;
+            };
+            launch_copy_rows(p->lists, p->ctr->list_count, p->rb, p->toff, row_ptr_out, p->tcol, p->tw, gcol, gw,
+                             co(1), s);
             if (p->huge_scratch)
                 launch_copy_rows(p->lists + n_mid, p->ctr->list_count + 1, p->rb, p->toff, row_ptr_out, p->tcol, p->tw,
-                                 gcol, gw, s);
+                                 gcol, gw, co(2), s);
         }
         check_launch("numeric");
     }
