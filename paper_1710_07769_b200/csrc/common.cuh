@@ -50,7 +50,7 @@ constexpr int kSymBins = kNumSymBins + 1;  // + huge
 struct DevCounters {
     int err;
     int holes;          // numeric pass dropped an entry (|c| <= tol or exact 0)
-    unsigned long_cols; // columns longer than the short-sort limit
+    int pad0;
     int max_len;        // longest A row (in the shard) on the merge path
     int64_t products;   // sum f_i over the shard
     int64_t n_mid;      // rows not on the merge path
@@ -60,6 +60,11 @@ struct DevCounters {
     int64_t sym_count[8];
     int64_t list_count[2]; // mid / huge list lengths (device side)
     int64_t defer_count[2];// rows deferred by the small / big mid kernels
+    // shape statistics (k_shape_stats, right after the column histogram)
+    int64_t max_col;       // longest column of A
+    int64_t p_full;        // sum over columns of len^2 = products of the full matrix (>= the shard's)
+    int64_t max_row;       // longest row of A in the shard
+    int64_t shard_nnz;     // entries of A in the shard's rows
 };
 
 __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
@@ -100,10 +105,14 @@ int num_sms();
 // k_prep.cu
 void launch_validate(const Csr &A, int *err, cudaStream_t s);
 void launch_col_hist(const Csr &A, unsigned *cnt, unsigned *rank /*nullable*/, cudaStream_t s);
+// max_col, p_full, max_row, shard_nnz into ctr (zeroed) from the column counts
+// and the row pointers of rows [rb, re)
+void launch_shape_stats(const unsigned *cnt, int64_t m, const int64_t *rp, int64_t rb, int64_t re, DevCounters *ctr,
+                        cudaStream_t s);
 // k_transpose.cu: bucketed a1 + a2 (see there for the CSC layout with sentinels)
 int64_t transpose_buckets(int64_t nnz, int64_t ncols);
 constexpr size_t kTransposeRecBytes = 16;
-// bcur: u64[transpose_buckets] zeroed; gcur: u32[ncols] zeroed; big: int[1 + transpose_buckets]
+// bcur: u64[transpose_buckets] (initialised here); gcur: u32[ncols] zeroed; big: int[1 + transpose_buckets]
 // with big[0] zeroed (list of buckets too large for the warp sort).
 void launch_transpose(const Csr &A, int scale, const int64_t *cp, double *ahat, unsigned long long *bcur,
                       void *rec, unsigned *gcur, int *big, int32_t *ri, double *vt, int *err, cudaStream_t s);

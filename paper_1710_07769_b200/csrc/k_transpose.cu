@@ -105,7 +105,7 @@ __global__ void __launch_bounds__(kScatterThreads) k_bucket_scatter(Csr A, int s
         __syncwarp();
         const int64_t lo = __shfl_sync(kFull, my_s, 0);
         int cnt = NE ? 1 : 0;  // nonempty rows starting at or before c0
-        constexpr int U = 4;  // chunks per group: their bucket atomics are in flight together
+        constexpr int U = 2;  // chunks per group: their bucket atomics are in flight together
         for (int64_t g0 = lo; g0 < hi; g0 += 32 * U) {
             int kk[U], row[U], bb[U];
             double xx[U];
@@ -140,7 +140,7 @@ __global__ void __launch_bounds__(kScatterThreads) k_bucket_scatter(Csr A, int s
             for (int u = 0; u < U; ++u) {
                 const unsigned long long o = __shfl_sync(kFull, off[u], __ffs(gg[u]) - 1);
                 if (bb[u] >= 0) {
-                    const int64_t pos = cp[(int64_t)bb[u] << shift] + (int64_t)o + __popc(gg[u] & lt);
+                    const int64_t pos = (int64_t)o + __popc(gg[u] & lt);  // bcur holds absolute positions
                     Rec r;
                     r.col = kk[u];
                     r.row = (int32_t)(r0 + row[u]);
@@ -175,6 +175,13 @@ __device__ void bitonic_sort_block(int64_t len, KeyAt key, Swap swap) {
             __syncthreads();
         }
     }
+}
+
+// Bucket cursors start at the bucket's first record slot (cp of its first
+// column), so the scatter's atomics return absolute positions.
+__global__ void k_bucket_init(const int64_t *__restrict__ cp, int64_t nb, int shift, unsigned long long *bcur) {
+    for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < nb; b += (int64_t)gridDim.x * blockDim.x)
+        bcur[b] = (unsigned long long)cp[b << shift];
 }
 
 constexpr int kSortThreads = 64;  // 2 warps: one bucket per warp
@@ -352,6 +359,13 @@ int64_t transpose_buckets(int64_t nnz, int64_t ncols) {
 void launch_transpose(const Csr &A, int scale, const int64_t *cp, double *ahat, unsigned long long *bcur,
                       void *rec, unsigned *gcur, int *big, int32_t *ri, double *vt, int *err, cudaStream_t s) {
     const int shift = transpose_shift(A.nnz, A.ncols);
+    if (A.ncols > 0) {
+        const int64_t nb = (A.ncols + (1 << shift) - 1) >> shift;
+        int64_t g = (nb + 255) / 256;
+        g = g > (int64_t)num_sms() * 4 ? (int64_t)num_sms() * 4 : g;
+        k_bucket_init<<<(unsigned)g, 256, 0, s>>>(cp, nb, shift, bcur);
+        note_launch();
+    }
     if (A.nrows > 0) {
         int64_t g = (A.nrows + kScatterThreads - 1) / kScatterThreads;
         const int64_t cap = (int64_t)num_sms() * 8;

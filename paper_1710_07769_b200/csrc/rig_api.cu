@@ -146,7 +146,7 @@ static void ensure_pool() {
 
 // Pinned host staging for the counters read back at syncs (per thread).
 struct HostStage {
-    DevCounters ctr;
+    DevCounters ctr, shape;
     int64_t v[4];
     int holes;
 };
@@ -158,6 +158,12 @@ static HostStage *host_stage() {
         hs = static_cast<HostStage *>(p);
     }
     return hs;
+}
+
+static cudaEvent_t shape_event() {  // per thread, reused
+    static thread_local cudaEvent_t ev = nullptr;
+    if (!ev) CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    return ev;
 }
 
 // Bump layout over one allocation: add() records 256-byte aligned offsets.
@@ -289,6 +295,8 @@ struct rig_plan {
     int huge_slots_n = 0;
     int64_t nnz_upper = 0;  // >= graph nnz: sum (f_i - len_i)
     bool cached = false;    // simple API: internal buffers from the per-thread cache
+    bool early = false;     // all rows on the merge path, decided before the transpose ran:
+                            // no synchronisation until the end (errors are read there)
     explicit rig_plan(cudaStream_t st) : s(st), arena(st) {}
 };
 
@@ -296,7 +304,7 @@ struct rig_plan {
 // transpose, products / paths / merge-row structure (analyze), and the
 // ordered lists and temporary of the rows off the merge path.  One host
 // synchronisation (sync 1: errors, products, list sizes).
-static void plan_build(rig_plan *p, const rig_csr_t *Ain) {
+static void plan_build(rig_plan *p, const rig_csr_t *Ain, bool allow_early = false) {
     cudaStream_t s = p->s;
     const int64_t n = Ain->nrows, m = Ain->ncols, nnz = Ain->nnz, nloc = p->nloc;
     Csr A0{n, m, nnz, Ain->row_ptr, Ain->col_idx, Ain->val};
@@ -340,10 +348,18 @@ static void plan_build(rig_plan *p, const rig_csr_t *Ain) {
         const int err = hs->ctr.err;
         if (err) throw Error(err_to_code(err), err_msg(err_to_code(err)));
     }
-    // a2: column counts -> col_ptr
+    // a2: column counts -> col_ptr; shape statistics read back while the
+    // transpose and the analysis run (simple API)
+    cudaEvent_t ev_shape = nullptr;
     {
         Prof pf(P_COLPTR, s);
         if (nnz > 0) launch_col_hist(A0, cnt, nullptr, s);
+        if (allow_early && nloc > 0) {
+            launch_shape_stats(cnt, m, A0.rp, p->rb, p->re, p->ctr, s);
+            CK(cudaMemcpyAsync(&hs->shape, p->ctr, sizeof(DevCounters), cudaMemcpyDeviceToHost, s));
+            ev_shape = shape_event();
+            CK(cudaEventRecord(ev_shape, s));
+        }
         scan_u32(cnt, m, cp, ws + o_st1, 0, s);
     }
     // a1 + a2: scale rows (optional), bucketed transpose into the CSC
@@ -363,6 +379,21 @@ static void plan_build(rig_plan *p, const rig_csr_t *Ain) {
         launch_analyze_sym(sa, bin8, p->ctr, s);
     }
     check_launch("analyze");
+    if (ev_shape) {
+        CK(cudaEventSynchronize(ev_shape));
+        const DevCounters &sh = hs->shape;
+        if (sh.max_row <= kMergeMaxLen && sh.max_col * kMergeMaxLen <= kMergeMaxF) {
+            // every row of the shard is a merge row: size the output from the
+            // bound sum_k len_k^2 - nnz(shard) >= sum_i (f_i - len_i); the
+            // exact counters (and any error flag) are read at the final sync
+            p->early = true;
+            p->h = DevCounters{};
+            p->h.max_len = (int)sh.max_row;
+            p->h.products = sh.p_full;
+            p->nnz_upper = sh.p_full - sh.shard_nnz;
+            return;
+        }
+    }
     // sync 1: errors, products, path sizes
     CK(cudaMemcpyAsync(&hs->ctr, p->ctr, sizeof(DevCounters), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
@@ -494,7 +525,9 @@ static int64_t plan_numeric(rig_plan *p, int32_t *gcol, double *gw, double *diag
     HostStage *hs = host_stage();
     CK(cudaMemcpyAsync(&hs->holes, holes_d, sizeof(int), cudaMemcpyDeviceToHost, s));
     CK(cudaMemcpyAsync(&hs->v[0], row_ptr_out + p->nloc, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    if (p->early) CK(cudaMemcpyAsync(&hs->ctr.err, &p->ctr->err, sizeof(int), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
+    if (p->early && hs->ctr.err) throw Error(err_to_code(hs->ctr.err), err_msg(err_to_code(hs->ctr.err)));
     const int holes = hs->holes;
     const int64_t ub = hs->v[0];
     if (!holes) return ub;
@@ -603,7 +636,7 @@ static void build_owned(const rig_csr_t *A, int scale_rows, double drop_tol, uin
     unsigned char *block = nullptr;
     try {
         CK(cudaMallocAsync((void **)&rp, sizeof(int64_t) * (size_t)(p->nloc + 1), s));
-        plan_build(p, A);
+        plan_build(p, A, true);
         const int64_t cap = std::max<int64_t>(p->nnz_upper, 1);
         Layout L;
         const size_t o_col = L.add(sizeof(int32_t) * (size_t)cap);
