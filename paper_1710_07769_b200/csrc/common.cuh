@@ -4,6 +4,7 @@
 // of the ordering contract (DESIGN.md §3 R4) or of the compensated cutsize.
 #pragma once
 #include <cuda_runtime.h>
+#include <cstdio>
 
 #include <climits>
 #include <cstdint>

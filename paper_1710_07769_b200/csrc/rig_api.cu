@@ -125,8 +125,20 @@ static thread_local std::string t_last_error;
                         std::string(#call) + ": " + cudaGetErrorString(e_));                    \
     } while (0)
 
+// RIG_SYNC_CHECK=1 (debugging): synchronise at every check so a fault is
+// attributed to the pass that caused it.
+static bool sync_check() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("RIG_SYNC_CHECK");
+        v = (e && atoi(e)) ? 1 : 0;
+    }
+    return v == 1;
+}
+
 static void check_launch(const char *what) {
-    cudaError_t e = cudaGetLastError();
+    cudaError_t e = sync_check() ? cudaDeviceSynchronize() : cudaSuccess;
+    if (e == cudaSuccess) e = cudaGetLastError();
     if (e != cudaSuccess) throw Error(RIG_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
 }
 
@@ -404,7 +416,10 @@ static void plan_build(rig_plan *p, const rig_csr_t *Ain, bool allow_early = fal
     if (n_mid == 0) return;
     // ---- rows off the merge path: ordered lists, temporary layout
     Prof pf(P_SYMBOLIC, s);
-    const bool need_huge = p->h.max_f > kMidSmallCap;  // far lists beyond the mid kernel go to the huge path
+    // the huge path takes the huge bin and every row the mid kernel defers (far
+    // list beyond its capacity, or far keys crowding one sort bucket); with
+    // short rows only the latter can happen, so a few slots suffice
+    const bool need_huge = true;
     const size_t nbc = bins_count_elems(nloc);
     Layout LB;
     const size_t o_toff = LB.add(sizeof(int64_t) * (size_t)(nloc + 1));
@@ -418,7 +433,7 @@ static void plan_build(rig_plan *p, const rig_csr_t *Ain, bool allow_early = fal
     const size_t o_tw = LB.add(sizeof(double) * (size_t)p->h.mid_slots);
     size_t o_huge = 0;
     if (need_huge) {
-        p->huge_slots_n = huge_slots(n, n_mid);
+        p->huge_slots_n = huge_slots(n, p->h.max_f > kMidSmallCap ? n_mid : std::min<int64_t>(n_mid, 8));
         o_huge = LB.add(huge_scratch_bytes(n, p->huge_slots_n, true));
     }
     unsigned char *wb = p->cached ? ws_get(1, LB.bytes, s) : p->arena.raw(LB.bytes);
@@ -472,14 +487,17 @@ static int64_t plan_numeric(rig_plan *p, int32_t *gcol, double *gw, double *diag
             MidArgs ma{p->A,     p->T,     p->rb,  p->lists, p->ctr->list_count, p->toff, p->tcol, p->tw,
                        p->nnzc,  p->defer, p->ctr->defer_count, dg, p->tol, debug_mask()};
             launch_num_mid(ma, kMidSmallCap, s);
+            check_launch("mid rows");
             if (p->huge_scratch) {
                 MidArgs hu = ma;
                 hu.list = p->lists + n_mid;  // f_i beyond the mid bins
                 hu.count = p->ctr->list_count + 1;
                 launch_num_huge(hu, p->huge_slots_n, p->huge_scratch, s);
+                check_launch("huge rows");
                 hu.list = p->defer;  // far list beyond the mid kernel's capacity
                 hu.count = p->ctr->defer_count;
                 launch_num_huge(hu, p->huge_slots_n, p->huge_scratch, s);
+                check_launch("deferred rows");
             }
         }
         {
@@ -496,13 +514,15 @@ static int64_t plan_numeric(rig_plan *p, int32_t *gcol, double *gw, double *diag
                    dg,
                    p->tol,
                    holes_d,
-                   (cut && !(debug_mask() & 256)) ? cut->part : nullptr,
+                   cut ? cut->part : nullptr,
                    cut ? cut->K : 0,
                    cutp,
                    badp,
                    used,
                    stage_cap_for(p->h.products, p->nloc)};
+        check_launch("graph row pointers");
         if (p->nloc > 0) launch_num_merge(na, p->h.max_len, s);
+        check_launch("merge rows");
         if (n_mid > 0) {  // cut-partial segments: 0 merge rows, 1 mid rows, 2 huge rows
             auto co = [&](int g) {
                 CutOut c{nullptr, 0, nullptr, nullptr, nullptr};
