@@ -142,6 +142,8 @@ struct SymArgs {
     int64_t rb, re;
     int64_t *nnzc;  // [re-rb] merge rows: structural nnz(C_i) incl. the diagonal
     int64_t *fnm;   // [re-rb] rows off the merge path: f_i - len_i (temporary slots), else 0
+    int32_t *qs;    // [nnz] or null: per A entry of a merge row its CSC run start csc_begin(k);
+                    // -1 at the first entry of a row of <= kMergeMaxLen entries off the merge path
 };
 struct NumArgs {
     Csr A;
@@ -162,6 +164,7 @@ struct NumArgs {
     int *bad_part;
     int *cut_used;  // this launch's number of written partials (= gridDim.x)
     int stage_cap;  // merge path: staged graph entries per warp (set by the launcher)
+    const int32_t *qs;  // SymArgs::qs (null: run starts gathered from the col_ptr)
 };
 
 // Neumaier-compensated running sum (compiled with --fmad=false).

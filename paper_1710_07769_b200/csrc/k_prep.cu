@@ -89,6 +89,7 @@ __global__ void __launch_bounds__(256) k_shape_stats(const unsigned *__restrict_
         const unsigned long long len = (unsigned long long)(rp[i + 1] - rp[i]);
         mr = len > mr ? len : mr;
     }
+    __syncwarp();
     ps = warp_sum(ps);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -118,7 +119,7 @@ __global__ void __launch_bounds__(256) k_shape_stats(const unsigned *__restrict_
 
 void launch_shape_stats(const unsigned *cnt, int64_t m, const int64_t *rp, int64_t rb, int64_t re, DevCounters *ctr,
                         cudaStream_t s) {
-    k_shape_stats<<<grid_for(std::max<int64_t>(m, re - rb), 256, 2), 256, 0, s>>>(cnt, m, rp, rb, re, ctr);
+    k_shape_stats<<<grid_for(std::max<int64_t>(m, re - rb), 256, 16), 256, 0, s>>>(cnt, m, rp, rb, re, ctr);
     note_launch();
 }
 

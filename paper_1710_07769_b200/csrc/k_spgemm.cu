@@ -25,7 +25,7 @@ static int g_sms_cache = 0;
 // IdxT: int32 CSC offsets when nnz < 2^31 (fewer registers), else int64.
 // Columns end in an INT_MAX sentinel (csc_begin), so a run needs no end bound.
 template <int R, typename IdxT>
-__device__ __forceinline__ int64_t sym_merge_row(const Csr &A, const Csc &T, int64_t s) {
+__device__ __forceinline__ int64_t sym_merge_row(const Csr &A, const Csc &T, int64_t s, int32_t *qs = nullptr) {
     int32_t h[R];
     IdxT q[R];
     int64_t f = 0;
@@ -37,6 +37,10 @@ __device__ __forceinline__ int64_t sym_merge_row(const Csr &A, const Csc &T, int
         f += c1 - c0;
     }
     if (f > kMergeMaxF) return -1;
+    if (qs) {  // run starts for the numeric pass (saves it the col_ptr gathers)
+#pragma unroll
+        for (int t = 0; t < R; ++t) qs[s + t] = (int32_t)q[t];
+    }
 #pragma unroll
     for (int t = 0; t < R; ++t) h[t] = T.ri[q[t]];
     int64_t cnt = 0;
@@ -63,16 +67,25 @@ __device__ __forceinline__ void num_merge_row(const NumArgs &a, int64_t i, int64
     int32_t h[R];
     IdxT q[R];
     double av[R], hv[R];
-    int64_t f = 0;
+    if (a.qs) {  // run starts from the analysis (int32 offsets only)
 #pragma unroll
-    for (int t = 0; t < R; ++t) {
-        const int k = a.A.ci[s + t];
-        av[t] = a.A.v[s + t];
-        const int64_t c0 = a.T.cp[k], c1 = a.T.cp[k + 1];
-        q[t] = (IdxT)(c0 + k);
-        f += c1 - c0;
+        for (int t = 0; t < R; ++t) {
+            q[t] = (IdxT)a.qs[s + t];
+            av[t] = a.A.v[s + t];
+        }
+        if ((int64_t)q[0] < 0) return;  // not a merge row
+    } else {
+        int64_t f = 0;
+#pragma unroll
+        for (int t = 0; t < R; ++t) {
+            const int k = a.A.ci[s + t];
+            av[t] = a.A.v[s + t];
+            const int64_t c0 = a.T.cp[k], c1 = a.T.cp[k + 1];
+            q[t] = (IdxT)(c0 + k);
+            f += c1 - c0;
+        }
+        if (f > kMergeMaxF) return;
     }
-    if (f > kMergeMaxF) return;
 #pragma unroll
     for (int t = 0; t < R; ++t) {
         h[t] = a.T.ri[q[t]];
@@ -249,14 +262,14 @@ __global__ void __launch_bounds__(kMergeThreads) k_analyze_sym(SymArgs a, uint8_
             maxlen = max(maxlen, len);
             int64_t c = 0;
             switch (len) {
-                case 1: c = sym_merge_row<1, IdxT>(a.A, a.T, s); break;
-                case 2: c = sym_merge_row<2, IdxT>(a.A, a.T, s); break;
-                case 3: c = sym_merge_row<3, IdxT>(a.A, a.T, s); break;
-                case 4: c = sym_merge_row<4, IdxT>(a.A, a.T, s); break;
-                case 5: c = sym_merge_row<5, IdxT>(a.A, a.T, s); break;
-                case 6: c = sym_merge_row<6, IdxT>(a.A, a.T, s); break;
-                case 7: c = sym_merge_row<7, IdxT>(a.A, a.T, s); break;
-                case 8: c = sym_merge_row<8, IdxT>(a.A, a.T, s); break;
+                case 1: c = sym_merge_row<1, IdxT>(a.A, a.T, s, a.qs); break;
+                case 2: c = sym_merge_row<2, IdxT>(a.A, a.T, s, a.qs); break;
+                case 3: c = sym_merge_row<3, IdxT>(a.A, a.T, s, a.qs); break;
+                case 4: c = sym_merge_row<4, IdxT>(a.A, a.T, s, a.qs); break;
+                case 5: c = sym_merge_row<5, IdxT>(a.A, a.T, s, a.qs); break;
+                case 6: c = sym_merge_row<6, IdxT>(a.A, a.T, s, a.qs); break;
+                case 7: c = sym_merge_row<7, IdxT>(a.A, a.T, s, a.qs); break;
+                case 8: c = sym_merge_row<8, IdxT>(a.A, a.T, s, a.qs); break;
                 default: break;
             }
             a.nnzc[r] = c;
@@ -268,6 +281,7 @@ __global__ void __launch_bounds__(kMergeThreads) k_analyze_sym(SymArgs a, uint8_
             if (lg < kSymBinMinLog) lg = kSymBinMinLog;
             const int b = lg > kSymBinMaxLog ? kNumSymBins : lg - kSymBinMinLog;
             bin8[r] = (uint8_t)b;
+            if (a.qs && e - s <= kMergeMaxLen) a.qs[s] = -1;  // the merge kernel skips it
             a.fnm[r] = fi - (e - s);  // >= its off-diagonal entries: temporary slots
             slots += fi - (e - s);
             maxf = max(maxf, fi);

@@ -297,6 +297,7 @@ struct rig_plan {
     DevCounters *ctr = nullptr;  // device
     DevCounters h{};             // host copy (after sync 1)
     int64_t *nnzc = nullptr;     // [nloc] merge rows: structural nnz(C_i); others: kept + 1 (numeric)
+    int32_t *qs = nullptr;       // merge rows' CSC run starts (SymArgs::qs)
     // rows off the merge path (h.n_mid > 0): exact rows in the temporary
     int32_t *lists = nullptr;    // [2 * n_mid]: mid rows, huge rows (ascending)
     int32_t *defer = nullptr;    // [2 * n_mid]: deferred by the small / big mid kernel
@@ -337,6 +338,8 @@ static void plan_build(rig_plan *p, const rig_csr_t *Ain, bool allow_early = fal
     const size_t o_nnzc = L.add(sizeof(int64_t) * (size_t)nloc);
     const size_t o_fnm = L.add(sizeof(int64_t) * (size_t)nloc);
     const size_t o_bin8 = L.add((size_t)nloc);
+    const bool use_qs = nnz + m <= (int64_t)INT32_MAX;  // run starts fit int32
+    const size_t o_qs = use_qs ? L.add(sizeof(int32_t) * (size_t)nnz) : 0;
     unsigned char *ws = p->cached ? ws_get(0, L.bytes, s) : p->arena.raw(L.bytes);
     CK(cudaMemsetAsync(ws, 0, zero_bytes, s));
     p->ctr = reinterpret_cast<DevCounters *>(ws + o_ctr);
@@ -385,7 +388,8 @@ static void plan_build(rig_plan *p, const rig_csr_t *Ain, bool allow_early = fal
     p->A = Csr{n, m, nnz, Ain->row_ptr, Ain->col_idx, p->scale ? ahat : Ain->val};
     p->T = Csc{cp, ri, vt};
     // a3 + a4 (merge rows): products, merge-row nnzC, paths of the others
-    SymArgs sa{p->A, p->T, p->rb, p->re, p->nnzc, fnm};
+    p->qs = use_qs ? reinterpret_cast<int32_t *>(ws + o_qs) : nullptr;
+    SymArgs sa{p->A, p->T, p->rb, p->re, p->nnzc, fnm, p->qs};
     if (nloc > 0) {
         Prof pf(P_ANALYZE, s);
         launch_analyze_sym(sa, bin8, p->ctr, s);
@@ -519,7 +523,8 @@ static int64_t plan_numeric(rig_plan *p, int32_t *gcol, double *gw, double *diag
                    cutp,
                    badp,
                    used,
-                   stage_cap_for(p->h.products, p->nloc)};
+                   stage_cap_for(p->h.products, p->nloc),
+                   p->qs};
         check_launch("graph row pointers");
         if (p->nloc > 0) launch_num_merge(na, p->h.max_len, s);
         check_launch("merge rows");
