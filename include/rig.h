@@ -99,11 +99,16 @@ typedef struct rig_plan rig_plan_t;
  *   flags      RIG_FLAG_VALIDATE | RIG_FLAG_DIAG.
  *   out        filled with device arrays allocated by the library (stream-
  *              ordered on `stream`); release them with rig_graph_free.
- * Synchronises `stream` to size allocations. */
+ *              col_idx / w are allocated with the capacity bound
+ *              sum_i (f_i - len_i) (f_i: products of row i) >= out->nnz.
+ * Synchronises `stream` to size allocations and to read the graph nnz: twice
+ * in general, once when every row takes the merge path (the decision and the
+ * bound come from the column histogram while the transpose runs, DESIGN.md
+ * §4.5); device-side errors are reported at that synchronisation. */
 RIG_API int rig_build(const rig_csr_t *A, int scale_rows, double drop_tol, uint32_t flags, rig_graph_t *out,
               rig_stream_t stream);
 
-/* Release the arrays of a graph returned by rig_build / rig_build_sharded;
+/* Release the arrays of a graph returned by rig_build / rig_build_rows / rig_build_cut;
  * zeroes *g.  NULL arrays are ignored. */
 RIG_API int rig_graph_free(rig_graph_t *g, rig_stream_t stream);
 
@@ -125,19 +130,23 @@ RIG_API int rig_build_cut(const rig_csr_t *A, int scale_rows, double drop_tol, u
 /* ---- staged API: caller-owned output (estimate -> allocate -> compute) --- */
 
 /* Runs steps a0-a4 for rows [row_begin, row_end): validation, scaling,
- * transpose, flop count and the symbolic pass.  Synchronises once. */
+ * transpose, flop count, the merge rows' symbolic pass and the lists of the
+ * other rows.  Synchronises once. */
 RIG_API int rig_plan_create(const rig_csr_t *A, int scale_rows, double drop_tol, uint32_t flags, int64_t row_begin,
                     int64_t row_end, rig_plan_t **plan, rig_stream_t stream);
 
-/* nnz_upper: graph capacity needed (structural off-diagonal nnz of the
- * shard); products: Gustavson intermediate products of the shard;
- * workspace_bytes: device bytes rig_plan_execute needs in `workspace`. */
+/* nnz_upper: graph capacity needed, the bound sum_i (f_i - len_i) >= the
+ * shard's off-diagonal nnz (every row i of A meets itself in each of its
+ * len_i columns); products: Gustavson intermediate products of the shard
+ * (sum f_i); workspace_bytes: device bytes rig_plan_execute needs in
+ * `workspace` (0: internal temporaries are stream-ordered allocations). */
 RIG_API int rig_plan_query(const rig_plan_t *plan, int64_t *nnz_upper, int64_t *products, size_t *workspace_bytes);
 
 /* Steps a5-a6 into caller arrays: out->row_ptr [n+1], out->col_idx and
  * out->w with capacity >= nnz_upper, out->diag [n] or NULL.  `workspace`
  * must hold workspace_bytes (may be NULL if that is 0).  Sets out->n and
- * out->nnz.  Synchronises once (to read the kept count). */
+ * out->nnz.  Synchronises once (to read the nnz; again only if a merge row
+ * dropped an entry by value and the graph is compacted). */
 RIG_API int rig_plan_execute(rig_plan_t *plan, void *workspace, rig_graph_t *out, rig_stream_t stream);
 
 RIG_API int rig_plan_destroy(rig_plan_t *plan);
@@ -160,6 +169,32 @@ RIG_API int rig_row_split(const rig_csr_t *A, int32_t parts, int64_t *split, rig
  * asynchronous (no host sync).  Multi-GPU: allreduce cut_dev outside. */
 RIG_API int rig_cutsize(const rig_graph_t *g, int64_t row_begin, int64_t n_global, const int32_t *part, int32_t K,
                 double *cut_dev, rig_stream_t stream);
+
+/* ---- partition quality ------------------------------ */
+
+/* Inter-block inner-product matrix of a K-way block-row partition
+ * (eq. ip_km): ip_km = sum of |c_ij| = w_ij over stored
+ * edges with part[i] = k != m = part[j] (symmetric; sum_{k<m} ip_km =
+ * cutsize), and part weights (eq16, 1141-1146 eq. Wk):
+ * W_k = sum of w(v_i) over rows i of part k, w(v_i) = nnz(r_i) when
+ * a_row_ptr (device, A's row pointers) is given, else 1.
+ *   acc  device int64 [4*K*K + 1], ZEROED by the caller: every weight is added
+ *        exactly as four 32-bit limbs of trunc(w * 2^64) in separate 64-bit
+ *        counters (integer sums: order-independent and deterministic); the
+ *        last element is an error flag (part id outside [0, K), or a weight
+ *        outside [0, 2^63)).
+ *   W    device int64 [K], ZEROED by the caller.
+ * Rows of g are [row_begin, row_begin + g->n) of the global graph.
+ * Accumulates, asynchronously.  Multi-GPU: allreduce acc and W (int64 sums)
+ * before rig_partition_ip_finalize. */
+RIG_API int rig_partition_ip(const rig_graph_t *g, int64_t row_begin, int64_t n_global, const int32_t *part,
+                             int32_t K, const int64_t *a_row_ptr, int64_t *acc, int64_t *W, rig_stream_t stream);
+
+/* HOST function: ip_host[K*K] (row-major, zero diagonal) from a host copy of
+ * acc: each cell's fixed-point sum converted to double (one correctly
+ * rounded conversion while the sum fits 2^63).  RIG_ERR_INVALID if the error
+ * flag is set. */
+RIG_API int rig_partition_ip_finalize(const int64_t *acc_host, int32_t K, double *ip_host);
 
 /* ---- end-to-end from host memory --------------------------------------- */
 

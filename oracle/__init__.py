@@ -7,7 +7,8 @@ product package ``paper_1710_07769_b200`` never imports it.
 Thin ctypes marshalling over ``rig_oracle.c`` (every arithmetic step lives in
 that file, with its PAPER.md citation).  Pins: ``tests/test_oracle_pins.py``.
 Parity pinned for: scaling, transpose, products, build (structure, values,
-diag, nnz(C)), cutsize.  Unpinned: nothing the build path uses; the paper's
+diag, nnz(C)), cutsize, inter-block inner-product matrix and part weights
+(SURVEY.md §8(f) f2).  Unpinned: nothing the build path uses; the paper's
 12x12 sample is in a missing figure and is not
 reproduced.
 """
@@ -50,6 +51,7 @@ def lib():
                                    p, p, p, p, p, p]
         _lib.orc_free.argtypes = [p]
         _lib.orc_cutsize.argtypes = [i64, i64, p, p, p, i64, p, i32, p, p, p]
+        _lib.orc_ip_matrix.argtypes = [i64, i64, p, p, p, i64, p, i32, p, p, p]
     return _lib
 
 
@@ -175,3 +177,19 @@ def cutsize(g_row_ptr, g_col, g_w, part, K, row_begin=0):
     if st:
         raise OracleError(st, "cutsize")
     return out[0], out[1], out[2]
+
+
+def ip_matrix(g_row_ptr, g_col, g_w, part, K, row_begin=0, a_row_ptr=None):
+    """Inter-block inner-product matrix ip[K, K] and part
+    weights W[K]: unit weights, or nnz(r_i)
+    when A's row pointers are given.  Returns (ip, W)."""
+    g_row_ptr, g_col, g_w = _c(g_row_ptr, np.int64), _c(g_col, np.int32), _c(g_w, np.float64)
+    part = _c(part, np.int32)
+    ip = np.zeros((K, K), dtype=np.float64)
+    W = np.zeros(K, dtype=np.int64)
+    arp = _c(a_row_ptr, np.int64) if a_row_ptr is not None else None
+    st = lib().orc_ip_matrix(g_row_ptr.size - 1, row_begin, _p(g_row_ptr), _p(g_col), _p(g_w), part.size,
+                             _p(part), int(K), _p(arp) if arp is not None else None, _p(ip), _p(W))
+    if st:
+        raise OracleError(st, "ip_matrix")
+    return ip, W

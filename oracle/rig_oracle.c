@@ -239,3 +239,39 @@ int orc_cutsize(int64_t nloc, int64_t row_begin, const int64_t *g_row_ptr,
     if (intra) *intra = si + ci;
     return ORC_OK;
 }
+
+/* ---------------------------------------------------------------- f2
+ * Inter-block inner-product matrix of a K-way block-row partition
+ * (eq. ip_km):
+ *   ip_km = sum over r_i in R_k, r_j in R_m of |r_i r_j^T| = sum |c_ij|, k != m,
+ * i.e. the sum of the stored graph weights w_ij of edges with part[i] = k and
+ * part[j] = m (both orientations are stored, so ip is symmetric), and the
+ * part weights (eq16 and 1141-1146 eq. Wk):
+ *   W_k = sum over v_i in V_k of w(v_i), w(v_i) = 1 or nnz(r_i).
+ * ip[K*K] (row-major, diagonal 0) is summed per cell with Neumaier
+ * compensation over the rows in ascending order; W[K] counts exactly.
+ * a_row_ptr: A's row pointers for nnz weights, or NULL for unit weights.
+ * Rows are [row_begin, row_begin + nloc) of the global graph. */
+int orc_ip_matrix(int64_t nloc, int64_t row_begin, const int64_t *g_row_ptr, const int32_t *g_col,
+                  const double *g_w, int64_t n_global, const int32_t *part, int32_t K,
+                  const int64_t *a_row_ptr, double *ip, int64_t *W) {
+    for (int64_t v = 0; v < n_global; ++v)
+        if (part[v] < 0 || part[v] >= K) return ORC_ERR_INVALID;
+    double *comp = (double *)calloc((size_t)K * (size_t)K, sizeof(double));
+    if (!comp) return ORC_ERR_NOMEM;
+    memset(ip, 0, sizeof(double) * (size_t)K * (size_t)K);
+    memset(W, 0, sizeof(int64_t) * (size_t)K);
+    for (int64_t r = 0; r < nloc; ++r) {
+        const int64_t i = row_begin + r;
+        const int32_t k = part[i];
+        W[k] += a_row_ptr ? a_row_ptr[i + 1] - a_row_ptr[i] : 1;
+        for (int64_t e = g_row_ptr[r]; e < g_row_ptr[r + 1]; ++e) {
+            const int32_t m = part[g_col[e]];
+            if (m == k) continue;
+            neumaier(&ip[(int64_t)k * K + m], &comp[(int64_t)k * K + m], g_w[e]);
+        }
+    }
+    for (int64_t c = 0; c < (int64_t)K * K; ++c) ip[c] += comp[c];
+    free(comp);
+    return ORC_OK;
+}

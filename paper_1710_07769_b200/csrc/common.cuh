@@ -276,5 +276,11 @@ int cutsize_blocks();
 void launch_cut_final(const double *partials, const int *used, int nseg, int stride, const int *bad, double *cut,
                       cudaStream_t s);
 void launch_split(const int64_t *fprefix, int64_t n, int32_t parts, int64_t *split, cudaStream_t s);
+// f2: fixed-point limbs of the inter-block inner products (acc [4*K*K]) and
+// part weights (wsum [K]), both accumulated (caller-zeroed); *bad set on an
+// out-of-range part id or a weight outside [0, 2^63)
+void launch_partition_ip(const int64_t *grp, const int32_t *gcol, const double *gw, int64_t nloc, int64_t rb,
+                         int64_t n_global, const int32_t *part, int32_t K, const int64_t *arp, unsigned long long *acc,
+                         unsigned long long *wsum, int *bad, cudaStream_t s);
 
 }  // namespace rig

@@ -1,6 +1,8 @@
 // k_post.cu -- a6 compaction (only when the numeric pass dropped entries),
 // a7 cutsize (§2.2; eq. partcut) and the
 // flop-balanced row split for multi-GPU sharding.
+#include <algorithm>
+
 #include "common.cuh"
 
 namespace rig {
@@ -186,6 +188,90 @@ void launch_cutsize(const int64_t *grp, const int32_t *gcol, const double *gw, i
     k_cutsize<<<nblocks, kCutThreads, 0, s>>>(grp, gcol, gw, nloc, rb, n_global, part, K, partials, bad);
     k_cutsize_final<<<1, kCutThreads, 0, s>>>(partials, nblocks, bad, cut);
     note_launch(2);
+}
+
+// ------------------------------------------------------------------ f2: IP matrix, part weights
+// ip_km = sum of the stored weights w_ij with part[i] = k != m = part[j]
+// (eq. ip_km), W_k = sum of w(v_i) over part k, w = 1 or
+// nnz(r_i) (eq16, 1141-1146 eq. Wk).  Every weight is added
+// as the fixed-point value trunc(w * 2^64) split into four 32-bit limbs, each
+// summed in its own 64-bit counter: integer sums, so the result is exact and
+// independent of the summation order (deterministic under any schedule and
+// across GPUs: ranks allreduce the counters as integers).  For K <= 32 a CTA
+// accumulates in shared memory first.
+constexpr int kIpThreads = 256;
+constexpr int kIpSmemK = 32;
+
+__device__ __forceinline__ bool add_fixed(unsigned long long *acc4, double w) {
+    if (!(w >= 0.0) || w >= 9.2233720368547758e18) return false;  // 2^63: outside the fixed-point range
+    const unsigned long long hi = (unsigned long long)w;            // floor (w >= 0)
+    const unsigned long long lo = __double2ull_rz((w - (double)hi) * 18446744073709551616.0);  // frac * 2^64
+    const unsigned long long l[4] = {lo & 0xffffffffull, lo >> 32, hi & 0xffffffffull, hi >> 32};
+#pragma unroll
+    for (int t = 0; t < 4; ++t)
+        if (l[t]) atomicAdd(&acc4[t], l[t]);
+    return true;
+}
+
+__global__ void __launch_bounds__(kIpThreads) k_partition_ip(const int64_t *__restrict__ grp,
+                                                             const int32_t *__restrict__ gcol,
+                                                             const double *__restrict__ gw, int64_t nloc, int64_t rb,
+                                                             int64_t n_global, const int32_t *__restrict__ part,
+                                                             int32_t K, const int64_t *__restrict__ arp,
+                                                             unsigned long long *acc, unsigned long long *wsum,
+                                                             int *bad) {
+    __shared__ unsigned long long s_acc[4 * kIpSmemK * kIpSmemK];
+    __shared__ unsigned long long s_w[kIpSmemK];
+    const bool priv = K <= kIpSmemK;
+    if (priv) {
+        for (int t = threadIdx.x; t < 4 * K * K; t += kIpThreads) s_acc[t] = 0ull;
+        for (int t = threadIdx.x; t < K; t += kIpThreads) s_w[t] = 0ull;
+        __syncthreads();
+    }
+    const int l = lane_id();
+    int badp = 0;
+    for (int64_t v = (int64_t)blockIdx.x * kIpThreads + threadIdx.x; v < n_global; v += (int64_t)gridDim.x * kIpThreads) {
+        const int32_t p = part[v];
+        badp |= (p < 0) | (p >= K);
+    }
+    if (__syncthreads_or(badp)) {  // ids are checked before any use as an index
+        if (threadIdx.x == 0) atomicOr(bad, 1);
+        return;
+    }
+    const int64_t nwarps = ((int64_t)gridDim.x * kIpThreads) >> 5;
+    for (int64_t r = ((int64_t)blockIdx.x * kIpThreads + threadIdx.x) >> 5; r < nloc; r += nwarps) {
+        const int64_t i = rb + r;
+        const int32_t k = part[i];
+        if (l == 0) {
+            const unsigned long long wv = arp ? (unsigned long long)(arp[i + 1] - arp[i]) : 1ull;
+            atomicAdd(priv ? &s_w[k] : &wsum[k], wv);
+        }
+        for (int64_t e = grp[r] + l; e < grp[r + 1]; e += 32) {
+            const int32_t m = part[gcol[e]];
+            if (m == k) continue;
+            const int64_t cell = (int64_t)k * K + m;
+            if (!add_fixed(priv ? &s_acc[4 * cell] : &acc[4 * cell], gw[e])) badp = 1;
+        }
+    }
+    if (priv) {
+        __syncthreads();
+        for (int t = threadIdx.x; t < 4 * K * K; t += kIpThreads)
+            if (s_acc[t]) atomicAdd(&acc[t], s_acc[t]);
+        for (int t = threadIdx.x; t < K; t += kIpThreads)
+            if (s_w[t]) atomicAdd(&wsum[t], s_w[t]);
+    }
+    if (__syncthreads_or(badp) && threadIdx.x == 0) atomicOr(bad, 1);
+}
+
+void launch_partition_ip(const int64_t *grp, const int32_t *gcol, const double *gw, int64_t nloc, int64_t rb,
+                         int64_t n_global, const int32_t *part, int32_t K, const int64_t *arp, unsigned long long *acc,
+                         unsigned long long *wsum, int *bad, cudaStream_t s) {
+    int64_t g = (std::max<int64_t>(nloc, 1) * 32 + kIpThreads - 1) / kIpThreads;
+    const int64_t cap = (int64_t)num_sms() * 8;
+    g = g < 1 ? 1 : (g > cap ? cap : g);
+    k_partition_ip<<<(unsigned)g, kIpThreads, 0, s>>>(grp, gcol, gw, nloc, rb, n_global, part, K, arp, acc, wsum,
+                                                      bad);
+    note_launch();
 }
 
 // ------------------------------------------------------------------ row split

@@ -59,11 +59,11 @@ enum Pass {
     P_COMPACT,   // a6 holes path
     P_CUTSIZE,   // a7 (standalone kernel or fused final reduction)
     P_SPLIT,
-    P_OTHER,
+    P_KERNEL,  // the dominant numeric kernel alone (merge kernel, or the mid-row kernel)
 };
 static const char *kPassNames[RIG_NPASS] = {"validate", "colptr",   "scale_scatter", "colsort",
                                             "analyze",  "symbolic", "ub_scan",       "numeric",
-                                            "compact",  "cutsize",  "split",         "other"};
+                                            "compact",  "cutsize",  "split",         "numeric_kernel"};
 static std::mutex g_prof_mu;
 static std::atomic<uint32_t> g_prof_mask{0};
 struct ProfRec {
@@ -96,7 +96,7 @@ struct Prof {
     cudaStream_t s;
     cudaEvent_t a = nullptr;
     Prof(int p, cudaStream_t st) : pass(p), s(st) {
-        if (g_prof_mask.load(std::memory_order_relaxed) & (1u << p)) {
+        if (p >= 0 && (g_prof_mask.load(std::memory_order_relaxed) & (1u << p))) {
             a = ev_get();
             cudaEventRecord(a, s);
         }
@@ -490,7 +490,10 @@ static int64_t plan_numeric(rig_plan *p, int32_t *gcol, double *gw, double *diag
         if (n_mid > 0) {
             MidArgs ma{p->A,     p->T,     p->rb,  p->lists, p->ctr->list_count, p->toff, p->tcol, p->tw,
                        p->nnzc,  p->defer, p->ctr->defer_count, dg, p->tol, debug_mask()};
-            launch_num_mid(ma, kMidSmallCap, s);
+            {
+                Prof pk(P_KERNEL, s);
+                launch_num_mid(ma, kMidSmallCap, s);
+            }
             check_launch("mid rows");
             if (p->huge_scratch) {
                 MidArgs hu = ma;
@@ -526,7 +529,10 @@ static int64_t plan_numeric(rig_plan *p, int32_t *gcol, double *gw, double *diag
                    stage_cap_for(p->h.products, p->nloc),
                    p->qs};
         check_launch("graph row pointers");
-        if (p->nloc > 0) launch_num_merge(na, p->h.max_len, s);
+        if (p->nloc > 0) {
+            Prof pk(n_mid > 0 ? -1 : P_KERNEL, s);
+            launch_num_merge(na, p->h.max_len, s);
+        }
         check_launch("merge rows");
         if (n_mid > 0) {  // cut-partial segments: 0 merge rows, 1 mid rows, 2 huge rows
             auto co = [&](int g) {
@@ -881,6 +887,46 @@ int rig_cutsize(const rig_graph_t *g, int64_t row_begin, int64_t n_global, const
     Prof pf(P_CUTSIZE, s);
     launch_cutsize(g->row_ptr, g->col_idx, g->w, g->n, row_begin, n_global, part, K, partials, nb, cut_dev, s);
     check_launch("cutsize");
+    return RIG_OK;
+    ABI_END
+}
+
+int rig_partition_ip(const rig_graph_t *g, int64_t row_begin, int64_t n_global, const int32_t *part, int32_t K,
+                     const int64_t *a_row_ptr, int64_t *acc, int64_t *W, rig_stream_t stream) {
+    ABI_BEGIN
+    if (!g || !part || !acc || !W) throw Error(RIG_ERR_INVALID, "NULL argument");
+    if (K < 1 || K > 65536 || n_global < 0 || row_begin < 0 || row_begin + g->n > n_global)
+        throw Error(RIG_ERR_INVALID, "bad K / row range");
+    if (!g->row_ptr || (g->nnz > 0 && (!g->col_idx || !g->w))) throw Error(RIG_ERR_INVALID, "graph arrays NULL");
+    cudaStream_t s = (cudaStream_t)stream;
+    Prof pf(P_CUTSIZE, s);
+    unsigned long long *a = reinterpret_cast<unsigned long long *>(acc);
+    launch_partition_ip(g->row_ptr, g->col_idx, g->w, g->n, row_begin, n_global, part, K, a_row_ptr, a,
+                        reinterpret_cast<unsigned long long *>(W), reinterpret_cast<int *>(a + 4 * (int64_t)K * K), s);
+    check_launch("partition_ip");
+    return RIG_OK;
+    ABI_END
+}
+
+int rig_partition_ip_finalize(const int64_t *acc_host, int32_t K, double *ip_host) {
+    ABI_BEGIN
+    if (!acc_host || !ip_host || K < 1) throw Error(RIG_ERR_INVALID, "NULL argument or K < 1");
+    const int64_t cells = (int64_t)K * K;
+    if (acc_host[4 * cells]) throw Error(RIG_ERR_INVALID, "part id outside [0, K) or weight outside [0, 2^63)");
+    for (int64_t c = 0; c < cells; ++c) {
+        const uint64_t *l = reinterpret_cast<const uint64_t *>(acc_host + 4 * c);
+        // value * 2^64 = l3 2^96 + l2 2^64 + l1 2^32 + l0 (each limb sum < 2^63)
+        const unsigned __int128 lo = ((unsigned __int128)l[1] << 32) + l[0];
+        const unsigned __int128 hi = ((unsigned __int128)l[3] << 32) + l[2];  // integer part - carry
+        const unsigned __int128 ip = hi + (lo >> 64);
+        const uint64_t fr = (uint64_t)lo;
+        if ((ip >> 63) == 0) {  // fits 127 bits: one correctly rounded conversion
+            const unsigned __int128 v = (ip << 64) | fr;
+            ip_host[c] = std::ldexp((double)v, -64);
+        } else {
+            ip_host[c] = (double)ip + std::ldexp((double)fr, -64);
+        }
+    }
     return RIG_OK;
     ABI_END
 }

@@ -59,6 +59,8 @@ def _load():
     L.rig_row_split.argtypes = [P, I32, P, P]
     L.rig_cutsize.argtypes = [P, I64, I64, P, I32, P, P]
     L.rig_build_host.argtypes = [P, ctypes.c_int, D, U32, P, I32, P, I64, P, P]
+    L.rig_partition_ip.argtypes = [P, I64, I64, P, I32, P, P, P, P]
+    L.rig_partition_ip_finalize.argtypes = [P, I32, P]
     L.rig_last_error.restype = ctypes.c_char_p
     L.rig_launch_count.restype = ctypes.c_uint64
     L.rig_version.restype = ctypes.c_char_p
@@ -273,6 +275,42 @@ def rig_cutsize(g, part: torch.Tensor, K: int, n_global=None, out=None, stream=N
     _check(lib.rig_cutsize(ctypes.byref(gc), int(g.row_begin), n_global, ctypes.c_void_p(part.data_ptr()), int(K),
                            ctypes.c_void_p(out.data_ptr()), _stream(stream)))
     return out
+
+
+def rig_partition_ip_accumulate(g, part: torch.Tensor, K: int, a_row_ptr=None, acc=None, W=None, n_global=None,
+                                stream=None):
+    """Accumulate the fixed-point inter-block inner products and part weights
+    of graph (shard) g into device int64 tensors acc [4K^2+1] and W [K]
+    (zeroed here when not given).  Asynchronous.  Multi-GPU: all_reduce(SUM)
+    both, then rig_partition_ip_finalize."""
+    part = part if part.dtype == torch.int32 else part.to(torch.int32)
+    n_global = part.numel() if n_global is None else int(n_global)
+    dev = part.device
+    if acc is None:
+        acc = torch.zeros(4 * K * K + 1, dtype=torch.int64, device=dev)
+    if W is None:
+        W = torch.zeros(K, dtype=torch.int64, device=dev)
+    gc = g.c()
+    arp = ctypes.c_void_p(a_row_ptr.data_ptr()) if a_row_ptr is not None else None
+    _check(lib.rig_partition_ip(ctypes.byref(gc), int(g.row_begin), n_global, ctypes.c_void_p(part.data_ptr()), int(K),
+                                arp, ctypes.c_void_p(acc.data_ptr()), ctypes.c_void_p(W.data_ptr()), _stream(stream)))
+    return acc, W
+
+
+def rig_partition_ip_finalize(acc, K: int):
+    """Host conversion of the accumulated limbs: returns a float64 [K, K]
+    CPU tensor (ip_km)."""
+    a = acc.detach().to("cpu", torch.int64).contiguous()
+    ip = torch.empty((K, K), dtype=torch.float64)
+    _check(lib.rig_partition_ip_finalize(ctypes.c_void_p(a.data_ptr()), int(K), ctypes.c_void_p(ip.data_ptr())))
+    return ip
+
+
+def rig_partition_ip(g, part: torch.Tensor, K: int, a_row_ptr=None, stream=None):
+    """ip [K, K] (CPU float64) and part weights W [K] (CPU int64) of graph g
+    under `part`.  Synchronises (reads the result)."""
+    acc, W = rig_partition_ip_accumulate(g, part, K, a_row_ptr, stream=stream)
+    return rig_partition_ip_finalize(acc, K), W.cpu()
 
 
 def rig_build_host(row_ptr, col_idx, val, ncols, scale_rows, drop_tol, flags, part, K, out_row_ptr, out_col,

@@ -24,7 +24,7 @@ def test_header_symbols_exported(rig):
     expected = {"rig_build", "rig_build_rows", "rig_build_cut", "rig_graph_free", "rig_plan_create", "rig_plan_query",
                 "rig_plan_execute", "rig_plan_destroy", "rig_row_split", "rig_cutsize", "rig_build_host",
                 "rig_last_error", "rig_launch_count", "rig_version", "rig_profile_enable", "rig_profile_read", "rig_trim",
-                "rig_pass_name"}
+                "rig_pass_name", "rig_partition_ip", "rig_partition_ip_finalize"}
     assert set(names) == expected
     so = ctypes.CDLL(rig.LIB_PATH)
     for n in names:
@@ -63,3 +63,28 @@ def test_null_arguments_rejected_on_host(rig):
     assert L.rig_build(ctypes.byref(A), 1, float("nan"), 0, ctypes.byref(rig.rig_graph_t()), None) == rig.RIG_ERR_INVALID
     assert L.rig_row_split(ctypes.byref(A), 0, None, None) == rig.RIG_ERR_INVALID
     assert rig.lib.rig_version().startswith(b"librig")
+
+
+def test_partition_ip_finalize_host(rig):
+    """The host conversion of the f2 fixed-point limbs (no GPU needed): each
+    cell holds four 64-bit sums of 32-bit limbs of trunc(w * 2^64)."""
+    import torch
+
+    def limbs(w):
+        hi = int(w)
+        lo = int((w - hi) * 2**64)
+        return [lo & 0xFFFFFFFF, lo >> 32, hi & 0xFFFFFFFF, hi >> 32]
+
+    K = 2
+    vals = {1: [1.5, 0.25, 3.0], 2: [2.0**-40, 7.0]}  # cells (0,1) and (1,0)
+    acc = [0] * (4 * K * K + 1)
+    for cell, ws in vals.items():
+        for w in ws:
+            for t, x in enumerate(limbs(w)):
+                acc[4 * cell + t] += x
+    ip = rig.rig_partition_ip_finalize(torch.tensor(acc, dtype=torch.int64), K)
+    assert ip[0, 0] == 0 and ip[1, 1] == 0
+    assert ip[0, 1] == 4.75 and ip[1, 0] == 7.0 + 2.0**-40
+    acc[-1] = 1  # error flag: bad part id / weight
+    with pytest.raises(rig.RigError):
+        rig.rig_partition_ip_finalize(torch.tensor(acc, dtype=torch.int64), K)

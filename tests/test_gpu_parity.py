@@ -298,3 +298,41 @@ def test_full_configs_sampled(rig, cfg):
         assert abs(c - oc) <= REL * max(oc, 1e-300)
     # symmetry spot check via total: sum over j>i equals sum over j<i bitwise-symmetric weights
     assert rig.rig_cutsize(g, torch.zeros(w.n, dtype=torch.int32, device="cuda"), 1).item() == 0.0
+
+
+@pytest.mark.parametrize("cfg", [1, 2, 3, 4, 5])
+def test_partition_ip_matrix(rig, cfg):
+    """f2: inter-block inner-product matrix and part weights vs the oracle
+    (303-309, 1141-1146).  Fixed-point sums: each term is
+    truncated at 2^-64 and the total rounded once, so |gpu - oracle| <=
+    count * 2^-64 + 4 ulp; the matrix is bitwise symmetric (C is)."""
+    w = make_small(cfg)
+    orc = oracle.build(w.row_ptr, w.col_idx, w.val, scale_rows=w.scale_rows, drop_tol=w.drop_tol)
+    K = w.K
+    A = rig.CSR(w.row_ptr, w.col_idx, w.val)
+    g = rig.rig_build(A, w.scale_rows, w.drop_tol)
+    part = torch.as_tensor(w.part, device="cuda")
+    for arp in (None, A.row_ptr):
+        ip, W = rig.rig_partition_ip(g, part, K, a_row_ptr=arp)
+        oip, oW = oracle.ip_matrix(orc.row_ptr, orc.col, orc.w, w.part, K,
+                                   a_row_ptr=None if arp is None else w.row_ptr)
+        ip = ip.numpy()
+        np.testing.assert_array_equal(W.numpy(), oW)
+        tol = orc.nnz * 2.0 ** -64 + 8 * 2.0 ** -53 * np.abs(oip)
+        assert (np.abs(ip - oip) <= tol).all()
+        assert ip.tobytes() == ip.T.copy().tobytes()
+        assert np.diag(ip).tolist() == [0.0] * K
+    cut = rig.rig_cutsize(g, part, K).item()
+    assert abs(np.triu(ip, 1).sum() - cut) <= 1e-12 * cut
+    # multi-GPU form: shards accumulate into the same counters (an allreduce)
+    split = rig.rig_row_split(A, 3)
+    acc = torch.zeros(4 * K * K + 1, dtype=torch.int64, device="cuda")
+    Wt = torch.zeros(K, dtype=torch.int64, device="cuda")
+    for a, b in zip(split[:-1], split[1:]):
+        s = rig.rig_build_rows(A, a, b, w.scale_rows, w.drop_tol)
+        rig.rig_partition_ip_accumulate(s, part, K, acc=acc, W=Wt)
+    assert rig.rig_partition_ip_finalize(acc, K).numpy().tobytes() == ip.tobytes()
+    # bad part id -> error at finalize
+    acc2, _ = rig.rig_partition_ip_accumulate(g, torch.full_like(part, K), K)
+    with pytest.raises(rig.RigError):
+        rig.rig_partition_ip_finalize(acc2, K)

@@ -370,3 +370,56 @@ def test_uniform_partition_sizes_golden():
         n, K = int(l[0]), int(l[1])
         sizes = np.bincount(part_contiguous(n, K), minlength=K).tolist()
         assert sizes == [int(x) for x in l[2:]]
+
+
+def test_ip_matrix_pins():
+    """f2: the oracle's inter-block inner-product matrix
+    (eq. ip_km) against exact per-cell sums of the graph,
+    brute-force dense row inner products, sum_{k<m} ip_km = cutsize
+    (PAPER.md:519-529), symmetry, and the part weights (eq16,
+    1141-1146 eq. Wk)."""
+    w = make(1)
+    g = oracle.build(w.row_ptr, w.col_idx, w.val, scale_rows=1, drop_tol=0.0, keep_intermediates=True)
+    n, K = w.n, w.K
+    ip, W = oracle.ip_matrix(g.row_ptr, g.col, g.w, w.part, K)
+    rows = np.repeat(np.arange(n), np.diff(g.row_ptr))
+    pk, pm = w.part[rows], w.part[g.col]
+    for k in range(K):
+        assert ip[k, k] == 0.0
+        for m in range(K):
+            if m != k:
+                exact = math.fsum(g.w[(pk == k) & (pm == m)])
+                assert abs(ip[k, m] - exact) <= 2 * U * exact
+    assert np.allclose(ip, ip.T, rtol=4 * U, atol=0)
+    cut = oracle.cutsize(g.row_ptr, g.col, g.w, w.part, K)[0]
+    assert abs(np.triu(ip, 1).sum() - cut) <= 1e-13 * cut
+    # brute force from dense A_hat A_hat^T (independent of the graph build)
+    Ah = sp.csr_matrix((g.a_hat, w.col_idx, w.row_ptr), shape=(n, n)).toarray()
+    C = np.abs(Ah @ Ah.T)
+    for k in range(K):
+        for m in range(K):
+            if m != k:
+                ref = C[np.ix_(w.part == k, w.part == m)].sum()
+                assert abs(ip[k, m] - ref) <= 1e-12 * ref
+    # part weights: unit and nnz(r_i)
+    np.testing.assert_array_equal(W, np.bincount(w.part, minlength=K))
+    _, Wn = oracle.ip_matrix(g.row_ptr, g.col, g.w, w.part, K, a_row_ptr=w.row_ptr)
+    np.testing.assert_array_equal(Wn, np.bincount(w.part, weights=np.diff(w.row_ptr), minlength=K).astype(np.int64))
+    assert Wn.sum() == w.nnz
+    # K = 1: nothing is inter-block
+    ip1, W1 = oracle.ip_matrix(g.row_ptr, g.col, g.w, np.zeros(n, np.int32), 1)
+    assert ip1[0, 0] == 0.0 and W1[0] == n
+    with pytest.raises(oracle.OracleError):
+        oracle.ip_matrix(g.row_ptr, g.col, g.w, np.full(n, K, np.int32), K)
+
+
+def test_ip_matrix_block_diagonal_zero():
+    rng = np.random.default_rng(9)
+    D1, _ = rand_csr(30, 30, 0.15, rng)
+    D2, _ = rand_csr(25, 25, 0.15, rng)
+    D = np.zeros((55, 55)); D[:30, :30] = D1; D[30:, 30:] = D2
+    rp, ci, v = from_dense(D)
+    g = oracle.build(rp, ci, v, scale_rows=1)
+    part = np.r_[np.zeros(30, np.int32), np.ones(25, np.int32)]
+    ip, W = oracle.ip_matrix(g.row_ptr, g.col, g.w, part, 2)
+    assert not ip.any() and W.tolist() == [30, 25]

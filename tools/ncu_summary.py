@@ -8,7 +8,7 @@ import subprocess
 import sys
 
 WANT = [
-    ("gpu__time_duration.sum", "dur"),
+    ("gpu__time_duration.sum", "dur_us"),
     ("dram__bytes_read.sum", "dram_rd"),
     ("dram__bytes_write.sum", "dram_wr"),
     ("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "dram_pct"),
@@ -34,7 +34,8 @@ STALL = "smsp__average_warps_issue_stalled_"
 
 def scale(v, unit):
     f = float(v.replace(",", ""))
-    mul = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-3, "usecond": 1, "msecond": 1e3}
+    mul = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-3, "usecond": 1, "msecond": 1e3,
+           "ns": 1e-3, "us": 1, "ms": 1e3, "s": 1e6, "B": 1, "KB": 1e3, "MB": 1e6, "GB": 1e9}
     return f * mul.get(unit, 1)
 
 
