@@ -92,6 +92,11 @@ __device__ __forceinline__ void num_merge_row(const NumArgs &a, int64_t i, int64
         hv[t] = a.T.vt[q[t]];
     }
     int64_t o = 0;
+    // fused cut, one output behind: the part[] load of a kept edge j > i is
+    // issued when the edge is emitted and consumed at the next emission, so
+    // its latency overlaps a merge step instead of stalling it
+    int32_t pend_pj = pi;
+    double pend_w = 0.0;
     while (true) {
         int m = h[0];
 #pragma unroll
@@ -116,12 +121,17 @@ __device__ __forceinline__ void num_merge_row(const NumArgs &a, int64_t i, int64
                 ow[o] = w;
                 ++o;
                 if (a.part && (int64_t)m > i) {
-                    const int32_t pj = a.part[m];
-                    badp |= (pj < 0) | (pj >= a.K);
-                    if (pj != pi) cut.add(w);
+                    badp |= (pend_pj < 0) | (pend_pj >= a.K);
+                    if (pend_pj != pi) cut.add(pend_w);
+                    pend_pj = a.part[m];
+                    pend_w = w;
                 }
             }
         }
+    }
+    if (a.part) {
+        badp |= (pend_pj < 0) | (pend_pj >= a.K);
+        if (pend_pj != pi) cut.add(pend_w);
     }
     if (o < ub) {
         for (int64_t t = o; t < ub; ++t) oc[t] = -1;
