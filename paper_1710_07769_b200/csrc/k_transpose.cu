@@ -24,8 +24,8 @@ namespace rig {
 // sentinel per column fit kBucketSlots, larger buckets go to a CTA-wide pass.
 constexpr int kMinShift = 3, kMaxShift = 9;
 constexpr int kMaxBucketCols = 1 << kMaxShift;
-constexpr int kBucketTarget = 384;
-constexpr int kBucketSlots = 1024;
+constexpr int kBucketTarget = 256;
+constexpr int kBucketSlots = 640;
 
 struct __align__(16) Rec {
     int32_t col, row;
