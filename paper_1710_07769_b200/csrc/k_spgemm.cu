@@ -253,18 +253,43 @@ __global__ void __launch_bounds__(kMergeThreads) k_analyze_sym(SymArgs a, uint8_
     // per-thread bin counts, two 32-bit counters per register (bins 0..7;
     // a thread sees at most nloc / stride rows, far below 2^32)
     unsigned long long pc0 = 0, pc1 = 0, pc2 = 0, pc3 = 0;
-    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < nloc; r += stride) {
+    const int lane = lane_id();
+    // warp-uniform trip count: rows longer than kLongRow get f_i from the whole
+    // warp (a thread walking a 5000-entry row would hold its CTA back)
+    constexpr int64_t kLongRow = 64;
+    for (int64_t rbase = blockIdx.x * (int64_t)blockDim.x + (threadIdx.x & ~31); rbase < nloc; rbase += stride) {
+        const int64_t r = rbase + lane;
+        const bool valid = r < nloc;
         const int64_t i = a.rb + r;
-        const int64_t s = a.A.rp[i], e = a.A.rp[i + 1];
-        int64_t fi = 0;
-        for (int64_t p0 = s; p0 < e; p0 += 8) {  // 8 independent gathers in flight
-            int k[8];
-#pragma unroll
-            for (int u = 0; u < 8; ++u) k[u] = p0 + u < e ? a.A.ci[p0 + u] : -1;
-#pragma unroll
-            for (int u = 0; u < 8; ++u)
-                if (k[u] >= 0) fi += a.T.cp[k[u] + 1] - a.T.cp[k[u]];
+        int64_t s = 0, e = 0;
+        if (valid) {
+            s = a.A.rp[i];
+            e = a.A.rp[i + 1];
         }
+        const bool longrow = e - s > kLongRow;
+        int64_t fi = 0;
+        if (!longrow) {
+            for (int64_t p0 = s; p0 < e; p0 += 8) {  // 8 independent gathers in flight
+                int k[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) k[u] = p0 + u < e ? a.A.ci[p0 + u] : -1;
+#pragma unroll
+                for (int u = 0; u < 8; ++u)
+                    if (k[u] >= 0) fi += a.T.cp[k[u] + 1] - a.T.cp[k[u]];
+            }
+        }
+        for (unsigned lm = __ballot_sync(kFull, longrow); lm; lm &= lm - 1) {
+            const int u = __ffs(lm) - 1;
+            const int64_t su = __shfl_sync(kFull, s, u), eu = __shfl_sync(kFull, e, u);
+            int64_t part = 0;
+            for (int64_t p = su + lane; p < eu; p += 32) {
+                const int k = a.A.ci[p];
+                part += a.T.cp[k + 1] - a.T.cp[k];
+            }
+            part = warp_sum(part);
+            if (lane == u) fi = part;
+        }
+        if (!valid) continue;
         local += fi;
         nnzr += e - s;
         const int len = (int)min(e - s, (int64_t)kMergeMaxLen + 1);
