@@ -61,7 +61,7 @@ struct DevCounters {
     int64_t sym_count[8];
     int64_t list_count[2]; // mid / huge list lengths (device side)
     int64_t defer_count[2];// rows deferred by the small / big mid kernels
-    // shape statistics (k_shape_stats, right after the column histogram)
+    // shape statistics (scan_u32_shape, on the column counts and row pointers)
     int64_t max_col;       // longest column of A
     int64_t p_full;        // sum over columns of len^2 = products of the full matrix (>= the shard's)
     int64_t max_row;       // longest row of A in the shard
@@ -106,10 +106,6 @@ int num_sms();
 // k_prep.cu
 void launch_validate(const Csr &A, int *err, cudaStream_t s);
 void launch_col_hist(const Csr &A, unsigned *cnt, unsigned *rank /*nullable*/, cudaStream_t s);
-// max_col, p_full, max_row, shard_nnz into ctr (zeroed) from the column counts
-// and the row pointers of rows [rb, re)
-void launch_shape_stats(const unsigned *cnt, int64_t m, const int64_t *rp, int64_t rb, int64_t re, DevCounters *ctr,
-                        cudaStream_t s);
 // k_transpose.cu: bucketed a1 + a2 (see there for the CSC layout with sentinels)
 int64_t transpose_buckets(int64_t nnz, int64_t ncols);
 constexpr size_t kTransposeRecBytes = 16;
@@ -133,6 +129,11 @@ enum class ScanOp { Identity, UbOffDiag };
 void scan_i64(const int64_t *in, int64_t n, int64_t *out, ScanOp op, void *tmp, size_t tmp_bytes,
               cudaStream_t s);
 void scan_u32(const unsigned *in, int64_t n, int64_t *out, void *tmp, size_t tmp_bytes, cudaStream_t s);
+// scan_u32 of the column counts that also takes the shape statistics
+// (DevCounters max_col, p_full, max_row, shard_nnz of rows [rb, re)) into
+// ctr, copies ctr to host_copy and records `ready` before the second kernel.
+void scan_u32_shape(const unsigned *in, int64_t n, int64_t *out, void *tmp, DevCounters *ctr, const int64_t *rp,
+                    int64_t rb, int64_t re, void *host_copy, cudaEvent_t ready, cudaStream_t s);
 size_t scan_tmp_bytes(int64_t n);
 
 // k_spgemm.cu

@@ -71,58 +71,6 @@ void launch_col_hist(const Csr &A, unsigned *cnt, unsigned *rank, cudaStream_t s
     note_launch();
 }
 
-// Shape statistics right after the histogram: they bound the products and
-// decide, before the transpose finishes, whether every row takes the merge
-// path (row length <= kMergeMaxLen and column length <= kMergeMaxF / that).
-__global__ void __launch_bounds__(256) k_shape_stats(const unsigned *__restrict__ cnt, int64_t m,
-                                                     const int64_t *__restrict__ rp, int64_t rb, int64_t re,
-                                                     DevCounters *ctr) {
-    const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    unsigned long long mc = 0, ps = 0, mr = 0;
-    for (int64_t k = tid; k < m; k += stride) {  // (256 threads = 8 warps)
-        const unsigned long long c = cnt[k];
-        mc = c > mc ? c : mc;
-        ps += c * c;
-    }
-    for (int64_t i = rb + tid; i < re; i += stride) {
-        const unsigned long long len = (unsigned long long)(rp[i + 1] - rp[i]);
-        mr = len > mr ? len : mr;
-    }
-    __syncwarp();
-    ps = warp_sum(ps);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        mc = max(mc, __shfl_xor_sync(kFull, mc, o));
-        mr = max(mr, __shfl_xor_sync(kFull, mr, o));
-    }
-    __shared__ unsigned long long red[3][8];  // one atomic per counter per CTA
-    const int w = threadIdx.x >> 5;
-    if (lane_id() == 0) {
-        red[0][w] = ps;
-        red[1][w] = mc;
-        red[2][w] = mr;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        for (int k = 1; k < 8; ++k) {
-            ps += red[0][k];
-            mc = max(mc, red[1][k]);
-            mr = max(mr, red[2][k]);
-        }
-        if (ps) atomicAdd((unsigned long long *)&ctr->p_full, ps);
-        if (mc) atomicMax((unsigned long long *)&ctr->max_col, mc);
-        if (mr) atomicMax((unsigned long long *)&ctr->max_row, mr);
-    }
-    if (tid == 0) ctr->shard_nnz = rp[re] - rp[rb];
-}
-
-void launch_shape_stats(const unsigned *cnt, int64_t m, const int64_t *rp, int64_t rb, int64_t re, DevCounters *ctr,
-                        cudaStream_t s) {
-    k_shape_stats<<<grid_for(std::max<int64_t>(m, re - rb), 256, 16), 256, 0, s>>>(cnt, m, rp, rb, re, ctr);
-    note_launch();
-}
-
 // a1 + a2 (scaling, CSC): k_transpose.cu
 
 // ------------------------------------------------------------------ a3

@@ -37,19 +37,63 @@ __device__ __forceinline__ int64_t block_excl_scan(int64_t v, int64_t *total) {
     return r;
 }
 
+// Optional shape statistics, taken on the column counts while they are summed
+// (and on the row pointers of the shard): max column, sum of len^2, max row,
+// shard nnz -- see DevCounters.
+struct ShapeOut {
+    DevCounters *ctr;  // null: no statistics
+    const int64_t *rp;
+    int64_t rb, re;
+};
+
 template <typename T>
 __global__ void __launch_bounds__(kScanThreads) k_tile_sum(const T *__restrict__ in, int64_t n, ScanOp op,
-                                                           int64_t *tile_sums) {
+                                                           int64_t *tile_sums, ShapeOut so) {
     const int64_t base = blockIdx.x * kTile;
     int64_t s = 0;
+    unsigned long long ps = 0, mc = 0, mr = 0;
 #pragma unroll
     for (int j = 0; j < kScanItems; ++j) {
         const int64_t i = base + (int64_t)j * kScanThreads + threadIdx.x;
-        if (i < n) s += scan_load(in, i, op);
+        if (i < n) {
+            const int64_t x = scan_load(in, i, op);
+            s += x;
+            ps += (unsigned long long)x * (unsigned long long)x;
+            mc = max(mc, (unsigned long long)x);
+        }
     }
     s = warp_sum(s);
     __shared__ int64_t ws[kScanThreads / 32];
     if (lane_id() == 0) ws[threadIdx.x >> 5] = s;
+    if (so.ctr) {
+        const int64_t stride = (int64_t)gridDim.x * kScanThreads;
+        for (int64_t i = so.rb + blockIdx.x * (int64_t)kScanThreads + threadIdx.x; i < so.re; i += stride)
+            mr = max(mr, (unsigned long long)(so.rp[i + 1] - so.rp[i]));
+        ps = warp_sum(ps);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            mc = max(mc, __shfl_xor_sync(kFull, mc, o));
+            mr = max(mr, __shfl_xor_sync(kFull, mr, o));
+        }
+        __shared__ unsigned long long red[3][kScanThreads / 32];
+        if (lane_id() == 0) {
+            red[0][threadIdx.x >> 5] = ps;
+            red[1][threadIdx.x >> 5] = mc;
+            red[2][threadIdx.x >> 5] = mr;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            for (int k = 1; k < kScanThreads / 32; ++k) {
+                ps += red[0][k];
+                mc = max(mc, red[1][k]);
+                mr = max(mr, red[2][k]);
+            }
+            if (ps) atomicAdd((unsigned long long *)&so.ctr->p_full, ps);
+            if (mc) atomicMax((unsigned long long *)&so.ctr->max_col, mc);
+            if (mr) atomicMax((unsigned long long *)&so.ctr->max_row, mr);
+            if (blockIdx.x == 0) so.ctr->shard_nnz = so.rp[so.re] - so.rp[so.rb];
+        }
+    }
     __syncthreads();
     if (threadIdx.x == 0) {
         int64_t t = 0;
@@ -111,14 +155,16 @@ size_t scan_tmp_bytes(int64_t n) {
 }
 
 template <typename T>
-static void scan_impl(const T *in, int64_t n, int64_t *out, ScanOp op, void *tmp, cudaStream_t s) {
+static void scan_impl(const T *in, int64_t n, int64_t *out, ScanOp op, void *tmp, cudaStream_t s,
+                      ShapeOut so = ShapeOut{nullptr, nullptr, 0, 0}, cudaEvent_t after_sum = nullptr) {
     const int64_t ntiles = (n + kTile - 1) / kTile;
     if (ntiles == 0) {
         cudaMemsetAsync(out, 0, sizeof(int64_t), s);
         return;
     }
     int64_t *ts = static_cast<int64_t *>(tmp);
-    k_tile_sum<T><<<(unsigned)ntiles, kScanThreads, 0, s>>>(in, n, op, ts);
+    k_tile_sum<T><<<(unsigned)ntiles, kScanThreads, 0, s>>>(in, n, op, ts, so);
+    if (after_sum) cudaEventRecord(after_sum, s);
     k_tile_scan<T><<<(unsigned)ntiles, kScanThreads, 0, s>>>(in, n, op, ts, ntiles, out);
     note_launch(2);
 }
@@ -129,6 +175,24 @@ void scan_i64(const int64_t *in, int64_t n, int64_t *out, ScanOp op, void *tmp, 
 
 void scan_u32(const unsigned *in, int64_t n, int64_t *out, void *tmp, size_t, cudaStream_t s) {
     scan_impl<unsigned>(in, n, out, ScanOp::Identity, tmp, s);
+}
+
+void scan_u32_shape(const unsigned *in, int64_t n, int64_t *out, void *tmp, DevCounters *ctr, const int64_t *rp,
+                    int64_t rb, int64_t re, void *host_copy, cudaEvent_t ready, cudaStream_t s) {
+    const int64_t ntiles = (n + kTile - 1) / kTile;
+    if (ntiles == 0) {  // no columns: the statistics are zeros except the shard
+        cudaMemsetAsync(out, 0, sizeof(int64_t), s);
+        cudaMemcpyAsync(host_copy, ctr, sizeof(DevCounters), cudaMemcpyDeviceToHost, s);
+        cudaEventRecord(ready, s);
+        return;
+    }
+    int64_t *ts = static_cast<int64_t *>(tmp);
+    k_tile_sum<unsigned><<<(unsigned)ntiles, kScanThreads, 0, s>>>(in, n, ScanOp::Identity, ts,
+                                                                    ShapeOut{ctr, rp, rb, re});
+    cudaMemcpyAsync(host_copy, ctr, sizeof(DevCounters), cudaMemcpyDeviceToHost, s);
+    cudaEventRecord(ready, s);
+    k_tile_scan<unsigned><<<(unsigned)ntiles, kScanThreads, 0, s>>>(in, n, ScanOp::Identity, ts, ntiles, out);
+    note_launch(2);
 }
 
 }  // namespace rig

@@ -370,12 +370,11 @@ static void plan_build(rig_plan *p, const rig_csr_t *Ain, bool allow_early = fal
         Prof pf(P_COLPTR, s);
         if (nnz > 0) launch_col_hist(A0, cnt, nullptr, s);
         if (allow_early && nloc > 0) {
-            launch_shape_stats(cnt, m, A0.rp, p->rb, p->re, p->ctr, s);
-            CK(cudaMemcpyAsync(&hs->shape, p->ctr, sizeof(DevCounters), cudaMemcpyDeviceToHost, s));
             ev_shape = shape_event();
-            CK(cudaEventRecord(ev_shape, s));
+            scan_u32_shape(cnt, m, cp, ws + o_st1, p->ctr, A0.rp, p->rb, p->re, &hs->shape, ev_shape, s);
+        } else {
+            scan_u32(cnt, m, cp, ws + o_st1, 0, s);
         }
-        scan_u32(cnt, m, cp, ws + o_st1, 0, s);
     }
     // a1 + a2: scale rows (optional), bucketed transpose into the CSC
     {
