@@ -8,7 +8,8 @@ Thin ctypes marshalling over ``rig_oracle.c`` (every arithmetic step lives in
 that file, with its PAPER.md citation).  Pins: ``tests/test_oracle_pins.py``.
 Parity pinned for: scaling, transpose, products, build (structure, values,
 diag, nnz(C)), cutsize, inter-block inner-product matrix and part weights
-(SURVEY.md §8(f) f2).  Unpinned: nothing the build path uses; the paper's
+(SURVEY.md §8(f) f2), dense-column sparsification and integer edge weights
+(f1).  Unpinned: nothing the build path uses; the paper's
 12x12 sample is in a missing figure and is not
 reproduced.
 """
@@ -24,7 +25,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "rig_oracle.c")
 _LIB = os.path.join(_HERE, "liboracle.so")
 
-CFLAGS = ["-O2", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared", "-std=c99"]
+CFLAGS = ["-O2", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared", "-std=gnu99"]
 
 
 def build_lib(force: bool = False) -> str:
@@ -52,6 +53,10 @@ def lib():
         _lib.orc_free.argtypes = [p]
         _lib.orc_cutsize.argtypes = [i64, i64, p, p, p, i64, p, i32, p, p, p]
         _lib.orc_ip_matrix.argtypes = [i64, i64, p, p, p, i64, p, i32, p, p, p]
+        _lib.orc_dense_threshold.argtypes = [i64]
+        _lib.orc_dense_threshold.restype = i64
+        _lib.orc_sparsify.argtypes = [i64, i64, p, p, p, p, p, p, p]
+        _lib.orc_int_weights.argtypes = [i64, p, i64, p]
     return _lib
 
 
@@ -193,3 +198,36 @@ def ip_matrix(g_row_ptr, g_col, g_w, part, K, row_begin=0, a_row_ptr=None):
     if st:
         raise OracleError(st, "ip_matrix")
     return ip, W
+
+
+def dense_threshold(n):
+    """T = ceil(sqrt(n)) (reading R20)."""
+    return int(lib().orc_dense_threshold(int(n)))
+
+
+def sparsify(row_ptr, col_idx, val, ncols=None):
+    """A~: columns with more than T nonzeros keep their T largest |values|,
+    ties to the lower row.  Returns (row_ptr, col, val)."""
+    row_ptr, col_idx, val = _c(row_ptr, np.int64), _c(col_idx, np.int32), _c(val, np.float64)
+    nrows = row_ptr.size - 1
+    ncols = nrows if ncols is None else int(ncols)
+    nnz = int(row_ptr[-1])
+    orp = np.empty(nrows + 1, dtype=np.int64)
+    oc = np.empty(max(nnz, 1), dtype=np.int32)
+    ov = np.empty(max(nnz, 1), dtype=np.float64)
+    nout = ctypes.c_int64()
+    st = lib().orc_sparsify(nrows, ncols, _p(row_ptr), _p(col_idx), _p(val), _p(orp), _p(oc), _p(ov),
+                            ctypes.byref(nout))
+    if st:
+        raise OracleError(st, "sparsify")
+    return orp, oc[:nout.value].copy(), ov[:nout.value].copy()
+
+
+def int_weights(w, alpha):
+    """wgt = ceil(alpha * w), exact (PAPER.md:611)."""
+    w = _c(w, np.float64)
+    out = np.empty(w.size, dtype=np.int64)
+    st = lib().orc_int_weights(w.size, _p(w), int(alpha), _p(out))
+    if st:
+        raise OracleError(st, "int_weights")
+    return out

@@ -14,6 +14,9 @@
  *   PAPER.md:560-562  (§2.3)           C computed by basic (Gustavson) SpGEMM
  *   PAPER.md:393-405, 1150-1154 (§2.2, eq. partcut)
  *                                      cutsize(Pi) = sum of costs of cut edges
+ *   PAPER.md:506-519  (§2.2, eq. ip_km) inter-block inner products (f2)
+ *   PAPER.md:572-576  (§2.3)           dense-column sparsification A~ (f1)
+ *   PAPER.md:611      (§2.3)           integer edge weights ceil(alpha*cost) (f1)
  *
  * Readings where the paper is silent:
  *   - ordering contract: for each (i,j), c_ij = fma-chain over the shared
@@ -273,5 +276,125 @@ int orc_ip_matrix(int64_t nloc, int64_t row_begin, const int64_t *g_row_ptr, con
     }
     for (int64_t c = 0; c < (int64_t)K * K; ++c) ip[c] += comp[c];
     free(comp);
+    return ORC_OK;
+}
+
+/* ---------------------------------------------------------------- f1
+ * Dense-column threshold (§2.3): a column is dense if it holds
+ * more than sqrt(n) nonzeros, and a dense column keeps its sqrt(n) largest
+ * entries.  Reading R20: the kept count
+ * is T = ceil(sqrt(n)), the smallest integer t with t*t >= n, n = nrows;
+ * "nnz > sqrt(n)" and "nnz > T" select the same columns to shrink, since a
+ * column with nnz <= T keeps all of its entries either way. */
+int64_t orc_dense_threshold(int64_t n) {
+    int64_t t = 0;
+    while (t * t < n) ++t;
+    return t;
+}
+
+typedef struct {
+    double mag;
+    int32_t row;
+    int64_t pos; /* position in the CSR */
+} orc_entry;
+
+/* (|value| descending, row ascending): ties go to the lower row */
+static int cmp_entry(const void *a, const void *b) {
+    const orc_entry *x = (const orc_entry *)a, *y = (const orc_entry *)b;
+    if (x->mag != y->mag) return x->mag > y->mag ? -1 : 1;
+    return (x->row > y->row) - (x->row < y->row);
+}
+
+/* A~ from A (§2.3): every column with more than T nonzeros
+ * keeps the T entries of largest absolute value (ties: lower row), every
+ * other column is unchanged.  Values are copied, not re-normalised (reading
+ * R21: A~ is extracted from the already scaled A; SPEC.md:242 open question).
+ * Output CSR (rows ascending, columns ascending within a row, as the input)
+ * into caller arrays of capacity nnz(A); *nnz_out = nnz(A~). */
+int orc_sparsify(int64_t nrows, int64_t ncols, const int64_t *row_ptr, const int32_t *col_idx,
+                 const double *val, int64_t *out_row_ptr, int32_t *out_col, double *out_val,
+                 int64_t *nnz_out) {
+    const int64_t T = orc_dense_threshold(nrows);
+    const int64_t nnz = row_ptr[nrows];
+    int64_t *col_ptr = (int64_t *)calloc((size_t)ncols + 1, sizeof(int64_t));
+    orc_entry *ent = (orc_entry *)malloc(sizeof(orc_entry) * (size_t)(nnz > 0 ? nnz : 1));
+    unsigned char *keep = (unsigned char *)malloc((size_t)(nnz > 0 ? nnz : 1));
+    int64_t *next = (int64_t *)malloc(sizeof(int64_t) * (size_t)(ncols > 0 ? ncols : 1));
+    if (!col_ptr || !ent || !keep || !next) {
+        free(col_ptr); free(ent); free(keep); free(next);
+        return ORC_ERR_NOMEM;
+    }
+    for (int64_t p = 0; p < nnz; ++p) {
+        if (col_idx[p] < 0 || col_idx[p] >= ncols) {
+            free(col_ptr); free(ent); free(keep); free(next);
+            return ORC_ERR_INVALID;
+        }
+        col_ptr[col_idx[p] + 1] += 1;
+    }
+    for (int64_t k = 0; k < ncols; ++k) col_ptr[k + 1] += col_ptr[k];
+    for (int64_t k = 0; k < ncols; ++k) next[k] = col_ptr[k];
+    for (int64_t i = 0; i < nrows; ++i)
+        for (int64_t p = row_ptr[i]; p < row_ptr[i + 1]; ++p) {
+            orc_entry e = {fabs(val[p]), (int32_t)i, p};
+            ent[next[col_idx[p]]++] = e;
+        }
+    for (int64_t p = 0; p < nnz; ++p) keep[p] = 1;
+    for (int64_t k = 0; k < ncols; ++k) {
+        const int64_t len = col_ptr[k + 1] - col_ptr[k];
+        if (len <= T) continue;
+        qsort(ent + col_ptr[k], (size_t)len, sizeof(orc_entry), cmp_entry);
+        for (int64_t q = col_ptr[k] + T; q < col_ptr[k + 1]; ++q) keep[ent[q].pos] = 0;
+    }
+    int64_t o = 0;
+    out_row_ptr[0] = 0;
+    for (int64_t i = 0; i < nrows; ++i) {
+        for (int64_t p = row_ptr[i]; p < row_ptr[i + 1]; ++p)
+            if (keep[p]) {
+                out_col[o] = col_idx[p];
+                out_val[o] = val[p];
+                ++o;
+            }
+        out_row_ptr[i + 1] = o;
+    }
+    *nnz_out = o;
+    free(col_ptr); free(ent); free(keep); free(next);
+    return ORC_OK;
+}
+
+/* Integer edge weights for the partitioner (§2.3):
+ *   wgt(v_i,v_j) = ceil(alpha * cost(v_i,v_j)),  alpha a positive integer.
+ * Exact: w = m * 2^e with m a 53-bit integer (frexp), so alpha * w =
+ * (alpha * m) * 2^e with alpha * m exact in 128-bit integers; the ceiling is
+ * a shift (e >= 0) or a rounded-up division by 2^-e (e < 0).  Requires
+ * 1 <= alpha <= 2^53 and w >= 0 finite; ORC_ERR_INVALID otherwise or if a
+ * result exceeds 2^62. */
+int orc_int_weights(int64_t n, const double *w, int64_t alpha, int64_t *wgt) {
+    if (alpha < 1 || alpha > ((int64_t)1 << 53)) return ORC_ERR_INVALID;
+    for (int64_t e = 0; e < n; ++e) {
+        const double x = w[e];
+        if (!(x >= 0.0) || !isfinite(x)) return ORC_ERR_INVALID;
+        if (x == 0.0) {
+            wgt[e] = 0;
+            continue;
+        }
+        int ex;
+        const double fr = frexp(x, &ex);             /* x = fr * 2^ex, fr in [0.5, 1) */
+        const int64_t m = (int64_t)ldexp(fr, 53);     /* exact: x = m * 2^(ex - 53) */
+        const int sh = ex - 53;
+        const unsigned __int128 prod = (unsigned __int128)(uint64_t)alpha * (uint64_t)m;
+        unsigned __int128 q;
+        if (sh >= 0) {
+            if (sh > 62) return ORC_ERR_INVALID;
+            q = prod << sh;
+            if ((q >> sh) != prod) return ORC_ERR_INVALID;
+        } else if (-sh >= 127) {
+            q = 1; /* 0 < alpha * x < 1 */
+        } else {
+            const unsigned __int128 d = (unsigned __int128)1 << (-sh);
+            q = prod / d + (prod % d != 0);
+        }
+        if (q > ((unsigned __int128)1 << 62)) return ORC_ERR_INVALID;
+        wgt[e] = (int64_t)q;
+    }
     return ORC_OK;
 }

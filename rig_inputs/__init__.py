@@ -14,6 +14,7 @@ from .configs import (  # noqa: F401
     stencil3d,
     powerlaw,
     banded,
+    dense_columns,
     uniform_rows,
     part_contiguous,
     part_random_balanced,

@@ -263,6 +263,44 @@ def banded(n, rng, bw=50, in_band=19, far=3, chunk=1 << 18):
     return row_ptr, col, val
 
 
+def dense_columns(n, rng, per_row=5, n_dense=4, dense_nnz=None, ncols=None, levels=0):
+    """Sparse rows plus planted dense columns (the LP-matrix shape that
+    motivates the sparsification of PAPER.md:565-576): every row has
+    `per_row` distinct uniform columns, and `n_dense` evenly spaced columns
+    hold `dense_nnz` (default n // 4) uniformly chosen rows each.  Values
+    N(0,1), or with `levels` > 0 drawn from {+-1, ..., +-levels} so that
+    |value| ties are common (the tie rule of SPEC.md:229)."""
+    m = n if ncols is None else int(ncols)
+    dense_nnz = n // 4 if dense_nnz is None else int(dense_nnz)
+    dcols = (np.arange(n_dense, dtype=np.int64) * m) // max(n_dense, 1) + m // (2 * max(n_dense, 1))
+    rows = [np.repeat(np.arange(n, dtype=np.int64), per_row)]
+    keys = rng.random((n, m)) if n * m <= (1 << 24) else None
+    if keys is not None:
+        keys[:, dcols] = 2.0  # the dense columns come from their own draw
+        cols = [np.sort(np.argpartition(keys, per_row - 1, axis=1)[:, :per_row], axis=1).reshape(-1)]
+    else:
+        c = rng.integers(0, m, size=(n, per_row * 2))
+        cols_l = []
+        for i in range(n):
+            u = np.unique(c[i][~np.isin(c[i], dcols)])[:per_row]
+            while u.size < per_row:
+                u = np.unique(np.r_[u, rng.integers(0, m, per_row)])
+                u = u[~np.isin(u, dcols)][:per_row]
+            cols_l.append(np.sort(u))
+        cols = [np.concatenate(cols_l)]
+    for k in dcols:
+        r = np.sort(rng.choice(n, size=dense_nnz, replace=False))
+        rows.append(r)
+        cols.append(np.full(r.size, k, dtype=np.int64))
+    rows = np.concatenate(rows)
+    cols = np.concatenate(cols)
+    if levels > 0:
+        vals = rng.integers(1, levels + 1, size=rows.size) * rng.choice([-1.0, 1.0], size=rows.size)
+    else:
+        vals = _nonzero_normal(rng, rows.size)
+    return from_triplets(n, m, rows, cols, vals)
+
+
 # --------------------------------------------------------------------------
 # BASELINE.json configs
 # --------------------------------------------------------------------------

@@ -18,6 +18,12 @@ index, transposed operand, wrong rounding/order, wrong drop rule) fails one:
   * cutsize: math.fsum over the cut edges, cut = total - intra, K=1 -> 0, all
     parts distinct -> total, block-diagonal -> 0, brute-force interIP from
     dense row inner products (eq. ip_km)
+  * f1 sparsification: the paper's 25x25 dense-column example keeps 5 entries
+    (PAPER.md:567-577); the kept set equals a brute-force rank count per entry
+    (#entries of its column that beat it < T); T = ceil(sqrt(n)) against
+    math.isqrt; no dense column -> A~ = A; ties -> lowest rows
+  * f1 integer weights: exact ceil(alpha * w) by fractions.Fraction, and the
+    paper's range [1, alpha] for costs in (0, 1]
 """
 import math
 from fractions import Fraction
@@ -27,7 +33,7 @@ import pytest
 import scipy.sparse as sp
 
 import oracle
-from rig_inputs import from_dense, from_triplets, make, make_small, part_contiguous, stencil2d, stencil3d
+from rig_inputs import dense_columns, from_dense, from_triplets, make, make_small, part_contiguous, stencil2d, stencil3d
 from rig_testutil import read_golden
 
 U = 2.0 ** -53
@@ -423,3 +429,109 @@ def test_ip_matrix_block_diagonal_zero():
     part = np.r_[np.zeros(30, np.int32), np.ones(25, np.int32)]
     ip, W = oracle.ip_matrix(g.row_ptr, g.col, g.w, part, 2)
     assert not ip.any() and W.tolist() == [30, 25]
+
+
+# ---------------------------------------------------------------- f1
+def test_dense_threshold_is_ceil_sqrt():
+    for n in list(range(0, 200)) + [10**6, 4_000_000, 4_000_001, (1 << 31) - 1]:
+        t = oracle.dense_threshold(n)
+        assert t == (math.isqrt(n - 1) + 1 if n > 0 else 0)
+
+
+def brute_kept(rp, ci, v, T):
+    """Entry (i, k) survives iff fewer than T entries of column k beat it
+    (larger |value|, or equal |value| and a lower row)."""
+    n = rp.size - 1
+    rows = np.repeat(np.arange(n), np.diff(rp))
+    keep = np.ones(ci.size, bool)
+    for p in range(ci.size):
+        same = ci == ci[p]
+        if same.sum() <= T:
+            continue
+        a = np.abs(v)
+        beats = same & ((a > a[p]) | ((a == a[p]) & (rows < rows[p])))
+        keep[p] = beats.sum() < T
+    return keep
+
+
+def test_sparsify_paper_25x25_example():
+    kv = {l[0]: l[1:] for l in read_golden("paper_531.txt")}
+    n = int(kv["n"][0])
+    dc = int(kv["dense_col"][0]) - 1
+    out = {int(x) - 1 for x in kv["rows_not_in_dense_col"]}
+    D = np.eye(n)
+    for r in range(n):
+        if r not in out:
+            D[r, dc] = 1.0 + r / 7.0
+    rp, ci, v = from_dense(D)
+    ahat, _ = oracle.scale(rp, v)
+    trp, tci, tv = oracle.sparsify(rp, ci, ahat)
+    # "keeping 5 largest nonzeros in the dense column" (PAPER.md:577)
+    assert np.count_nonzero(tci == dc) == 5
+    for k in range(n):
+        if k != dc:
+            assert np.count_nonzero(tci == k) == np.count_nonzero(ci == k)
+    # row dc holds only its dense-column entry (|a_hat| = 1, the largest), the
+    # other rows' |a_hat| = d / sqrt(1 + d^2) grows with d = 1 + r/7
+    kept_rows = sorted(np.repeat(np.arange(n), np.diff(trp))[tci == dc].tolist())
+    assert kept_rows == [dc, 21, 22, 23, 24]
+    # C~ = A~ A~^T: a 5-clique plus the other 20 diagonals -> 45 (vs 531)
+    g = oracle.build(trp, tci, tv, scale_rows=0)
+    assert int(g.nnzc.sum()) == 45 and g.nnz == 20
+
+
+@pytest.mark.parametrize("seed,levels", [(0, 0), (1, 0), (2, 2), (3, 1)])
+def test_sparsify_brute_force_rank(seed, levels):
+    rng = np.random.default_rng(700 + seed)
+    n = 60 + 7 * seed
+    rp, ci, v = dense_columns(n, rng, per_row=3, n_dense=3, dense_nnz=n // 3, levels=levels)
+    T = oracle.dense_threshold(n)
+    keep = brute_kept(rp, ci, v, T)
+    trp, tci, tv = oracle.sparsify(rp, ci, v)
+    rows = np.repeat(np.arange(n), np.diff(rp))
+    assert np.array_equal(trp, np.r_[0, np.cumsum(np.bincount(rows[keep], minlength=n))])
+    assert np.array_equal(tci, ci[keep]) and np.array_equal(tv, v[keep])
+    assert np.bincount(tci, minlength=n).max() <= T
+
+
+def test_sparsify_ties_take_lowest_rows():
+    n = 16  # T = 4
+    rows = np.arange(n)
+    rp, ci, v = from_triplets(n, 40, np.r_[rows, rows], np.r_[np.full(n, 3), rows + 8],
+                              np.r_[np.full(n, -2.0), np.ones(n)])
+    trp, tci, tv = oracle.sparsify(rp, ci, v, ncols=40)
+    kept = np.repeat(np.arange(n), np.diff(trp))[tci == 3]
+    assert kept.tolist() == [0, 1, 2, 3]
+    # columns 8..23 hold one entry each: unchanged
+    assert np.count_nonzero(tci != 3) == n
+
+
+def test_sparsify_no_dense_column_is_identity():
+    w = make_small(2)  # 5-point stencil: column counts <= 5 <= ceil(sqrt(n))
+    trp, tci, tv = oracle.sparsify(w.row_ptr, w.col_idx, w.val)
+    assert np.array_equal(trp, w.row_ptr) and np.array_equal(tci, w.col_idx) and np.array_equal(tv, w.val)
+
+
+def test_int_weights_exact_ceiling():
+    rng = np.random.default_rng(5)
+    w = np.r_[rng.random(2000), rng.random(200) * 1e-9, 0.1, 0.3, 1.0, 0.5, 2.0 ** -60,
+              np.nextafter(1.0, 0.0), 5e-324, 0.0]
+    for alpha in (1, 3, 10_000, 2 ** 31 - 1, 2 ** 53):
+        got = oracle.int_weights(w, alpha)
+        want = [math.ceil(Fraction(alpha) * Fraction(float(x))) for x in w]
+        assert got.tolist() == want
+    # 0.1 is slightly above 1/10, so ceil(10^4 * 0.1) = 1001 (1000 in naive fp)
+    assert oracle.int_weights(np.array([0.1]), 10_000)[0] == 1001
+
+
+def test_int_weights_paper_range():
+    # costs in (0, 1] after prescaling -> weights in [1, alpha] (PAPER.md:613)
+    wl = make_small(1)
+    g = oracle.build(wl.row_ptr, wl.col_idx, wl.val, scale_rows=1)
+    alpha = 10_000
+    wg = oracle.int_weights(g.w, alpha)
+    assert wg.min() >= 1 and wg.max() <= alpha
+    with pytest.raises(oracle.OracleError):
+        oracle.int_weights(np.array([0.5]), 0)
+    with pytest.raises(oracle.OracleError):
+        oracle.int_weights(np.array([-0.5]), 10)
