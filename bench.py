@@ -284,8 +284,8 @@ def main():
     gc.enable()
     launches = rig.launch_count() - launches0
     rig.lib.rig_profile_enable(0)
-    pms = (ctypes.c_double * 12)()
-    pcnt = (ctypes.c_int64 * 12)()
+    pms = (ctypes.c_double * 13)()
+    pcnt = (ctypes.c_int64 * 13)()
     rig.lib.rig_profile_read(pms, pcnt)
     clk = clocks.stop()
     step_ms = [a.elapsed_time(b) for a, b in ev]
@@ -302,7 +302,7 @@ def main():
     torch.cuda.synchronize()
     rig.lib.rig_profile_enable(0)
     rig.lib.rig_profile_read(pms, pcnt)
-    pass_ms = {rig.lib.rig_pass_name(i).decode(): pms[i] / nprof for i in range(12) if pcnt[i]}
+    pass_ms = {rig.lib.rig_pass_name(i).decode(): pms[i] / nprof for i in range(13) if pcnt[i]}
     if dist:
         t = torch.tensor([my_ms, num_ms, ker_ms], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)

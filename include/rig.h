@@ -61,6 +61,14 @@ extern "C" {
 /* ---- flags ------------------------------------------------------------- */
 #define RIG_FLAG_VALIDATE 0x1u /* a0: check canonical CSR and finite values on the device */
 #define RIG_FLAG_DIAG 0x2u     /* also return diag[i] = c_ii (0 for an empty row) */
+/* f1: build the sparsified graph G~_RIP = graph of A~ A~^T (PAPER.md:572-579,
+ * §2.3) instead: every column of A_hat with more than T = ceil(sqrt(nrows))
+ * nonzeros keeps its T entries of largest |a_hat| (ties: the lower row;
+ * DESIGN.md readings R20-R21; no re-normalisation after the cut).  Costs one
+ * extra host synchronisation (the size of A~), and the whole A~ is formed on
+ * every rank (columns are global).  Without dense columns the graph equals
+ * the one built without the flag. */
+#define RIG_FLAG_SPARSIFY 0x4u
 
 typedef void *rig_stream_t; /* a cudaStream_t */
 
@@ -96,7 +104,7 @@ typedef struct rig_plan rig_plan_t;
  *   A          device CSR (borrowed).
  *   scale_rows 1: scale rows to unit 2-norm first; 0: use A as is.
  *   drop_tol   >= 0; an off-diagonal entry is an edge iff |c_ij| > drop_tol.
- *   flags      RIG_FLAG_VALIDATE | RIG_FLAG_DIAG.
+ *   flags      RIG_FLAG_VALIDATE | RIG_FLAG_DIAG | RIG_FLAG_SPARSIFY.
  *   out        filled with device arrays allocated by the library (stream-
  *              ordered on `stream`); release them with rig_graph_free.
  *              col_idx / w are allocated with the capacity bound
@@ -196,6 +204,24 @@ RIG_API int rig_partition_ip(const rig_graph_t *g, int64_t row_begin, int64_t n_
  * flag is set. */
 RIG_API int rig_partition_ip_finalize(const int64_t *acc_host, int32_t K, double *ip_host);
 
+/* ---- steps next to the path ------------------------ */
+
+/* A~ alone: the (optionally row-scaled, as in rig_build)
+ * matrix with every column holding more than T = ceil(sqrt(nrows)) nonzeros
+ * cut to its T largest |values| (ties: the lower row).  out receives
+ * library-owned DEVICE arrays (one allocation, stream-ordered) in canonical
+ * CSR, values bit-identical to A_hat's; release with rig_csr_free.  flags:
+ * RIG_FLAG_VALIDATE or 0.  Synchronises. */
+RIG_API int rig_sparsify(const rig_csr_t *A, int scale_rows, uint32_t flags, rig_csr_t *out, rig_stream_t stream);
+RIG_API int rig_csr_free(rig_csr_t *A, rig_stream_t stream);
+
+/* Integer edge weights for a partitioner:
+ * wgt[e] = ceil(alpha * w[e]) exactly (no rounding of the product), for
+ * device arrays w [n] and wgt [n]; 1 <= alpha <= 2^53 (else RIG_ERR_INVALID).
+ * An element with w < 0, w not finite, or a result beyond 2^62 gets -1.
+ * Costs in (0, 1] (scaled rows) give weights in [1, alpha].  Asynchronous. */
+RIG_API int rig_int_weights(const double *w, int64_t n, int64_t alpha, int64_t *wgt, rig_stream_t stream);
+
 /* ---- end-to-end from host memory --------------------------------------- */
 
 /* Host-to-host convenience for the whole path: copies A (HOST CSR) and part
@@ -222,7 +248,7 @@ RIG_API int rig_build_host(const rig_csr_t *A_host, int scale_rows, double drop_
  * cache (stream-ordered frees). */
 RIG_API int rig_trim(void);
 
-#define RIG_NPASS 12
+#define RIG_NPASS 13
 RIG_API int rig_profile_enable(int on);
 RIG_API int rig_profile_read(double *ms, int64_t *count);
 RIG_API const char *rig_pass_name(int pass);

@@ -124,6 +124,16 @@ size_t bins_count_elems(int64_t nloc);
 void launch_bins(const uint8_t *bin8, int64_t rb, int64_t nloc, unsigned *cnt, int64_t *off, void *scan_tmp,
                  int32_t *lists, int64_t cap, int64_t *counts, cudaStream_t s);
 
+// k_sparsify.cu (f1): dense-column cutoffs on the CSC of A_hat (columns with
+// cnt > T; list: int[ncols], count zeroed), the A~ row filter (pass 0: nk[i]
+// kept per row; pass 1: write at rp2), and exact integer weights.
+void launch_sparsify_cutoffs(const unsigned *cnt, int64_t m, int64_t T, const Csc &Tc, int32_t *list, int *count,
+                             unsigned long long *ckey, int32_t *crow, cudaStream_t s);
+void launch_sparsify_filter(int pass, const Csr &A, const unsigned *cnt, int64_t T, const unsigned long long *ckey,
+                            const int32_t *crow, int64_t *nk, const int64_t *rp2, int32_t *ci2, double *v2,
+                            cudaStream_t s);
+void launch_int_weights(const double *w, int64_t n, int64_t alpha, int64_t *wgt, cudaStream_t s);
+
 // k_scan.cu: out[0..n] = exclusive prefix of in[0..n-1] (out[n] = total).
 enum class ScanOp { Identity, UbOffDiag };
 void scan_i64(const int64_t *in, int64_t n, int64_t *out, ScanOp op, void *tmp, size_t tmp_bytes,

@@ -60,10 +60,12 @@ enum Pass {
     P_CUTSIZE,   // a7 (standalone kernel or fused final reduction)
     P_SPLIT,
     P_KERNEL,  // the dominant numeric kernel alone (merge kernel, or the mid-row kernel)
+    P_SPARSIFY,  // f1: dense-column cutoffs, A~ filter, transpose of A~
 };
 static const char *kPassNames[RIG_NPASS] = {"validate", "colptr",   "scale_scatter", "colsort",
                                             "analyze",  "symbolic", "ub_scan",       "numeric",
-                                            "compact",  "cutsize",  "split",         "numeric_kernel"};
+                                            "compact",  "cutsize",  "split",         "numeric_kernel",
+                                            "sparsify"};
 static std::mutex g_prof_mu;
 static std::atomic<uint32_t> g_prof_mask{0};
 struct ProfRec {
@@ -284,6 +286,16 @@ static void check_csr(const rig_csr_t *A) {
 
 using namespace rig;
 
+// f1: T = ceil(sqrt(n)), the smallest t with t * t >= n (PAPER.md:572-574,
+// DESIGN.md reading R20)
+static int64_t dense_threshold(int64_t n) {
+    if (n <= 0) return 0;
+    int64_t t = (int64_t)std::sqrt((double)n);
+    while (t * t < n) ++t;
+    while (t > 0 && (t - 1) * (t - 1) >= n) --t;
+    return t;
+}
+
 // ---------------------------------------------------------------- the plan
 struct rig_plan {
     cudaStream_t s;
@@ -329,6 +341,8 @@ static void plan_build(rig_plan *p, const rig_csr_t *Ain, bool allow_early = fal
     const size_t o_bcur = L.add(sizeof(unsigned long long) * (size_t)transpose_buckets(nnz, m));
     const size_t o_gcur = L.add(sizeof(unsigned) * (size_t)m);
     const size_t o_big = L.add(sizeof(int) * (size_t)(1 + transpose_buckets(nnz, m)));
+    const bool sparsify = (p->flags & RIG_FLAG_SPARSIFY) != 0;
+    const size_t o_ndense = sparsify ? L.add(sizeof(int)) : 0;
     const size_t zero_bytes = L.bytes;
     const size_t o_cp = L.add(sizeof(int64_t) * (size_t)(m + 1));
     const size_t o_rec = L.add(kTransposeRecBytes * (size_t)nnz);
@@ -340,6 +354,18 @@ static void plan_build(rig_plan *p, const rig_csr_t *Ain, bool allow_early = fal
     const size_t o_bin8 = L.add((size_t)nloc);
     const bool use_qs = nnz + m <= (int64_t)INT32_MAX;  // run starts fit int32
     const size_t o_qs = use_qs ? L.add(sizeof(int32_t) * (size_t)nnz) : 0;
+    // f1 (RIG_FLAG_SPARSIFY): dense-column list and cutoffs, A~ in CSR
+    size_t o_dlist = 0, o_ckey = 0, o_crow = 0, o_nk = 0, o_rp2 = 0, o_ci2 = 0, o_v2 = 0, o_st3 = 0;
+    if (sparsify) {
+        o_dlist = L.add(sizeof(int32_t) * (size_t)m);
+        o_ckey = L.add(sizeof(unsigned long long) * (size_t)m);
+        o_crow = L.add(sizeof(int32_t) * (size_t)m);
+        o_nk = L.add(sizeof(int64_t) * (size_t)n);
+        o_rp2 = L.add(sizeof(int64_t) * (size_t)(n + 1));
+        o_ci2 = L.add(sizeof(int32_t) * (size_t)nnz);
+        o_v2 = L.add(sizeof(double) * (size_t)nnz);
+        o_st3 = L.add(scan_tmp_bytes(n));
+    }
     unsigned char *ws = p->cached ? ws_get(0, L.bytes, s) : p->arena.raw(L.bytes);
     CK(cudaMemsetAsync(ws, 0, zero_bytes, s));
     p->ctr = reinterpret_cast<DevCounters *>(ws + o_ctr);
@@ -369,7 +395,7 @@ static void plan_build(rig_plan *p, const rig_csr_t *Ain, bool allow_early = fal
     {
         Prof pf(P_COLPTR, s);
         if (nnz > 0) launch_col_hist(A0, cnt, nullptr, s);
-        if (allow_early && nloc > 0) {
+        if (allow_early && nloc > 0 && !sparsify) {
             ev_shape = shape_event();
             scan_u32_shape(cnt, m, cp, ws + o_st1, p->ctr, A0.rp, p->rb, p->re, &hs->shape, ev_shape, s);
         } else {
@@ -386,6 +412,42 @@ static void plan_build(rig_plan *p, const rig_csr_t *Ain, bool allow_early = fal
     check_launch("prep");
     p->A = Csr{n, m, nnz, Ain->row_ptr, Ain->col_idx, p->scale ? ahat : Ain->val};
     p->T = Csc{cp, ri, vt};
+    if (sparsify && nnz > 0) {
+        // f1: A~ from A_hat: cutoffs of the dense columns
+        // on the CSC just built, the CSR filter, then column access to A~
+        // (its values are already scaled: transposed as they are)
+        Prof pf(P_SPARSIFY, s);
+        const int64_t Tn = dense_threshold(n);
+        auto *ckey = reinterpret_cast<unsigned long long *>(ws + o_ckey);
+        auto *crow = reinterpret_cast<int32_t *>(ws + o_crow);
+        auto *nk = reinterpret_cast<int64_t *>(ws + o_nk);
+        auto *rp2 = reinterpret_cast<int64_t *>(ws + o_rp2);
+        auto *ci2 = reinterpret_cast<int32_t *>(ws + o_ci2);
+        auto *v2 = reinterpret_cast<double *>(ws + o_v2);
+        launch_sparsify_cutoffs(cnt, m, Tn, p->T, reinterpret_cast<int32_t *>(ws + o_dlist),
+                                reinterpret_cast<int *>(ws + o_ndense), ckey, crow, s);
+        launch_sparsify_filter(0, p->A, cnt, Tn, ckey, crow, nk, nullptr, nullptr, nullptr, s);
+        scan_i64(nk, n, rp2, ScanOp::Identity, ws + o_st3, 0, s);
+        check_launch("sparsify");
+        int64_t nnz2 = 0;
+        CK(cudaMemcpyAsync(&hs->v[0], rp2 + n, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(&hs->ctr.err, &p->ctr->err, sizeof(int), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        nnz2 = hs->v[0];
+        if (hs->ctr.err) throw Error(err_to_code(hs->ctr.err), err_msg(err_to_code(hs->ctr.err)));
+        if (nnz2 < nnz) {
+            launch_sparsify_filter(1, p->A, cnt, Tn, ckey, crow, nullptr, rp2, ci2, v2, s);
+            CK(cudaMemsetAsync(ws + o_cnt, 0, zero_bytes - o_cnt, s));
+            const Csr A2{n, m, nnz2, rp2, ci2, v2};
+            if (nnz2 > 0) launch_col_hist(A2, cnt, nullptr, s);
+            scan_u32(cnt, m, cp, ws + o_st1, 0, s);
+            launch_transpose(A2, 0, cp, nullptr, reinterpret_cast<unsigned long long *>(ws + o_bcur), ws + o_rec,
+                             reinterpret_cast<unsigned *>(ws + o_gcur), reinterpret_cast<int *>(ws + o_big), ri, vt,
+                             &p->ctr->err, s);
+            check_launch("sparsify transpose");
+            p->A = A2;
+        }
+    }
     // a3 + a4 (merge rows): products, merge-row nnzC, paths of the others
     p->qs = use_qs ? reinterpret_cast<int32_t *>(ws + o_qs) : nullptr;
     SymArgs sa{p->A, p->T, p->rb, p->re, p->nnzc, fnm, p->qs};
@@ -867,6 +929,72 @@ int rig_row_split(const rig_csr_t *A, int32_t parts, int64_t *split, rig_stream_
     check_launch("split");
     CK(cudaMemcpyAsync(split, sp, sizeof(int64_t) * (size_t)(parts + 1), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
+    return RIG_OK;
+    ABI_END
+}
+
+int rig_sparsify(const rig_csr_t *A, int scale_rows, uint32_t flags, rig_csr_t *out, rig_stream_t stream) {
+    ABI_BEGIN
+    if (!out) throw Error(RIG_ERR_INVALID, "out is NULL");
+    std::memset(out, 0, sizeof(*out));
+    cudaStream_t s = (cudaStream_t)stream;
+    rig_plan *p = new_plan(A, scale_rows, 0.0, (flags & RIG_FLAG_VALIDATE) | RIG_FLAG_SPARSIFY, 0, 0, s);
+    p->cached = true;
+    unsigned char *block = nullptr;
+    try {
+        plan_build(p, A);
+        const Csr &At = p->A;
+        Layout L;
+        const size_t o_rp = L.add(sizeof(int64_t) * (size_t)(At.nrows + 1));
+        const size_t o_ci = L.add(sizeof(int32_t) * (size_t)At.nnz);
+        const size_t o_v = L.add(sizeof(double) * (size_t)At.nnz);
+        CK(cudaMallocAsync((void **)&block, L.bytes, s));
+        CK(cudaMemcpyAsync(block + o_rp, At.rp, sizeof(int64_t) * (size_t)(At.nrows + 1), cudaMemcpyDeviceToDevice, s));
+        if (At.nnz > 0) {
+            CK(cudaMemcpyAsync(block + o_ci, At.ci, sizeof(int32_t) * (size_t)At.nnz, cudaMemcpyDeviceToDevice, s));
+            CK(cudaMemcpyAsync(block + o_v, At.v, sizeof(double) * (size_t)At.nnz, cudaMemcpyDeviceToDevice, s));
+        }
+        out->nrows = At.nrows;
+        out->ncols = At.ncols;
+        out->nnz = At.nnz;
+        out->row_ptr = reinterpret_cast<const int64_t *>(block + o_rp);
+        out->col_idx = reinterpret_cast<const int32_t *>(block + o_ci);
+        out->val = reinterpret_cast<const double *>(block + o_v);
+        std::lock_guard<std::mutex> lk(g_own_mu);
+        g_owned[block] = nullptr;
+    } catch (...) {
+        if (block) cudaFreeAsync(block, s);
+        delete p;
+        throw;
+    }
+    delete p;
+    return RIG_OK;
+    ABI_END
+}
+
+int rig_csr_free(rig_csr_t *A, rig_stream_t stream) {
+    ABI_BEGIN
+    if (!A) throw Error(RIG_ERR_INVALID, "NULL argument");
+    if (!A->row_ptr) return RIG_OK;
+    void *key = const_cast<int64_t *>(A->row_ptr);
+    {
+        std::lock_guard<std::mutex> lk(g_own_mu);
+        auto it = g_owned.find(key);
+        if (it == g_owned.end() || it->second != nullptr) throw Error(RIG_ERR_INVALID, "matrix was not allocated by rig_sparsify");
+        g_owned.erase(it);
+    }
+    CK(cudaFreeAsync(key, (cudaStream_t)stream));
+    std::memset(A, 0, sizeof(*A));
+    return RIG_OK;
+    ABI_END
+}
+
+int rig_int_weights(const double *w, int64_t n, int64_t alpha, int64_t *wgt, rig_stream_t stream) {
+    ABI_BEGIN
+    if (n < 0 || (n > 0 && (!w || !wgt))) throw Error(RIG_ERR_INVALID, "NULL argument or n < 0");
+    if (alpha < 1 || alpha > ((int64_t)1 << 53)) throw Error(RIG_ERR_INVALID, "alpha outside [1, 2^53]");
+    launch_int_weights(w, n, alpha, wgt, (cudaStream_t)stream);
+    check_launch("int_weights");
     return RIG_OK;
     ABI_END
 }

@@ -24,6 +24,7 @@ RIG_ERR_NOMEM = -5
 RIG_ERR_CUDA = -6
 RIG_FLAG_VALIDATE = 0x1
 RIG_FLAG_DIAG = 0x2
+RIG_FLAG_SPARSIFY = 0x4
 
 
 class rig_csr_t(ctypes.Structure):
@@ -61,6 +62,9 @@ def _load():
     L.rig_build_host.argtypes = [P, ctypes.c_int, D, U32, P, I32, P, I64, P, P]
     L.rig_partition_ip.argtypes = [P, I64, I64, P, I32, P, P, P, P]
     L.rig_partition_ip_finalize.argtypes = [P, I32, P]
+    L.rig_sparsify.argtypes = [P, ctypes.c_int, U32, P, P]
+    L.rig_csr_free.argtypes = [P, P]
+    L.rig_int_weights.argtypes = [P, I64, I64, P, P]
     L.rig_last_error.restype = ctypes.c_char_p
     L.rig_launch_count.restype = ctypes.c_uint64
     L.rig_version.restype = ctypes.c_char_p
@@ -311,6 +315,37 @@ def rig_partition_ip(g, part: torch.Tensor, K: int, a_row_ptr=None, stream=None)
     under `part`.  Synchronises (reads the result)."""
     acc, W = rig_partition_ip_accumulate(g, part, K, a_row_ptr, stream=stream)
     return rig_partition_ip_finalize(acc, K), W.cpu()
+
+
+def rig_sparsify(A: CSR, scale_rows=1, flags=0, stream=None) -> CSR:
+    """A~ as a torch-owned device CSR
+    (the library's arrays are copied, then released).  Synchronises."""
+    out = rig_csr_t()
+    _check(lib.rig_sparsify(ctypes.byref(A.c()), int(scale_rows), int(flags), ctypes.byref(out), _stream(stream)))
+    try:
+        dev = torch.device("cuda", torch.cuda.current_device())
+
+        def view(ptr, n, ts, dt):
+            return (torch.as_tensor(_Cai(ptr, n, ts, None), device=dev).clone() if n
+                    else torch.empty(0, dtype=dt, device=dev))
+
+        rp = view(out.row_ptr, out.nrows + 1, "<i8", torch.int64)
+        ci = view(out.col_idx, out.nnz, "<i4", torch.int32)
+        v = view(out.val, out.nnz, "<f8", torch.float64)
+    finally:
+        lib.rig_csr_free(ctypes.byref(out), _stream(stream))
+    return CSR(rp, ci, v, ncols=out.ncols if out.ncols else A.ncols, device=dev)
+
+
+def rig_int_weights(w: torch.Tensor, alpha: int, out=None, stream=None) -> torch.Tensor:
+    """wgt = ceil(alpha * w) exactly, device int64; -1 marks
+    an invalid element.  Asynchronous."""
+    w = w.contiguous()
+    if out is None:
+        out = torch.empty(w.numel(), dtype=torch.int64, device=w.device)
+    _check(lib.rig_int_weights(ctypes.c_void_p(w.data_ptr()), int(w.numel()), int(alpha),
+                               ctypes.c_void_p(out.data_ptr()), _stream(stream)))
+    return out
 
 
 def rig_build_host(row_ptr, col_idx, val, ncols, scale_rows, drop_tol, flags, part, K, out_row_ptr, out_col,

@@ -279,15 +279,16 @@ def dense_columns(n, rng, per_row=5, n_dense=4, dense_nnz=None, ncols=None, leve
         keys[:, dcols] = 2.0  # the dense columns come from their own draw
         cols = [np.sort(np.argpartition(keys, per_row - 1, axis=1)[:, :per_row], axis=1).reshape(-1)]
     else:
-        c = rng.integers(0, m, size=(n, per_row * 2))
-        cols_l = []
-        for i in range(n):
-            u = np.unique(c[i][~np.isin(c[i], dcols)])[:per_row]
-            while u.size < per_row:
-                u = np.unique(np.r_[u, rng.integers(0, m, per_row)])
-                u = u[~np.isin(u, dcols)][:per_row]
-            cols_l.append(np.sort(u))
-        cols = [np.concatenate(cols_l)]
+        free = np.delete(np.arange(m, dtype=np.int64), dcols)  # the non-dense columns
+        t = np.sort(rng.integers(0, free.size, size=(n, per_row)), axis=1)
+        while True:
+            dup = np.zeros_like(t, dtype=bool)
+            dup[:, 1:] = t[:, 1:] == t[:, :-1]
+            if not dup.any():
+                break
+            t[dup] = rng.integers(0, free.size, size=int(dup.sum()))
+            t.sort(axis=1)
+        cols = [free[t].reshape(-1)]
     for k in dcols:
         r = np.sort(rng.choice(n, size=dense_nnz, replace=False))
         rows.append(r)

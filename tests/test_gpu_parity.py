@@ -336,3 +336,119 @@ def test_partition_ip_matrix(rig, cfg):
     acc2, _ = rig.rig_partition_ip_accumulate(g, torch.full_like(part, K), K)
     with pytest.raises(rig.RigError):
         rig.rig_partition_ip_finalize(acc2, K)
+
+
+# ---------------------------------------------------------------- f1
+def _oracle_sparsified(rp, ci, v, ncols, scale_rows):
+    """Oracle pipeline of PAPER.md:572-579: [scale] -> A~ -> graph of A~ A~^T
+    (A~ keeps the scaled values, reading R21)."""
+    a = oracle.scale(rp, v)[0] if scale_rows else np.asarray(v, dtype=np.float64)
+    return oracle.sparsify(rp, ci, a, ncols=ncols)
+
+
+def _f1_cases():
+    from rig_inputs import dense_columns
+    cases = []
+    for seed, (n, per, nd, dn, lv, sc) in enumerate([
+            (3000, 5, 4, 700, 0, 1),     # scaled, distinct magnitudes
+            (2500, 4, 3, 900, 2, 0),     # unscaled, many |value| ties
+            (1200, 3, 2, 1100, 1, 0),    # all |values| equal: ties span many chunks
+            (5000, 6, 8, 60, 0, 1),      # dense columns just above T = 71? (no: 60 < 71) -> identity
+            (4099, 5, 5, 2000, 0, 1)]):  # ragged sizes
+        rng = np.random.default_rng(900 + seed)
+        rp, ci, v = dense_columns(n, rng, per_row=per, n_dense=nd, dense_nnz=dn, levels=lv)
+        cases.append((f"dense{seed}", n, rp, ci, v, sc))
+    # the paper's 25 x 25 example (PAPER.md:567-577)
+    D = np.eye(25)
+    for r in range(25):
+        if r not in (2, 19):
+            D[r, 11] = 1.0 + r / 7.0
+    rp, ci, v = from_dense(D)
+    cases.append(("paper25", 25, rp, ci, v, 1))
+    w = make_small(2)
+    cases.append(("stencil", w.n, w.row_ptr, w.col_idx, w.val, 1))
+    return cases
+
+
+@pytest.mark.parametrize("case", _f1_cases(), ids=lambda c: c[0])
+def test_sparsify_bitexact(rig, case):
+    name, n, rp, ci, v, sc = case
+    trp, tci, tv = _oracle_sparsified(rp, ci, v, n, sc)
+    A = rig.CSR(rp, ci, v, ncols=n)
+    At = rig.rig_sparsify(A, sc)
+    np.testing.assert_array_equal(to_np(At.row_ptr), trp)
+    np.testing.assert_array_equal(to_np(At.col_idx), tci)
+    assert to_np(At.val).tobytes() == tv.tobytes()
+
+
+@pytest.mark.parametrize("case", _f1_cases(), ids=lambda c: c[0])
+def test_sparsified_graph_bitexact(rig, case):
+    """G~_RIP (RIG_FLAG_SPARSIFY) == oracle graph of A~ A~^T; shards and the
+    staged API agree."""
+    name, n, rp, ci, v, sc = case
+    trp, tci, tv = _oracle_sparsified(rp, ci, v, n, sc)
+    orc = oracle.build(trp, tci, tv, ncols=n, scale_rows=0, drop_tol=0.0)
+    A = rig.CSR(rp, ci, v, ncols=n)
+    flags = rig.RIG_FLAG_DIAG | rig.RIG_FLAG_SPARSIFY
+    g = rig.rig_build(A, sc, 0.0, flags)
+    assert g.nnz == orc.nnz
+    assert_graph_equal(to_np(g.row_ptr), to_np(g.col_idx), to_np(g.w), orc, to_np(g.diag))
+    plan = rig.Plan(A, sc, 0.0, flags)
+    tg = plan.execute()
+    assert_graph_equal(to_np(tg.row_ptr), to_np(tg.col_idx), to_np(tg.w), orc, to_np(tg.diag))
+    plan.destroy()
+    split = rig.rig_row_split(A, 3)
+    cols, ws = [], []
+    for a, b in zip(split[:-1], split[1:]):
+        s = rig.rig_build_rows(A, a, b, sc, 0.0, flags)
+        cols.append(to_np(s.col_idx))
+        ws.append(to_np(s.w))
+    np.testing.assert_array_equal(np.concatenate(cols), orc.col)
+    assert np.concatenate(ws).tobytes() == orc.w.tobytes()
+
+
+def test_sparsify_large_bitexact(rig):
+    """Full-size f1 case: n = 1M rows, 8 dense columns of 60k rows (T = 1000),
+    A~ and the graph of A~ A~^T bit-exact."""
+    from rig_inputs import dense_columns
+    n = 1_000_000
+    rp, ci, v = dense_columns(n, np.random.default_rng(77), per_row=5, n_dense=8, dense_nnz=60_000)
+    trp, tci, tv = _oracle_sparsified(rp, ci, v, n, 1)
+    A = rig.CSR(rp, ci, v, ncols=n)
+    At = rig.rig_sparsify(A, 1)
+    np.testing.assert_array_equal(to_np(At.row_ptr), trp)
+    np.testing.assert_array_equal(to_np(At.col_idx), tci)
+    assert to_np(At.val).tobytes() == tv.tobytes()
+    orc = oracle.build(trp, tci, tv, ncols=n, scale_rows=0)
+    g = rig.rig_build(A, 1, 0.0, rig.RIG_FLAG_SPARSIFY)
+    np.testing.assert_array_equal(to_np(g.row_ptr), orc.row_ptr)
+    np.testing.assert_array_equal(to_np(g.col_idx), orc.col)
+    assert to_np(g.w).tobytes() == orc.w.tobytes()
+
+
+@pytest.mark.parametrize("cfg", [1, 2, 3, 4, 5])
+def test_int_weights_exact(rig, cfg):
+    """wgt = ceil(alpha * w) equals the oracle's exact integer
+    computation for every edge; scaled configs land in [1, alpha]."""
+    w = make_small(cfg)
+    orc = oracle.build(w.row_ptr, w.col_idx, w.val, scale_rows=w.scale_rows, drop_tol=w.drop_tol)
+    A = rig.CSR(w.row_ptr, w.col_idx, w.val)
+    g = rig.rig_build(A, w.scale_rows, w.drop_tol)
+    for alpha in (1, 10_000, 2 ** 31 - 1, 2 ** 53):
+        got = to_np(rig.rig_int_weights(g.w, alpha))
+        np.testing.assert_array_equal(got, oracle.int_weights(orc.w, alpha))
+        if w.scale_rows and got.size:
+            assert got.min() >= 1 and got.max() <= alpha
+
+
+def test_int_weights_edge_values(rig):
+    rng = np.random.default_rng(3)
+    x = np.r_[rng.random(5000), rng.random(500) * 1e-12, 0.1, 0.3, 0.7, 1.0, 0.5, 2.0 ** -60, 5e-324, 0.0,
+              np.nextafter(1.0, 0.0), np.nextafter(0.1, 1.0), 3.0, 300.0]
+    xt = torch.as_tensor(x, device="cuda")
+    for alpha in (1, 3, 10_000, 2 ** 31 - 1, 2 ** 53):
+        np.testing.assert_array_equal(to_np(rig.rig_int_weights(xt, alpha)), oracle.int_weights(x, alpha))
+    bad = torch.tensor([-0.5, float("inf"), float("nan"), 1e300], dtype=torch.float64, device="cuda")
+    assert to_np(rig.rig_int_weights(bad, 10)).tolist() == [-1, -1, -1, -1]
+    with pytest.raises(rig.RigError):
+        rig.rig_int_weights(xt, 0)
