@@ -41,7 +41,7 @@ struct Csr {
 // [cp[k] + k, cp[k+1] + k) (rows ascending) and ri[cp[k+1] + k] = INT_MAX.
 struct Csc {
     const int64_t *cp;  // [ncols+1] entry counts prefix (without sentinels)
-    const int32_t *ri;  // [nnz + ncols]
+    const int32_t *ri;  // [nnz + ncols], ri[-1] and vt[-1] readable (see plan_build)
     const double *vt;   // [nnz + ncols] bit-identical to the CSR value of (i,k)
 };
 __device__ __forceinline__ int64_t csc_begin(const Csc &T, int k) { return T.cp[k] + k; }
@@ -153,8 +153,9 @@ struct SymArgs {
     int64_t rb, re;
     int64_t *nnzc;  // [re-rb] merge rows: structural nnz(C_i) incl. the diagonal
     int64_t *fnm;   // [re-rb] rows off the merge path: f_i - len_i (temporary slots), else 0
-    int32_t *qs;    // [nnz] or null: per A entry of a merge row its CSC run start csc_begin(k);
-                    // -1 at the first entry of a row of <= kMergeMaxLen entries off the merge path
+    int2 *qs;       // [nnz] or null: per A entry of a merge row its CSC run (start csc_begin(k),
+                    // length nnz(col k)); x = -1 at the first entry of a row of <= kMergeMaxLen
+                    // entries off the merge path
 };
 struct NumArgs {
     Csr A;
@@ -175,7 +176,7 @@ struct NumArgs {
     int *bad_part;
     int *cut_used;  // this launch's number of written partials (= gridDim.x)
     int stage_cap;  // merge path: staged graph entries per warp (set by the launcher)
-    const int32_t *qs;  // SymArgs::qs (null: run starts gathered from the col_ptr)
+    const int2 *qs;  // SymArgs::qs (null: run starts gathered from the col_ptr)
 };
 
 // Neumaier-compensated running sum (compiled with --fmad=false).
@@ -220,6 +221,16 @@ inline int stage_cap_for(int64_t products, int64_t rows) {
     int64_t cap = (int64_t)(0.6 * 32.0 * mean) + 32;
     cap = (cap + 31) / 32 * 32;
     if (cap < kMinStageCap) cap = kMinStageCap;
+    if (cap > kMaxStageCap) cap = kMaxStageCap;
+    return (int)cap;
+}
+
+// Pair kernel output stage: 16-row tiles, same estimate as stage_cap_for().
+inline int pair_stage_cap_for(int64_t products, int64_t rows) {
+    const double mean = rows > 0 ? (double)products / (double)rows : 0.0;
+    int64_t cap = (int64_t)(0.6 * 16.0 * mean) + 32;
+    cap = (cap + 31) / 32 * 32;
+    if (cap < 128) cap = 128;
     if (cap > kMaxStageCap) cap = kMaxStageCap;
     return (int)cap;
 }

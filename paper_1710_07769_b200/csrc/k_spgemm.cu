@@ -14,6 +14,8 @@
 //    ascending k; the dense accumulator's bitmap yields j-sorted output.
 #include "common.cuh"
 
+#include <algorithm>
+
 namespace rig {
 
 static int g_sms_cache = 0;
@@ -25,21 +27,23 @@ static int g_sms_cache = 0;
 // IdxT: int32 CSC offsets when nnz < 2^31 (fewer registers), else int64.
 // Columns end in an INT_MAX sentinel (csc_begin), so a run needs no end bound.
 template <int R, typename IdxT>
-__device__ __forceinline__ int64_t sym_merge_row(const Csr &A, const Csc &T, int64_t s, int32_t *qs = nullptr) {
+__device__ __forceinline__ int64_t sym_merge_row(const Csr &A, const Csc &T, int64_t s, int2 *qs = nullptr) {
     int32_t h[R];
     IdxT q[R];
     int64_t f = 0;
+    int32_t cl[R];
 #pragma unroll
     for (int t = 0; t < R; ++t) {
         const int k = A.ci[s + t];
         const int64_t c0 = T.cp[k], c1 = T.cp[k + 1];
         q[t] = (IdxT)(c0 + k);
+        cl[t] = (int32_t)min(c1 - c0, (int64_t)INT32_MAX);
         f += c1 - c0;
     }
     if (f > kMergeMaxF) return -1;
-    if (qs) {  // run starts for the numeric pass (saves it the col_ptr gathers)
+    if (qs) {  // runs for the numeric pass (saves it the col_ptr gathers)
 #pragma unroll
-        for (int t = 0; t < R; ++t) qs[s + t] = (int32_t)q[t];
+        for (int t = 0; t < R; ++t) qs[s + t] = make_int2((int32_t)q[t], cl[t]);
     }
 #pragma unroll
     for (int t = 0; t < R; ++t) h[t] = T.ri[q[t]];
@@ -70,7 +74,7 @@ __device__ __forceinline__ void num_merge_row(const NumArgs &a, int64_t i, int64
     if (a.qs) {  // run starts from the analysis (int32 offsets only)
 #pragma unroll
         for (int t = 0; t < R; ++t) {
-            q[t] = (IdxT)a.qs[s + t];
+            q[t] = (IdxT)a.qs[s + t].x;
             av[t] = a.A.v[s + t];
         }
         if ((int64_t)q[0] < 0) return;  // not a merge row
@@ -236,6 +240,243 @@ __global__ void __launch_bounds__(kMergeThreads) k_num_merge(NumArgs a) {
     }
 }
 
+// ======================================================== pair kernel
+// The merge path with two lanes per row.  A warp takes 16 consecutive rows:
+// lane q (< 16) merges row q's keys j < i ascending from the run starts, lane
+// q + 16 its keys j >= i descending from the run ends.  Every run of row i
+// (column k with a_ik != 0) contains i itself, so the ascending lane stops
+// when its minimum reaches i and the descending lane stops after processing
+// i (the diagonal): no split positions are needed, and each lane walks about
+// half of the row.  For every key the runs holding it are folded in ascending
+// k whichever direction the keys are visited in, so each c_ij is exactly the
+// R4 chain.  Both lanes run one instruction stream (no divergence): the
+// descending lane sees each key as key ^ ~0 (order reversed) and takes the
+// minimum like the ascending one.  Runs come from the analysis (qs: start,
+// length).  Output goes through a per-warp shared-memory stage (swizzled) and
+// is streamed out coalesced; the descending lane fills its row from the end.
+constexpr int kPairThreads = 128;
+constexpr int kPairWarps = kPairThreads / 32;
+constexpr int kPairRows = 16;
+
+__device__ __forceinline__ unsigned smem_u32(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ int lds_s32(unsigned a) {
+    int v;
+    asm volatile("ld.shared.s32 %0, [%1];\n" : "=r"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ double lds_f64(unsigned a) {
+    double v;
+    asm volatile("ld.shared.f64 %0, [%1];\n" : "=d"(v) : "r"(a));
+    return v;
+}
+__device__ __forceinline__ void sts_s32(unsigned a, int v) { asm volatile("st.shared.s32 [%0], %1;\n" ::"r"(a), "r"(v)); }
+__device__ __forceinline__ void sts_f64(unsigned a, double v) { asm volatile("st.shared.f64 [%0], %1;\n" ::"r"(a), "d"(v)); }
+
+// Output stage index swizzle: entry e of the tile goes to e ^ ((e >> 5) & 31),
+// a permutation inside each aligned block of 32 entries.  Rows of equal
+// length would otherwise put every lane's n-th entry in the same few banks;
+// the flush reads aligned blocks of 32, conflict-free either way.
+__device__ __forceinline__ unsigned out_swz(unsigned e) { return e ^ ((e >> 5) & 31u); }
+
+template <int N>
+__device__ __forceinline__ int tree_min(const int (&h)[N]) {
+    int v[N];
+#pragma unroll
+    for (int t = 0; t < N; ++t) v[t] = h[t];
+#pragma unroll
+    for (int w = 1; w < N; w <<= 1) {
+#pragma unroll
+        for (int t = 0; t + w < N; t += 2 * w) v[t] = min(v[t], v[t + w]);
+    }
+    return v[0];
+}
+
+// One half row.  q0[t]: CSC position of run t's first (ascending) or last
+// (descending) entry, or -1 for an empty run (t >= len).  Kept entries go to
+// the swizzled output stage at tile index ob, ob +- 1, ...  Returns the count.
+template <int R>
+__device__ __forceinline__ int pair_half_row(const NumArgs &a, bool desc, int64_t i, int64_t r, const int *q0,
+                                             const double *av0, unsigned oc0, unsigned ow0, unsigned ob, Comp &cut,
+                                             int32_t pi, int &badp) {
+    int h[R], q[R];
+    double av[R], hv[R];
+    const int xm = desc ? -1 : 0;
+    const int step = desc ? -1 : 1;
+#pragma unroll
+    for (int t = 0; t < R; ++t) {
+        q[t] = q0[t];
+        av[t] = av0[t];
+        h[t] = INT_MAX;
+        hv[t] = 0.0;
+        if (q[t] >= 0) {
+            h[t] = a.T.ri[q[t]] ^ xm;
+            hv[t] = a.T.vt[q[t]];
+        }
+    }
+    const int ik = (int)i ^ xm;
+    unsigned oe = ob;
+    const unsigned ostep = desc ? 0xffffffffu : 1u;
+    int o = 0;
+    int32_t pend_pj = pi;
+    double pend_w = 0.0;
+    while (true) {
+        const int m = tree_min<R>(h);
+        if (m == ik && !desc) break;  // every run holds i: no key < i is left
+        double acc = +0.0;
+#pragma unroll
+        for (int t = 0; t < R; ++t) {
+            if (h[t] == m) {  // runs visited in ascending k: the ordered chain
+                acc = __fma_rn(av[t], hv[t], acc);
+                q[t] += step;  // ascending lanes stop at i, descending ones
+                               // at i too: a run is never left
+                h[t] = a.T.ri[q[t]] ^ xm;
+                hv[t] = a.T.vt[q[t]];
+            }
+        }
+        if (m == ik) {  // descending lane: the diagonal comes last
+            if (a.diag) a.diag[r] = acc;
+            break;
+        }
+        const double w = fabs(acc);
+        if (w > a.tol) {
+            const int j = m ^ xm;
+            const unsigned e = out_swz(oe);
+            sts_s32(oc0 + 4 * e, j);
+            sts_f64(ow0 + 8 * e, w);
+            oe += ostep;
+            ++o;
+            if (desc && a.part) {  // j > i: each undirected edge counted once
+                badp |= (pend_pj < 0) | (pend_pj >= a.K);
+                if (pend_pj != pi) cut.add(pend_w);
+                pend_pj = a.part[j];
+                pend_w = w;
+            }
+        }
+    }
+    if (desc && a.part) {
+        badp |= (pend_pj < 0) | (pend_pj >= a.K);
+        if (pend_pj != pi) cut.add(pend_w);
+    }
+    return o;
+}
+
+template <int RMAX>
+__device__ __forceinline__ int pair_half_row_r(int len, const NumArgs &a, bool desc, int64_t i, int64_t r,
+                                               const int *q0, const double *av0, unsigned oc0, unsigned ow0,
+                                               unsigned ob, Comp &cut, int32_t pi, int &badp) {
+    if (len <= 2) return pair_half_row<2>(a, desc, i, r, q0, av0, oc0, ow0, ob, cut, pi, badp);
+    if (RMAX > 4 && len <= 4) return pair_half_row<4>(a, desc, i, r, q0, av0, oc0, ow0, ob, cut, pi, badp);
+    return pair_half_row<RMAX>(a, desc, i, r, q0, av0, oc0, ow0, ob, cut, pi, badp);
+}
+
+// Rows whose output does not fit the stage are merged by num_merge_row with
+// direct global stores (the ascending lane; its partner idles).
+template <int RMAX>
+__global__ void __launch_bounds__(kPairThreads) k_num_pair(NumArgs a) {
+    extern __shared__ __align__(16) unsigned char pair_smem[];
+    const int cap = a.stage_cap;
+    const int w = threadIdx.x >> 5, l = lane_id();
+    const int qr = l & (kPairRows - 1);
+    const bool desc = l >= kPairRows;
+    double *st_wp = reinterpret_cast<double *>(pair_smem) + (size_t)w * cap;
+    int32_t *st_cp = reinterpret_cast<int32_t *>(reinterpret_cast<double *>(pair_smem) + (size_t)kPairWarps * cap) +
+                     (size_t)w * cap;
+    const unsigned oc0 = smem_u32(st_cp), ow0 = smem_u32(st_wp);
+    const int64_t nloc = a.re - a.rb;
+    const int64_t ntiles = (nloc + kPairRows - 1) / kPairRows;
+    Comp cut;
+    int badp = 0;
+    for (int64_t tile = (int64_t)blockIdx.x * kPairWarps + w; tile < ntiles; tile += (int64_t)gridDim.x * kPairWarps) {
+        const int64_t r0 = tile * kPairRows;
+        const int rows = (int)min((int64_t)kPairRows, nloc - r0);
+        const int64_t r = r0 + qr;
+        const int64_t g0 = a.gptr[r0];
+        const int64_t span_out = a.gptr[r0 + rows] - g0;
+        const bool staged = span_out <= cap;
+        const int64_t i = a.rb + r;
+        int64_t s = 0, gr = 0, ub = 0;
+        int len = 0;
+        bool mrow = false;
+        int32_t pi = 0;
+        if (qr < rows) {
+            s = a.A.rp[i];
+            len = (int)min(a.A.rp[i + 1] - s, (int64_t)kMergeMaxLen + 1);
+            gr = a.gptr[r];
+            ub = a.gptr[r + 1] - gr;
+            if (len >= 1 && len <= RMAX) mrow = a.qs[s].x >= 0;
+            if (a.part) {
+                pi = a.part[i];
+                badp |= (pi < 0) | (pi >= a.K);
+            }
+        }
+        int o = 0;
+        if (mrow && staged) {
+            int qv[RMAX];
+            double av[RMAX];
+#pragma unroll
+            for (int t = 0; t < RMAX; ++t) {
+                qv[t] = -1;
+                av[t] = 0.0;
+                if (t < len) {
+                    const int2 run = a.qs[s + t];
+                    qv[t] = desc ? run.x + run.y - 1 : run.x;
+                    av[t] = a.A.v[s + t];
+                }
+            }
+            const unsigned ob = (unsigned)(gr - g0) + (desc ? (unsigned)(ub - 1) : 0u);
+            o = pair_half_row_r<RMAX>(len, a, desc, i, r, qv, av, oc0, ow0, ob, cut, pi, badp);
+        } else if (mrow && !desc) {  // output beyond the stage: direct global stores
+            int32_t *oc = a.gcol + gr;
+            double *ow = a.gw + gr;
+            switch (len) {
+                case 1: num_merge_row<1, int32_t>(a, i, r, s, oc, ow, ub, cut, pi, badp); break;
+                case 2: num_merge_row<2, int32_t>(a, i, r, s, oc, ow, ub, cut, pi, badp); break;
+                case 3: num_merge_row<3, int32_t>(a, i, r, s, oc, ow, ub, cut, pi, badp); break;
+                case 4: num_merge_row<4, int32_t>(a, i, r, s, oc, ow, ub, cut, pi, badp); break;
+                case 5: if constexpr (RMAX >= 5) num_merge_row<5, int32_t>(a, i, r, s, oc, ow, ub, cut, pi, badp); break;
+                case 6: if constexpr (RMAX >= 6) num_merge_row<6, int32_t>(a, i, r, s, oc, ow, ub, cut, pi, badp); break;
+                case 7: if constexpr (RMAX >= 7) num_merge_row<7, int32_t>(a, i, r, s, oc, ow, ub, cut, pi, badp); break;
+                case 8: if constexpr (RMAX >= 8) num_merge_row<8, int32_t>(a, i, r, s, oc, ow, ub, cut, pi, badp); break;
+                default: break;
+            }
+        } else if (qr < rows && len == 0 && !desc) {
+            if (a.diag) a.diag[r] = 0.0;
+        }
+        if (!staged) continue;
+        // dropped entries (|c| <= tol or exact zero): the descending half moves
+        // down behind the ascending half; the tail becomes holes
+        const int o_asc = __shfl_sync(kFull, o, qr);
+        if (desc && mrow && o_asc + o < ub) {
+            const unsigned base = (unsigned)(gr - g0);
+            for (int t = 0; t < o; ++t) {
+                const unsigned src = out_swz(base + (unsigned)(ub - o + t));
+                const unsigned dst = out_swz(base + (unsigned)(o_asc + t));
+                sts_s32(oc0 + 4 * dst, lds_s32(oc0 + 4 * src));
+                sts_f64(ow0 + 8 * dst, lds_f64(ow0 + 8 * src));
+            }
+            for (int64_t t = o_asc + o; t < ub; ++t) sts_s32(oc0 + 4 * out_swz(base + (unsigned)t), -1);
+            atomicOr(a.holes, 1);
+        }
+        __syncwarp();
+        // slots of rows off the merge path are garbage here: k_copy_rows
+        // places those rows afterwards
+        for (int64_t t = l; t < span_out; t += 32) {
+            const unsigned e = out_swz((unsigned)t);
+            a.gcol[g0 + t] = lds_s32(oc0 + 4 * e);
+            a.gw[g0 + t] = lds_f64(ow0 + 8 * e);
+        }
+        __syncwarp();  // the stage is reused by the next tile
+    }
+    if (a.part) {  // fused a7: per-CTA partial of the cut
+        const double v = block_tree_sum<kPairThreads>(cut.value());
+        if (threadIdx.x == 0) {
+            a.cutp[blockIdx.x] = v;
+            if (blockIdx.x == 0) *a.cut_used = (int)gridDim.x;
+        }
+        if (__syncthreads_or(badp) && threadIdx.x == 0) atomicOr(a.bad_part, 1);
+    }
+}
+
 static int sms() {
     if (!g_sms_cache) g_sms_cache = num_sms();
     return g_sms_cache;
@@ -316,7 +557,7 @@ __global__ void __launch_bounds__(kMergeThreads) k_analyze_sym(SymArgs a, uint8_
             if (lg < kSymBinMinLog) lg = kSymBinMinLog;
             const int b = lg > kSymBinMaxLog ? kNumSymBins : lg - kSymBinMinLog;
             bin8[r] = (uint8_t)b;
-            if (a.qs && e - s <= kMergeMaxLen) a.qs[s] = -1;  // the merge kernel skips it
+            if (a.qs && e - s <= kMergeMaxLen) a.qs[s] = make_int2(-1, 0);  // the merge kernel skips it
             a.fnm[r] = fi - (e - s);  // >= its off-diagonal entries: temporary slots
             slots += fi - (e - s);
             maxf = max(maxf, fi);
@@ -426,7 +667,38 @@ void launch_sym_merge(const SymArgs &a, int maxlen, cudaStream_t s) {
         launch_merge_r<int64_t>(maxlen, &a, nullptr, s);
 }
 
+template <int RMAX>
+static void launch_pair_t(const NumArgs &na, cudaStream_t s) {
+    const size_t smem = (size_t)kPairWarps * (size_t)na.stage_cap * (sizeof(double) + sizeof(int32_t));
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_num_pair<RMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)((size_t)kPairWarps * kMaxStageCap * (sizeof(double) + sizeof(int32_t))));
+        attr = true;
+    }
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_num_pair<RMAX>, kPairThreads, smem);
+    if (per_sm < 1) per_sm = 1;
+    const int64_t nloc = na.re - na.rb;
+    const int64_t ntiles = (nloc + kPairRows - 1) / kPairRows;
+    int64_t g = (ntiles + kPairWarps - 1) / kPairWarps;
+    const int64_t gmax = std::min<int64_t>((int64_t)sms() * per_sm, kCutSlotsPerLaunch);
+    g = g < 1 ? 1 : (g > gmax ? gmax : g);
+    k_num_pair<RMAX><<<(unsigned)g, kPairThreads, smem, s>>>(na);
+    note_launch();
+}
+
 void launch_num_merge(const NumArgs &a, int maxlen, cudaStream_t s) {
+    if (a.qs) {  // int32 CSC offsets and runs from the analysis
+        switch (maxlen <= 4 ? 4 : maxlen) {
+            case 4: launch_pair_t<4>(a, s); break;
+            case 5: launch_pair_t<5>(a, s); break;
+            case 6: launch_pair_t<6>(a, s); break;
+            case 7: launch_pair_t<7>(a, s); break;
+            default: launch_pair_t<8>(a, s); break;
+        }
+        return;
+    }
     if (a.A.nnz <= INT32_MAX)
         launch_merge_r<int32_t>(maxlen, nullptr, &a, s);
     else

@@ -309,7 +309,7 @@ struct rig_plan {
     DevCounters *ctr = nullptr;  // device
     DevCounters h{};             // host copy (after sync 1)
     int64_t *nnzc = nullptr;     // [nloc] merge rows: structural nnz(C_i); others: kept + 1 (numeric)
-    int32_t *qs = nullptr;       // merge rows' CSC run starts (SymArgs::qs)
+    int2 *qs = nullptr;          // merge rows' CSC runs (SymArgs::qs)
     // rows off the merge path (h.n_mid > 0): exact rows in the temporary
     int32_t *lists = nullptr;    // [2 * n_mid]: mid rows, huge rows (ascending)
     int32_t *defer = nullptr;    // [2 * n_mid]: deferred by the small / big mid kernel
@@ -347,13 +347,15 @@ static void plan_build(rig_plan *p, const rig_csr_t *Ain, bool allow_early = fal
     const size_t o_cp = L.add(sizeof(int64_t) * (size_t)(m + 1));
     const size_t o_rec = L.add(kTransposeRecBytes * (size_t)nnz);
     const size_t o_ahat = p->scale ? L.add(sizeof(double) * (size_t)nnz) : 0;
-    const size_t o_ri = L.add(sizeof(int32_t) * (size_t)(nnz + m));  // + one sentinel per column
-    const size_t o_vt = L.add(sizeof(double) * (size_t)(nnz + m));
+    // + one sentinel per column, + one leading pad entry: a descending merge
+    // lane's last advance may read the entry before its run (never used)
+    const size_t o_ri = L.add(sizeof(int32_t) * (size_t)(nnz + m + 2));
+    const size_t o_vt = L.add(sizeof(double) * (size_t)(nnz + m + 1));
     const size_t o_nnzc = L.add(sizeof(int64_t) * (size_t)nloc);
     const size_t o_fnm = L.add(sizeof(int64_t) * (size_t)nloc);
     const size_t o_bin8 = L.add((size_t)nloc);
     const bool use_qs = nnz + m <= (int64_t)INT32_MAX;  // run starts fit int32
-    const size_t o_qs = use_qs ? L.add(sizeof(int32_t) * (size_t)nnz) : 0;
+    const size_t o_qs = use_qs ? L.add(sizeof(int2) * (size_t)nnz) : 0;
     // f1 (RIG_FLAG_SPARSIFY): dense-column list and cutoffs, A~ in CSR
     size_t o_dlist = 0, o_ckey = 0, o_crow = 0, o_nk = 0, o_rp2 = 0, o_ci2 = 0, o_v2 = 0, o_st3 = 0;
     if (sparsify) {
@@ -372,8 +374,8 @@ static void plan_build(rig_plan *p, const rig_csr_t *Ain, bool allow_early = fal
     unsigned *cnt = reinterpret_cast<unsigned *>(ws + o_cnt);
     int64_t *cp = reinterpret_cast<int64_t *>(ws + o_cp);
     double *ahat = p->scale ? reinterpret_cast<double *>(ws + o_ahat) : nullptr;
-    int32_t *ri = reinterpret_cast<int32_t *>(ws + o_ri);
-    double *vt = reinterpret_cast<double *>(ws + o_vt);
+    int32_t *ri = reinterpret_cast<int32_t *>(ws + o_ri) + 1;
+    double *vt = reinterpret_cast<double *>(ws + o_vt) + 1;
     p->nnzc = reinterpret_cast<int64_t *>(ws + o_nnzc);
     int64_t *fnm = reinterpret_cast<int64_t *>(ws + o_fnm);
     uint8_t *bin8 = reinterpret_cast<uint8_t *>(ws + o_bin8);
@@ -449,7 +451,7 @@ static void plan_build(rig_plan *p, const rig_csr_t *Ain, bool allow_early = fal
         }
     }
     // a3 + a4 (merge rows): products, merge-row nnzC, paths of the others
-    p->qs = use_qs ? reinterpret_cast<int32_t *>(ws + o_qs) : nullptr;
+    p->qs = use_qs ? reinterpret_cast<int2 *>(ws + o_qs) : nullptr;
     SymArgs sa{p->A, p->T, p->rb, p->re, p->nnzc, fnm, p->qs};
     if (nloc > 0) {
         Prof pf(P_ANALYZE, s);
@@ -587,7 +589,7 @@ static int64_t plan_numeric(rig_plan *p, int32_t *gcol, double *gw, double *diag
                    cutp,
                    badp,
                    used,
-                   stage_cap_for(p->h.products, p->nloc),
+                   p->qs ? pair_stage_cap_for(p->h.products, p->nloc) : stage_cap_for(p->h.products, p->nloc),
                    p->qs};
         check_launch("graph row pointers");
         if (p->nloc > 0) {

@@ -172,10 +172,15 @@ def test_empty_and_errors(rig):
     with pytest.raises(rig.RigError) as e:
         rig.rig_build(A, 1, 0.0)
     assert e.value.code == rig.RIG_ERR_ZERO_ROW
-    A = rig.CSR(np.array([0, 2, 3]), np.array([0, 1, 2], np.int32), np.array([1.0, np.inf, 3.0]))
+    # 2 x 3: column 2 is in range (ncols given; unvalidated out-of-range columns are undefined)
+    A = rig.CSR(np.array([0, 2, 3]), np.array([0, 1, 2], np.int32), np.array([1.0, np.inf, 3.0]), ncols=3)
     with pytest.raises(rig.RigError) as e:
         rig.rig_build(A, 1, 0.0)
     assert e.value.code == rig.RIG_ERR_NONFINITE
+    # a rectangular A with finite values: C = A A^T is 2 x 2 with no off-diagonal entry
+    A = rig.CSR(np.array([0, 2, 3]), np.array([0, 1, 2], np.int32), np.array([1.0, 2.0, 3.0]), ncols=3)
+    g = rig.rig_build(A, 1, 0.0)
+    assert g.n == 2 and g.nnz == 0
     A = rig.CSR(np.array([0, 2, 3]), np.array([1, 0, 2], np.int32), np.array([1.0, 2.0, 3.0]))
     with pytest.raises(rig.RigError) as e:
         rig.rig_build(A, 1, 0.0, rig.RIG_FLAG_VALIDATE)
