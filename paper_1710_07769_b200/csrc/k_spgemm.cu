@@ -254,7 +254,19 @@ __global__ void __launch_bounds__(kMergeThreads) k_num_merge(NumArgs a) {
 // minimum like the ascending one.  Runs come from the analysis (qs: start,
 // length).  Output goes through a per-warp shared-memory stage (swizzled) and
 // is streamed out coalesced; the descending lane fills its row from the end.
-constexpr int kPairThreads = 128;
+// RIG_PAIR_THREADS / RIG_PAIR_MINB (experiments, tools/build_variant.sh): CTA
+// size and a register budget fitted to RIG_PAIR_MINB CTAs per SM.  The
+// default leaves registers to ptxas (96 for R = 7): more warps only raised
+// the L1 miss rate of the run gathers, which bound this kernel (measured).
+#ifndef RIG_PAIR_THREADS
+#define RIG_PAIR_THREADS 128
+#endif
+#ifdef RIG_PAIR_MINB
+#define RIG_PAIR_BOUNDS __launch_bounds__(RIG_PAIR_THREADS, RIG_PAIR_MINB)
+#else
+#define RIG_PAIR_BOUNDS __launch_bounds__(RIG_PAIR_THREADS)
+#endif
+constexpr int kPairThreads = RIG_PAIR_THREADS;
 constexpr int kPairWarps = kPairThreads / 32;
 constexpr int kPairRows = 16;
 
@@ -372,7 +384,7 @@ __device__ __forceinline__ int pair_half_row_r(int len, const NumArgs &a, bool d
 // Rows whose output does not fit the stage are merged by num_merge_row with
 // direct global stores (the ascending lane; its partner idles).
 template <int RMAX>
-__global__ void __launch_bounds__(kPairThreads) k_num_pair(NumArgs a) {
+__global__ void RIG_PAIR_BOUNDS k_num_pair(NumArgs a) {
     extern __shared__ __align__(16) unsigned char pair_smem[];
     const int cap = a.stage_cap;
     const int w = threadIdx.x >> 5, l = lane_id();

@@ -12,7 +12,7 @@ import re
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "librig.so")
+LIB_PATH = os.environ.get("RIG_LIB_VARIANT") or os.path.join(_HERE, "librig.so")
 HEADER = os.path.join(os.path.dirname(_HERE), "include", "rig.h")
 
 RIG_OK = 0
