@@ -345,15 +345,36 @@ __global__ void __launch_bounds__(kCopyThreads) k_copy_rows(const int32_t *__res
             pi = __ldg(&cut.part[i]);
             badp |= (pi < 0) | (pi >= cut.K);
         }
-        for (int64_t t = l; t < len; t += 32) {
-            const int32_t j = tcol[src + t];
-            const double w = tw[src + t];
-            gcol[d + t] = j;
-            gw[d + t] = w;
-            if (cut.part && (int64_t)j > i) {
-                const int32_t pj = __ldg(&cut.part[j]);
-                badp |= (pj < 0) | (pj >= cut.K);
-                if (pj != pi) acc.add(w);
+        constexpr int U = 4;  // 4 chunks of loads (and part gathers) in flight per lane
+        for (int64_t t0 = 0; t0 < len; t0 += 32 * U) {
+            int32_t j[U], pj[U];
+            double w[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int64_t t = t0 + 32 * u + l;
+                j[u] = -1;
+                w[u] = 0.0;
+                if (t < len) {
+                    j[u] = tcol[src + t];
+                    w[u] = tw[src + t];
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int64_t t = t0 + 32 * u + l;
+                if (t < len) {
+                    gcol[d + t] = j[u];
+                    gw[d + t] = w[u];
+                }
+                pj[u] = pi;
+                if (cut.part && (int64_t)j[u] > i) pj[u] = __ldg(&cut.part[j[u]]);
+            }
+            if (cut.part) {
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    badp |= (pj[u] < 0) | (pj[u] >= cut.K);
+                    if (pj[u] != pi) acc.add(w[u]);
+                }
             }
         }
     }

@@ -225,6 +225,50 @@ def test_long_rows_and_columns(rig):
     assert_graph_equal(to_np(g.row_ptr), to_np(g.col_idx), to_np(g.w), orc, to_np(g.diag))
 
 
+@pytest.mark.parametrize("seed", range(3))
+def test_mid_rows_deferred(rig, seed):
+    """Every row off the merge path (> 8 entries), none huge: rows of 9..40
+    random columns overflow the mid kernel's far list (deferred to the huge
+    kernel); banded rows with a few far columns do not.  Graph, diag and cut
+    against the oracle, with and without drops, and on a shard."""
+    rng = np.random.default_rng(500 + seed)
+    n = 6000
+    rows, cols = [], []
+    for r in range(n):
+        if r % 7 == 0:  # random columns: every key far from the diagonal
+            k = int(rng.integers(9, 40))
+            cc = rng.choice(n, k, replace=False)
+        else:  # banded, a few far columns
+            cc = np.unique(np.concatenate([np.clip(r + rng.integers(-30, 31, 14), 0, n - 1),
+                                           rng.integers(0, n, 3)]))
+            if cc.size < 9:
+                cc = np.unique(np.concatenate([cc, rng.choice(n, 9, replace=False)]))
+        rows += [r] * cc.size; cols += list(cc)
+    rows, cols = np.array(rows), np.array(cols)
+    key = np.unique(rows.astype(np.int64) * n + cols)
+    rows, cols = key // n, key % n
+    vals = rng.standard_normal(rows.size)
+    rp, ci, v = from_triplets(n, n, rows, cols, vals)
+    K = 16
+    part = rng.integers(0, K, n).astype(np.int32)
+    A = rig.CSR(rp, ci, v)
+    for scale, tol in ((1, 0.0), (1, 0.05)):
+        orc = oracle.build(rp, ci, v, scale_rows=scale, drop_tol=tol)
+        g = rig.rig_build(A, scale, tol, rig.RIG_FLAG_DIAG)
+        assert_graph_equal(to_np(g.row_ptr), to_np(g.col_idx), to_np(g.w), orc, to_np(g.diag))
+        ocut = oracle.cutsize(orc.row_ptr, orc.col, orc.w, part, K)[0]
+        gc, cut = rig.rig_build_cut(A, torch.as_tensor(part, device="cuda"), K, 0, n, scale, tol)
+        assert_graph_equal(to_np(gc.row_ptr), to_np(gc.col_idx), to_np(gc.w), orc)
+        assert abs(cut.item() - ocut) <= REL * ocut
+    # a shard (local row pointers, global columns)
+    a, b = 1234, 4321
+    o3 = oracle.build(rp, ci, v, scale_rows=1, drop_tol=0.0, row_begin=a, row_end=b)
+    oc3 = oracle.cutsize(o3.row_ptr, o3.col, o3.w, part, K, row_begin=a)[0]
+    g3, cut3 = rig.rig_build_cut(A, torch.as_tensor(part, device="cuda"), K, a, b, 1, 0.0)
+    assert_graph_equal(to_np(g3.row_ptr), to_np(g3.col_idx), to_np(g3.w), o3)
+    assert abs(cut3.item() - oc3) <= REL * oc3
+
+
 @pytest.mark.parametrize("seed", range(4))
 def test_random_mixed(rig, seed):
     rng = np.random.default_rng(1000 + seed)
