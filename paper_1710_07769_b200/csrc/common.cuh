@@ -69,6 +69,13 @@ struct DevCounters {
 };
 
 __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
+
+// Device-side guard of the general transpose (see launch_sym_transpose): a
+// kernel given `guard` runs only if *guard != 0 (the pattern-symmetric fast
+// path failed); guard == nullptr: always runs.
+__device__ __forceinline__ bool guard_skip(const int *guard) {
+    return guard != nullptr && *reinterpret_cast<const volatile int *>(guard) == 0;
+}
 __device__ __forceinline__ unsigned lanemask_lt() {
     unsigned m;
     asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
@@ -105,14 +112,26 @@ int num_sms();
 // ---------------------------------------------------------------- kernels
 // k_prep.cu
 void launch_validate(const Csr &A, int *err, cudaStream_t s);
-void launch_col_hist(const Csr &A, unsigned *cnt, unsigned *rank /*nullable*/, cudaStream_t s);
+void launch_col_hist(const Csr &A, unsigned *cnt, unsigned *rank /*nullable*/, cudaStream_t s,
+                     const int *guard = nullptr);
 // k_transpose.cu: bucketed a1 + a2 (see there for the CSC layout with sentinels)
 int64_t transpose_buckets(int64_t nnz, int64_t ncols);
 constexpr size_t kTransposeRecBytes = 16;
 // bcur: u64[transpose_buckets] (initialised here); gcur: u32[ncols] zeroed; big: int[1 + transpose_buckets]
 // with big[0] zeroed (list of buckets too large for the warp sort).
 void launch_transpose(const Csr &A, int scale, const int64_t *cp, double *ahat, unsigned long long *bcur,
-                      void *rec, unsigned *gcur, int *big, int32_t *ri, double *vt, int *err, cudaStream_t s);
+                      void *rec, unsigned *gcur, int *big, int32_t *ri, double *vt, int *err, cudaStream_t s,
+                      const int *guard = nullptr);
+// Pattern-symmetric fast path of a1 + a2 (square A): when every entry (i,k)
+// has its mirror (k,i), column k's rows are row k's columns, so col_ptr =
+// row_ptr and the CSC is a gather (each value a_jk found in row j) -- no
+// histogram, no buckets, no sort.  Row norms first (nrm, y = RN(1/nrm)); an
+// entry without its mirror sets *fail and the guarded general path (given
+// `fail` as its guard) rebuilds everything.  With `shape`, the shape
+// statistics (DevCounters) are taken from the row pointers instead of the
+// column counts, by a kernel that runs only if the gather succeeded.
+void launch_sym_transpose(const Csr &A, int scale, double *nrm, double *y, double *ahat, int64_t *cp, int32_t *ri,
+                          double *vt, int *fail, int *err, DevCounters *shape, int64_t rb, int64_t re, cudaStream_t s);
 void launch_analyze(const Csr &A, const int64_t *cp, int64_t rb, int64_t re, int64_t *f, DevCounters *ctr,
                     cudaStream_t s);
 // Ordered row lists (k_prep.cu): list 0 = mid rows (bin8 < kNumSymBins),
@@ -138,12 +157,14 @@ void launch_int_weights(const double *w, int64_t n, int64_t alpha, int64_t *wgt,
 enum class ScanOp { Identity, UbOffDiag };
 void scan_i64(const int64_t *in, int64_t n, int64_t *out, ScanOp op, void *tmp, size_t tmp_bytes,
               cudaStream_t s);
-void scan_u32(const unsigned *in, int64_t n, int64_t *out, void *tmp, size_t tmp_bytes, cudaStream_t s);
+void scan_u32(const unsigned *in, int64_t n, int64_t *out, void *tmp, size_t tmp_bytes, cudaStream_t s,
+              const int *guard = nullptr);
 // scan_u32 of the column counts that also takes the shape statistics
 // (DevCounters max_col, p_full, max_row, shard_nnz of rows [rb, re)) into
 // ctr, copies ctr to host_copy and records `ready` before the second kernel.
 void scan_u32_shape(const unsigned *in, int64_t n, int64_t *out, void *tmp, DevCounters *ctr, const int64_t *rp,
-                    int64_t rb, int64_t re, void *host_copy, cudaEvent_t ready, cudaStream_t s);
+                    int64_t rb, int64_t re, void *host_copy, cudaEvent_t ready, cudaStream_t s,
+                    const int *guard = nullptr);
 size_t scan_tmp_bytes(int64_t n);
 
 // k_spgemm.cu

@@ -49,7 +49,9 @@ void launch_validate(const Csr &A, int *err, cudaStream_t s) {
 // ------------------------------------------------------------------ a2 (histogram)
 // Column counts; with `rank`, also each entry's arrival slot in its column
 // (the returned old count), so the scatter needs no atomics.
-__global__ void k_col_hist(const int32_t *__restrict__ ci, int64_t nnz, unsigned *cnt, unsigned *rank) {
+__global__ void k_col_hist(const int32_t *__restrict__ ci, int64_t nnz, unsigned *cnt, unsigned *rank,
+                           const int *guard) {
+    if (guard_skip(guard)) return;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (rank) {
@@ -66,8 +68,8 @@ __global__ void k_col_hist(const int32_t *__restrict__ ci, int64_t nnz, unsigned
     }
 }
 
-void launch_col_hist(const Csr &A, unsigned *cnt, unsigned *rank, cudaStream_t s) {
-    k_col_hist<<<grid_for(A.nnz, 256, 16), 256, 0, s>>>(A.ci, A.nnz, cnt, rank);
+void launch_col_hist(const Csr &A, unsigned *cnt, unsigned *rank, cudaStream_t s, const int *guard) {
+    k_col_hist<<<grid_for(A.nnz, 256, 16), 256, 0, s>>>(A.ci, A.nnz, cnt, rank, guard);
     note_launch();
 }
 

@@ -48,7 +48,8 @@ struct ShapeOut {
 
 template <typename T>
 __global__ void __launch_bounds__(kScanThreads) k_tile_sum(const T *__restrict__ in, int64_t n, ScanOp op,
-                                                           int64_t *tile_sums, ShapeOut so) {
+                                                           int64_t *tile_sums, ShapeOut so, const int *guard) {
+    if (guard_skip(guard)) return;
     const int64_t base = blockIdx.x * kTile;
     int64_t s = 0;
     unsigned long long ps = 0, mc = 0, mr = 0;
@@ -105,7 +106,8 @@ __global__ void __launch_bounds__(kScanThreads) k_tile_sum(const T *__restrict__
 template <typename T>
 __global__ void __launch_bounds__(kScanThreads) k_tile_scan(const T *__restrict__ in, int64_t n, ScanOp op,
                                                             const int64_t *__restrict__ tile_sums, int64_t ntiles,
-                                                            int64_t *out) {
+                                                            int64_t *out, const int *guard) {
+    if (guard_skip(guard)) return;
     __shared__ int64_t sv[kTile + kTile / 16];  // padded: conflict-free blocked <-> striped transpose
     __shared__ int64_t tot_s, pre_s;
     // prefix of the earlier tiles' totals
@@ -156,16 +158,17 @@ size_t scan_tmp_bytes(int64_t n) {
 
 template <typename T>
 static void scan_impl(const T *in, int64_t n, int64_t *out, ScanOp op, void *tmp, cudaStream_t s,
-                      ShapeOut so = ShapeOut{nullptr, nullptr, 0, 0}, cudaEvent_t after_sum = nullptr) {
+                      ShapeOut so = ShapeOut{nullptr, nullptr, 0, 0}, cudaEvent_t after_sum = nullptr,
+                      const int *guard = nullptr) {
     const int64_t ntiles = (n + kTile - 1) / kTile;
     if (ntiles == 0) {
         cudaMemsetAsync(out, 0, sizeof(int64_t), s);
         return;
     }
     int64_t *ts = static_cast<int64_t *>(tmp);
-    k_tile_sum<T><<<(unsigned)ntiles, kScanThreads, 0, s>>>(in, n, op, ts, so);
+    k_tile_sum<T><<<(unsigned)ntiles, kScanThreads, 0, s>>>(in, n, op, ts, so, guard);
     if (after_sum) cudaEventRecord(after_sum, s);
-    k_tile_scan<T><<<(unsigned)ntiles, kScanThreads, 0, s>>>(in, n, op, ts, ntiles, out);
+    k_tile_scan<T><<<(unsigned)ntiles, kScanThreads, 0, s>>>(in, n, op, ts, ntiles, out, guard);
     note_launch(2);
 }
 
@@ -173,12 +176,13 @@ void scan_i64(const int64_t *in, int64_t n, int64_t *out, ScanOp op, void *tmp, 
     scan_impl<int64_t>(in, n, out, op, tmp, s);
 }
 
-void scan_u32(const unsigned *in, int64_t n, int64_t *out, void *tmp, size_t, cudaStream_t s) {
-    scan_impl<unsigned>(in, n, out, ScanOp::Identity, tmp, s);
+void scan_u32(const unsigned *in, int64_t n, int64_t *out, void *tmp, size_t, cudaStream_t s, const int *guard) {
+    scan_impl<unsigned>(in, n, out, ScanOp::Identity, tmp, s, ShapeOut{nullptr, nullptr, 0, 0}, nullptr, guard);
 }
 
 void scan_u32_shape(const unsigned *in, int64_t n, int64_t *out, void *tmp, DevCounters *ctr, const int64_t *rp,
-                    int64_t rb, int64_t re, void *host_copy, cudaEvent_t ready, cudaStream_t s) {
+                    int64_t rb, int64_t re, void *host_copy, cudaEvent_t ready, cudaStream_t s,
+                    const int *guard) {
     const int64_t ntiles = (n + kTile - 1) / kTile;
     if (ntiles == 0) {  // no columns: the statistics are zeros except the shard
         cudaMemsetAsync(out, 0, sizeof(int64_t), s);
@@ -188,10 +192,10 @@ void scan_u32_shape(const unsigned *in, int64_t n, int64_t *out, void *tmp, DevC
     }
     int64_t *ts = static_cast<int64_t *>(tmp);
     k_tile_sum<unsigned><<<(unsigned)ntiles, kScanThreads, 0, s>>>(in, n, ScanOp::Identity, ts,
-                                                                    ShapeOut{ctr, rp, rb, re});
+                                                                    ShapeOut{ctr, rp, rb, re}, guard);
     cudaMemcpyAsync(host_copy, ctr, sizeof(DevCounters), cudaMemcpyDeviceToHost, s);
     cudaEventRecord(ready, s);
-    k_tile_scan<unsigned><<<(unsigned)ntiles, kScanThreads, 0, s>>>(in, n, ScanOp::Identity, ts, ntiles, out);
+    k_tile_scan<unsigned><<<(unsigned)ntiles, kScanThreads, 0, s>>>(in, n, ScanOp::Identity, ts, ntiles, out, guard);
     note_launch(2);
 }
 

@@ -65,7 +65,8 @@ constexpr int kScatterThreads = 256;
 __global__ void __launch_bounds__(kScatterThreads) k_bucket_scatter(Csr A, int scale, double *__restrict__ ahat,
                                                                     const int64_t *__restrict__ cp,
                                                                     unsigned long long *bcur, Rec *__restrict__ rec,
-                                                                    int *err, int shift) {
+                                                                    int *err, int shift, const int *guard) {
+    if (guard_skip(guard)) return;
     __shared__ int s_nz[kScatterThreads / 32][32];  // lane of the k-th nonempty row of the tile
     const int l = lane_id(), w = threadIdx.x >> 5;
     const unsigned lt = lanemask_lt();
@@ -179,7 +180,9 @@ __device__ void bitonic_sort_block(int64_t len, KeyAt key, Swap swap) {
 
 // Bucket cursors start at the bucket's first record slot (cp of its first
 // column), so the scatter's atomics return absolute positions.
-__global__ void k_bucket_init(const int64_t *__restrict__ cp, int64_t nb, int shift, unsigned long long *bcur) {
+__global__ void k_bucket_init(const int64_t *__restrict__ cp, int64_t nb, int shift, unsigned long long *bcur,
+                              const int *guard) {
+    if (guard_skip(guard)) return;
     for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < nb; b += (int64_t)gridDim.x * blockDim.x)
         bcur[b] = (unsigned long long)cp[b << shift];
 }
@@ -197,7 +200,8 @@ template <bool RANK>
 __global__ void __launch_bounds__(kSortThreads) k_bucket_sort(const Rec *__restrict__ rec,
                                                               const int64_t *__restrict__ cp, int64_t ncols,
                                                               int32_t *ri, double *vt, int shift, int *big_list,
-                                                              int *big_count) {
+                                                              int *big_count, const int *guard) {
+    if (guard_skip(guard)) return;
     __shared__ int32_t s_ri[kSortWarps][kBucketSlots];
     __shared__ double s_vt[kSortWarps][kBucketSlots];
     constexpr int RS = RANK ? kBucketSlots : 1;
@@ -304,7 +308,9 @@ __global__ void __launch_bounds__(kSortThreads) k_bucket_sort(const Rec *__restr
 // sort each column in global memory (correct for any skew, slower).
 __global__ void __launch_bounds__(128) k_bucket_sort_big(const Rec *__restrict__ rec, const int64_t *__restrict__ cp,
                                                          int64_t ncols, unsigned *gcur, int32_t *ri, double *vt,
-                                                         int shift, const int *big_list, const int *big_count) {
+                                                         int shift, const int *big_list, const int *big_count,
+                                                         const int *guard) {
+    if (guard_skip(guard)) return;
     const int bcols = 1 << shift;
     const int nbig = *big_count;
     for (int q = blockIdx.x; q < nbig; q += gridDim.x) {
@@ -357,13 +363,14 @@ int64_t transpose_buckets(int64_t nnz, int64_t ncols) {
 }
 
 void launch_transpose(const Csr &A, int scale, const int64_t *cp, double *ahat, unsigned long long *bcur,
-                      void *rec, unsigned *gcur, int *big, int32_t *ri, double *vt, int *err, cudaStream_t s) {
+                      void *rec, unsigned *gcur, int *big, int32_t *ri, double *vt, int *err, cudaStream_t s,
+                      const int *guard) {
     const int shift = transpose_shift(A.nnz, A.ncols);
     if (A.ncols > 0) {
         const int64_t nb = (A.ncols + (1 << shift) - 1) >> shift;
         int64_t g = (nb + 255) / 256;
         g = g > (int64_t)num_sms() * 4 ? (int64_t)num_sms() * 4 : g;
-        k_bucket_init<<<(unsigned)g, 256, 0, s>>>(cp, nb, shift, bcur);
+        k_bucket_init<<<(unsigned)g, 256, 0, s>>>(cp, nb, shift, bcur, guard);
         note_launch();
     }
     if (A.nrows > 0) {
@@ -371,7 +378,7 @@ void launch_transpose(const Csr &A, int scale, const int64_t *cp, double *ahat, 
         const int64_t cap = (int64_t)num_sms() * 8;
         g = g < 1 ? 1 : (g > cap ? cap : g);
         k_bucket_scatter<<<(unsigned)g, kScatterThreads, 0, s>>>(A, scale, ahat, cp, bcur, static_cast<Rec *>(rec),
-                                                                 err, shift);
+                                                                 err, shift, guard);
         note_launch();
     }
     if (A.ncols > 0) {
@@ -383,13 +390,193 @@ void launch_transpose(const Csr &A, int scale, const int64_t *cp, double *ahat, 
         // long columns: parallel ranking; short ones: per-lane insertion sorts
         if (A.nnz > (int64_t)12 * A.ncols)
             k_bucket_sort<true><<<(unsigned)g, kSortThreads, 0, s>>>(static_cast<const Rec *>(rec), cp, A.ncols, ri,
-                                                                     vt, shift, big + 1, big);
+                                                                     vt, shift, big + 1, big, guard);
         else
             k_bucket_sort<false><<<(unsigned)g, kSortThreads, 0, s>>>(static_cast<const Rec *>(rec), cp, A.ncols, ri,
-                                                                      vt, shift, big + 1, big);
+                                                                      vt, shift, big + 1, big, guard);
         k_bucket_sort_big<<<(unsigned)num_sms(), 128, 0, s>>>(static_cast<const Rec *>(rec), cp, A.ncols, gcur, ri,
-                                                              vt, shift, big + 1, big);
+                                                              vt, shift, big + 1, big, guard);
         note_launch(2);
+    }
+}
+
+// ------------------------------------------------------------------ pattern-symmetric fast path
+static int sym_grid(int64_t work, int block, int per_sm) {
+    int64_t g = (work + block - 1) / block;
+    const int64_t cap = (int64_t)num_sms() * per_sm;
+    if (g > cap) g = cap;
+    if (g < 1) g = 1;
+    return (int)g;
+}
+
+// Row norms for the gather: nrm_i = sqrt_rn(ordered fma chain of a_ik^2), y_i =
+// RN(1/nrm_i) (the same arithmetic as k_bucket_scatter, R5).
+__global__ void k_row_norms(Csr A, double *nrm, double *y, int *err, const int *fail) {
+    if (*reinterpret_cast<const volatile int *>(fail)) return;  // the probe found a missing mirror
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < A.nrows;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t s = A.rp[i], e = A.rp[i + 1];
+        double ss = +0.0;
+        for (int64_t p0 = s; p0 < e; p0 += 8) {  // 8 loads in flight, chain in order
+            double av[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) av[u] = p0 + u < e ? A.v[p0 + u] : 0.0;
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+                if (p0 + u < e) ss = __fma_rn(av[u], av[u], ss);
+        }
+        double nm = 1.0, yy = 1.0;
+        if (!isfinite(ss)) {
+            atomicOr(err, kErrNonFinite);
+        } else if (ss == 0.0) {
+            atomicOr(err, kErrZeroRow);
+        } else {
+            nm = __dsqrt_rn(ss);
+            yy = __drcp_rn(nm);
+        }
+        nrm[i] = nm;
+        y[i] = yy;
+    }
+}
+
+// Probe before the gather: 4096 entries spread over A; one without its mirror
+// (or in a row longer than 64) sets *fail, so a non-symmetric matrix costs a
+// few skipped launches instead of a failed gather.
+__global__ void k_sym_probe(Csr A, int *fail) {
+    const int64_t nprobe = 4096;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < nprobe && t < A.nnz;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t p = A.nnz <= nprobe ? t : t * (A.nnz / nprobe);
+        // row of p: binary search of row_ptr
+        int64_t lo = 0, hi = A.nrows;  // rp[lo] <= p < rp[hi]
+        while (hi - lo > 1) {
+            const int64_t mid = (lo + hi) >> 1;
+            if (A.rp[mid] <= p) lo = mid; else hi = mid;
+        }
+        const int j = A.ci[p];
+        const int64_t sj = A.rp[j], ej = A.rp[j + 1];
+        bool found = false;
+        if (ej - sj <= 64)
+            for (int64_t q = sj; q < ej && !found; ++q) found = A.ci[q] == (int)lo;
+        if (!found) atomicOr(fail, 1);
+    }
+}
+
+// Column k of the CSC is row k's column list (mirror pattern), so
+// col_ptr[k+1] = row_ptr[k+1] and CSR entry p of row k goes to CSC slot p + k
+// (one sentinel per earlier column).  A warp takes 32 consecutive rows and
+// walks their entries 32 at a time (coalesced loads and stores); lane p finds
+// its row k by a shuffle binary search over the tile's row pointers, and the
+// value a_hat_jk of the mirror entry (j, k) in row j: first at the mirrored
+// position (stencil rows share their offset pattern: entry t of row k and
+// entry len_j - 1 - t of row j are each other's mirror), else by a search of
+// row j.  A missing mirror sets *fail; every warp then stops at its next chunk.
+constexpr int kSymThreads = 128;
+__global__ void __launch_bounds__(kSymThreads) k_sym_transpose(Csr A, int scale, const double *__restrict__ nrm,
+                                                               const double *__restrict__ y, double *ahat, int64_t *cp,
+                                                               int32_t *ri, double *vt, int *fail) {
+    const int l = lane_id();
+    const int64_t ntiles = (A.nrows + 31) / 32;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t tile = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; tile < ntiles; tile += nw) {
+        if (*reinterpret_cast<volatile int *>(fail)) return;
+        const int64_t r0 = tile * 32;
+        const int rows = (int)min((int64_t)32, A.nrows - r0);
+        const int64_t my_s = l < rows ? A.rp[r0 + l] : A.rp[r0 + rows];
+        const int64_t hi = A.rp[r0 + rows];
+        if (l < rows) {
+            cp[r0 + l + 1] = A.rp[r0 + l + 1];
+            ri[A.rp[r0 + l + 1] + r0 + l] = INT_MAX;  // sentinel of column r0 + l
+            vt[A.rp[r0 + l + 1] + r0 + l] = 0.0;
+        }
+        if (r0 == 0 && l == 0) cp[0] = 0;
+        const double my_n = scale && l < rows ? nrm[r0 + l] : 1.0, my_y = scale && l < rows ? y[r0 + l] : 1.0;
+        for (int64_t c0 = __shfl_sync(kFull, my_s, 0); c0 < hi; c0 += 32) {
+            if (*reinterpret_cast<volatile int *>(fail)) return;
+            const int64_t p = c0 + l;
+            // row of p: the last lane u < rows with rp[r0 + u] <= p
+            int u = 0;
+#pragma unroll
+            for (int b = 16; b > 0; b >>= 1) {
+                const int64_t sv = __shfl_sync(kFull, my_s, u + b < rows ? u + b : rows - 1);
+                if (u + b < rows && sv <= p) u += b;
+            }
+            const int64_t k = r0 + u;
+            const int64_t sk = __shfl_sync(kFull, my_s, u);
+            const double nk = shfl_d(my_n, u), yk = shfl_d(my_y, u);
+            if (p >= hi) continue;
+            const int j = A.ci[p];
+            const double akj = A.v[p];
+            const int64_t sj = A.rp[j], ej = A.rp[j + 1];
+            // mirrored position guess, then a search of row j (short rows
+            // only: a longer one ends the attempt)
+            int64_t q = ej - 1 - (p - sk);
+            if (q < sj || q >= ej || A.ci[q] != (int)k) {
+                q = -1;
+                if (ej - sj <= 64) {
+                    for (int64_t b0 = sj; b0 < ej && q < 0; b0 += 8) {
+                        int cc[8];
+#pragma unroll
+                        for (int t = 0; t < 8; ++t) cc[t] = b0 + t < ej ? A.ci[b0 + t] : -1;
+#pragma unroll
+                        for (int t = 0; t < 8; ++t)
+                            if (cc[t] == (int)k) q = b0 + t;
+                    }
+                }
+            }
+            if (q < 0) {  // no mirror entry (j, k): not pattern-symmetric
+                atomicOr(fail, 1);
+                continue;
+            }
+            const double ajk = A.v[q];
+            ri[p + k] = j;
+            vt[p + k] = scale ? div_rn_fast(ajk, nrm[j], y[j]) : ajk;
+            if (scale) ahat[p] = div_rn_fast(akj, nk, yk);
+        }
+    }
+}
+
+// Shape statistics (DevCounters, see scan_u32_shape) from the row pointers:
+// with a mirror pattern column k has as many entries as row k.  Runs only if
+// the gather succeeded (guard = fail, inverted).
+__global__ void k_sym_shape(const int64_t *__restrict__ rp, int64_t n, int64_t rb, int64_t re, DevCounters *ctr,
+                            const int *fail) {
+    if (*reinterpret_cast<const volatile int *>(fail)) return;
+    unsigned long long ps = 0, mc = 0, mr = 0;
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
+        const unsigned long long len = (unsigned long long)(rp[k + 1] - rp[k]);
+        ps += len * len;
+        mc = max(mc, len);
+        if (k >= rb && k < re) mr = max(mr, len);
+    }
+    ps = warp_sum(ps);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        mc = max(mc, __shfl_xor_sync(kFull, mc, o));
+        mr = max(mr, __shfl_xor_sync(kFull, mr, o));
+    }
+    if (lane_id() == 0) {
+        if (ps) atomicAdd((unsigned long long *)&ctr->p_full, ps);
+        if (mc) atomicMax((unsigned long long *)&ctr->max_col, mc);
+        if (mr) atomicMax((unsigned long long *)&ctr->max_row, mr);
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) ctr->shard_nnz = rp[re] - rp[rb];
+}
+
+void launch_sym_transpose(const Csr &A, int scale, double *nrm, double *y, double *ahat, int64_t *cp, int32_t *ri,
+                          double *vt, int *fail, int *err, DevCounters *shape, int64_t rb, int64_t re, cudaStream_t s) {
+    if (A.nrows <= 0) return;
+    k_sym_probe<<<16, 256, 0, s>>>(A, fail);
+    note_launch();
+    if (scale) {
+        k_row_norms<<<sym_grid(A.nrows, 256, 8), 256, 0, s>>>(A, nrm, y, err, fail);
+        note_launch();
+    }
+    k_sym_transpose<<<sym_grid((A.nrows + 31) / 32 * 32, kSymThreads, 16), kSymThreads, 0, s>>>(A, scale, nrm, y, ahat, cp, ri, vt, fail);
+    note_launch();
+    if (shape) {
+        k_sym_shape<<<sym_grid(A.nrows, 256, 8), 256, 0, s>>>(A.rp, A.nrows, rb, re, shape, fail);
+        note_launch();
     }
 }
 

@@ -197,6 +197,21 @@ def test_empty_and_errors(rig):
     assert math.isnan(rig.rig_cutsize(g, bad, 4).item())
 
 
+def test_sym_transpose_path(rig):
+    """Pattern-symmetric transpose (a gather) and its fallback, forced on small
+    inputs in a fresh process (tests/sym_path_check.py)."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, RIG_SYM_MIN_NNZ="1", PYTHONPATH=root)
+    r = subprocess.run([sys.executable, os.path.join(root, "tests", "sym_path_check.py")], env=env, cwd=root,
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-4000:]
+    assert "sym path ok" in r.stdout
+
+
 def test_long_rows_and_columns(rig):
     """Warp-hash, huge-row and long-column-sort paths."""
     rng = np.random.default_rng(11)
