@@ -343,8 +343,9 @@ def main():
     alg = numeric_alg_bytes(w.n, w.nnz, nnz_c) / max(world, 1) if world > 1 else numeric_alg_bytes(w.n, w.nnz, nnz_c)
     merge_only = "symbolic" not in pass_ms  # every row on the merge path: one kernel does all of a5-a6
     roof_ms = ker_ms if merge_only else num_ms
-    roof_kernel = ("k_num_merge (a5+a6 fused, all rows; CUDA events around the launch)" if merge_only else
-                   "numeric pass (k_num_mid + k_num_huge + k_num_merge + k_copy_rows; CUDA events around the pass)")
+    roof_kernel = ("k_num_pair (a5+a6 fused merge path, two lanes per row, all rows; CUDA events around the launch)"
+                   if merge_only else
+                   "numeric pass (k_num_mid + k_num_huge + k_num_pair + k_copy_rows; CUDA events around the pass)")
     achieved = alg / (roof_ms * 1e-3) / 1e9
     traffic, traffic_src = load_traffic(args.config)
     line = {
