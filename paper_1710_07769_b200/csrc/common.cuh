@@ -304,7 +304,7 @@ void launch_copy_rows(const int32_t *list, const int64_t *count, int64_t rb, con
 // huge rows: CTA per row, dense accumulator + bitmap in global scratch
 size_t huge_scratch_bytes(int64_t nrows, int slots, bool numeric);
 size_t huge_bitmap_bytes(int64_t nrows, int slots);  // zeroed prefix of the scratch
-int huge_slots(int64_t nrows, int64_t n_huge);
+int huge_slots(int64_t nrows, int64_t n_huge, bool heavy);  // heavy: the shard has huge rows
 void launch_num_huge(const MidArgs &a, int slots, void *scratch, cudaStream_t s);
 
 // k_post.cu

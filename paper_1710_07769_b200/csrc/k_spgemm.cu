@@ -737,8 +737,10 @@ size_t huge_scratch_bytes(int64_t nrows, int slots, bool numeric) {
 }
 
 // Row slots of the huge path: each is a dense accumulator over all rows plus
-// a bitmap, so slots cost memory; 8 per SM measured fastest on config 4
-// (huge + deferred rows: 4.3 -> 2.9 ms against 2 per SM), within a budget of
+// a bitmap, so slots cost memory.  With huge rows present (heavy-tailed
+// matrices, whose long mid rows also defer) 8 per SM measured fastest on
+// config 4 (huge + deferred rows: 4.3 -> 2.9 ms against 2 per SM); otherwise
+// only the odd deferred row comes here and 2 per SM do.  Within a budget of
 // RIG_HUGE_BUDGET_GB (24) and a quarter of the free device memory.
 #ifndef RIG_HUGE_BUDGET_GB
 #define RIG_HUGE_BUDGET_GB 24
@@ -746,7 +748,7 @@ size_t huge_scratch_bytes(int64_t nrows, int slots, bool numeric) {
 #ifndef RIG_HUGE_PER_SM
 #define RIG_HUGE_PER_SM 8
 #endif
-int huge_slots(int64_t nrows, int64_t n_huge) {
+int huge_slots(int64_t nrows, int64_t n_huge, bool heavy) {
     const size_t per = huge_scratch_bytes(nrows, 1, true);
     static size_t free_q = 0;
     if (!free_q) {
@@ -756,7 +758,7 @@ int huge_slots(int64_t nrows, int64_t n_huge) {
     }
     const size_t bud = std::min(((size_t)RIG_HUGE_BUDGET_GB << 30), free_q);
     int64_t budget = (int64_t)bud / (int64_t)(per ? per : 1);
-    int64_t s = RIG_HUGE_PER_SM * (int64_t)sms();
+    int64_t s = (heavy ? RIG_HUGE_PER_SM : 2) * (int64_t)sms();
     if (s > budget) s = budget;
     if (s > n_huge) s = n_huge;
     if (s < 1) s = 1;

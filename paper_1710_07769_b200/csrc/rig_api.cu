@@ -528,7 +528,8 @@ static void plan_build(rig_plan *p, const rig_csr_t *Ain, bool allow_early = fal
     const size_t o_tw = LB.add(sizeof(double) * (size_t)p->h.mid_slots);
     size_t o_huge = 0;
     if (need_huge) {
-        p->huge_slots_n = huge_slots(n, p->h.max_f > kMidSmallCap ? n_mid : std::min<int64_t>(n_mid, 8));
+        p->huge_slots_n = huge_slots(n, p->h.max_f > kMidSmallCap ? n_mid : std::min<int64_t>(n_mid, 8),
+                                     p->h.sym_count[kNumSymBins] > 0);
         o_huge = LB.add(huge_scratch_bytes(n, p->huge_slots_n, true));
     }
     unsigned char *wb = p->cached ? ws_get(1, LB.bytes, s) : p->arena.raw(LB.bytes);
