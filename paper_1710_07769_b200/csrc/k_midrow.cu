@@ -44,20 +44,23 @@ struct MidSmem {
     int elen[32];
     double ea[32];
     int bcnt[32];                 // bucket counts / cursors of the far sort
+    int bst[32];                  // bucket starts
 };
 
 __device__ __forceinline__ int it_key(uint64_t v) { return (int)(uint32_t)(v >> 32); }
 __device__ __forceinline__ int it_pos(uint64_t v) { return (int)(uint32_t)v; }
 
-// Sort n unique far items src -> dst: 32 value buckets (one per lane) filled
-// stably in arrival order, then a per-lane insertion sort.  Returns
-// false (nothing usable) if a bucket would exceed kMaxBucket.
-__device__ __forceinline__ bool bucket_sort_far(const uint64_t *__restrict__ src, uint64_t *__restrict__ dst,
-                                                int *cnt, int n) {
+// Sort n unique far items in place (a, via tmp): 32 value buckets filled
+// stably in arrival order (tmp), then every item is placed at its bucket's
+// start plus its rank in the bucket (the count of smaller items there; items
+// are unique), back into a.  Returns false (nothing usable) if a bucket would
+// exceed kMaxBucket.
+__device__ __forceinline__ bool bucket_sort_far(uint64_t *__restrict__ a, uint64_t *__restrict__ tmp, int *cnt,
+                                                int *bst, int n) {
     const int l = lane_id();
     int mn = INT_MAX, mx = INT_MIN;
     for (int p = l; p < n; p += 32) {
-        const int k = it_key(src[p]);
+        const int k = it_key(a[p]);
         mn = min(mn, k);
         mx = max(mx, k);
     }
@@ -65,9 +68,10 @@ __device__ __forceinline__ bool bucket_sort_far(const uint64_t *__restrict__ src
     mx = __reduce_max_sync(kFull, mx);
     // bucket(k) = floor((k - mn) * mul / 2^32) in [0, 32), monotone in k
     const uint64_t mul = ((1ull << 37) - 1) / (uint64_t)((int64_t)mx - mn + 1);
+    auto bucket = [&](uint64_t v) { return (int)(((uint64_t)(uint32_t)(it_key(v) - mn) * mul) >> 32); };
     cnt[l] = 0;
     __syncwarp();
-    for (int p = l; p < n; p += 32) atomicAdd(&cnt[(int)(((uint64_t)(uint32_t)(it_key(src[p]) - mn) * mul) >> 32)], 1);
+    for (int p = l; p < n; p += 32) atomicAdd(&cnt[bucket(a[p])], 1);
     __syncwarp();
     const int c = cnt[l];
     if (__any_sync(kFull, c > kMaxBucket)) return false;
@@ -75,26 +79,27 @@ __device__ __forceinline__ bool bucket_sort_far(const uint64_t *__restrict__ src
     const int base = warp_incl_scan(c) - c;
     __syncwarp();
     cnt[l] = base;  // running cursor of bucket l
+    bst[l] = base;
     __syncwarp();
     const unsigned lt = lanemask_lt();
-    for (int p0 = 0; p0 < n; p0 += 32) {  // arrival order (stable): buckets nearly sorted
+    for (int p0 = 0; p0 < n; p0 += 32) {  // arrival order (stable)
         const int p = p0 + l;
-        const uint64_t v = p < n ? src[p] : 0ull;
-        const int b = p < n ? (int)(((uint64_t)(uint32_t)(it_key(v) - mn) * mul) >> 32) : 32 + l;
+        const uint64_t v = p < n ? a[p] : 0ull;
+        const int b = p < n ? bucket(v) : 32 + l;
         const unsigned g = __match_any_sync(kFull, b);
-        if (p < n) dst[cnt[b] + __popc(g & lt)] = v;
+        if (p < n) tmp[cnt[b] + __popc(g & lt)] = v;
         __syncwarp();
         if (p < n && (g & lt) == 0) cnt[b] += __popc(g);
         __syncwarp();
     }
-    for (int q = base + 1; q < base + c; ++q) {  // insertion sort of bucket l
-        const uint64_t v = dst[q];
-        int t = q - 1;
-        while (t >= base && dst[t] > v) {
-            dst[t + 1] = dst[t];
-            --t;
-        }
-        dst[t + 1] = v;
+    // rank in the bucket: [bst[b], cnt[b]) holds bucket b
+    for (int p = l; p < n; p += 32) {
+        const uint64_t v = tmp[p];
+        const int b = bucket(v);
+        const int b0 = bst[b], b1 = cnt[b];
+        int rank = 0;
+        for (int q = b0; q < b1; ++q) rank += tmp[q] < v;
+        a[b0 + rank] = v;
     }
     __syncwarp();
     return true;
@@ -237,8 +242,7 @@ __global__ void __launch_bounds__(kMidThreads, 8) k_num_mid(MidArgs a) {
         bool ok = nfar <= FCAP;
         if (a.dbg & 2) nfar = 0;
         if (ok && nfar > 1 && !(a.dbg & 1)) {
-            ok = bucket_sort_far(S.m0, S.m1, S.bcnt, nfar);
-            srt = S.m1;
+            ok = bucket_sort_far(S.m0, S.m1, S.bcnt, S.bst, nfar);  // sorted in place (m0)
         }
         if (!ok) {
             for (int t = l; t < kMidWin; t += 32) S.wv[t] = +0.0;
