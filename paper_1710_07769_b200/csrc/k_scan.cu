@@ -68,6 +68,7 @@ __global__ void __launch_bounds__(kScanThreads) k_tile_sum(const T *__restrict__
     if (lane_id() == 0) ws[threadIdx.x >> 5] = s;
     if (so.ctr) {
         const int64_t stride = (int64_t)gridDim.x * kScanThreads;
+#pragma unroll 8
         for (int64_t i = so.rb + blockIdx.x * (int64_t)kScanThreads + threadIdx.x; i < so.re; i += stride)
             mr = max(mr, (unsigned long long)(so.rp[i + 1] - so.rp[i]));
         ps = warp_sum(ps);
