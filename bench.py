@@ -62,6 +62,12 @@ def load_peaks():
     return 6650.0, "fallback (B200_PROFILING.md)"
 
 
+def workload_label(w):
+    if w.cfg_id <= 5:
+        return f"{w.name} (BASELINE configs[{w.cfg_id - 1}])"
+    return f"{w.name} (SURVEY 8(f) f3 stress config {w.cfg_id})"
+
+
 def load_traffic(cfg):
     """dram__bytes_read.sum + dram__bytes_write.sum per launch of the numeric
     kernel from the committed ncu --set full summary, if present."""
@@ -179,7 +185,7 @@ def run_reference(args):
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "products/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"{w.name} (BASELINE configs[{w.cfg_id - 1}])", "n": w.n, "nnz_A": w.nnz,
+            "config": {"workload": workload_label(w), "n": w.n, "nnz_A": w.nnz,
                        "products": P, "K": w.K},
             "cpu_baseline": {"value": v, "unit": "products/s", "cores": 1, "kind": "oracle",
                              "sample": f"full {w.name} workload per step (scale+CSC+Gustavson+cutsize)"},
@@ -361,7 +367,7 @@ def main():
         "vs_baseline": None,
         "dtype": "f64",
         "data": "synthetic",
-        "config": {"workload": f"{w.name} (BASELINE configs[{w.cfg_id - 1}])", "n": w.n, "nnz_A": w.nnz,
+        "config": {"workload": workload_label(w), "n": w.n, "nnz_A": w.nnz,
                    "products": P_total, "nnz_C": nnz_c, "graph_nnz": g_total, "K": w.K,
                    "scale_rows": w.scale_rows, "drop_tol": w.drop_tol,
                    "l2": f"flushed between timed steps ({L2_FLUSH_BYTES >> 20} MiB write)",

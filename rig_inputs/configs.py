@@ -25,6 +25,8 @@ CONFIG_NAMES = {
     3: "stencil3d",
     4: "powerlaw",
     5: "banded",
+    6: "powerlaw12",
+    7: "denserows",
 }
 
 
@@ -263,6 +265,35 @@ def banded(n, rng, bw=50, in_band=19, far=3, chunk=1 << 18):
     return row_ptr, col, val
 
 
+def dense_rows(n, rng, per_row=64, bw=1000):
+    """Config 7: row i = diagonal + (per_row - 1) distinct
+    uniform columns with 1 <= |i-j| <= bw (clipped to the matrix); U(-1,1)
+    off-diagonals, diagonal 1 + sum |off| -- FEM-like rows of nnz/n ~ 64, the
+    regime of the paper's largest-nnz matrices."""
+    offs = np.concatenate([np.arange(-bw, 0), np.arange(1, bw + 1)]).astype(np.int64)
+    m = per_row - 1
+    R = np.arange(n, dtype=np.int64)
+    cand = R[:, None] + offs[None, :]
+    valid = (cand >= 0) & (cand < n)
+    keys = rng.random((n, offs.size))
+    keys[~valid] = 2.0
+    pick = np.argpartition(keys, m - 1, axis=1)[:, :m]
+    cols = np.take_along_axis(cand, pick, axis=1)
+    ok = np.take_along_axis(valid, pick, axis=1)
+    offv = _nonzero_uniform(rng, -1.0, 1.0, n * m).reshape(n, m)
+    offv[~ok] = 0.0
+    cols[~ok] = -1
+    diag = 1.0 + np.abs(offv).sum(axis=1)
+    cols = np.concatenate([R[:, None], cols], axis=1)
+    vals = np.concatenate([diag[:, None], offv], axis=1)
+    mask = cols >= 0
+    order = np.argsort(np.where(mask, cols, np.iinfo(np.int64).max), axis=1)
+    cols = np.take_along_axis(cols, order, axis=1)
+    vals = np.take_along_axis(vals, order, axis=1)
+    mask = np.take_along_axis(mask, order, axis=1)
+    return _rows_to_csr(n, cols, mask, vals)
+
+
 def dense_columns(n, rng, per_row=5, n_dense=4, dense_nnz=None, ncols=None, levels=0):
     """Sparse rows plus planted dense columns (the LP-matrix shape that
     motivates the sparsification of PAPER.md:565-576): every row has
@@ -306,10 +337,10 @@ def dense_columns(n, rng, per_row=5, n_dense=4, dense_nnz=None, ncols=None, leve
 # BASELINE.json configs
 # --------------------------------------------------------------------------
 
-FULL = {1: 2000, 2: 1000, 3: 200, 4: 2_000_000, 5: 4_000_000}
+FULL = {1: 2000, 2: 1000, 3: 200, 4: 2_000_000, 5: 4_000_000, 6: 2_000_000, 7: 100_000}
 # reduced twins: same recipe, sizes the oracle finishes in seconds while still
 # spanning many tiles/CTAs and a ragged tail
-SMALL = {1: 2000, 2: 151, 3: 23, 4: 40_001, 5: 30_011}
+SMALL = {1: 2000, 2: 151, 3: 23, 4: 40_001, 5: 30_011, 6: 20_011, 7: 3_001}
 
 
 def make(cfg_id: int, size=None) -> Workload:
@@ -349,6 +380,18 @@ def make(cfg_id: int, size=None) -> Workload:
         scale, tol, K = 0, 1e-6, 256
         part = part_contiguous(n, K)
         recipe = f"n={n}, bw 50: 19 in-band + 3 far cols/row, U(-1,1), diag 1+sum|off|, unscaled, drop_tol=1e-6, K=256 contiguous"
+    elif cfg_id == 6:  # SURVEY §8(f) f3 / §8(d) D2 "4-alt": BASELINE's "mean ~12"
+        n = size
+        rp, ci, v = powerlaw(n, rng, shift=8)
+        scale, tol, K = 1, 0.0, 128
+        part = part_random_iid(n, K, prng)
+        recipe = f"n={n}, row nnz ~ Zipf(2.1)+8 clipped [1,5000] (mean ~12.3), diag forced, N(0,1), scaled, drop_tol=0, K=128 iid"
+    elif cfg_id == 7:  # dense rows
+        n = size
+        rp, ci, v = dense_rows(n, rng)
+        scale, tol, K = 1, 0.0, 32
+        part = part_contiguous(n, K)
+        recipe = f"n={n}, 64 entries/row: diag + 63 uniform cols with |i-j|<=1000, U(-1,1), diag 1+sum|off|, scaled, drop_tol=0, K=32 contiguous"
     else:
         raise ValueError(f"unknown config {cfg_id}")
     return Workload(CONFIG_NAMES[cfg_id], cfg_id, n, n, rp, ci, v, scale, tol, part, K, recipe)

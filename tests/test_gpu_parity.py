@@ -51,7 +51,7 @@ def gpu_build(rig, w, flags=None, **kw):
     return A, g
 
 
-@pytest.mark.parametrize("cfg", [1, 2, 3, 4, 5])
+@pytest.mark.parametrize("cfg", [1, 2, 3, 4, 5, 6, 7])
 def test_small_configs_bitexact(rig, cfg):
     w = make_small(cfg)
     orc = oracle.build(w.row_ptr, w.col_idx, w.val, scale_rows=w.scale_rows, drop_tol=w.drop_tol)

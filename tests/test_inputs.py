@@ -21,7 +21,7 @@ def check_canonical(w):
     assert w.part.min() >= 0 and w.part.max() < w.K
 
 
-@pytest.mark.parametrize("cfg", [1, 2, 3, 4, 5])
+@pytest.mark.parametrize("cfg", [1, 2, 3, 4, 5, 6, 7])
 def test_small_configs_canonical_and_deterministic(cfg):
     a, b = make_small(cfg), make_small(cfg)
     check_canonical(a)
@@ -32,6 +32,14 @@ def test_small_configs_canonical_and_deterministic(cfg):
 
 
 def test_recipe_shapes():
+    # f3 stress configs: mean row length ~12.3 (Zipf + 8), and 64-entry rows
+    # with every column within 1000 of the diagonal
+    w = make_small(6)
+    assert 11.0 < w.nnz / w.n < 13.5
+    w = make_small(7)
+    assert np.all(np.diff(w.row_ptr) == 64)
+    rows = np.repeat(np.arange(w.n), 64)
+    assert np.abs(w.col_idx.astype(np.int64) - rows).max() <= 1000
     w = make(2)
     assert w.n == 1_000_000 and w.nnz == 4_996_000  # N^2 + 4N(N-1)
     w = make_small(3)

@@ -260,7 +260,7 @@ def test_config2_full_counts():
 
 
 # ------------------------------------------------------------------ invariants
-@pytest.mark.parametrize("cfg", [1, 2, 3, 4, 5])
+@pytest.mark.parametrize("cfg", [1, 2, 3, 4, 5, 6, 7])
 def test_invariants_small_configs(cfg):
     w = make_small(cfg)
     g = oracle.build(w.row_ptr, w.col_idx, w.val, scale_rows=w.scale_rows, drop_tol=w.drop_tol,
