@@ -298,6 +298,8 @@ struct CutOut {
 int debug_mask();  // RIG_DEBUG_MASK environment variable (performance experiments only)
 constexpr int kMidSmallCap = 256, kMidBigCap = 2048;  // far-list capacities of the two mid kernels
 void launch_num_mid(const MidArgs &a, int fcap, cudaStream_t s);
+// second pass over the rows launch_num_mid deferred: window |j - i| < 2048
+void launch_num_mid_wide(const MidArgs &a, cudaStream_t s);
 void launch_copy_rows(const int32_t *list, const int64_t *count, int64_t rb, const int64_t *toff, const int64_t *gptr,
                       const int32_t *tcol, const double *tw, int32_t *gcol, double *gw, const CutOut &cut,
                       cudaStream_t s);

@@ -33,11 +33,12 @@ constexpr int kMidThreads = 64;  // 2 warps per CTA: fine-grained shared-memory 
 constexpr int kMidWarps = kMidThreads / 32;
 constexpr int kMidWinHalf = 128;
 constexpr int kMidWin = 2 * kMidWinHalf;
+constexpr int kWideWinHalf = 2048, kWideCap = 64;  // second pass over the deferred rows
 constexpr int kMaxBucket = 96;
 
-template <int FCAP>
+template <int FCAP, int WIN = kMidWin>
 struct MidSmem {
-    double wv[kMidWin];
+    double wv[WIN];
     double fa[FCAP], fb[FCAP];    // factors of the far products (arrival order)
     uint64_t m0[FCAP], m1[FCAP];  // far items (key << 32 | arrival position); sorted copy
     int64_t ecs[32];              // batch of row entries: CSC start, length, a_hat_ik
@@ -105,10 +106,15 @@ __device__ __forceinline__ bool bucket_sort_far(uint64_t *__restrict__ a, uint64
     return true;
 }
 
-template <int FCAP>
+// WH: window half-width.  kMidWinHalf for the mid bins; kWideWinHalf for the
+// rows the first pass deferred (their far list overflowed): rows of banded or
+// FEM-like matrices with long rows keep every key within a few thousand of
+// the diagonal, and a wide window takes them all without sorting.
+template <int FCAP, int WH>
 __global__ void __launch_bounds__(kMidThreads, 8) k_num_mid(MidArgs a) {
+    constexpr int kMidWinHalf = WH, kMidWin = 2 * WH;
     extern __shared__ __align__(16) unsigned char mid_smem[];
-    MidSmem<FCAP> &S = reinterpret_cast<MidSmem<FCAP> *>(mid_smem)[threadIdx.x >> 5];
+    MidSmem<FCAP, kMidWin> &S = reinterpret_cast<MidSmem<FCAP, kMidWin> *>(mid_smem)[threadIdx.x >> 5];
     const int l = lane_id();
     const unsigned lt = lanemask_lt();
     for (int t = l; t < kMidWin; t += 32) S.wv[t] = +0.0;
@@ -233,6 +239,7 @@ __global__ void __launch_bounds__(kMidThreads, 8) k_num_mid(MidArgs a) {
                 }
             }
             __syncwarp();
+            if (FCAP < kMidSmallCap && nfar > FCAP) break;  // wide pass: the row goes on to the huge path
         }
         if (!prefetched) load_meta(idx + nw, nxt);
         cur = nxt;
@@ -306,23 +313,25 @@ __global__ void __launch_bounds__(kMidThreads, 8) k_num_mid(MidArgs a) {
     }
 }
 
-template <int FCAP>
+template <int FCAP, int WH>
 static void launch_mid_t(const MidArgs &a, cudaStream_t s) {
-    const size_t smem = (size_t)kMidWarps * sizeof(MidSmem<FCAP>);
-    cudaFuncSetAttribute(k_num_mid<FCAP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const size_t smem = (size_t)kMidWarps * sizeof(MidSmem<FCAP, 2 * WH>);
+    cudaFuncSetAttribute(k_num_mid<FCAP, WH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_num_mid<FCAP>, kMidThreads, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_num_mid<FCAP, WH>, kMidThreads, smem);
     if (per_sm < 1) per_sm = 1;
     int g = num_sms() * per_sm;
     if (g > kCutSlotsPerLaunch) g = kCutSlotsPerLaunch;
-    k_num_mid<FCAP><<<g, kMidThreads, smem, s>>>(a);
+    k_num_mid<FCAP, WH><<<g, kMidThreads, smem, s>>>(a);
     note_launch();
 }
 
 void launch_num_mid(const MidArgs &a, int fcap, cudaStream_t s) {
     (void)fcap;
-    launch_mid_t<kMidSmallCap>(a, s);
+    launch_mid_t<kMidSmallCap, kMidWinHalf>(a, s);
 }
+
+void launch_num_mid_wide(const MidArgs &a, cudaStream_t s) { launch_mid_t<kWideCap, kWideWinHalf>(a, s); }
 
 // Rows off the merge path: temporary (toff[r], exact count) -> final graph
 // slots [gptr[r], gptr[r+1]).  One warp per row, coalesced.  The fused cut

@@ -589,12 +589,21 @@ static int64_t plan_numeric(rig_plan *p, int32_t *gcol, double *gw, double *diag
             check_launch("mid rows");
             if (p->huge_scratch) {
                 MidArgs hu = ma;
-                hu.list = p->lists + n_mid;  // f_i beyond the mid bins
-                hu.count = p->ctr->list_count + 1;
-                launch_num_huge(hu, p->huge_slots_n, p->huge_scratch, s);
-                check_launch("huge rows");
-                hu.list = p->defer;  // far list beyond the mid kernel's capacity
-                hu.count = p->ctr->defer_count;
+                // rows beyond the mid bins and rows whose far list overflowed:
+                // a wide-window pass (|j - i| < 2048: banded / FEM rows), then
+                // the huge kernel for what that pass defers in turn
+                MidArgs wd = ma;
+                wd.defer_list = p->defer + n_mid;
+                wd.defer_count = p->ctr->defer_count + 1;
+                wd.list = p->lists + n_mid;  // f_i beyond the mid bins
+                wd.count = p->ctr->list_count + 1;
+                launch_num_mid_wide(wd, s);
+                wd.list = p->defer;
+                wd.count = p->ctr->defer_count;
+                launch_num_mid_wide(wd, s);
+                check_launch("huge and deferred rows (wide window)");
+                hu.list = p->defer + n_mid;
+                hu.count = p->ctr->defer_count + 1;
                 launch_num_huge(hu, p->huge_slots_n, p->huge_scratch, s);
                 check_launch("deferred rows");
             }
