@@ -60,7 +60,7 @@ struct DevCounters {
     int64_t mid_slots;     // sum (f_i - len_i) off the merge path: temporary entries
     int64_t sym_count[8];
     int64_t list_count[2]; // mid / huge list lengths (device side)
-    int64_t defer_count[2];// rows deferred by the small / big mid kernels
+    int64_t defer_count[3];// rows deferred by the mid, big-far-list and wide-window passes
     // shape statistics (scan_u32_shape, on the column counts and row pointers)
     int64_t max_col;       // longest column of A
     int64_t p_full;        // sum over columns of len^2 = products of the full matrix (>= the shard's)
@@ -300,6 +300,8 @@ constexpr int kMidSmallCap = 256, kMidBigCap = 2048;  // far-list capacities of 
 void launch_num_mid(const MidArgs &a, int fcap, cudaStream_t s);
 // second pass over the rows launch_num_mid deferred: window |j - i| < 2048
 void launch_num_mid_wide(const MidArgs &a, cudaStream_t s);
+// pass over the rows launch_num_mid deferred with a 1024-item far list
+void launch_num_mid_big(const MidArgs &a, cudaStream_t s);
 void launch_copy_rows(const int32_t *list, const int64_t *count, int64_t rb, const int64_t *toff, const int64_t *gptr,
                       const int32_t *tcol, const double *tw, int32_t *gcol, double *gw, const CutOut &cut,
                       cudaStream_t s);

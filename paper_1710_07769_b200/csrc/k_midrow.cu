@@ -33,8 +33,16 @@ constexpr int kMidThreads = 64;  // 2 warps per CTA: fine-grained shared-memory 
 constexpr int kMidWarps = kMidThreads / 32;
 constexpr int kMidWinHalf = 128;
 constexpr int kMidWin = 2 * kMidWinHalf;
-constexpr int kWideWinHalf = 2048, kWideCap = 64;  // second pass over the deferred rows
+constexpr int kWideWinHalf = 2048, kWideCap = 64;  // a later pass over the deferred rows
+#ifndef RIG_MID_BIG_CAP
+#define RIG_MID_BIG_CAP 768  // measured: 512 / 768 / 1024 on configs 4 and 6
+#endif
+constexpr int kMidBigFarCap = RIG_MID_BIG_CAP;      // the pass between: long far lists (random columns)
 constexpr int kMaxBucket = 96;
+
+// far-sort buckets: 32 for the small far lists, FCAP/8 for bigger ones
+template <int FCAP>
+__host__ __device__ constexpr int far_buckets() { return FCAP <= 256 ? 32 : FCAP / 8; }
 
 template <int FCAP, int WIN = kMidWin>
 struct MidSmem {
@@ -44,20 +52,22 @@ struct MidSmem {
     int64_t ecs[32];              // batch of row entries: CSC start, length, a_hat_ik
     int elen[32];
     double ea[32];
-    int bcnt[32];                 // bucket counts / cursors of the far sort
-    int bst[32];                  // bucket starts
+    int bcnt[far_buckets<FCAP>()];  // bucket counts / cursors of the far sort
+    int bst[far_buckets<FCAP>()];   // bucket starts
 };
 
 __device__ __forceinline__ int it_key(uint64_t v) { return (int)(uint32_t)(v >> 32); }
 __device__ __forceinline__ int it_pos(uint64_t v) { return (int)(uint32_t)v; }
 
-// Sort n unique far items in place (a, via tmp): 32 value buckets filled
-// stably in arrival order (tmp), then every item is placed at its bucket's
-// start plus its rank in the bucket (the count of smaller items there; items
-// are unique), back into a.  Returns false (nothing usable) if a bucket would
-// exceed kMaxBucket.
+// Sort n unique far items in place (a, via tmp): NB value buckets (NB/32 per
+// lane) filled stably in arrival order (tmp), then every item is placed at its
+// bucket's start plus its rank in the bucket (the count of smaller items there;
+// items are unique), back into a.  NB ~ n/4 keeps buckets short for uniform
+// keys.  Returns false (nothing usable) if a bucket would exceed kMaxBucket.
+template <int NB>
 __device__ __forceinline__ bool bucket_sort_far(uint64_t *__restrict__ a, uint64_t *__restrict__ tmp, int *cnt,
                                                 int *bst, int n) {
+    constexpr int PER = NB / 32;
     const int l = lane_id();
     int mn = INT_MAX, mx = INT_MIN;
     for (int p = l; p < n; p += 32) {
@@ -67,26 +77,36 @@ __device__ __forceinline__ bool bucket_sort_far(uint64_t *__restrict__ a, uint64
     }
     mn = __reduce_min_sync(kFull, mn);
     mx = __reduce_max_sync(kFull, mx);
-    // bucket(k) = floor((k - mn) * mul / 2^32) in [0, 32), monotone in k
-    const uint64_t mul = ((1ull << 37) - 1) / (uint64_t)((int64_t)mx - mn + 1);
+    // bucket(k) = floor((k - mn) * mul / 2^32) in [0, NB), monotone in k
+    const uint64_t mul = (((uint64_t)NB << 32) - 1) / (uint64_t)((int64_t)mx - mn + 1);
     auto bucket = [&](uint64_t v) { return (int)(((uint64_t)(uint32_t)(it_key(v) - mn) * mul) >> 32); };
-    cnt[l] = 0;
+#pragma unroll
+    for (int u = 0; u < PER; ++u) cnt[l * PER + u] = 0;
     __syncwarp();
     for (int p = l; p < n; p += 32) atomicAdd(&cnt[bucket(a[p])], 1);
     __syncwarp();
-    const int c = cnt[l];
-    if (__any_sync(kFull, c > kMaxBucket)) return false;
-
-    const int base = warp_incl_scan(c) - c;
+    int c[PER], tot = 0, big = 0;
+#pragma unroll
+    for (int u = 0; u < PER; ++u) {
+        c[u] = cnt[l * PER + u];
+        tot += c[u];
+        big |= c[u] > kMaxBucket;
+    }
+    if (__any_sync(kFull, big)) return false;
+    int base = warp_incl_scan(tot) - tot;
     __syncwarp();
-    cnt[l] = base;  // running cursor of bucket l
-    bst[l] = base;
+#pragma unroll
+    for (int u = 0; u < PER; ++u) {  // running cursors, bucket starts
+        cnt[l * PER + u] = base;
+        bst[l * PER + u] = base;
+        base += c[u];
+    }
     __syncwarp();
     const unsigned lt = lanemask_lt();
     for (int p0 = 0; p0 < n; p0 += 32) {  // arrival order (stable)
         const int p = p0 + l;
         const uint64_t v = p < n ? a[p] : 0ull;
-        const int b = p < n ? bucket(v) : 32 + l;
+        const int b = p < n ? bucket(v) : NB + l;
         const unsigned g = __match_any_sync(kFull, b);
         if (p < n) tmp[cnt[b] + __popc(g & lt)] = v;
         __syncwarp();
@@ -239,7 +259,7 @@ __global__ void __launch_bounds__(kMidThreads, 8) k_num_mid(MidArgs a) {
                 }
             }
             __syncwarp();
-            if (FCAP < kMidSmallCap && nfar > FCAP) break;  // wide pass: the row goes on to the huge path
+            if (FCAP != kMidSmallCap && nfar > FCAP) break;  // later passes: the row goes on
         }
         if (!prefetched) load_meta(idx + nw, nxt);
         cur = nxt;
@@ -249,7 +269,7 @@ __global__ void __launch_bounds__(kMidThreads, 8) k_num_mid(MidArgs a) {
         bool ok = nfar <= FCAP;
         if (a.dbg & 2) nfar = 0;
         if (ok && nfar > 1 && !(a.dbg & 1)) {
-            ok = bucket_sort_far(S.m0, S.m1, S.bcnt, S.bst, nfar);  // sorted in place (m0)
+            ok = bucket_sort_far<far_buckets<FCAP>()>(S.m0, S.m1, S.bcnt, S.bst, nfar);  // sorted in place (m0)
         }
         if (!ok) {
             for (int t = l; t < kMidWin; t += 32) S.wv[t] = +0.0;
@@ -332,6 +352,8 @@ void launch_num_mid(const MidArgs &a, int fcap, cudaStream_t s) {
 }
 
 void launch_num_mid_wide(const MidArgs &a, cudaStream_t s) { launch_mid_t<kWideCap, kWideWinHalf>(a, s); }
+
+void launch_num_mid_big(const MidArgs &a, cudaStream_t s) { launch_mid_t<kMidBigFarCap, kMidWinHalf>(a, s); }
 
 // Rows off the merge path: temporary (toff[r], exact count) -> final graph
 // slots [gptr[r], gptr[r+1]).  One warp per row, coalesced.  The fused cut

@@ -520,7 +520,7 @@ static void plan_build(rig_plan *p, const rig_csr_t *Ain, bool allow_early = fal
     const size_t o_toff = LB.add(sizeof(int64_t) * (size_t)(nloc + 1));
     const size_t o_st2 = LB.add(scan_tmp_bytes(nloc));
     const size_t o_lists = LB.add(sizeof(int32_t) * 2 * (size_t)n_mid);
-    const size_t o_defer = LB.add(sizeof(int32_t) * 2 * (size_t)n_mid);
+    const size_t o_defer = LB.add(sizeof(int32_t) * 3 * (size_t)n_mid);
     const size_t o_bcnt = LB.add(sizeof(unsigned) * nbc);
     const size_t o_boff = LB.add(sizeof(int64_t) * (nbc + 1));
     const size_t o_bst = LB.add(scan_tmp_bytes((int64_t)nbc));
@@ -589,21 +589,30 @@ static int64_t plan_numeric(rig_plan *p, int32_t *gcol, double *gw, double *diag
             check_launch("mid rows");
             if (p->huge_scratch) {
                 MidArgs hu = ma;
-                // rows beyond the mid bins and rows whose far list overflowed:
-                // a wide-window pass (|j - i| < 2048: banded / FEM rows), then
-                // the huge kernel for what that pass defers in turn
+                // rows whose far list overflowed: a pass with a 1024-item far
+                // list (long rows of random columns); then the rows beyond the
+                // mid bins and what that pass deferred: a wide-window pass
+                // (|j - i| < 2048: banded / FEM rows); the huge kernel takes
+                // what remains
+                MidArgs bg = ma;
+                bg.list = p->defer;
+                bg.count = p->ctr->defer_count;
+                bg.defer_list = p->defer + n_mid;
+                bg.defer_count = p->ctr->defer_count + 1;
+                launch_num_mid_big(bg, s);
+                check_launch("deferred rows (long far lists)");
                 MidArgs wd = ma;
-                wd.defer_list = p->defer + n_mid;
-                wd.defer_count = p->ctr->defer_count + 1;
+                wd.defer_list = p->defer + 2 * n_mid;
+                wd.defer_count = p->ctr->defer_count + 2;
                 wd.list = p->lists + n_mid;  // f_i beyond the mid bins
                 wd.count = p->ctr->list_count + 1;
                 launch_num_mid_wide(wd, s);
-                wd.list = p->defer;
-                wd.count = p->ctr->defer_count;
+                wd.list = p->defer + n_mid;
+                wd.count = p->ctr->defer_count + 1;
                 launch_num_mid_wide(wd, s);
                 check_launch("huge and deferred rows (wide window)");
-                hu.list = p->defer + n_mid;
-                hu.count = p->ctr->defer_count + 1;
+                hu.list = p->defer + 2 * n_mid;
+                hu.count = p->ctr->defer_count + 2;
                 launch_num_huge(hu, p->huge_slots_n, p->huge_scratch, s);
                 check_launch("deferred rows");
             }
