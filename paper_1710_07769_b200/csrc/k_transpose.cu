@@ -491,47 +491,82 @@ __global__ void __launch_bounds__(kSymThreads) k_sym_transpose(Csr A, int scale,
         }
         if (r0 == 0 && l == 0) cp[0] = 0;
         const double my_n = scale && l < rows ? nrm[r0 + l] : 1.0, my_y = scale && l < rows ? y[r0 + l] : 1.0;
-        for (int64_t c0 = __shfl_sync(kFull, my_s, 0); c0 < hi; c0 += 32) {
+#ifndef RIG_SYM_U
+#define RIG_SYM_U 4  // measured 1, 2, 4 on config 3
+#endif
+        constexpr int U = RIG_SYM_U;  // chunks of 32 entries in flight per warp
+        for (int64_t c0 = __shfl_sync(kFull, my_s, 0); c0 < hi; c0 += 32 * U) {
             if (*reinterpret_cast<volatile int *>(fail)) return;
-            const int64_t p = c0 + l;
-            // row of p: the last lane u < rows with rp[r0 + u] <= p
-            int u = 0;
+            int64_t p[U], k[U], q[U];
+            int j[U], cq[U];
+            double akj[U], nk[U], yk[U], nj[U], yj[U], vq[U];
 #pragma unroll
-            for (int b = 16; b > 0; b >>= 1) {
-                const int64_t sv = __shfl_sync(kFull, my_s, u + b < rows ? u + b : rows - 1);
-                if (u + b < rows && sv <= p) u += b;
+            for (int t = 0; t < U; ++t) {  // round 1: the entry, its row (shuffle search)
+                p[t] = c0 + 32 * t + l;
+                int u = 0;
+#pragma unroll
+                for (int b = 16; b > 0; b >>= 1) {
+                    const int64_t sv = __shfl_sync(kFull, my_s, u + b < rows ? u + b : rows - 1);
+                    if (u + b < rows && sv <= p[t]) u += b;
+                }
+                k[t] = r0 + u;
+                q[t] = __shfl_sync(kFull, my_s, u);  // row start, for the mirror guess
+                nk[t] = shfl_d(my_n, u);
+                yk[t] = shfl_d(my_y, u);
+                j[t] = p[t] < hi ? A.ci[p[t]] : -1;
+                akj[t] = p[t] < hi ? A.v[p[t]] : 0.0;
             }
-            const int64_t k = r0 + u;
-            const int64_t sk = __shfl_sync(kFull, my_s, u);
-            const double nk = shfl_d(my_n, u), yk = shfl_d(my_y, u);
-            if (p >= hi) continue;
-            const int j = A.ci[p];
-            const double akj = A.v[p];
-            const int64_t sj = A.rp[j], ej = A.rp[j + 1];
-            // mirrored position guess, then a search of row j (short rows
-            // only: a longer one ends the attempt)
-            int64_t q = ej - 1 - (p - sk);
-            if (q < sj || q >= ej || A.ci[q] != (int)k) {
-                q = -1;
-                if (ej - sj <= 64) {
-                    for (int64_t b0 = sj; b0 < ej && q < 0; b0 += 8) {
-                        int cc[8];
+            int64_t sj[U], ej[U];
 #pragma unroll
-                        for (int t = 0; t < 8; ++t) cc[t] = b0 + t < ej ? A.ci[b0 + t] : -1;
-#pragma unroll
-                        for (int t = 0; t < 8; ++t)
-                            if (cc[t] == (int)k) q = b0 + t;
+            for (int t = 0; t < U; ++t) {  // round 2: row j's bounds and scale
+                sj[t] = 0;
+                ej[t] = 0;
+                nj[t] = 1.0;
+                yj[t] = 1.0;
+                if (j[t] >= 0) {
+                    sj[t] = A.rp[j[t]];
+                    ej[t] = A.rp[j[t] + 1];
+                    if (scale) {
+                        nj[t] = nrm[j[t]];
+                        yj[t] = y[j[t]];
                     }
                 }
             }
-            if (q < 0) {  // no mirror entry (j, k): not pattern-symmetric
-                atomicOr(fail, 1);
-                continue;
+#pragma unroll
+            for (int t = 0; t < U; ++t) {  // round 3: the mirrored position, column and value together
+                q[t] = ej[t] - 1 - (p[t] - q[t]);
+                cq[t] = -1;
+                vq[t] = 0.0;
+                if (j[t] >= 0 && q[t] >= sj[t] && q[t] < ej[t]) {
+                    cq[t] = A.ci[q[t]];
+                    vq[t] = A.v[q[t]];
+                }
             }
-            const double ajk = A.v[q];
-            ri[p + k] = j;
-            vt[p + k] = scale ? div_rn_fast(ajk, nrm[j], y[j]) : ajk;
-            if (scale) ahat[p] = div_rn_fast(akj, nk, yk);
+#pragma unroll
+            for (int t = 0; t < U; ++t) {
+                if (j[t] < 0) continue;
+                if (cq[t] != (int)k[t]) {  // search row j (short rows only: a longer one ends the attempt)
+                    q[t] = -1;
+                    if (ej[t] - sj[t] <= 64) {
+                        for (int64_t b0 = sj[t]; b0 < ej[t] && q[t] < 0; b0 += 8) {
+                            int cc[8];
+#pragma unroll
+                            for (int z = 0; z < 8; ++z) cc[z] = b0 + z < ej[t] ? A.ci[b0 + z] : -1;
+#pragma unroll
+                            for (int z = 0; z < 8; ++z)
+                                if (cc[z] == (int)k[t]) q[t] = b0 + z;
+                        }
+                    }
+                    if (q[t] < 0) {  // no mirror entry (j, k): not pattern-symmetric
+                        atomicOr(fail, 1);
+                        continue;
+                    }
+                    vq[t] = A.v[q[t]];
+                }
+                ri[p[t] + k[t]] = j[t];
+                vt[p[t] + k[t]] = scale ? div_rn_fast(vq[t], nj[t], yj[t]) : vq[t];
+                if (scale) ahat[p[t]] = div_rn_fast(akj[t], nk[t], yk[t]);
+            }
         }
     }
 }
