@@ -213,7 +213,10 @@ __global__ void __launch_bounds__(kMidThreads, 8) k_num_mid(MidArgs a) {
                 prefetched = true;
             }
             if (short_cols) {
-                constexpr int kDepth = 8;  // columns in flight
+#ifndef RIG_MID_DEPTH
+#define RIG_MID_DEPTH 12  // measured 4, 8, 12, 16 on config 5
+#endif
+                constexpr int kDepth = RIG_MID_DEPTH;  // columns in flight
                 int pj[kDepth];
                 double pb[kDepth];
 #pragma unroll
