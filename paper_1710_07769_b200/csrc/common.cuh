@@ -296,7 +296,10 @@ struct CutOut {
     int *used;
 };
 int debug_mask();  // RIG_DEBUG_MASK environment variable (performance experiments only)
-constexpr int kMidSmallCap = 256, kMidBigCap = 2048;  // far-list capacities of the two mid kernels
+#ifndef RIG_MID_CAP
+#define RIG_MID_CAP 256
+#endif
+constexpr int kMidSmallCap = RIG_MID_CAP, kMidBigCap = 2048;  // far-list capacities of the mid kernels
 void launch_num_mid(const MidArgs &a, int fcap, cudaStream_t s);
 // second pass over the rows launch_num_mid deferred: window |j - i| < 2048
 void launch_num_mid_wide(const MidArgs &a, cudaStream_t s);
