@@ -60,7 +60,7 @@ struct DevCounters {
     int64_t mid_slots;     // sum (f_i - len_i) off the merge path: temporary entries
     int64_t sym_count[8];
     int64_t list_count[2]; // mid / huge list lengths (device side)
-    int64_t defer_count[3];// rows deferred by the mid, big-far-list and wide-window passes
+    int64_t defer_count[4];// rows deferred by the mid, big-far-list, wide-window and global-far-list passes
     // shape statistics (scan_u32_shape, on the column counts and row pointers)
     int64_t max_col;       // longest column of A
     int64_t p_full;        // sum over columns of len^2 = products of the full matrix (>= the shard's)
@@ -285,6 +285,8 @@ struct MidArgs {
     double *diag;           // may be null
     double tol;
     int dbg;  // experiment switches (RIG_DEBUG_MASK); 0 in normal operation
+    void *fscratch;          // far lists of launch_num_mid_gfar (mid_gfar_scratch_bytes)
+    int64_t fscratch_bytes;
 };
 // Fused a7 partials of one launch (part == nullptr: off): each CTA writes the
 // Neumaier sum of its cut edges to cutp[blockIdx.x], *used = gridDim.x.
@@ -303,8 +305,12 @@ constexpr int kMidSmallCap = RIG_MID_CAP, kMidBigCap = 2048;  // far-list capaci
 void launch_num_mid(const MidArgs &a, int fcap, cudaStream_t s);
 // second pass over the rows launch_num_mid deferred: window |j - i| < 2048
 void launch_num_mid_wide(const MidArgs &a, cudaStream_t s);
-// pass over the rows launch_num_mid deferred with a 1024-item far list
+// pass over the rows launch_num_mid deferred with a 768-item far list
 void launch_num_mid_big(const MidArgs &a, cudaStream_t s);
+// pass with a 4096-item far list in global scratch (MidArgs::fscratch)
+void launch_num_mid_gfar(const MidArgs &a, cudaStream_t s);
+size_t mid_gfar_scratch_bytes();
+constexpr int kMidBigFarCapHost = 768;  // = kMidBigFarCap (k_midrow.cu): rows with f_i beyond it may reach the gfar pass
 void launch_copy_rows(const int32_t *list, const int64_t *count, int64_t rb, const int64_t *toff, const int64_t *gptr,
                       const int32_t *tcol, const double *tw, int32_t *gcol, double *gw, const CutOut &cut,
                       cudaStream_t s);

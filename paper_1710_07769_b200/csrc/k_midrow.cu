@@ -38,17 +38,21 @@ constexpr int kWideWinHalf = 2048, kWideCap = 64;  // a later pass over the defe
 #define RIG_MID_BIG_CAP 768  // measured: 512 / 768 / 1024 on configs 4 and 6
 #endif
 constexpr int kMidBigFarCap = RIG_MID_BIG_CAP;      // the pass between: long far lists (random columns)
+constexpr int kMidGlobalFarCap = 4096;              // far lists in global scratch: rows up to f_i ~ 4096
 constexpr int kMaxBucket = 96;
 
 // far-sort buckets: 32 for the small far lists, FCAP/8 for bigger ones
 template <int FCAP>
 __host__ __device__ constexpr int far_buckets() { return FCAP <= 256 ? 32 : FCAP / 8; }
 
-template <int FCAP, int WIN = kMidWin>
+// GFAR: the far list lives in a per-warp slice of global scratch (MidArgs::
+// fscratch) instead of shared memory -- long lists, few rows.
+template <int FCAP, int WIN = kMidWin, bool GFAR = false>
 struct MidSmem {
+    static constexpr int FS = GFAR ? 1 : FCAP;
     double wv[WIN];
-    double fa[FCAP], fb[FCAP];    // factors of the far products (arrival order)
-    uint64_t m0[FCAP], m1[FCAP];  // far items (key << 32 | arrival position); sorted copy
+    double fa[FS], fb[FS];        // factors of the far products (arrival order)
+    uint64_t m0[FS], m1[FS];      // far items (key << 32 | arrival position); sorted copy
     int64_t ecs[32];              // batch of row entries: CSC start, length, a_hat_ik
     int elen[32];
     double ea[32];
@@ -130,11 +134,21 @@ __device__ __forceinline__ bool bucket_sort_far(uint64_t *__restrict__ a, uint64
 // rows the first pass deferred (their far list overflowed): rows of banded or
 // FEM-like matrices with long rows keep every key within a few thousand of
 // the diagonal, and a wide window takes them all without sorting.
-template <int FCAP, int WH>
+template <int FCAP, int WH, bool GFAR>
 __global__ void __launch_bounds__(kMidThreads, 8) k_num_mid(MidArgs a) {
     constexpr int kMidWinHalf = WH, kMidWin = 2 * WH;
     extern __shared__ __align__(16) unsigned char mid_smem[];
-    MidSmem<FCAP, kMidWin> &S = reinterpret_cast<MidSmem<FCAP, kMidWin> *>(mid_smem)[threadIdx.x >> 5];
+    MidSmem<FCAP, kMidWin, GFAR> &S = reinterpret_cast<MidSmem<FCAP, kMidWin, GFAR> *>(mid_smem)[threadIdx.x >> 5];
+    double *far_a = S.fa, *far_b = S.fb;
+    uint64_t *far_m0 = S.m0, *far_m1 = S.m1;
+    if constexpr (GFAR) {  // this warp's slice: m0, m1, fa, fb (FCAP each)
+        const int64_t gw = (int64_t)blockIdx.x * kMidWarps + (threadIdx.x >> 5);
+        uint64_t *base = reinterpret_cast<uint64_t *>(a.fscratch) + gw * 4 * (int64_t)FCAP;
+        far_m0 = base;
+        far_m1 = base + FCAP;
+        far_a = reinterpret_cast<double *>(base + 2 * FCAP);
+        far_b = reinterpret_cast<double *>(base + 3 * FCAP);
+    }
     const int l = lane_id();
     const unsigned lt = lanemask_lt();
     for (int t = l; t < kMidWin; t += 32) S.wv[t] = +0.0;
@@ -182,9 +196,9 @@ __global__ void __launch_bounds__(kMidThreads, 8) k_num_mid(MidArgs a) {
             const unsigned fm = __ballot_sync(kFull, far);
             const int pos = nfar + __popc(fm & lt);
             if (far && pos < FCAP && !(a.dbg & 2)) {
-                S.m0[pos] = ((uint64_t)(uint32_t)j << 32) | (uint32_t)pos;
-                S.fa[pos] = at;
-                S.fb[pos] = b;
+                far_m0[pos] = ((uint64_t)(uint32_t)j << 32) | (uint32_t)pos;
+                far_a[pos] = at;
+                far_b[pos] = b;
             }
             nfar += __popc(fm);
         };
@@ -268,11 +282,11 @@ __global__ void __launch_bounds__(kMidThreads, 8) k_num_mid(MidArgs a) {
         cur = nxt;
         __syncwarp();
         // ---- sort the far items (or defer the row to the huge path)
-        const uint64_t *srt = S.m0;
+        const uint64_t *srt = far_m0;
         bool ok = nfar <= FCAP;
         if (a.dbg & 2) nfar = 0;
         if (ok && nfar > 1 && !(a.dbg & 1)) {
-            ok = bucket_sort_far<far_buckets<FCAP>()>(S.m0, S.m1, S.bcnt, S.bst, nfar);  // sorted in place (m0)
+            ok = bucket_sort_far<far_buckets<FCAP>()>(far_m0, far_m1, S.bcnt, S.bst, nfar);  // sorted in place (m0)
         }
         if (!ok) {
             for (int t = l; t < kMidWin; t += 32) S.wv[t] = +0.0;
@@ -306,7 +320,7 @@ __global__ void __launch_bounds__(kMidThreads, 8) k_num_mid(MidArgs a) {
                         int q = p;
                         do {
                             const int x = it_pos(srt[q]);
-                            acc = __fma_rn(S.fa[x], S.fb[x], acc);
+                            acc = __fma_rn(far_a[x], far_b[x], acc);
                             ++q;
                         } while (q < nfar && it_key(srt[q]) == key);
                         w = fabs(acc);
@@ -336,16 +350,21 @@ __global__ void __launch_bounds__(kMidThreads, 8) k_num_mid(MidArgs a) {
     }
 }
 
-template <int FCAP, int WH>
+template <int FCAP, int WH, bool GFAR = false>
 static void launch_mid_t(const MidArgs &a, cudaStream_t s) {
-    const size_t smem = (size_t)kMidWarps * sizeof(MidSmem<FCAP, 2 * WH>);
-    cudaFuncSetAttribute(k_num_mid<FCAP, WH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const size_t smem = (size_t)kMidWarps * sizeof(MidSmem<FCAP, 2 * WH, GFAR>);
+    cudaFuncSetAttribute(k_num_mid<FCAP, WH, GFAR>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_num_mid<FCAP, WH>, kMidThreads, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_num_mid<FCAP, WH, GFAR>, kMidThreads, smem);
     if (per_sm < 1) per_sm = 1;
     int g = num_sms() * per_sm;
     if (g > kCutSlotsPerLaunch) g = kCutSlotsPerLaunch;
-    k_num_mid<FCAP, WH><<<g, kMidThreads, smem, s>>>(a);
+    if (GFAR) {  // the global far lists: a slice per warp
+        const int64_t cap = a.fscratch_bytes / ((int64_t)kMidWarps * 4 * 8 * FCAP);
+        if (g > cap) g = (int)cap;
+        if (g < 1) return;
+    }
+    k_num_mid<FCAP, WH, GFAR><<<g, kMidThreads, smem, s>>>(a);
     note_launch();
 }
 
@@ -357,6 +376,10 @@ void launch_num_mid(const MidArgs &a, int fcap, cudaStream_t s) {
 void launch_num_mid_wide(const MidArgs &a, cudaStream_t s) { launch_mid_t<kWideCap, kWideWinHalf>(a, s); }
 
 void launch_num_mid_big(const MidArgs &a, cudaStream_t s) { launch_mid_t<kMidBigFarCap, kMidWinHalf>(a, s); }
+
+void launch_num_mid_gfar(const MidArgs &a, cudaStream_t s) { launch_mid_t<kMidGlobalFarCap, kMidWinHalf, true>(a, s); }
+
+size_t mid_gfar_scratch_bytes() { return (size_t)num_sms() * 16 * kMidWarps * 4 * 8 * kMidGlobalFarCap; }
 
 // Rows off the merge path: temporary (toff[r], exact count) -> final graph
 // slots [gptr[r], gptr[r+1]).  One warp per row, coalesced.  The fused cut

@@ -328,6 +328,7 @@ struct rig_plan {
     int32_t *tcol = nullptr;
     double *tw = nullptr;
     void *huge_scratch = nullptr;
+    void *gfar = nullptr;  // far-list scratch of launch_num_mid_gfar
     int huge_slots_n = 0;
     int64_t nnz_upper = 0;  // >= graph nnz: sum (f_i - len_i)
     bool cached = false;    // simple API: internal buffers from the per-thread cache
@@ -520,12 +521,15 @@ static void plan_build(rig_plan *p, const rig_csr_t *Ain, bool allow_early = fal
     const size_t o_toff = LB.add(sizeof(int64_t) * (size_t)(nloc + 1));
     const size_t o_st2 = LB.add(scan_tmp_bytes(nloc));
     const size_t o_lists = LB.add(sizeof(int32_t) * 2 * (size_t)n_mid);
-    const size_t o_defer = LB.add(sizeof(int32_t) * 3 * (size_t)n_mid);
+    const size_t o_defer = LB.add(sizeof(int32_t) * 4 * (size_t)n_mid);
     const size_t o_bcnt = LB.add(sizeof(unsigned) * nbc);
     const size_t o_boff = LB.add(sizeof(int64_t) * (nbc + 1));
     const size_t o_bst = LB.add(scan_tmp_bytes((int64_t)nbc));
     const size_t o_tcol = LB.add(sizeof(int32_t) * (size_t)p->h.mid_slots);
     const size_t o_tw = LB.add(sizeof(double) * (size_t)p->h.mid_slots);
+    // far lists of the global-far-list pass (rows that can outgrow the 768-item list)
+    const bool need_gfar = p->h.max_f > kMidBigFarCapHost;
+    const size_t o_gfar = need_gfar ? LB.add(mid_gfar_scratch_bytes()) : 0;
     size_t o_huge = 0;
     if (need_huge) {
         p->huge_slots_n = huge_slots(n, p->h.max_f > kMidSmallCap ? n_mid : std::min<int64_t>(n_mid, 8),
@@ -536,6 +540,7 @@ static void plan_build(rig_plan *p, const rig_csr_t *Ain, bool allow_early = fal
     p->toff = reinterpret_cast<int64_t *>(wb + o_toff);
     p->lists = reinterpret_cast<int32_t *>(wb + o_lists);
     p->defer = reinterpret_cast<int32_t *>(wb + o_defer);
+    p->gfar = need_gfar ? wb + o_gfar : nullptr;
     p->tcol = reinterpret_cast<int32_t *>(wb + o_tcol);
     p->tw = reinterpret_cast<double *>(wb + o_tw);
     if (need_huge) {
@@ -613,6 +618,19 @@ static int64_t plan_numeric(rig_plan *p, int32_t *gcol, double *gw, double *diag
                 check_launch("huge and deferred rows (wide window)");
                 hu.list = p->defer + 2 * n_mid;
                 hu.count = p->ctr->defer_count + 2;
+                if (p->gfar) {  // far lists up to 4096 items in global scratch
+                    MidArgs gf = ma;
+                    gf.list = p->defer + 2 * n_mid;
+                    gf.count = p->ctr->defer_count + 2;
+                    gf.defer_list = p->defer + 3 * n_mid;
+                    gf.defer_count = p->ctr->defer_count + 3;
+                    gf.fscratch = p->gfar;
+                    gf.fscratch_bytes = (int64_t)mid_gfar_scratch_bytes();
+                    launch_num_mid_gfar(gf, s);
+                    check_launch("deferred rows (global far lists)");
+                    hu.list = p->defer + 3 * n_mid;
+                    hu.count = p->ctr->defer_count + 3;
+                }
                 launch_num_huge(hu, p->huge_slots_n, p->huge_scratch, s);
                 check_launch("deferred rows");
             }
