@@ -287,6 +287,7 @@ struct MidArgs {
     int dbg;  // experiment switches (RIG_DEBUG_MASK); 0 in normal operation
     void *fscratch;          // far lists of launch_num_mid_gfar (mid_gfar_scratch_bytes)
     int64_t fscratch_bytes;
+    const int64_t *fnm;      // [nloc] f_i - len_i (gfar pass: rows far beyond its capacity skip it)
 };
 // Fused a7 partials of one launch (part == nullptr: off): each CTA writes the
 // Neumaier sum of its cut edges to cutp[blockIdx.x], *used = gridDim.x.

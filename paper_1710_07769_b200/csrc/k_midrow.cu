@@ -187,6 +187,13 @@ __global__ void __launch_bounds__(kMidThreads, 8) k_num_mid(MidArgs a) {
         const int wbase = (int)i - kMidWinHalf;
         int nfar = 0;
         bool prefetched = false;
+        if (GFAR && a.fnm && a.fnm[r] > 2 * (int64_t)FCAP) {  // far beyond this pass: on to the huge kernel
+            if (l == 0) a.defer_list[atomicAdd((unsigned long long *)a.defer_count, 1ull)] = (int32_t)i;
+            load_meta(idx + nw, nxt);
+            cur = nxt;
+            __syncwarp();
+            continue;
+        }
         // one column step: lanes hold rows j of a column of a_ik = at
         auto apply = [&](int j, double b, double at, bool v) {
             const int d = j - wbase;

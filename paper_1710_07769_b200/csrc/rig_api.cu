@@ -329,6 +329,7 @@ struct rig_plan {
     double *tw = nullptr;
     void *huge_scratch = nullptr;
     void *gfar = nullptr;  // far-list scratch of launch_num_mid_gfar
+    int64_t *fnm = nullptr;  // [nloc] f_i - len_i off the merge path
     int huge_slots_n = 0;
     int64_t nnz_upper = 0;  // >= graph nnz: sum (f_i - len_i)
     bool cached = false;    // simple API: internal buffers from the per-thread cache
@@ -398,6 +399,7 @@ static void plan_build(rig_plan *p, const rig_csr_t *Ain, bool allow_early = fal
     double *vt = reinterpret_cast<double *>(ws + o_vt) + 1;
     p->nnzc = reinterpret_cast<int64_t *>(ws + o_nnzc);
     int64_t *fnm = reinterpret_cast<int64_t *>(ws + o_fnm);
+    p->fnm = fnm;
     uint8_t *bin8 = reinterpret_cast<uint8_t *>(ws + o_bin8);
     HostStage *hs = host_stage();
 
@@ -626,6 +628,7 @@ static int64_t plan_numeric(rig_plan *p, int32_t *gcol, double *gw, double *diag
                     gf.defer_count = p->ctr->defer_count + 3;
                     gf.fscratch = p->gfar;
                     gf.fscratch_bytes = (int64_t)mid_gfar_scratch_bytes();
+                    gf.fnm = p->fnm;
                     launch_num_mid_gfar(gf, s);
                     check_launch("deferred rows (global far lists)");
                     hu.list = p->defer + 3 * n_mid;
