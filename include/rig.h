@@ -222,6 +222,38 @@ RIG_API int rig_csr_free(rig_csr_t *A, rig_stream_t stream);
  * Costs in (0, 1] (scaled rows) give weights in [1, alpha].  Asynchronous. */
 RIG_API int rig_int_weights(const double *w, int64_t n, int64_t alpha, int64_t *wgt, rig_stream_t stream);
 
+/* ---- f4: first stage of a multilevel partitioner ----- */
+
+/* Coarse graph of one coarsening step: library-owned DEVICE arrays (one
+ * allocation, stream-ordered), released with rig_coarse_free. */
+typedef struct {
+    int64_t n;        /* coarse vertices */
+    int64_t nnz;      /* stored coarse edges (both directions) */
+    int64_t *row_ptr; /* [n+1] */
+    int32_t *col_idx; /* [nnz] coarse ids, ascending per row */
+    int64_t *wgt;     /* [nnz] summed fine edge weights */
+    int64_t *vwgt;    /* [n] summed fine vertex weights */
+    int32_t *cmap;    /* [n_fine] coarse id of every fine vertex */
+} rig_coarse_t;
+
+/* Heavy-edge matching on a symmetric graph with int64 edge weights (the
+ * METIS input of PAPER.md:609-613: rig_int_weights of G_RIP), all DEVICE
+ * arrays: row_ptr [n+1], col [nnz] (no self loops), wgt [nnz]; match [n]
+ * receives each vertex's partner or -1.  DESIGN.md R23: in each of `rounds`
+ * rounds every unmatched vertex picks its heaviest unmatched neighbour (ties:
+ * the smaller index) and mutual picks match.  Asynchronous. */
+RIG_API int rig_hem_match(const int64_t *row_ptr, const int32_t *col, const int64_t *wgt, int64_t n,
+                          int32_t rounds, int32_t *match, rig_stream_t stream);
+
+/* One coarsening step (R24-R25): matched pairs and unmatched
+ * vertices become coarse vertices numbered by their smaller member; coarse
+ * edge weights sum the fine edges between the groups (the contracted edges
+ * vanish); vwgt [n] (DEVICE, may be NULL: unit weights) are summed.  Integer
+ * sums: exact.  Synchronises twice (coarse size, coarse nnz). */
+RIG_API int rig_coarsen(const int64_t *row_ptr, const int32_t *col, const int64_t *wgt, const int64_t *vwgt,
+                        int64_t n, const int32_t *match, rig_coarse_t *out, rig_stream_t stream);
+RIG_API int rig_coarse_free(rig_coarse_t *c, rig_stream_t stream);
+
 /* ---- end-to-end from host memory --------------------------------------- */
 
 /* Host-to-host convenience for the whole path: copies A (HOST CSR) and part

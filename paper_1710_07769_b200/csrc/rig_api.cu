@@ -1059,6 +1059,114 @@ int rig_csr_free(rig_csr_t *A, rig_stream_t stream) {
     ABI_END
 }
 
+int rig_hem_match(const int64_t *row_ptr, const int32_t *col, const int64_t *wgt, int64_t n, int32_t rounds,
+                  int32_t *match, rig_stream_t stream) {
+    ABI_BEGIN
+    if (n < 0 || rounds < 0 || (n > 0 && (!row_ptr || !col || !wgt || !match)))
+        throw Error(RIG_ERR_INVALID, "NULL argument, n < 0 or rounds < 0");
+    if (n == 0) return RIG_OK;
+    cudaStream_t s = (cudaStream_t)stream;
+    Arena ar(s);
+    int32_t *cand = ar.get<int32_t>(n);
+    CK(cudaMemsetAsync(match, 0xff, sizeof(int32_t) * (size_t)n, s));  // -1: unmatched
+    for (int r = 0; r < rounds; ++r) launch_hem_round(row_ptr, col, wgt, n, match, cand, s);
+    check_launch("hem_match");
+    return RIG_OK;
+    ABI_END
+}
+
+int rig_coarsen(const int64_t *row_ptr, const int32_t *col, const int64_t *wgt, const int64_t *vwgt, int64_t n,
+                const int32_t *match, rig_coarse_t *out, rig_stream_t stream) {
+    ABI_BEGIN
+    if (!out || n < 0 || (n > 0 && (!row_ptr || !col || !wgt || !match))) throw Error(RIG_ERR_INVALID, "NULL argument");
+    std::memset(out, 0, sizeof(*out));
+    if (n == 0) return RIG_OK;
+    cudaStream_t s = (cudaStream_t)stream;
+    Arena ar(s);
+    int64_t *flag = ar.get<int64_t>(n);
+    int64_t *cid = ar.get<int64_t>(n + 1);
+    void *st = ar.raw(scan_tmp_bytes(n));
+    int32_t *lead = ar.get<int32_t>(n);
+    int64_t *cvw_tmp = ar.get<int64_t>(n);
+    unsigned long long *maxit = ar.get<unsigned long long>(1);
+    CK(cudaMemsetAsync(maxit, 0, sizeof(unsigned long long), s));
+    unsigned char *block = nullptr;
+    try {
+        // cmap lives in the output block; allocate it with the vertex arrays once nc is known
+        int32_t *cmap_tmp = ar.get<int32_t>(n);
+        launch_leader_flags(match, n, flag, s);
+        scan_i64(flag, n, cid, ScanOp::Identity, st, 0, s);
+        launch_coarse_map(row_ptr, match, vwgt, n, cid, cmap_tmp, lead, cvw_tmp, maxit, s);
+        check_launch("coarse map");
+        HostStage *hs = host_stage();
+        CK(cudaMemcpyAsync(&hs->v[0], cid + n, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(&hs->v[1], maxit, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        const int64_t nc = hs->v[0], maxitems = hs->v[1];
+        int64_t *ccnt = ar.get<int64_t>(nc);
+        int64_t *crp_tmp = ar.get<int64_t>(nc + 1);
+        void *st2 = ar.raw(scan_tmp_bytes(nc));
+        // coarse rows beyond 1024 items: per-warp global scratch (keys + weights)
+        int64_t gcap = 1;
+        while (gcap < maxitems) gcap <<= 1;
+        const int big_warps = maxitems > 1024 ? 4 * num_sms() : 0;
+        uint64_t *gs = big_warps ? ar.get<uint64_t>((size_t)big_warps * 2 * (size_t)gcap) : nullptr;
+        launch_coarse_rows(0, row_ptr, col, wgt, match, cmap_tmp, lead, nc, ccnt, nullptr, nullptr, nullptr, gs, gcap,
+                           big_warps, s);
+        scan_i64(ccnt, nc, crp_tmp, ScanOp::Identity, st2, 0, s);
+        check_launch("coarse counts");
+        CK(cudaMemcpyAsync(&hs->v[0], crp_tmp + nc, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        const int64_t cnnz = hs->v[0];
+        Layout L;
+        const size_t o_rp = L.add(sizeof(int64_t) * (size_t)(nc + 1));
+        const size_t o_col = L.add(sizeof(int32_t) * (size_t)std::max<int64_t>(cnnz, 1));
+        const size_t o_w = L.add(sizeof(int64_t) * (size_t)std::max<int64_t>(cnnz, 1));
+        const size_t o_vw = L.add(sizeof(int64_t) * (size_t)nc);
+        const size_t o_cm = L.add(sizeof(int32_t) * (size_t)n);
+        CK(cudaMallocAsync((void **)&block, L.bytes, s));
+        out->row_ptr = reinterpret_cast<int64_t *>(block + o_rp);
+        out->col_idx = reinterpret_cast<int32_t *>(block + o_col);
+        out->wgt = reinterpret_cast<int64_t *>(block + o_w);
+        out->vwgt = reinterpret_cast<int64_t *>(block + o_vw);
+        out->cmap = reinterpret_cast<int32_t *>(block + o_cm);
+        CK(cudaMemcpyAsync(out->row_ptr, crp_tmp, sizeof(int64_t) * (size_t)(nc + 1), cudaMemcpyDeviceToDevice, s));
+        CK(cudaMemcpyAsync(out->vwgt, cvw_tmp, sizeof(int64_t) * (size_t)nc, cudaMemcpyDeviceToDevice, s));
+        CK(cudaMemcpyAsync(out->cmap, cmap_tmp, sizeof(int32_t) * (size_t)n, cudaMemcpyDeviceToDevice, s));
+        launch_coarse_rows(1, row_ptr, col, wgt, match, cmap_tmp, lead, nc, ccnt, out->row_ptr, out->col_idx, out->wgt,
+                           gs, gcap, big_warps, s);
+        check_launch("coarse rows");
+        out->n = nc;
+        out->nnz = cnnz;
+        std::lock_guard<std::mutex> lk(g_own_mu);
+        g_owned[block] = reinterpret_cast<void *>(1);  // tag: a coarse graph
+    } catch (...) {
+        if (block) cudaFreeAsync(block, s);
+        std::memset(out, 0, sizeof(*out));
+        throw;
+    }
+    return RIG_OK;
+    ABI_END
+}
+
+int rig_coarse_free(rig_coarse_t *c, rig_stream_t stream) {
+    ABI_BEGIN
+    if (!c) throw Error(RIG_ERR_INVALID, "NULL argument");
+    if (!c->row_ptr) return RIG_OK;
+    void *key = c->row_ptr;
+    {
+        std::lock_guard<std::mutex> lk(g_own_mu);
+        auto it = g_owned.find(key);
+        if (it == g_owned.end() || it->second != reinterpret_cast<void *>(1))
+            throw Error(RIG_ERR_INVALID, "graph was not allocated by rig_coarsen");
+        g_owned.erase(it);
+    }
+    CK(cudaFreeAsync(key, (cudaStream_t)stream));
+    std::memset(c, 0, sizeof(*c));
+    return RIG_OK;
+    ABI_END
+}
+
 int rig_int_weights(const double *w, int64_t n, int64_t alpha, int64_t *wgt, rig_stream_t stream) {
     ABI_BEGIN
     if (n < 0 || (n > 0 && (!w || !wgt))) throw Error(RIG_ERR_INVALID, "NULL argument or n < 0");

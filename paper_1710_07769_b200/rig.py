@@ -65,6 +65,9 @@ def _load():
     L.rig_sparsify.argtypes = [P, ctypes.c_int, U32, P, P]
     L.rig_csr_free.argtypes = [P, P]
     L.rig_int_weights.argtypes = [P, I64, I64, P, P]
+    L.rig_hem_match.argtypes = [P, P, P, I64, I32, P, P]
+    L.rig_coarsen.argtypes = [P, P, P, P, I64, P, P, P]
+    L.rig_coarse_free.argtypes = [P, P]
     L.rig_last_error.restype = ctypes.c_char_p
     L.rig_launch_count.restype = ctypes.c_uint64
     L.rig_version.restype = ctypes.c_char_p
@@ -345,6 +348,46 @@ def rig_int_weights(w: torch.Tensor, alpha: int, out=None, stream=None) -> torch
         out = torch.empty(w.numel(), dtype=torch.int64, device=w.device)
     _check(lib.rig_int_weights(ctypes.c_void_p(w.data_ptr()), int(w.numel()), int(alpha),
                                ctypes.c_void_p(out.data_ptr()), _stream(stream)))
+    return out
+
+
+class rig_coarse_t(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_int64), ("nnz", ctypes.c_int64), ("row_ptr", ctypes.c_void_p),
+                ("col_idx", ctypes.c_void_p), ("wgt", ctypes.c_void_p), ("vwgt", ctypes.c_void_p),
+                ("cmap", ctypes.c_void_p)]
+
+
+def rig_hem_match(row_ptr: torch.Tensor, col: torch.Tensor, wgt: torch.Tensor, rounds=4, stream=None) -> torch.Tensor:
+    """f4 (R23): heavy-edge matching of a symmetric device graph
+    with int64 edge weights; returns match (device int32, partner or -1)."""
+    n = row_ptr.numel() - 1
+    match = torch.empty(max(n, 1), dtype=torch.int32, device=row_ptr.device)
+    _check(lib.rig_hem_match(ctypes.c_void_p(row_ptr.data_ptr()), ctypes.c_void_p(col.data_ptr()),
+                             ctypes.c_void_p(wgt.data_ptr()), n, int(rounds), ctypes.c_void_p(match.data_ptr()),
+                             _stream(stream)))
+    return match[:n]
+
+
+def rig_coarsen(row_ptr, col, wgt, match, vwgt=None, stream=None):
+    """f4 (R24-R25): one coarsening step.  Returns a dict of device
+    tensors (row_ptr, col_idx, wgt, vwgt, cmap) and the coarse sizes; the
+    library block is copied into torch tensors and released."""
+    n = row_ptr.numel() - 1
+    c = rig_coarse_t()
+    vp = ctypes.c_void_p(vwgt.data_ptr()) if vwgt is not None else None
+    _check(lib.rig_coarsen(ctypes.c_void_p(row_ptr.data_ptr()), ctypes.c_void_p(col.data_ptr()),
+                           ctypes.c_void_p(wgt.data_ptr()), vp, n, ctypes.c_void_p(match.data_ptr()),
+                           ctypes.byref(c), _stream(stream)))
+    out = {"n": int(c.n), "nnz": int(c.nnz)}
+    if c.row_ptr:
+        for name, ptr, cnt, ts, dt in (("row_ptr", c.row_ptr, c.n + 1, "<i8", torch.int64),
+                                       ("col_idx", c.col_idx, c.nnz, "<i4", torch.int32),
+                                       ("wgt", c.wgt, c.nnz, "<i8", torch.int64),
+                                       ("vwgt", c.vwgt, c.n, "<i8", torch.int64),
+                                       ("cmap", c.cmap, n, "<i4", torch.int32)):
+            out[name] = torch.as_tensor(_Cai(ptr, cnt, ts, None), device=row_ptr.device).clone() if cnt else \
+                torch.empty(0, dtype=dt, device=row_ptr.device)
+        _check(lib.rig_coarse_free(ctypes.byref(c), _stream(stream)))
     return out
 
 

@@ -516,3 +516,62 @@ def test_int_weights_edge_values(rig):
     assert to_np(rig.rig_int_weights(bad, 10)).tolist() == [-1, -1, -1, -1]
     with pytest.raises(rig.RigError):
         rig.rig_int_weights(xt, 0)
+
+
+# ------------------------------------------------------------------ f4
+def _sym_int_graph(n, edges):
+    r, c, w = [], [], []
+    for u, v, x in edges:
+        r += [u, v]
+        c += [v, u]
+        w += [x, x]
+    rp, ci, vv = from_triplets(n, n, np.array(r), np.array(c), np.array(w, dtype=np.float64))
+    return rp, ci, vv.astype(np.int64)
+
+
+def _check_f4(rig, rp, ci, wg, vw=None, rounds=4):
+    from oracle.coarsen import coarsen, hem_match
+
+    m_o = hem_match(rp, ci, wg, rounds=rounds)
+    dev = lambda a: torch.as_tensor(a, device="cuda")  # noqa: E731
+    m_g = rig.rig_hem_match(dev(rp), dev(ci), dev(wg), rounds=rounds)
+    np.testing.assert_array_equal(to_np(m_g), m_o)
+    cmap, nc, crp, cci, cw, cvw = coarsen(rp, ci, wg, m_o, vwgt=vw)
+    out = rig.rig_coarsen(dev(rp), dev(ci), dev(wg), m_g, vwgt=None if vw is None else dev(vw))
+    assert out["n"] == nc and out["nnz"] == cci.size
+    np.testing.assert_array_equal(to_np(out["cmap"]), cmap)
+    np.testing.assert_array_equal(to_np(out["row_ptr"]), crp)
+    np.testing.assert_array_equal(to_np(out["col_idx"]), cci)
+    np.testing.assert_array_equal(to_np(out["wgt"]), cw)
+    np.testing.assert_array_equal(to_np(out["vwgt"]), cvw)
+
+
+@pytest.mark.parametrize("cfg", [1, 2, 3])
+def test_f4_matching_and_coarsening_on_grip(rig, cfg):
+    """Heavy-edge matching and one coarsening step of G_RIP with the METIS
+    weights ceil(1e4 * cost): device == oracle, exactly."""
+    w = make_small(cfg)
+    A, g = gpu_build(rig, w, flags=0)
+    wg = rig.rig_int_weights(g.w, 10_000)
+    vw = np.diff(w.row_ptr).astype(np.int64)  # vertex weight: nnz of the row
+    _check_f4(rig, to_np(g.row_ptr), to_np(g.col_idx), to_np(wg), vw=vw)
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_f4_random_ties_and_big_rows(rig, seed):
+    """Small integer weights (many ties, smallest-index rule), isolated
+    vertices, and a hub of 1500 neighbours (coarse rows beyond 1024 items take
+    the global-scratch sort)."""
+    rng = np.random.default_rng(77 + seed)
+    n = 3000
+    edges = {}
+    for _ in range(9000):
+        u, v = map(int, rng.integers(0, n - 50, 2))  # the last 50 vertices stay isolated
+        if u != v:
+            edges[(min(u, v), max(u, v))] = int(rng.integers(1, 4))
+    hub = int(rng.integers(0, n - 50))
+    for v in rng.choice(n - 50, 1500, replace=False):
+        if int(v) != hub:
+            edges[(min(hub, int(v)), max(hub, int(v)))] = int(rng.integers(1, 4))
+    rp, ci, wg = _sym_int_graph(n, [(u, v, x) for (u, v), x in edges.items()])
+    _check_f4(rig, rp, ci, wg, rounds=1 + seed * 3)
