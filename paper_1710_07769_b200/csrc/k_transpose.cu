@@ -444,20 +444,17 @@ __global__ void k_row_norms(Csr A, double *nrm, double *y, int *err, const int *
 // few skipped launches instead of a failed gather.
 __global__ void k_sym_probe(Csr A, int *fail) {
     const int64_t nprobe = 4096;
-    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < nprobe && t < A.nnz;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < nprobe && t < A.nrows;
          t += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t p = A.nnz <= nprobe ? t : t * (A.nnz / nprobe);
-        // row of p: binary search of row_ptr
-        int64_t lo = 0, hi = A.nrows;  // rp[lo] <= p < rp[hi]
-        while (hi - lo > 1) {
-            const int64_t mid = (lo + hi) >> 1;
-            if (A.rp[mid] <= p) lo = mid; else hi = mid;
-        }
-        const int j = A.ci[p];
+        // row k spread over the matrix, an entry of it chosen by t
+        const int64_t k = A.nrows <= nprobe ? t : t * (A.nrows / nprobe);
+        const int64_t s = A.rp[k], e = A.rp[k + 1];
+        if (e == s) continue;
+        const int j = A.ci[s + (t % (e - s))];
         const int64_t sj = A.rp[j], ej = A.rp[j + 1];
         bool found = false;
         if (ej - sj <= 64)
-            for (int64_t q = sj; q < ej && !found; ++q) found = A.ci[q] == (int)lo;
+            for (int64_t q = sj; q < ej && !found; ++q) found = A.ci[q] == (int)k;
         if (!found) atomicOr(fail, 1);
     }
 }
@@ -578,6 +575,7 @@ __global__ void k_sym_shape(const int64_t *__restrict__ rp, int64_t n, int64_t r
                             const int *fail) {
     if (*reinterpret_cast<const volatile int *>(fail)) return;
     unsigned long long ps = 0, mc = 0, mr = 0;
+#pragma unroll 4
     for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
         const unsigned long long len = (unsigned long long)(rp[k + 1] - rp[k]);
         ps += len * len;
@@ -590,7 +588,20 @@ __global__ void k_sym_shape(const int64_t *__restrict__ rp, int64_t n, int64_t r
         mc = max(mc, __shfl_xor_sync(kFull, mc, o));
         mr = max(mr, __shfl_xor_sync(kFull, mr, o));
     }
+    __shared__ unsigned long long red[3][8];  // one atomic per counter per CTA (<= 256 threads)
+    const int w = threadIdx.x >> 5;
     if (lane_id() == 0) {
+        red[0][w] = ps;
+        red[1][w] = mc;
+        red[2][w] = mr;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int k = 1; k < (int)(blockDim.x >> 5); ++k) {
+            ps += red[0][k];
+            mc = max(mc, red[1][k]);
+            mr = max(mr, red[2][k]);
+        }
         if (ps) atomicAdd((unsigned long long *)&ctr->p_full, ps);
         if (mc) atomicMax((unsigned long long *)&ctr->max_col, mc);
         if (mr) atomicMax((unsigned long long *)&ctr->max_row, mr);
