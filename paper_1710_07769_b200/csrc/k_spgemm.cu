@@ -410,31 +410,34 @@ __global__ void RIG_PAIR_BOUNDS k_num_pair(NumArgs a) {
         int len = 0;
         bool mrow = false;
         int32_t pi = 0;
+        int qv[RMAX];
+        double av[RMAX];
         if (qr < rows) {
             s = a.A.rp[i];
             len = (int)min(a.A.rp[i + 1] - s, (int64_t)kMergeMaxLen + 1);
             gr = a.gptr[r];
             ub = a.gptr[r + 1] - gr;
-            if (len >= 1 && len <= RMAX) mrow = a.qs[s].x >= 0;
             if (a.part) {
                 pi = a.part[i];
                 badp |= (pi < 0) | (pi >= a.K);
             }
         }
+        // the row's runs and values, loaded before the merge-row test (run 0's
+        // start is -1 off the merge path) so they cost no extra round trip
+        const int lq = (len >= 1 && len <= RMAX) ? len : 0;
+#pragma unroll
+        for (int t = 0; t < RMAX; ++t) {
+            qv[t] = -1;
+            av[t] = 0.0;
+            if (t < lq) {
+                const int2 run = a.qs[s + t];
+                if (t == 0) mrow = run.x >= 0;
+                qv[t] = desc ? run.x + run.y - 1 : run.x;
+                av[t] = a.A.v[s + t];
+            }
+        }
         int o = 0;
         if (mrow && staged) {
-            int qv[RMAX];
-            double av[RMAX];
-#pragma unroll
-            for (int t = 0; t < RMAX; ++t) {
-                qv[t] = -1;
-                av[t] = 0.0;
-                if (t < len) {
-                    const int2 run = a.qs[s + t];
-                    qv[t] = desc ? run.x + run.y - 1 : run.x;
-                    av[t] = a.A.v[s + t];
-                }
-            }
             const unsigned ob = (unsigned)(gr - g0) + (desc ? (unsigned)(ub - 1) : 0u);
             o = pair_half_row_r<RMAX>(len, a, desc, i, r, qv, av, oc0, ow0, ob, cut, pi, badp);
         } else if (mrow && !desc) {  // output beyond the stage: direct global stores
