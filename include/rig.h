@@ -249,7 +249,7 @@ RIG_API int rig_hem_match(const int64_t *row_ptr, const int32_t *col, const int6
  * vertices become coarse vertices numbered by their smaller member; coarse
  * edge weights sum the fine edges between the groups (the contracted edges
  * vanish); vwgt [n] (DEVICE, may be NULL: unit weights) are summed.  Integer
- * sums: exact.  Synchronises twice (coarse size, coarse nnz). */
+ * sums: exact.  Synchronises three times (coarse size, temporary size, coarse nnz). */
 RIG_API int rig_coarsen(const int64_t *row_ptr, const int32_t *col, const int64_t *wgt, const int64_t *vwgt,
                         int64_t n, const int32_t *match, rig_coarse_t *out, rig_stream_t stream);
 RIG_API int rig_coarse_free(rig_coarse_t *c, rig_stream_t stream);

@@ -345,7 +345,10 @@ void launch_hem_round(const int64_t *rp, const int32_t *col, const int64_t *wgt,
                       int32_t *cand, cudaStream_t s);
 void launch_leader_flags(const int32_t *match, int64_t n, int64_t *flag, cudaStream_t s);
 void launch_coarse_map(const int64_t *rp, const int32_t *match, const int64_t *vwgt, int64_t n, const int64_t *cid,
-                       int32_t *cmap, int32_t *lead, int64_t *cvwgt, unsigned long long *maxit, cudaStream_t s);
+                       int32_t *cmap, int32_t *lead, int64_t *cvwgt, int64_t *citems, unsigned long long *maxit,
+                       cudaStream_t s);
+void launch_coarse_copy(const int64_t *toff, const int64_t *crp, int64_t nc, const int32_t *tcol, const int64_t *tw,
+                        int32_t *ccol, int64_t *cw, cudaStream_t s);
 void launch_coarse_rows(int pass, const int64_t *rp, const int32_t *col, const int64_t *wgt, const int32_t *match,
                         const int32_t *cmap, const int32_t *lead, int64_t nc, int64_t *ccnt, const int64_t *crp,
                         int32_t *ccol, int64_t *cw, uint64_t *gscratch, int64_t gcap, int big_warps,

@@ -15,8 +15,10 @@
 //    neighbour lists of its members as items (cmap(j) << 32 | position),
 //    bitonic-sorts them (shared memory up to 1024 items; a per-warp slice of
 //    global scratch beyond, in a separate launch), sums the weights of equal
-//    keys (integers: order-free, exact) and drops its own id.  Pass 0 counts,
-//    pass 1 writes the coarse CSR at the scanned offsets.
+//    keys (integers: order-free, exact) and drops its own id, writing the row
+//    with its exact count into a temporary at offsets from the rows' item
+//    bounds (pass 2); after the scan of the counts, k_coarse_copy places the
+//    rows (pass 0/1: count, then write at the scanned offsets, sort twice).
 #include "common.cuh"
 
 namespace rig {
@@ -81,7 +83,8 @@ __global__ void k_leader_flags(const int32_t *__restrict__ match, int64_t n, int
 // the largest item count of a coarse row (the members' degrees).
 __global__ void k_coarse_map(const int64_t *__restrict__ rp, const int32_t *__restrict__ match,
                              const int64_t *__restrict__ vwgt, int64_t n, const int64_t *__restrict__ cid,
-                             int32_t *cmap, int32_t *lead, int64_t *cvwgt, unsigned long long *maxit) {
+                             int32_t *cmap, int32_t *lead, int64_t *cvwgt, int64_t *citems,
+                             unsigned long long *maxit) {
     unsigned long long mx = 0;
     for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x) {
         const int m = match[v];
@@ -97,6 +100,7 @@ __global__ void k_coarse_map(const int64_t *__restrict__ rp, const int32_t *__re
                 it += rp[m + 1] - rp[m];
             }
             cvwgt[c] = w;
+            citems[c] = it;  // >= the coarse row's entries: its slots in the temporary
             mx = max(mx, (unsigned long long)it);
         }
     }
@@ -174,7 +178,7 @@ __global__ void __launch_bounds__(kCoarseThreads) k_coarse_rows(CoarseArgs a) {
         __syncwarp();
         warp_bitonic(key, N);
         // runs of equal coarse id: the first item of a run sums it
-        int64_t base = PASS ? a.crp[c] : 0;
+        int64_t base = PASS ? a.crp[c] : 0;  // PASS 2: crp holds the temporary offsets
         int64_t kept = 0;
         for (int64_t t0 = 0; t0 < nit; t0 += 32) {
             const int64_t t = t0 + l;
@@ -200,9 +204,33 @@ __global__ void __launch_bounds__(kCoarseThreads) k_coarse_rows(CoarseArgs a) {
             }
             kept += __popc(bal);
         }
-        if (!PASS && l == 0) a.ccnt[c] = kept;
+        if (PASS != 1 && l == 0) a.ccnt[c] = kept;
         __syncwarp();
     }
+}
+
+// Coarse rows from the temporary (toff, exact counts) to their final slots.
+__global__ void k_coarse_copy(const int64_t *__restrict__ toff, const int64_t *__restrict__ crp, int64_t nc,
+                              const int32_t *__restrict__ tcol, const int64_t *__restrict__ tw, int32_t *ccol,
+                              int64_t *cw) {
+    const int l = lane_id();
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t c = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; c < nc; c += nw) {
+        const int64_t src = toff[c], dst = crp[c], len = crp[c + 1] - dst;
+        for (int64_t t = l; t < len; t += 32) {
+            ccol[dst + t] = tcol[src + t];
+            cw[dst + t] = tw[src + t];
+        }
+    }
+}
+
+void launch_coarse_copy(const int64_t *toff, const int64_t *crp, int64_t nc, const int32_t *tcol, const int64_t *tw,
+                        int32_t *ccol, int64_t *cw, cudaStream_t s) {
+    if (nc <= 0) return;
+    int64_t g = (nc * 32 + 255) / 256;
+    if (g > (int64_t)num_sms() * 16) g = (int64_t)num_sms() * 16;
+    k_coarse_copy<<<(unsigned)g, 256, 0, s>>>(toff, crp, nc, tcol, tw, ccol, cw);
+    note_launch();
 }
 
 void launch_hem_round(const int64_t *rp, const int32_t *col, const int64_t *wgt, int64_t n, int32_t *match,
@@ -225,10 +253,11 @@ void launch_leader_flags(const int32_t *match, int64_t n, int64_t *flag, cudaStr
 }
 
 void launch_coarse_map(const int64_t *rp, const int32_t *match, const int64_t *vwgt, int64_t n, const int64_t *cid,
-                       int32_t *cmap, int32_t *lead, int64_t *cvwgt, unsigned long long *maxit, cudaStream_t s) {
+                       int32_t *cmap, int32_t *lead, int64_t *cvwgt, int64_t *citems, unsigned long long *maxit,
+                       cudaStream_t s) {
     int64_t g = (n + 255) / 256;
     g = g < 1 ? 1 : (g > (int64_t)num_sms() * 16 ? (int64_t)num_sms() * 16 : g);
-    k_coarse_map<<<(unsigned)g, 256, 0, s>>>(rp, match, vwgt, n, cid, cmap, lead, cvwgt, maxit);
+    k_coarse_map<<<(unsigned)g, 256, 0, s>>>(rp, match, vwgt, n, cid, cmap, lead, cvwgt, citems, maxit);
     note_launch();
 }
 
@@ -242,14 +271,18 @@ void launch_coarse_rows(int pass, const int64_t *rp, const int32_t *col, const i
     CoarseArgs a{rp, col, wgt, match, cmap, lead, nc, ccnt, crp, ccol, cw, gscratch, gcap};
     int64_t g = (nc + kCoarseWarps - 1) / kCoarseWarps;
     if (g > (int64_t)num_sms() * 16) g = (int64_t)num_sms() * 16;
-    if (pass == 0)
+    if (pass == 2)
+        k_coarse_rows<2, false><<<(unsigned)g, kCoarseThreads, 0, s>>>(a);
+    else if (pass == 0)
         k_coarse_rows<0, false><<<(unsigned)g, kCoarseThreads, 0, s>>>(a);
     else
         k_coarse_rows<1, false><<<(unsigned)g, kCoarseThreads, 0, s>>>(a);
     note_launch();
     if (gscratch && big_warps > 0) {
         const unsigned gb = (unsigned)((big_warps + kCoarseWarps - 1) / kCoarseWarps);
-        if (pass == 0)
+        if (pass == 2)
+            k_coarse_rows<2, true><<<gb, kCoarseThreads, 0, s>>>(a);
+        else if (pass == 0)
             k_coarse_rows<0, true><<<gb, kCoarseThreads, 0, s>>>(a);
         else
             k_coarse_rows<1, true><<<gb, kCoarseThreads, 0, s>>>(a);

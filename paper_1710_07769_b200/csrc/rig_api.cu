@@ -1088,6 +1088,7 @@ int rig_coarsen(const int64_t *row_ptr, const int32_t *col, const int64_t *wgt, 
     void *st = ar.raw(scan_tmp_bytes(n));
     int32_t *lead = ar.get<int32_t>(n);
     int64_t *cvw_tmp = ar.get<int64_t>(n);
+    int64_t *citems = ar.get<int64_t>(n);
     unsigned long long *maxit = ar.get<unsigned long long>(1);
     CK(cudaMemsetAsync(maxit, 0, sizeof(unsigned long long), s));
     unsigned char *block = nullptr;
@@ -1096,7 +1097,7 @@ int rig_coarsen(const int64_t *row_ptr, const int32_t *col, const int64_t *wgt, 
         int32_t *cmap_tmp = ar.get<int32_t>(n);
         launch_leader_flags(match, n, flag, s);
         scan_i64(flag, n, cid, ScanOp::Identity, st, 0, s);
-        launch_coarse_map(row_ptr, match, vwgt, n, cid, cmap_tmp, lead, cvw_tmp, maxit, s);
+        launch_coarse_map(row_ptr, match, vwgt, n, cid, cmap_tmp, lead, cvw_tmp, citems, maxit, s);
         check_launch("coarse map");
         HostStage *hs = host_stage();
         CK(cudaMemcpyAsync(&hs->v[0], cid + n, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
@@ -1105,16 +1106,24 @@ int rig_coarsen(const int64_t *row_ptr, const int32_t *col, const int64_t *wgt, 
         const int64_t nc = hs->v[0], maxitems = hs->v[1];
         int64_t *ccnt = ar.get<int64_t>(nc);
         int64_t *crp_tmp = ar.get<int64_t>(nc + 1);
+        int64_t *toff = ar.get<int64_t>(nc + 1);
         void *st2 = ar.raw(scan_tmp_bytes(nc));
         // coarse rows beyond 1024 items: per-warp global scratch (keys + weights)
         int64_t gcap = 1;
         while (gcap < maxitems) gcap <<= 1;
         const int big_warps = maxitems > 1024 ? 4 * num_sms() : 0;
         uint64_t *gs = big_warps ? ar.get<uint64_t>((size_t)big_warps * 2 * (size_t)gcap) : nullptr;
-        launch_coarse_rows(0, row_ptr, col, wgt, match, cmap_tmp, lead, nc, ccnt, nullptr, nullptr, nullptr, gs, gcap,
-                           big_warps, s);
+        // one sorting pass: rows into a temporary at their item bounds, with counts
+        scan_i64(citems, nc, toff, ScanOp::Identity, st2, 0, s);
+        CK(cudaMemcpyAsync(&hs->v[2], toff + nc, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        const int64_t tslots = std::max<int64_t>(hs->v[2], 1);
+        int32_t *tcol = ar.get<int32_t>(tslots);
+        int64_t *tw = ar.get<int64_t>(tslots);
+        launch_coarse_rows(2, row_ptr, col, wgt, match, cmap_tmp, lead, nc, ccnt, toff, tcol, tw, gs, gcap, big_warps,
+                           s);
         scan_i64(ccnt, nc, crp_tmp, ScanOp::Identity, st2, 0, s);
-        check_launch("coarse counts");
+        check_launch("coarse rows");
         CK(cudaMemcpyAsync(&hs->v[0], crp_tmp + nc, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
         const int64_t cnnz = hs->v[0];
@@ -1133,8 +1142,7 @@ int rig_coarsen(const int64_t *row_ptr, const int32_t *col, const int64_t *wgt, 
         CK(cudaMemcpyAsync(out->row_ptr, crp_tmp, sizeof(int64_t) * (size_t)(nc + 1), cudaMemcpyDeviceToDevice, s));
         CK(cudaMemcpyAsync(out->vwgt, cvw_tmp, sizeof(int64_t) * (size_t)nc, cudaMemcpyDeviceToDevice, s));
         CK(cudaMemcpyAsync(out->cmap, cmap_tmp, sizeof(int32_t) * (size_t)n, cudaMemcpyDeviceToDevice, s));
-        launch_coarse_rows(1, row_ptr, col, wgt, match, cmap_tmp, lead, nc, ccnt, out->row_ptr, out->col_idx, out->wgt,
-                           gs, gcap, big_warps, s);
+        launch_coarse_copy(toff, out->row_ptr, nc, tcol, tw, out->col_idx, out->wgt, s);
         check_launch("coarse rows");
         out->n = nc;
         out->nnz = cnnz;
