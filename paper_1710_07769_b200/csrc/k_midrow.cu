@@ -422,17 +422,17 @@ __global__ void __launch_bounds__(kCopyThreads) k_copy_rows(const int32_t *__res
                 const int64_t t = t0 + 32 * u + l;
                 j[u] = -1;
                 w[u] = 0.0;
-                if (t < len) {
-                    j[u] = tcol[src + t];
-                    w[u] = tw[src + t];
+                if (t < len) {  // streamed: the temporary is read once
+                    j[u] = __ldcs(tcol + src + t);
+                    w[u] = __ldcs(tw + src + t);
                 }
             }
 #pragma unroll
             for (int u = 0; u < U; ++u) {
                 const int64_t t = t0 + 32 * u + l;
                 if (t < len) {
-                    gcol[d + t] = j[u];
-                    gw[d + t] = w[u];
+                    __stcs(gcol + d + t, j[u]);
+                    __stcs(gw + d + t, w[u]);
                 }
                 pj[u] = pi;
                 if (cut.part && (int64_t)j[u] > i) pj[u] = __ldg(&cut.part[j[u]]);
