@@ -308,8 +308,8 @@ __global__ void __launch_bounds__(kMidThreads, 8) k_num_mid(MidArgs a) {
             const unsigned bal = __ballot_sync(kFull, keep);
             if (keep && !(a.dbg & 4)) {
                 const int64_t pos = g0 + o + __popc(bal & lt);
-                a.tcol[pos] = key;
-                a.tw[pos] = w;
+                __stcs(a.tcol + pos, key);  // streamed: keeps the CSC gathers in L2
+                __stcs(a.tw + pos, w);
             }
             o += __popc(bal);
         };

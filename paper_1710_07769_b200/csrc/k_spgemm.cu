@@ -477,8 +477,8 @@ __global__ void RIG_PAIR_BOUNDS k_num_pair(NumArgs a) {
         // places those rows afterwards
         for (int64_t t = l; t < span_out; t += 32) {
             const unsigned e = out_swz((unsigned)t);
-            a.gcol[g0 + t] = lds_s32(oc0 + 4 * e);
-            a.gw[g0 + t] = lds_f64(ow0 + 8 * e);
+            __stcs(a.gcol + g0 + t, lds_s32(oc0 + 4 * e));  // streamed: keeps the CSC gathers in L2
+            __stcs(a.gw + g0 + t, lds_f64(ow0 + 8 * e));
         }
         __syncwarp();  // the stage is reused by the next tile
     }
