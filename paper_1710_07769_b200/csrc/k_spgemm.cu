@@ -429,11 +429,11 @@ __global__ void RIG_PAIR_BOUNDS k_num_pair(NumArgs a) {
         for (int t = 0; t < RMAX; ++t) {
             qv[t] = -1;
             av[t] = 0.0;
-            if (t < lq) {
-                const int2 run = a.qs[s + t];
+            if (t < lq) {  // streamed: read once
+                const int2 run = __ldcs(a.qs + s + t);
                 if (t == 0) mrow = run.x >= 0;
                 qv[t] = desc ? run.x + run.y - 1 : run.x;
-                av[t] = a.A.v[s + t];
+                av[t] = __ldcs(a.A.v + s + t);
             }
         }
         int o = 0;
