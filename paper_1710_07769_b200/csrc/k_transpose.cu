@@ -241,7 +241,12 @@ __global__ void __launch_bounds__(kSortThreads) k_bucket_sort(const Rec *__restr
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
                 const int t = t0 + 32 * u + l;
-                if (t < (int)E) rr[u] = rec[e0 + t];
+                if (t < (int)E) {  // streamed: each record is read once
+                    const int4 q = __ldcs(reinterpret_cast<const int4 *>(rec + e0 + t));
+                    rr[u].col = q.x;
+                    rr[u].row = q.y;
+                    rr[u].x = __hiloint2double(q.w, q.z);
+                }
             }
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
