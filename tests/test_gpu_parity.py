@@ -284,6 +284,31 @@ def test_mid_rows_deferred(rig, seed):
     assert abs(cut3.item() - oc3) <= REL * oc3
 
 
+def test_mid_row_passes_long_far_lists(rig):
+    """Rows of 800..3500 random columns (every key far from the diagonal) run
+    through the mid pass, the 768-item far-list pass, the wide window and the
+    4096-item global far-list pass (and the huge kernel for the longest);
+    short rows take the merge path."""
+    rng = np.random.default_rng(4242)
+    n = 40000
+    rows, cols = [], []
+    for r in range(n):
+        k = int(rng.integers(800, 3500)) if r % 1500 == 7 else int(rng.integers(1, 4))
+        cc = rng.choice(n, k, replace=False)
+        rows += [r] * k
+        cols += list(cc)
+    rows += list(range(n))
+    cols += list(range(n))
+    rows, cols = np.array(rows), np.array(cols)
+    key = np.unique(rows.astype(np.int64) * n + cols)
+    rows, cols = key // n, key % n
+    vals = rng.standard_normal(rows.size)
+    rp, ci, v = from_triplets(n, n, rows, cols, vals)
+    orc = oracle.build(rp, ci, v, scale_rows=1, drop_tol=0.0)
+    g = rig.rig_build(rig.CSR(rp, ci, v), 1, 0.0, rig.RIG_FLAG_DIAG)
+    assert_graph_equal(to_np(g.row_ptr), to_np(g.col_idx), to_np(g.w), orc, to_np(g.diag))
+
+
 @pytest.mark.parametrize("seed", range(4))
 def test_random_mixed(rig, seed):
     rng = np.random.default_rng(1000 + seed)
