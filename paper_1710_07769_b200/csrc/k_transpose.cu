@@ -106,7 +106,10 @@ __global__ void __launch_bounds__(kScatterThreads) k_bucket_scatter(Csr A, int s
         __syncwarp();
         const int64_t lo = __shfl_sync(kFull, my_s, 0);
         int cnt = NE ? 1 : 0;  // nonempty rows starting at or before c0
-        constexpr int U = 2;  // chunks per group: their bucket atomics are in flight together
+#ifndef RIG_SCATTER_U
+#define RIG_SCATTER_U 2
+#endif
+        constexpr int U = RIG_SCATTER_U;  // chunks per group: their bucket atomics are in flight together
         for (int64_t g0 = lo; g0 < hi; g0 += 32 * U) {
             int kk[U], row[U], bb[U];
             double xx[U];
