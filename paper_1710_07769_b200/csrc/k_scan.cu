@@ -152,6 +152,91 @@ __global__ void __launch_bounds__(kScanThreads) k_tile_scan(const T *__restrict_
     if (blockIdx.x == ntiles - 1 && threadIdx.x == 0) out[n] = pre_s + tot_s;
 }
 
+// Single-pass variant (no shape statistics): tiles are taken in order from a
+// ticket, each publishes its total and then its inclusive prefix, found by a
+// decoupled look-back over the previous tiles' status words (a tile only waits
+// on tiles that started before it, so the chain always completes).  tmp holds
+// the status words [ntiles] and the ticket, zeroed before the launch.
+constexpr unsigned long long kScanAgg = 1ull << 62, kScanPre = 2ull << 62, kScanVal = (1ull << 62) - 1;
+
+template <typename T>
+__global__ void __launch_bounds__(kScanThreads) k_scan_1p(const T *__restrict__ in, int64_t n, ScanOp op,
+                                                          unsigned long long *status, unsigned *ticket, int64_t *out,
+                                                          const int *guard) {
+    if (guard_skip(guard)) return;
+    __shared__ int64_t sv[kTile + kTile / 16];
+    __shared__ int64_t tot_s, pre_s;
+    __shared__ unsigned tile_s;
+    if (threadIdx.x == 0) tile_s = atomicAdd(ticket, 1u);
+    __syncthreads();
+    const int64_t tile = tile_s;
+    const int64_t base = tile * kTile;
+#pragma unroll
+    for (int j = 0; j < kScanItems; ++j) {  // coalesced blocked load
+        const int64_t i = base + (int64_t)j * kScanThreads + threadIdx.x;
+        sv[pad(j * kScanThreads + threadIdx.x)] = i < n ? scan_load(in, i, op) : 0;
+    }
+    __syncthreads();
+    int64_t v[kScanItems];
+    int64_t sum = 0;
+#pragma unroll
+    for (int j = 0; j < kScanItems; ++j) {
+        v[j] = sv[pad(threadIdx.x * kScanItems + j)];
+        sum += v[j];
+    }
+    const int64_t ex = block_excl_scan(sum, &tot_s);
+    if (threadIdx.x < 32) {  // warp 0: publish the total, look back, publish the prefix
+        const int l = lane_id();
+        const unsigned long long tot = (unsigned long long)tot_s;
+        int64_t excl = 0;
+        if (tile == 0) {
+            if (l == 0) {
+                __threadfence();
+                atomicExch(&status[0], kScanPre | tot);
+            }
+        } else {
+            if (l == 0) {
+                __threadfence();
+                atomicExch(&status[tile], kScanAgg | tot);
+            }
+            int64_t b = tile - 1;
+            while (true) {
+                const int64_t j = b - l;
+                unsigned long long st = 2ull << 62;  // before tile 0: an inclusive prefix of 0
+                if (j >= 0) st = *reinterpret_cast<volatile unsigned long long *>(&status[j]);
+                const unsigned pm = __ballot_sync(kFull, (st & kScanPre) != 0);
+                const unsigned zm = __ballot_sync(kFull, (st & (kScanPre | kScanAgg)) == 0);
+                const int fp = pm ? __ffs(pm) - 1 : 31;
+                const unsigned need = fp == 31 ? kFull : ((2u << fp) - 1u);
+                if (zm & need) continue;  // a needed earlier tile has not published yet
+                __threadfence();
+                excl += warp_sum(((need >> l) & 1u) ? (int64_t)(st & kScanVal) : (int64_t)0);
+                if (pm) break;
+                b -= 32;
+            }
+            if (l == 0) {
+                __threadfence();
+                atomicExch(&status[tile], kScanPre | (unsigned long long)(excl + (int64_t)tot));
+            }
+        }
+        if (l == 0) pre_s = excl;
+    }
+    __syncthreads();
+    int64_t run = pre_s + ex;
+#pragma unroll
+    for (int j = 0; j < kScanItems; ++j) {
+        sv[pad(threadIdx.x * kScanItems + j)] = run;
+        run += v[j];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < kScanItems; ++j) {
+        const int64_t i = base + (int64_t)j * kScanThreads + threadIdx.x;
+        if (i < n) out[i] = sv[pad(j * kScanThreads + threadIdx.x)];
+    }
+    if (base + kTile >= n && threadIdx.x == 0) out[n] = pre_s + tot_s;
+}
+
 size_t scan_tmp_bytes(int64_t n) {
     const int64_t ntiles = (n + kTile - 1) / kTile;
     return (size_t)(ntiles + 1) * sizeof(int64_t);
@@ -164,6 +249,14 @@ static void scan_impl(const T *in, int64_t n, int64_t *out, ScanOp op, void *tmp
     const int64_t ntiles = (n + kTile - 1) / kTile;
     if (ntiles == 0) {
         cudaMemsetAsync(out, 0, sizeof(int64_t), s);
+        return;
+    }
+    if (!so.ctr && !after_sum) {  // single pass
+        auto *st = static_cast<unsigned long long *>(tmp);
+        cudaMemsetAsync(st, 0, sizeof(unsigned long long) * (size_t)(ntiles + 1), s);
+        k_scan_1p<T><<<(unsigned)ntiles, kScanThreads, 0, s>>>(in, n, op, st, reinterpret_cast<unsigned *>(st + ntiles),
+                                                                out, guard);
+        note_launch();
         return;
     }
     int64_t *ts = static_cast<int64_t *>(tmp);
