@@ -27,7 +27,8 @@ static int g_sms_cache = 0;
 // IdxT: int32 CSC offsets when nnz < 2^31 (fewer registers), else int64.
 // Columns end in an INT_MAX sentinel (csc_begin), so a run needs no end bound.
 template <int R, typename IdxT>
-__device__ __forceinline__ int64_t sym_merge_row(const Csr &A, const Csc &T, int64_t s, int2 *qs = nullptr) {
+__device__ __forceinline__ int64_t sym_merge_row(const Csr &A, const Csc &T, int64_t s, int2 *qs = nullptr,
+                                                 int64_t *f_out = nullptr) {
     int32_t h[R];
     IdxT q[R];
     int64_t f = 0;
@@ -40,6 +41,7 @@ __device__ __forceinline__ int64_t sym_merge_row(const Csr &A, const Csc &T, int
         cl[t] = (int32_t)min(c1 - c0, (int64_t)INT32_MAX);
         f += c1 - c0;
     }
+    if (f_out) *f_out = f;
     if (f > kMergeMaxF) return -1;
     if (qs) {  // runs for the numeric pass (saves it the col_ptr gathers)
 #pragma unroll
@@ -524,7 +526,8 @@ __global__ void __launch_bounds__(kMergeThreads) k_analyze_sym(SymArgs a, uint8_
         }
         const bool longrow = e - s > kLongRow;
         int64_t fi = 0;
-        if (!longrow) {
+        // rows of <= kMergeMaxLen entries get f_i from their merge count below
+        if (!longrow && e - s > kMergeMaxLen) {
             for (int64_t p0 = s; p0 < e; p0 += 8) {  // 8 independent gathers in flight
                 int k[8];
 #pragma unroll
@@ -546,23 +549,23 @@ __global__ void __launch_bounds__(kMergeThreads) k_analyze_sym(SymArgs a, uint8_
             if (lane == u) fi = part;
         }
         if (!valid) continue;
-        local += fi;
         nnzr += e - s;
         const int len = (int)min(e - s, (int64_t)kMergeMaxLen + 1);
-        if (len <= kMergeMaxLen && fi <= kMergeMaxF) {
+        int64_t c = len == 0 ? 0 : -1;  // merge count (an empty row: 0); -1: off the merge path
+        switch (len) {  // rows of <= 8 entries: f_i and, if small enough, the count in one pass
+            case 1: c = sym_merge_row<1, IdxT>(a.A, a.T, s, a.qs, &fi); break;
+            case 2: c = sym_merge_row<2, IdxT>(a.A, a.T, s, a.qs, &fi); break;
+            case 3: c = sym_merge_row<3, IdxT>(a.A, a.T, s, a.qs, &fi); break;
+            case 4: c = sym_merge_row<4, IdxT>(a.A, a.T, s, a.qs, &fi); break;
+            case 5: c = sym_merge_row<5, IdxT>(a.A, a.T, s, a.qs, &fi); break;
+            case 6: c = sym_merge_row<6, IdxT>(a.A, a.T, s, a.qs, &fi); break;
+            case 7: c = sym_merge_row<7, IdxT>(a.A, a.T, s, a.qs, &fi); break;
+            case 8: c = sym_merge_row<8, IdxT>(a.A, a.T, s, a.qs, &fi); break;
+            default: break;
+        }
+        local += fi;
+        if (len <= kMergeMaxLen && c >= 0) {
             maxlen = max(maxlen, len);
-            int64_t c = 0;
-            switch (len) {
-                case 1: c = sym_merge_row<1, IdxT>(a.A, a.T, s, a.qs); break;
-                case 2: c = sym_merge_row<2, IdxT>(a.A, a.T, s, a.qs); break;
-                case 3: c = sym_merge_row<3, IdxT>(a.A, a.T, s, a.qs); break;
-                case 4: c = sym_merge_row<4, IdxT>(a.A, a.T, s, a.qs); break;
-                case 5: c = sym_merge_row<5, IdxT>(a.A, a.T, s, a.qs); break;
-                case 6: c = sym_merge_row<6, IdxT>(a.A, a.T, s, a.qs); break;
-                case 7: c = sym_merge_row<7, IdxT>(a.A, a.T, s, a.qs); break;
-                case 8: c = sym_merge_row<8, IdxT>(a.A, a.T, s, a.qs); break;
-                default: break;
-            }
             a.nnzc[r] = c;
             a.fnm[r] = 0;
             bin8[r] = kBinNone;
