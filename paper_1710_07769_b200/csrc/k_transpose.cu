@@ -477,7 +477,10 @@ __global__ void k_sym_probe(Csr A, int *fail) {
 // entry len_j - 1 - t of row j are each other's mirror), else by a search of
 // row j.  A missing mirror sets *fail; every warp then stops at its next chunk.
 constexpr int kSymThreads = 128;
-__global__ void __launch_bounds__(kSymThreads) k_sym_transpose(Csr A, int scale, const double *__restrict__ nrm,
+#ifndef RIG_SYM_MINB  // CTAs per SM the register budget is fitted to (measured 1, 6, 8)
+#define RIG_SYM_MINB 8
+#endif
+__global__ void __launch_bounds__(kSymThreads, RIG_SYM_MINB) k_sym_transpose(Csr A, int scale, const double *__restrict__ nrm,
                                                                const double *__restrict__ y, double *ahat, int64_t *cp,
                                                                int32_t *ri, double *vt, int *fail) {
     const int l = lane_id();
@@ -497,7 +500,7 @@ __global__ void __launch_bounds__(kSymThreads) k_sym_transpose(Csr A, int scale,
         if (r0 == 0 && l == 0) cp[0] = 0;
         const double my_n = scale && l < rows ? nrm[r0 + l] : 1.0, my_y = scale && l < rows ? y[r0 + l] : 1.0;
 #ifndef RIG_SYM_U
-#define RIG_SYM_U 4  // measured 1, 2, 4 on config 3
+#define RIG_SYM_U 2  // measured 1, 2, 4 on config 3 (with 8 CTAs per SM: 2)
 #endif
         constexpr int U = RIG_SYM_U;  // chunks of 32 entries in flight per warp
         for (int64_t c0 = __shfl_sync(kFull, my_s, 0); c0 < hi; c0 += 32 * U) {
