@@ -62,7 +62,12 @@ constexpr int kScatterThreads = 256;
 // entry's row from the bitmask of row starts inside the chunk (no search),
 // scales it, writes a_hat and appends a 16-byte record (col, row, a_hat) to
 // the column's bucket; lanes hitting the same bucket share one atomic.
-__global__ void __launch_bounds__(kScatterThreads) k_bucket_scatter(Csr A, int scale, double *__restrict__ ahat,
+#ifdef RIG_SCATTER_MINB
+#define RIG_SCATTER_BOUNDS __launch_bounds__(kScatterThreads, RIG_SCATTER_MINB)
+#else
+#define RIG_SCATTER_BOUNDS __launch_bounds__(kScatterThreads)
+#endif
+__global__ void RIG_SCATTER_BOUNDS k_bucket_scatter(Csr A, int scale, double *__restrict__ ahat,
                                                                     const int64_t *__restrict__ cp,
                                                                     unsigned long long *bcur, Rec *__restrict__ rec,
                                                                     int *err, int shift, const int *guard) {
