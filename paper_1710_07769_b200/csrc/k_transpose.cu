@@ -24,8 +24,14 @@ namespace rig {
 // sentinel per column fit kBucketSlots, larger buckets go to a CTA-wide pass.
 constexpr int kMinShift = 3, kMaxShift = 9;
 constexpr int kMaxBucketCols = 1 << kMaxShift;
-constexpr int kBucketTarget = 256;
-constexpr int kBucketSlots = 640;
+#ifndef RIG_BUCKET_TARGET
+#define RIG_BUCKET_TARGET 256
+#endif
+constexpr int kBucketTarget = RIG_BUCKET_TARGET;
+#ifndef RIG_BUCKET_SLOTS
+#define RIG_BUCKET_SLOTS 640
+#endif
+constexpr int kBucketSlots = RIG_BUCKET_SLOTS;
 
 struct __align__(16) Rec {
     int32_t col, row;
