@@ -321,6 +321,39 @@ size_t huge_bitmap_bytes(int64_t nrows, int slots);  // zeroed prefix of the scr
 int huge_slots(int64_t nrows, int64_t n_huge, bool heavy);  // heavy: the shard has huge rows
 void launch_num_huge(const MidArgs &a, int slots, void *scratch, cudaStream_t s);
 
+// k_rowwin.cu: every row of the shard in one kernel, placed straight into the
+// graph by a decoupled look-back over the rows' kept counts (no temporary).
+struct RowArgs {
+    Csr A;
+    Csc T;            // CSC offsets must fit int32 (nnz + ncols < 2^31)
+    int64_t rb, nloc;
+    int32_t *gcol;
+    double *gw;
+    int64_t cap;      // capacity of gcol / gw; rows beyond it are not written (*overflow |= 1)
+    int64_t *row_ptr; // [nloc + 1] local graph row pointers (out)
+    unsigned long long *chain;   // [nloc] look-back status words, zeroed
+    unsigned long long *ticket;  // row ticket counter, zeroed
+    double *diag;     // may be null
+    double tol;
+    const int32_t *part;  // null: no cut
+    int32_t K;
+    double *cutrow;   // [nloc] per-row cut sums (when part)
+    int *bad_part;
+    int *overflow;    // bit 0: capacity too small; bit 1: far list beyond gcap (host bug)
+    void *gscratch;   // per-warp far-list slices (rowwin_scratch_bytes(gcap)), may be null if gcap == 0
+    int gcap;
+    int32_t *stage_col;  // [rowwin_stage_entries()] per-warp staging slots
+    double *stage_w;
+    int dbg;          // RIG_DEBUG_MASK experiments (0 in normal operation)
+};
+int rowwin_grid();
+size_t rowwin_scratch_bytes(int gcap);
+size_t rowwin_stage_entries();
+int rowwin_max_gcap();
+void launch_row_win(const RowArgs &a, cudaStream_t s);
+// per-row cut sums -> 256 partials (fixed segments) and *used = 256
+void launch_rowcut_partials(const double *cutrow, int64_t n, double *partials, int *used, cudaStream_t s);
+
 // k_post.cu
 void launch_count_kept(const int64_t *gptr_ub, int64_t nloc, const int32_t *gcol, int64_t *kept, cudaStream_t s);
 void launch_compact_move(const int64_t *gptr_ub, const int64_t *gptr, int64_t nloc, const int32_t *gcol_in,

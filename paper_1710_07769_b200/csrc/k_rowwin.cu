@@ -1,0 +1,733 @@
+// k_rowwin.cu -- steps a5 + a6 (+ the fused a7 partial) for shards whose rows
+// are all off the merge path (banded / FEM-like rows of many entries, e.g.
+// BASELINE configs[4]): one warp per row of C = A_hat A_hat^T (Gustavson,
+// PAPER.md:560-562), every row placed straight into the graph.  There is no
+// symbolic pass and no graph-sized temporary: a row's kept count is
+// published as soon as it is known, and its graph offset comes from a
+// decoupled look-back over the counts of the rows before it.  Rows are handed
+// out in order by a ticket counter.  So that a warp never idles waiting for
+// slower rows in flight, a finished row goes to a small per-warp staging
+// slot (L2-resident) and is copied to its offset after the warp has computed
+// its NEXT row -- by then the rows before it have published their counts.
+//
+// Per row i (ordering contract, DESIGN.md §3 R4: every c_ij is the fma chain
+// over the shared columns k in ascending k, from +0.0):
+//  * units: the row's entries k ascending, each column cut into 32-row chunks
+//    (keys inside one column are distinct, so a unit has no conflicts); a
+//    per-row table in shared memory holds each unit's CSC offset, lane count
+//    and a_ik.  The (j, a_jk) gathers run kRwDepth units ahead.
+//  * near keys -kRwWH <= j - i < kRwWH accumulate in a direct-mapped shared window
+//    wv[j - i + kRwWH] (+0.0 initially; a slot never touched stays +0.0 and is
+//    never kept, since kept means |c| > drop_tol >= 0).  Invalid lanes of a
+//    unit carry j = -1, b = 0: never far, and near only on the slot of key
+//    -1, which no real key uses and which stays +0.0.
+//  * far keys are appended (key, a_jk, unit) to a far list in arrival (=
+//    ascending k) order.  The list is sorted stably by key: value buckets
+//    filled in arrival order; each lane then insertion-sorts its own short
+//    buckets (key ties keep arrival order), and the warp ranks the rare long
+//    bucket found out of order.  Equal keys are folded in arrival order.
+//  * count pass (kept: j != i and |c| > tol; the folded
+//    far values are kept for the emission), publish the count, then the
+//    emission writes far-below, window, far-above in ascending j; the row's
+//    cut edges (j > i, part[i] != part[j]) go to a per-row
+//    Neumaier sum, summed later in a fixed tree (deterministic).
+//  * rows of more than 32 entries or more than kRwTcap units, and rows whose
+//    far list outgrows the shared one, run with their far list in a per-warp
+//    slice of global scratch (capacity >= the largest f_i, host-checked).
+#include "common.cuh"
+
+namespace rig {
+
+constexpr int kRwThreads = 128;
+constexpr int kRwWarps = kRwThreads / 32;
+constexpr int kRwWH = 128;           // window: -kRwWH <= j - i < kRwWH
+constexpr int kRwW = 2 * kRwWH;      // window slots
+constexpr int kRwFcap = 256;         // far items in shared memory
+constexpr int kRwNB = 256;           // sort buckets (shared mode)
+constexpr int kRwGNB = 512;          // sort buckets (global mode)
+constexpr int kRwTcap = 64;          // units per table fill
+constexpr int kRwSmallBucket = 8;    // buckets up to this size: per-lane insertion sort
+constexpr int kRwStageCap = 512;     // entries per staging slot
+#ifndef RIG_RW_DEPTH
+#define RIG_RW_DEPTH 4  // 80 registers without spills (6 CTAs of 128 threads per SM)
+#endif
+constexpr int kRwDepth = RIG_RW_DEPTH;  // units in flight
+
+struct RwSmem {
+    double wv[kRwW];      // window
+    double fb[kRwFcap];   // far: a_jk; after the count pass, at a group's head item: |c| (or -1: not kept)
+    double ta[kRwTcap + kRwDepth];   // unit: a_ik (padded: see accumulate)
+    int2 tcs[kRwTcap + kRwDepth];    // unit: (CSC offset of its first lane, lane count); tmp of the bucket rank
+    int fk[kRwFcap];      // far: key j
+    int bc[kRwNB];        // bucket cursors / ends
+    unsigned bad[kRwNB / 32];
+    int nbad;
+    int badlist[32];
+    uint16_t perm[kRwFcap];
+    uint8_t fu[kRwFcap];  // far: unit (a_ik = ta[unit])
+};
+
+// far list storage: shared memory (FarS, one batch of <= 32 entries and
+// <= kRwTcap units: a_ik comes from the unit table) or a per-warp slice of
+// global scratch (FarG, a_ik stored per item); same accessors.
+struct FarS {
+    RwSmem *S;
+    static constexpr int nb = kRwNB;
+    __device__ __forceinline__ int cap() const { return kRwFcap; }
+    __device__ __forceinline__ double a(int x) const { return S->ta[S->fu[x]]; }
+    __device__ __forceinline__ void put(int pos, int j, double b, double, int u) const {
+        S->fk[pos] = j;
+        S->fb[pos] = b;
+        S->fu[pos] = (uint8_t)u;
+    }
+    __device__ __forceinline__ double *fb() const { return S->fb; }
+    __device__ __forceinline__ int *fk() const { return S->fk; }
+    __device__ __forceinline__ int *bc() const { return S->bc; }
+    __device__ __forceinline__ unsigned *bad() const { return S->bad; }
+    __device__ __forceinline__ uint16_t *perm() const { return S->perm; }
+    __device__ __forceinline__ uint16_t *tmp() const { return reinterpret_cast<uint16_t *>(S->tcs); }
+    __device__ __forceinline__ int tmp_cap() const { return kRwTcap * 4; }
+    __device__ __forceinline__ int *nbad_ptr() const { return &S->nbad; }
+    __device__ __forceinline__ void nbad_set(int v) const { S->nbad = v; }
+    __device__ __forceinline__ int nbad_get() const { return *reinterpret_cast<volatile int *>(&S->nbad); }
+    __device__ __forceinline__ int *badlist() const { return S->badlist; }
+};
+
+__host__ __device__ __forceinline__ size_t rw_slice_bytes(int gcap) {
+    const size_t b = (size_t)gcap * (8 + 8 + 4 + 2 + 2) + (size_t)kRwGNB * 4 + (kRwGNB / 32) * 4 + 33 * 4;
+    return (b + 255) & ~(size_t)255;
+}
+
+struct FarG {
+    unsigned char *base;
+    int gcap;
+    static constexpr int nb = kRwGNB;
+    __device__ __forceinline__ int cap() const { return gcap; }
+    __device__ __forceinline__ double *fa() const { return reinterpret_cast<double *>(base); }
+    __device__ __forceinline__ double *fb() const { return fa() + gcap; }
+    __device__ __forceinline__ int *fk() const { return reinterpret_cast<int *>(fb() + gcap); }
+    __device__ __forceinline__ int *bc() const { return fk() + gcap; }
+    __device__ __forceinline__ unsigned *bad() const { return reinterpret_cast<unsigned *>(bc() + kRwGNB); }
+    __device__ __forceinline__ uint16_t *perm() const { return reinterpret_cast<uint16_t *>(bad() + kRwGNB / 32); }
+    __device__ __forceinline__ uint16_t *tmp() const { return perm() + gcap; }
+    __device__ __forceinline__ int tmp_cap() const { return gcap; }
+    __device__ __forceinline__ int *nbad_ptr() const { return reinterpret_cast<int *>(tmp() + gcap); }
+    __device__ __forceinline__ void nbad_set(int v) const { *nbad_ptr() = v; }
+    __device__ __forceinline__ int nbad_get() const { return *reinterpret_cast<volatile int *>(nbad_ptr()); }
+    __device__ __forceinline__ int *badlist() const { return nbad_ptr() + 1; }
+    __device__ __forceinline__ double a(int x) const { return fa()[x]; }
+    __device__ __forceinline__ void put(int pos, int j, double b, double at, int) const {
+        fk()[pos] = j;
+        fb()[pos] = b;
+        fa()[pos] = at;
+    }
+};
+
+// ---- look-back status words: count | kAgg (count published), prefix | kPre
+constexpr unsigned long long kAgg = 1ull << 62, kPre = 2ull << 62, kValMask = (1ull << 62) - 1;
+__device__ __forceinline__ void st_relaxed(unsigned long long *p, unsigned long long v) {
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;\n" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_relaxed(const unsigned long long *p) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];\n" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// Exclusive prefix of row idx's count; idx's own status is already published
+// (kAgg, or kPre for idx 0).  All lanes call it; lane 0 publishes idx's
+// inclusive prefix.  Every lower ticket is held by a running warp, which
+// publishes its count without waiting on anything: the walk ends.
+__device__ __forceinline__ int64_t lookback(unsigned long long *chain, int64_t idx, int64_t c) {
+    const int l = lane_id();
+    if (idx == 0) return 0;
+    int64_t excl = 0;
+    int64_t base = idx - 1;
+    while (true) {
+        const int64_t j = base - l;
+        unsigned long long v = j >= 0 ? ld_relaxed(&chain[j]) : kPre;
+        unsigned zm = __ballot_sync(kFull, (v >> 62) == 0);
+        unsigned pm = __ballot_sync(kFull, (v & kPre) != 0);
+        // wait for the nearest unpublished predecessor that is needed (one
+        // lane polls one word with backoff: no polling storm on the
+        // frontier's cache lines), then look at the window again
+        while (true) {
+            const int fp = pm ? __ffs(pm) - 1 : 31;
+            const unsigned need = fp == 31 ? kFull : ((2u << fp) - 1u);
+            const unsigned wz = zm & need;
+            if (!wz) break;
+            const int t = __ffs(wz) - 1;
+            if (l == t) {
+                unsigned ns = 64;
+                do {
+                    __nanosleep(ns);
+                    ns = ns < 2048 ? ns * 2 : 2048;
+                    v = ld_relaxed(&chain[j]);
+                } while ((v >> 62) == 0);
+            }
+            __syncwarp();
+            zm = __ballot_sync(kFull, (v >> 62) == 0);
+            pm = __ballot_sync(kFull, (v & kPre) != 0);
+        }
+        const int fp = pm ? __ffs(pm) - 1 : 31;
+        const unsigned need = fp == 31 ? kFull : ((2u << fp) - 1u);
+        const int64_t add = ((need >> l) & 1u) ? (int64_t)(v & kValMask) : 0;
+        excl += warp_sum(add);
+        if (pm) break;
+        base -= 32;
+    }
+    if (l == 0) st_relaxed(&chain[idx], kPre | (unsigned long long)(excl + c));
+    return excl;
+}
+
+// Stable sort of the n far items by key: F.perm()[sorted position] = item
+// (items are numbered in arrival order).  Value buckets (monotone fp32 map of
+// key - min) filled in arrival order; each lane insertion-sorts its own
+// buckets of <= kRwSmallBucket items; a longer bucket found out of order is
+// ranked by (key, arrival) by the whole warp.
+template <class F_>
+__device__ __forceinline__ void far_sort(const F_ &F, int n) {
+    const int l = lane_id();
+    const unsigned lt = lanemask_lt();
+    constexpr int NB = F_::nb, PER = NB / 32;
+    int *fk = F.fk(), *bc = F.bc();
+    uint16_t *perm = F.perm();
+    int mn = INT_MAX, mx = INT_MIN;
+    for (int p = l; p < n; p += 32) {
+        const int k = fk[p];
+        mn = min(mn, k);
+        mx = max(mx, k);
+    }
+    mn = __reduce_min_sync(kFull, mn);
+    mx = __reduce_max_sync(kFull, mx);
+    const float scale = (float)NB / ((float)((int64_t)mx - mn) + 1.0f);
+    auto bucket = [&](int k) { return min(NB - 1, (int)(__int2float_rz(k - mn) * scale)); };
+#pragma unroll
+    for (int u = 0; u < PER; ++u) bc[l * PER + u] = 0;
+    if (l < PER) F.bad()[l] = 0u;
+    __syncwarp();
+    for (int p = l; p < n; p += 32) atomicAdd(&bc[bucket(fk[p])], 1);
+    __syncwarp();
+    int c[PER], tot = 0;
+#pragma unroll
+    for (int u = 0; u < PER; ++u) {
+        c[u] = bc[l * PER + u];
+        tot += c[u];
+    }
+    const int start = warp_incl_scan(tot) - tot;
+    int base = start;
+    __syncwarp();
+#pragma unroll
+    for (int u = 0; u < PER; ++u) {
+        bc[l * PER + u] = base;  // running cursor; ends as the bucket end
+        base += c[u];
+    }
+    __syncwarp();
+    for (int p0 = 0; p0 < n; p0 += 32) {  // arrival order: stable
+        const int p = p0 + l;
+        const int b = p < n ? bucket(fk[p]) : NB + l;
+        const unsigned g = __match_any_sync(kFull, b);
+        if (p < n) perm[bc[b] + __popc(g & lt)] = (uint16_t)p;
+        __syncwarp();
+        if (p < n && (g & lt) == 0) bc[b] += __popc(g);
+        __syncwarp();
+    }
+    // buckets holding keys of several columns may be out of order: find
+    // descents (adjacent sorted positions, same bucket since buckets are
+    // ordered by value), list each such bucket once
+    if (l == 0) F.nbad_set(0);
+    __syncwarp();
+    for (int p = l + 1; p < n; p += 32) {
+        const int k2 = fk[perm[p]];
+        if (fk[perm[p - 1]] > k2) {
+            const int b = bucket(k2);
+            const unsigned bit = 1u << (b & 31);
+            if (!(atomicOr(&F.bad()[b >> 5], bit) & bit)) {
+                const int t = atomicAdd(F.nbad_ptr(), 1);
+                if (t < 32) F.badlist()[t] = b;
+            }
+        }
+    }
+    __syncwarp();
+    const int nbad = F.nbad_get();
+    if (nbad == 0) return;
+    // one lane per short bad bucket: insertion sort (key ties keep arrival
+    // order = item index); long ones (or > 32 bad buckets): the warp ranks
+    bool big = nbad > 32;
+    if (l < nbad && l < 32) {
+        const int b = F.badlist()[l];
+        const int e1 = bc[b], e0 = b > 0 ? bc[b - 1] : 0;
+        if (e1 - e0 <= kRwSmallBucket) {
+            for (int q = e0 + 1; q < e1; ++q) {
+                const int x = perm[q], kx = fk[x];
+                int p = q - 1;
+                int y = perm[p];
+                while (fk[y] > kx) {
+                    perm[p + 1] = (uint16_t)y;
+                    if (--p < e0) break;
+                    y = perm[p];
+                }
+                perm[p + 1] = (uint16_t)x;
+            }
+            const unsigned bit = 1u << (b & 31);
+            atomicAnd(&F.bad()[b >> 5], ~bit);  // done
+        } else {
+            big = true;
+        }
+    }
+    if (!__any_sync(kFull, big)) return;
+    __syncwarp();
+    uint16_t *tmp = F.tmp();
+    for (int wd = 0; wd < PER; ++wd) {
+        unsigned m = F.bad()[wd];
+        while (m) {
+            const int b = wd * 32 + __ffs(m) - 1;
+            m &= m - 1;
+            const int e1 = bc[b], e0 = b > 0 ? bc[b - 1] : 0, sz = e1 - e0;
+            if (sz > F.tmp_cap()) continue;  // cannot happen: the tmp holds a whole list
+            for (int q = l; q < sz; q += 32) tmp[q] = perm[e0 + q];
+            __syncwarp();
+            for (int r0 = 0; r0 < sz; r0 += 32) {
+                const int x = r0 + l < sz ? (int)tmp[r0 + l] : INT_MAX;
+                const int kx = x != INT_MAX ? fk[x] : INT_MAX;
+                int rank = 0;
+                for (int s0 = 0; s0 < sz; s0 += 32) {
+                    const int y = s0 + l < sz ? (int)tmp[s0 + l] : INT_MAX;
+                    const int ky = y != INT_MAX ? fk[y] : INT_MAX;
+                    const int cnt = min(32, sz - s0);
+                    for (int t = 0; t < cnt; ++t) {
+                        const int yt = __shfl_sync(kFull, y, t);
+                        const int kt = __shfl_sync(kFull, ky, t);
+                        rank += (kt < kx) || (kt == kx && yt < x);
+                    }
+                }
+                if (x != INT_MAX) perm[e0 + rank] = (uint16_t)x;
+            }
+            __syncwarp();
+        }
+    }
+}
+
+struct RowMeta {
+    int64_t s = 0, e = 0;
+    int k = 0;           // lane t: column of entry t
+    int cs = 0, cl = 0;  // lane t: CSC offset (sentinel layout) and length of column k
+    double av = 0.0;     // lane t: a_hat_ik
+    int32_t pi = 0;      // part[i]
+};
+
+// Row metadata in three dependent stages (row pointers; entries; column
+// bounds), issued at points of the previous row where their latency hides.
+__device__ __forceinline__ void meta_rows(const RowArgs &a, int64_t idx, RowMeta &M) {
+    M.s = M.e = 0;
+    if (idx >= a.nloc) return;
+    const int64_t i = a.rb + idx;
+    M.s = a.A.rp[i];
+    M.e = a.A.rp[i + 1];
+    if (a.part) M.pi = __ldg(&a.part[i]);
+}
+__device__ __forceinline__ void meta_entries(const RowArgs &a, RowMeta &M) {
+    const int l = lane_id();
+    M.k = -1;
+    if (l < M.e - M.s) {
+        M.k = a.A.ci[M.s + l];
+        M.av = a.A.v[M.s + l];
+    }
+}
+__device__ __forceinline__ void meta_cols(const RowArgs &a, RowMeta &M) {
+    M.cl = 0;
+    if (M.k >= 0) {
+        const int64_t c0 = a.T.cp[M.k];
+        M.cl = (int)(a.T.cp[M.k + 1] - c0);
+        M.cs = (int)(c0 + M.k);
+    }
+}
+
+// Accumulate row i (window + far list).  Returns the number of far products
+// (> F.cap(): the list overflowed and is incomplete).
+template <class F_>
+__device__ __forceinline__ int accumulate(const RowArgs &a, RwSmem &S, const F_ &F, int64_t i,
+                                          const RowMeta &M) {
+    const int l = lane_id();
+    const unsigned lt = lanemask_lt();
+    const int wbase = (int)i - kRwWH;
+    int nfar = 0;
+    for (int64_t bb = M.s; bb < M.e; bb += 32) {
+        const int nent = (int)min((int64_t)32, M.e - bb);
+        int cs = 0, cl = 0;
+        double av = 0.0;
+        if (bb == M.s) {
+            cs = M.cs;
+            cl = M.cl;
+            av = M.av;
+        } else if (l < nent) {
+            const int k = a.A.ci[bb + l];
+            const int64_t c0 = a.T.cp[k];
+            cl = (int)(a.T.cp[k + 1] - c0);
+            cs = (int)(c0 + k);
+            av = a.A.v[bb + l];
+        }
+        const int nch = l < nent ? (cl + 31) >> 5 : 0;
+        const int incl = warp_incl_scan(nch);
+        const int U = __shfl_sync(kFull, incl, 31);
+        auto apply = [&](int j, double b, double at, int u) {
+            const int d = j - wbase;
+            const bool near = (unsigned)d < (unsigned)kRwW;
+            if (near) S.wv[d] = __fma_rn(at, b, S.wv[d]);
+            const bool far = !near && j >= 0;
+            const unsigned fm = __ballot_sync(kFull, far);
+            if (fm) {
+                const int pos = nfar + __popc(fm & lt);
+                if (far && pos < F.cap()) F.put(pos, j, b, at, u);
+                nfar += __popc(fm);
+            }
+        };
+        if (U <= kRwTcap) {
+            // the table is padded with empty units up to a multiple of
+            // kRwDepth (+ kRwDepth for the look-ahead): no bounds checks in
+            // the pipeline
+            const int Up = (U + kRwDepth - 1) / kRwDepth * kRwDepth;
+            for (int c = 0, ex = incl - nch; c < nch; ++c) {
+                S.tcs[ex + c] = make_int2(cs + 32 * c, min(32, cl - 32 * c));
+                S.ta[ex + c] = av;
+            }
+            if (l < Up + kRwDepth - U) {
+                S.tcs[U + l] = make_int2(0, 0);
+                S.ta[U + l] = 0.0;
+            }
+            __syncwarp();
+            int pj[kRwDepth];
+            double pb[kRwDepth];
+            auto issue = [&](int u, int &j, double &b) {
+                const int2 t = S.tcs[u];
+                j = -1;
+                b = 0.0;
+                if (l < t.y) {
+                    j = __ldg(&a.T.ri[t.x + l]);
+                    b = __ldg(&a.T.vt[t.x + l]);
+                }
+            };
+#pragma unroll
+            for (int d = 0; d < kRwDepth; ++d) issue(d, pj[d], pb[d]);
+            for (int u0 = 0; u0 < Up; u0 += kRwDepth) {
+#pragma unroll
+                for (int d = 0; d < kRwDepth; ++d) {
+                    apply(pj[d], pb[d], S.ta[u0 + d], u0 + d);
+                    issue(u0 + d + kRwDepth, pj[d], pb[d]);
+                }
+            }
+        } else {  // very long columns: unit by unit (global far list: a_ik per item)
+            for (int t = 0; t < nent; ++t) {
+                const int tcs = __shfl_sync(kFull, cs, t), tcl = __shfl_sync(kFull, cl, t);
+                const double at = __shfl_sync(kFull, av, t);
+                for (int off = 0; off < tcl; off += 32) {
+                    int j = -1;
+                    double b = 0.0;
+                    if (off + l < tcl) {
+                        j = a.T.ri[tcs + off + l];
+                        b = a.T.vt[tcs + off + l];
+                    }
+                    apply(j, b, at, 0);
+                }
+            }
+        }
+        __syncwarp();
+    }
+    return nfar;
+}
+
+// Count pass over a sorted far list: the head of each equal-key group folds
+// the group in arrival order (the R4 chain of that key) and stores |c| (or
+// -1: not kept) in fb of the head item.  Returns kept far entries; nbelow =
+// far items with key < wbase.
+template <class F_>
+__device__ __forceinline__ int far_count(const F_ &F, int n, int wbase, double tol, int &nbelow) {
+    const int l = lane_id();
+    int kept = 0;
+    nbelow = 0;
+    const int *fk = F.fk();
+    const uint16_t *perm = F.perm();
+    double *fb = F.fb();
+    for (int p0 = 0; p0 < n; p0 += 32) {
+        const int p = p0 + l;
+        bool keep = false, below = false;
+        if (p < n) {
+            const int x = perm[p];
+            const int key = fk[x];
+            below = key < wbase;
+            if (p == 0 || fk[perm[p - 1]] != key) {
+                double acc = __fma_rn(F.a(x), fb[x], +0.0);
+                for (int q = p + 1; q < n; ++q) {
+                    const int y = perm[q];
+                    if (fk[y] != key) break;
+                    acc = __fma_rn(F.a(y), fb[y], acc);
+                }
+                const double w = fabs(acc);
+                keep = w > tol;
+                fb[x] = keep ? w : -1.0;
+            }
+        }
+        __syncwarp();
+        nbelow += __popc(__ballot_sync(kFull, below));
+        kept += __popc(__ballot_sync(kFull, keep));
+    }
+    return kept;
+}
+
+// Emit a counted row in ascending j to dst (col, w) from position 0: far
+// below the window, the window (re-zeroed), far above.  Cut edges (j > i,
+// part differs) go to acc; diag[idx] = c_ii.
+template <class F_>
+__device__ __forceinline__ void emit_row(const RowArgs &a, RwSmem &S, const F_ &F, int64_t idx, int n, int nbelow,
+                                         int32_t *dcol, double *dw, bool write, int32_t pi, Comp &acc, int &badp) {
+    const int l = lane_id();
+    const unsigned lt = lanemask_lt();
+    const int64_t i = a.rb + idx;
+    const int wbase = (int)i - kRwWH;
+    const bool cut = a.part != nullptr;
+    int o = 0;
+    auto put = [&](bool keep, int key, double w) {
+        const unsigned bal = __ballot_sync(kFull, keep);
+        if (keep && write) {
+            const int pos = o + __popc(bal & lt);
+            dcol[pos] = key;
+            dw[pos] = w;
+        }
+        o += __popc(bal);
+    };
+    auto far_range = [&](int f0, int f1) {
+        for (int b0 = f0; b0 < f1; b0 += 32) {
+            const int p = b0 + l;
+            bool keep = false;
+            int key = 0;
+            double w = 0.0;
+            if (p < f1) {
+                const int x = F.perm()[p];
+                key = F.fk()[x];
+                if (p == 0 || F.fk()[F.perm()[p - 1]] != key) {
+                    w = F.fb()[x];
+                    keep = w >= 0.0;
+                }
+            }
+            if (cut && keep && (int64_t)key > i) {
+                const int32_t pj = __ldg(&a.part[key]);
+                badp |= (pj < 0) | (pj >= a.K);
+                if (pj != pi) acc.add(w);
+            }
+            put(keep, key, w);
+        }
+    };
+    far_range(0, nbelow);
+#pragma unroll
+    for (int t0 = 0; t0 < kRwW; t0 += 32) {
+        const int t = t0 + l;
+        const int key = wbase + t;
+        double c = 0.0;
+        if (t < kRwW) {
+            c = S.wv[t];
+            S.wv[t] = +0.0;
+        }
+        if (t == kRwWH && a.diag) a.diag[idx] = c;
+        const double w = fabs(c);
+        const bool keep = t < kRwW && t != kRwWH && w > a.tol;
+        if (cut && keep && t > kRwWH) {
+            const int32_t pj = __ldg(&a.part[key]);
+            badp |= (pj < 0) | (pj >= a.K);
+            if (pj != pi) acc.add(w);
+        }
+        put(keep, key, w);
+    }
+    far_range(nbelow, n);
+}
+
+// Copy a staged row (n entries) to the graph at g0 (coalesced, streaming).
+__device__ __forceinline__ void copy_staged(const int32_t *scol, const double *sw, int n, int32_t *gcol, double *gw,
+                                            int64_t g0) {
+    const int l = lane_id();
+    for (int t = l; t < n; t += 32) {
+        const int32_t c = __ldcs(scol + t);
+        const double w = __ldcs(sw + t);
+        __stcs(gcol + g0 + t, c);
+        __stcs(gw + g0 + t, w);
+    }
+}
+
+__device__ __forceinline__ void finish_cut(const RowArgs &a, int64_t idx, Comp &acc, int badp) {
+    const int l = lane_id();
+    double v = acc.value();  // fixed lane tree: deterministic per row
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(kFull, v, off);
+    if (l == 0) a.cutrow[idx] = v;
+    if (__any_sync(kFull, badp) && l == 0) atomicOr(a.bad_part, 1);
+}
+
+__global__ void __launch_bounds__(kRwThreads, 6) k_row_win(RowArgs a) {
+    extern __shared__ __align__(16) unsigned char rw_smem[];
+    const int wid = threadIdx.x >> 5;
+    RwSmem &S = reinterpret_cast<RwSmem *>(rw_smem)[wid];
+    const int l = lane_id();
+    for (int t = l; t < kRwW; t += 32) S.wv[t] = +0.0;
+    __syncwarp();
+    const FarS FS{&S};
+    const int64_t gw = (int64_t)blockIdx.x * kRwWarps + wid;
+    const FarG FG{a.gscratch ? static_cast<unsigned char *>(a.gscratch) + (size_t)gw * rw_slice_bytes(a.gcap)
+                             : nullptr,
+                  a.gcap};
+    // staging: two slots per warp
+    int32_t *stc = a.stage_col + gw * 2 * kRwStageCap;
+    double *stw = a.stage_w + gw * 2 * kRwStageCap;
+    const bool staging = !(a.dbg & 2);
+    int64_t pidx = -1;  // staged row waiting for its offset
+    int pkept = 0, pslot = 0;
+    int64_t idx = 0;
+    if (l == 0) idx = (int64_t)atomicAdd(a.ticket, 1ull);
+    idx = __shfl_sync(kFull, idx, 0);
+    RowMeta cur, nxt;
+    meta_rows(a, idx, cur);
+    meta_entries(a, cur);
+    meta_cols(a, cur);
+    // the staged row: look back for its offset, copy it into place
+    auto flush = [&]() {
+        if (pidx < 0) return;
+        const int64_t g0 = lookback(a.chain, pidx, pkept);
+        const bool fits = g0 + pkept <= a.cap;
+        if (fits) copy_staged(stc + pslot * kRwStageCap, stw + pslot * kRwStageCap, pkept, a.gcol, a.gw, g0);
+        if (l == 0) {
+            a.row_ptr[pidx + 1] = g0 + pkept;
+            if (pidx == 0) a.row_ptr[0] = 0;
+            if (!fits) atomicOr(a.overflow, 1);
+        }
+        pidx = -1;
+    };
+    auto finish = [&](const auto &F, int nfar) {
+        const int64_t i = a.rb + idx;
+        const int wbase = (int)i - kRwWH;
+        if (nfar > 1)
+            far_sort(F, nfar);
+        else if (nfar == 1 && l == 0)
+            F.perm()[0] = 0;
+        __syncwarp();
+        int nbelow = 0;
+        int kept = far_count(F, nfar, wbase, a.tol, nbelow);
+#pragma unroll
+        for (int t0 = 0; t0 < kRwW; t0 += 32) {
+            const int t = t0 + l;
+            kept += __popc(__ballot_sync(kFull, t < kRwW && t != kRwWH && fabs(S.wv[t]) > a.tol));
+        }
+        // publish the count; take the next ticket now (a ticket taken earlier
+        // would be held while this warp waits, and rows behind it would wait
+        // on it); then place the previously staged row
+        if (l == 0) st_relaxed(&a.chain[idx], (idx == 0 ? kPre : kAgg) | (unsigned long long)kept);
+        int64_t nidx = 0;
+        if (l == 0) nidx = (int64_t)atomicAdd(a.ticket, 1ull);
+        flush();
+        Comp acc;
+        int badp = a.part ? ((cur.pi < 0) | (cur.pi >= a.K)) : 0;
+        nidx = __shfl_sync(kFull, nidx, 0);
+        meta_rows(a, nidx, nxt);
+        if (staging && kept <= kRwStageCap) {
+            const int slot = pslot ^ 1;
+            emit_row(a, S, F, idx, nfar, nbelow, stc + slot * kRwStageCap, stw + slot * kRwStageCap, true, cur.pi,
+                     acc, badp);
+            pidx = idx;
+            pkept = kept;
+            pslot = slot;
+        } else {  // wait for the offset, write in place
+            const int64_t g0 = (a.dbg & 1) ? min(idx * 280, a.cap - 1024) : lookback(a.chain, idx, kept);
+            const bool fits = g0 + kept <= a.cap;
+            emit_row(a, S, F, idx, nfar, nbelow, a.gcol + g0, a.gw + g0, fits, cur.pi, acc, badp);
+            if (l == 0) {
+                a.row_ptr[idx + 1] = g0 + kept;
+                if (idx == 0) a.row_ptr[0] = 0;
+                if (!fits) atomicOr(a.overflow, 1);
+            }
+        }
+        if (a.part) finish_cut(a, idx, acc, badp);
+        meta_entries(a, nxt);
+        meta_cols(a, nxt);
+        __syncwarp();
+        return nidx;
+    };
+    while (idx < a.nloc) {
+        const int64_t i = a.rb + idx;
+        const bool one_batch = cur.e - cur.s <= 32;
+        int nfar = 0;
+        bool global = !one_batch;
+        if (one_batch) {
+            // more than kRwTcap units leave no a_ik table: global
+            const int nch = l < (int)(cur.e - cur.s) ? (cur.cl + 31) >> 5 : 0;
+            global = __reduce_add_sync(kFull, (unsigned)nch) > (unsigned)kRwTcap;
+        }
+        if (!global) {
+            nfar = accumulate(a, S, FS, i, cur);
+            if (nfar > FS.cap()) {  // far list overflow: redo with the global far list
+                for (int t = l; t < kRwW; t += 32) S.wv[t] = +0.0;
+                __syncwarp();
+                global = true;
+            }
+        }
+        int64_t nidx;
+        if (!global) {
+            nidx = finish(FS, nfar);
+        } else {
+            nfar = accumulate(a, S, FG, i, cur);
+            if (nfar > FG.cap()) {  // cannot happen when gcap >= max f_i (host check)
+                if (l == 0) atomicOr(a.overflow, 2);
+                nfar = FG.cap();
+            }
+            nidx = finish(FG, nfar);
+        }
+        idx = nidx;
+        cur = nxt;
+    }
+    flush();
+}
+
+// Per-row cut partials -> kRowCutBlocks partials (fixed segments, fixed trees).
+constexpr int kRowCutThreads = 256, kRowCutBlocks = 256;
+__global__ void __launch_bounds__(kRowCutThreads) k_rowcut_partials(const double *__restrict__ cutrow, int64_t n,
+                                                                    double *partials, int *used) {
+    const int64_t seg = (n + kRowCutBlocks - 1) / kRowCutBlocks;
+    const int64_t r0 = (int64_t)blockIdx.x * seg, r1 = min(n, r0 + seg);
+    Comp c;
+    for (int64_t r = r0 + threadIdx.x; r < r1; r += kRowCutThreads) c.add(cutrow[r]);
+    const double v = block_tree_sum<kRowCutThreads>(c.value());
+    if (threadIdx.x == 0) {
+        partials[blockIdx.x] = v;
+        if (blockIdx.x == 0) *used = kRowCutBlocks;
+    }
+}
+
+static int rowwin_ctas_per_sm() {
+    static int cache[64] = {0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64) dev = 0;
+    if (!cache[dev]) {
+        const size_t smem = (size_t)kRwWarps * sizeof(RwSmem);
+        cudaFuncSetAttribute(k_row_win, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        int per_sm = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_row_win, kRwThreads, smem);
+        cache[dev] = per_sm > 0 ? per_sm : 1;
+    }
+    return cache[dev];
+}
+
+int rowwin_grid() { return num_sms() * rowwin_ctas_per_sm(); }
+size_t rowwin_scratch_bytes(int gcap) { return (size_t)rowwin_grid() * kRwWarps * rw_slice_bytes(gcap); }
+size_t rowwin_stage_entries() { return (size_t)rowwin_grid() * kRwWarps * 2 * kRwStageCap; }
+int rowwin_max_gcap() { return 65535; }  // perm entries are 16-bit
+
+void launch_row_win(const RowArgs &a, cudaStream_t s) {
+    const size_t smem = (size_t)kRwWarps * sizeof(RwSmem);
+    cudaFuncSetAttribute(k_row_win, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_row_win<<<rowwin_grid(), kRwThreads, smem, s>>>(a);
+    note_launch();
+}
+
+void launch_rowcut_partials(const double *cutrow, int64_t n, double *partials, int *used, cudaStream_t s) {
+    k_rowcut_partials<<<kRowCutBlocks, kRowCutThreads, 0, s>>>(cutrow, n, partials, used);
+    note_launch();
+}
+
+}  // namespace rig

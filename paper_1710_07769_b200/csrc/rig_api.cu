@@ -140,6 +140,19 @@ static int64_t sym_min_nnz() {
     return v;
 }
 
+// The row-window path (k_rowwin.cu) is taken when no row of the shard is on
+// the merge path and the longest row has at most kRowWinMaxF products;
+// RIG_ROWWIN=0 turns it off (tests compare both paths).
+constexpr int64_t kRowWinMaxF = 1024;
+static bool rowwin_enabled() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("RIG_ROWWIN");
+        v = (e && atoi(e) == 0) ? 0 : 1;
+    }
+    return v == 1;
+}
+
 static bool sync_check() {
     static int v = -1;
     if (v < 0) {
@@ -335,6 +348,9 @@ struct rig_plan {
     bool cached = false;    // simple API: internal buffers from the per-thread cache
     bool early = false;     // all rows on the merge path, decided before the transpose ran:
                             // no synchronisation until the end (errors are read there)
+    bool rowwin = false;    // no row on the merge path: one row-window kernel places every
+                            // row straight into the graph (k_rowwin.cu, no temporary)
+    int rw_gcap = 0;        // its global far-list capacity (0: shared lists only)
     explicit rig_plan(cudaStream_t st) : s(st), arena(st) {}
 };
 
@@ -512,6 +528,12 @@ static void plan_build(rig_plan *p, const rig_csr_t *Ain, bool allow_early = fal
     p->nnz_upper = p->h.products - p->h.nnz_rows;
     const int64_t n_mid = p->h.n_mid;
     if (n_mid == 0) return;
+    if (n_mid == nloc && rowwin_enabled() && p->h.max_f <= kRowWinMaxF &&
+        p->A.nnz + p->A.ncols + 2 < (int64_t)INT32_MAX) {
+        p->rowwin = true;  // every row in one kernel, placed by look-back
+        p->rw_gcap = (int)std::max<int64_t>(p->h.max_f, 1);  // global far lists: rows beyond the shared list
+        return;
+    }
     // ---- rows off the merge path: ordered lists, temporary layout
     Prof pf(P_SYMBOLIC, s);
     // the huge path takes the huge bin and every row the mid kernel defers (far
@@ -566,8 +588,72 @@ struct CutReq {
 // rows' counts into the graph row pointers, merge rows in place, the others
 // copied into place.  Returns the graph nnz.  Synchronises once (twice if a
 // merge row dropped an entry by value: compaction).
+// Row-window path: chain + ticket zeroed, the kernel, the fused cut from the
+// per-row sums; one synchronisation (overflow flag and nnz).  A capacity
+// below the graph nnz leaves the rows beyond it unwritten and throws
+// NeedCapacity (build_owned retries with the exact size).
+struct NeedCapacity {
+    int64_t nnz;
+};
+static int64_t rowwin_numeric(rig_plan *p, int32_t *gcol, double *gw, int64_t cap, double *dg, int64_t *row_ptr_out,
+                              unsigned char *wn, int *flag_d, int *used, double *cutp, const CutReq *cut) {
+    cudaStream_t s = p->s;
+    Layout L;
+    const size_t o_chain = L.add(sizeof(unsigned long long) * (size_t)(p->nloc + 1));
+    const size_t zero_bytes = L.bytes;
+    const size_t o_cutrow = cut ? L.add(sizeof(double) * (size_t)p->nloc) : 0;
+    const size_t o_g = L.add(rowwin_scratch_bytes(p->rw_gcap));
+    const size_t o_sc = L.add(sizeof(int32_t) * rowwin_stage_entries());
+    const size_t o_sw = L.add(sizeof(double) * rowwin_stage_entries());
+    unsigned char *wr = p->cached ? ws_get(1, L.bytes, s) : p->arena.raw(L.bytes);
+    CK(cudaMemsetAsync(wr, 0, zero_bytes, s));
+    auto *chain = reinterpret_cast<unsigned long long *>(wr + o_chain);
+    RowArgs ra{};
+    ra.A = p->A;
+    ra.T = p->T;
+    ra.rb = p->rb;
+    ra.nloc = p->nloc;
+    ra.gcol = gcol;
+    ra.gw = gw;
+    ra.cap = cap;
+    ra.row_ptr = row_ptr_out;
+    ra.chain = chain;
+    ra.ticket = chain + p->nloc;
+    ra.diag = dg;
+    ra.tol = p->tol;
+    ra.part = cut ? cut->part : nullptr;
+    ra.K = cut ? cut->K : 0;
+    ra.cutrow = cut ? reinterpret_cast<double *>(wr + o_cutrow) : nullptr;
+    ra.bad_part = used + kCutLaunches;
+    ra.overflow = flag_d;
+    ra.gscratch = wr + o_g;
+    ra.gcap = p->rw_gcap;
+    ra.stage_col = reinterpret_cast<int32_t *>(wr + o_sc);
+    ra.stage_w = reinterpret_cast<double *>(wr + o_sw);
+    ra.dbg = debug_mask();
+    {
+        Prof pf(P_NUMERIC, s);
+        Prof pk(P_KERNEL, s);
+        launch_row_win(ra, s);
+        check_launch("row-window numeric");
+    }
+    if (cut) {
+        Prof pf(P_CUTSIZE, s);
+        launch_rowcut_partials(ra.cutrow, p->nloc, cutp, used, s);
+        launch_cut_final(cutp, used, 1, kCutSlotsPerLaunch, ra.bad_part, cut->cut_dev, s);
+        check_launch("cut_final");
+    }
+    HostStage *hs = host_stage();
+    CK(cudaMemcpyAsync(&hs->holes, flag_d, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(&hs->v[0], row_ptr_out + p->nloc, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (hs->holes & 2) throw Error(RIG_ERR_CUDA, "row-window far list capacity exceeded");
+    if (hs->holes & 1) throw NeedCapacity{hs->v[0]};
+    return hs->v[0];
+}
+
 static int64_t plan_numeric(rig_plan *p, int32_t *gcol, double *gw, double *diag, int64_t *row_ptr_out,
-                            Arena &tmp_arena, const CutReq *cut) {
+                            Arena &tmp_arena, const CutReq *cut, int64_t cap = INT64_MAX) {
     cudaStream_t s = p->s;
     // zeroed: holes flag, fused-cut used counts + bad flag
     Layout L;
@@ -584,6 +670,7 @@ static int64_t plan_numeric(rig_plan *p, int32_t *gcol, double *gw, double *diag
     double *cutp = cut ? reinterpret_cast<double *>(wn + o_cutp) : nullptr;
     double *dg = (p->flags & RIG_FLAG_DIAG) ? diag : nullptr;
     const int64_t n_mid = p->h.n_mid;
+    if (p->rowwin) return rowwin_numeric(p, gcol, gw, cap, dg, row_ptr_out, wn, holes_d, used, cutp, cut);
     {
         Prof pf(P_NUMERIC, s);
         if (n_mid > 0) {
@@ -796,19 +883,37 @@ static void build_owned(const rig_csr_t *A, int scale_rows, double drop_tol, uin
     Arena tmp(s);
     int64_t *rp = nullptr;
     unsigned char *block = nullptr;
+    int32_t *col = nullptr;
+    double *w = nullptr, *diag = nullptr;
     try {
         CK(cudaMallocAsync((void **)&rp, sizeof(int64_t) * (size_t)(p->nloc + 1), s));
         plan_build(p, A, true);
-        const int64_t cap = std::max<int64_t>(p->nnz_upper, 1);
-        Layout L;
-        const size_t o_col = L.add(sizeof(int32_t) * (size_t)cap);
-        const size_t o_w = L.add(sizeof(double) * (size_t)cap);
-        const size_t o_diag = (flags & RIG_FLAG_DIAG) ? L.add(sizeof(double) * (size_t)std::max<int64_t>(p->nloc, 1)) : 0;
-        CK(cudaMallocAsync((void **)&block, L.bytes, s));
-        int32_t *col = reinterpret_cast<int32_t *>(block + o_col);
-        double *w = reinterpret_cast<double *>(block + o_w);
-        double *diag = (flags & RIG_FLAG_DIAG) ? reinterpret_cast<double *>(block + o_diag) : nullptr;
-        const int64_t g = plan_numeric(p, col, w, diag, rp, tmp, cut);
+        // capacity: the bound sum (f_i - len_i); on the row-window path a
+        // fraction of it (stencil / banded rows keep ~half their products as
+        // distinct keys), retried at the exact size if the rows outgrow it
+        int64_t cap = std::max<int64_t>(p->nnz_upper, 1);
+        if (p->rowwin) cap = std::min<int64_t>(cap, (int64_t)(0.6 * (double)p->nnz_upper) + 4096);
+        int64_t g = 0;
+        for (int attempt = 0;; ++attempt) {
+            Layout L;
+            const size_t o_col = L.add(sizeof(int32_t) * (size_t)cap);
+            const size_t o_w = L.add(sizeof(double) * (size_t)cap);
+            const size_t o_diag =
+                (flags & RIG_FLAG_DIAG) ? L.add(sizeof(double) * (size_t)std::max<int64_t>(p->nloc, 1)) : 0;
+            CK(cudaMallocAsync((void **)&block, L.bytes, s));
+            col = reinterpret_cast<int32_t *>(block + o_col);
+            w = reinterpret_cast<double *>(block + o_w);
+            diag = (flags & RIG_FLAG_DIAG) ? reinterpret_cast<double *>(block + o_diag) : nullptr;
+            try {
+                g = plan_numeric(p, col, w, diag, rp, tmp, cut, cap);
+                break;
+            } catch (const NeedCapacity &nc) {
+                if (attempt > 0) throw Error(RIG_ERR_CUDA, "graph capacity retry failed");
+                CK(cudaFreeAsync(block, s));
+                block = nullptr;
+                cap = std::max<int64_t>(nc.nnz, 1);
+            }
+        }
         out->n = p->nloc;
         out->nnz = g;
         out->row_ptr = rp;
@@ -949,7 +1054,7 @@ int rig_plan_execute(rig_plan_t *plan, void *workspace, rig_graph_t *out, rig_st
         throw Error(RIG_ERR_INVALID, "RIG_FLAG_DIAG needs out->diag");
     plan->s = (cudaStream_t)stream;
     Arena tmp(plan->s);
-    const int64_t g = plan_numeric(plan, out->col_idx, out->w, out->diag, out->row_ptr, tmp, nullptr);
+    const int64_t g = plan_numeric(plan, out->col_idx, out->w, out->diag, out->row_ptr, tmp, nullptr, plan->nnz_upper);
     out->n = plan->nloc;
     out->nnz = g;
     return RIG_OK;

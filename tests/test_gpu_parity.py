@@ -284,6 +284,53 @@ def test_mid_rows_deferred(rig, seed):
     assert abs(cut3.item() - oc3) <= REL * oc3
 
 
+@pytest.mark.parametrize("seed", range(2))
+def test_row_window_path(rig, seed):
+    """Row-window path (k_rowwin.cu: every row off the merge path, placed by
+    look-back).  Rows of 9..30 random columns keep nearly every product as a
+    distinct key, so the graph outgrows the first capacity guess (retry at the
+    exact size) and long far lists take the global-scratch redo; a banded
+    block exercises the window.  Graph, diag and cut vs the oracle; the cut is
+    run-to-run bitwise (per-row sums, fixed tree)."""
+    rng = np.random.default_rng(900 + seed)
+    n = 5000
+    rows, cols = [], []
+    for r in range(n):
+        if r < n // 2:
+            cc = rng.choice(n, int(rng.integers(9, 31)), replace=False)
+        else:
+            cc = np.unique(np.concatenate([[r], np.clip(r + rng.integers(-60, 61, 20), 0, n - 1),
+                                           rng.integers(0, n, 2)]))
+        rows += [r] * cc.size; cols += list(cc)
+    rows, cols = np.array(rows), np.array(cols)
+    key = np.unique(rows.astype(np.int64) * n + cols)
+    rows, cols = key // n, key % n
+    vals = rng.standard_normal(rows.size)
+    vals[rng.random(rows.size) < 0.2] = 1.0  # equal products: exact cancellations
+    vals[rng.random(rows.size) < 0.2] = -1.0
+    rp, ci, v = from_triplets(n, n, rows, cols, vals)
+    K = 8
+    part = rng.integers(0, K, n).astype(np.int32)
+    tpart = torch.as_tensor(part, device="cuda")
+    A = rig.CSR(rp, ci, v)
+    for scale, tol in ((1, 0.0), (0, 0.25)):
+        orc = oracle.build(rp, ci, v, scale_rows=scale, drop_tol=tol)
+        ocut = oracle.cutsize(orc.row_ptr, orc.col, orc.w, part, K)[0]
+        g = rig.rig_build(A, scale, tol, rig.RIG_FLAG_DIAG)
+        assert_graph_equal(to_np(g.row_ptr), to_np(g.col_idx), to_np(g.w), orc, to_np(g.diag))
+        cuts = []
+        for _ in range(2):
+            gc, cut = rig.rig_build_cut(A, tpart, K, 0, n, scale, tol)
+            assert_graph_equal(to_np(gc.row_ptr), to_np(gc.col_idx), to_np(gc.w), orc)
+            cuts.append(cut.item())
+        assert abs(cuts[0] - ocut) <= REL * ocut
+        assert cuts[0] == cuts[1]
+        plan = rig.Plan(A, scale, tol, rig.RIG_FLAG_DIAG)
+        tg = plan.execute()
+        assert_graph_equal(to_np(tg.row_ptr), to_np(tg.col_idx), to_np(tg.w), orc, to_np(tg.diag))
+        plan.destroy()
+
+
 def test_mid_row_passes_long_far_lists(rig):
     """Rows of 800..3500 random columns (every key far from the diagonal) run
     through the mid pass, the 768-item far-list pass, the wide window and the
