@@ -25,7 +25,15 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "rig_oracle.c")
 _LIB = os.path.join(_HERE, "liboracle.so")
 
-CFLAGS = ["-O2", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared", "-std=gnu99"]
+CFLAGS = ["-O2", "-ffp-contract=off", "-fno-fast-math", "-fopenmp", "-fPIC", "-shared", "-std=gnu99"]
+
+
+def default_threads() -> int:
+    """Host cores this process may use (os.sched_getaffinity), capped at 64."""
+    try:
+        return max(1, min(64, len(os.sched_getaffinity(0))))
+    except Exception:
+        return max(1, min(64, os.cpu_count() or 1))
 
 
 def build_lib(force: bool = False) -> str:
@@ -51,6 +59,8 @@ def lib():
         _lib.orc_build.argtypes = [i64, i64, p, p, p, p, p, p, ctypes.c_double, i64, i64,
                                    p, p, p, p, p, p]
         _lib.orc_free.argtypes = [p]
+        _lib.orc_build_par.argtypes = [i64, i64, p, p, p, p, p, p, ctypes.c_double, i64, i64, ctypes.c_int,
+                                       p, p, p, p, p, p]
         _lib.orc_cutsize.argtypes = [i64, i64, p, p, p, i64, p, i32, p, p, p]
         _lib.orc_ip_matrix.argtypes = [i64, i64, p, p, p, i64, p, i32, p, p, p]
         _lib.orc_dense_threshold.argtypes = [i64]
@@ -124,7 +134,10 @@ class Graph:
         return int(self.row_ptr[-1])
 
 
-def build_from_scaled(nrows, ncols, row_ptr, col_idx, val_hat, csc, drop_tol, row_begin=0, row_end=None):
+def build_from_scaled(nrows, ncols, row_ptr, col_idx, val_hat, csc, drop_tol, row_begin=0, row_end=None,
+                      threads=1):
+    """Rows [row_begin, row_end) of G_RIP; threads > 1 runs row chunks of the
+    same C routine concurrently (orc_build_par): identical output."""
     row_ptr, col_idx, val_hat = _c(row_ptr, np.int64), _c(col_idx, np.int32), _c(val_hat, np.float64)
     col_ptr, row_idx, valT = csc
     row_end = nrows if row_end is None else row_end
@@ -134,9 +147,14 @@ def build_from_scaled(nrows, ncols, row_ptr, col_idx, val_hat, csc, drop_tol, ro
     gnnz = ctypes.c_int64()
     diag = np.empty(nloc, dtype=np.float64)
     nnzc = np.empty(nloc, dtype=np.int64)
-    st = L.orc_build(nrows, ncols, _p(row_ptr), _p(col_idx), _p(val_hat), _p(col_ptr), _p(row_idx),
-                     _p(valT), float(drop_tol), row_begin, row_end, ctypes.byref(rp), ctypes.byref(gc),
-                     ctypes.byref(gw), ctypes.byref(gnnz), _p(diag), _p(nnzc))
+    if threads > 1:
+        st = L.orc_build_par(nrows, ncols, _p(row_ptr), _p(col_idx), _p(val_hat), _p(col_ptr), _p(row_idx),
+                             _p(valT), float(drop_tol), row_begin, row_end, int(threads), ctypes.byref(rp),
+                             ctypes.byref(gc), ctypes.byref(gw), ctypes.byref(gnnz), _p(diag), _p(nnzc))
+    else:
+        st = L.orc_build(nrows, ncols, _p(row_ptr), _p(col_idx), _p(val_hat), _p(col_ptr), _p(row_idx),
+                         _p(valT), float(drop_tol), row_begin, row_end, ctypes.byref(rp), ctypes.byref(gc),
+                         ctypes.byref(gw), ctypes.byref(gnnz), _p(diag), _p(nnzc))
     if st:
         raise OracleError(st, "build")
     g = gnnz.value
@@ -156,7 +174,7 @@ def build_from_scaled(nrows, ncols, row_ptr, col_idx, val_hat, csc, drop_tol, ro
 
 
 def build(row_ptr, col_idx, val, ncols=None, scale_rows=1, drop_tol=0.0, row_begin=0, row_end=None,
-          keep_intermediates=False):
+          keep_intermediates=False, threads=1):
     """Full oracle pipeline: [scale] -> CSC -> Gustavson rows -> graph."""
     row_ptr, col_idx, val = _c(row_ptr, np.int64), _c(col_idx, np.int32), _c(val, np.float64)
     nrows = row_ptr.size - 1
@@ -166,7 +184,7 @@ def build(row_ptr, col_idx, val, ncols=None, scale_rows=1, drop_tol=0.0, row_beg
     f, _ = row_products(row_ptr, col_idx, csc[0])
     row_end = nrows if row_end is None else row_end
     g_rp, g_col, g_w, diag, nnzc = build_from_scaled(nrows, ncols, row_ptr, col_idx, a_hat, csc, drop_tol,
-                                                     row_begin, row_end)
+                                                     row_begin, row_end, threads=threads)
     products = int(f[row_begin:row_end].sum())
     return Graph(g_rp, g_col, g_w, diag, nnzc, row_begin, products,
                  a_hat if keep_intermediates else None, csc if keep_intermediates else None)

@@ -27,8 +27,11 @@
  *   - cutsize sums each undirected cut edge once (stored j > i), Neumaier
  *     compensated (c2 #8-#9).
  *
- * Build: gcc -O2 -ffp-contract=off -fno-fast-math (no DAZ/FTZ); fma() is the
- * C99 correctly-rounded fused multiply-add.
+ * Build: gcc -O2 -ffp-contract=off -fno-fast-math -fopenmp (no DAZ/FTZ); fma()
+ * is the C99 correctly-rounded fused multiply-add.  OpenMP only runs row
+ * chunks of orc_build concurrently (orc_build_par, SURVEY.md §8(c) c1 step
+ * 6): every row is computed by the same code, so the result is identical for
+ * any thread count.
  */
 #include <math.h>
 #include <stdint.h>
@@ -201,6 +204,76 @@ int orc_build(int64_t nrows, int64_t ncols, const int64_t *row_ptr,
 }
 
 void orc_free(void *p) { free(p); }
+
+/* orc_build over rows [row_begin, row_end) in contiguous row chunks run by
+ * `nthreads` OpenMP threads (each chunk: its own dense accumulator), outputs
+ * concatenated in row order.  Same outputs as orc_build, bit for bit. */
+int orc_build_par(int64_t nrows, int64_t ncols, const int64_t *row_ptr,
+                  const int32_t *col_idx, const double *val, const int64_t *col_ptr,
+                  const int32_t *row_idx, const double *valT, double drop_tol,
+                  int64_t row_begin, int64_t row_end, int nthreads, int64_t **g_row_ptr,
+                  int32_t **g_col, double **g_w, int64_t *g_nnz, double *diag,
+                  int64_t *nnzc) {
+    if (row_begin < 0 || row_end > nrows || row_begin > row_end) return ORC_ERR_INVALID;
+    if (nthreads < 1) nthreads = 1;
+    int64_t nloc = row_end - row_begin;
+    int64_t nch = (int64_t)nthreads * 4;
+    if (nch > nloc) nch = nloc > 0 ? nloc : 1;
+    int64_t **rps = (int64_t **)calloc((size_t)nch, sizeof(int64_t *));
+    int32_t **gcs = (int32_t **)calloc((size_t)nch, sizeof(int32_t *));
+    double **gws = (double **)calloc((size_t)nch, sizeof(double *));
+    int64_t *cnt = (int64_t *)calloc((size_t)nch, sizeof(int64_t));
+    int *st = (int *)calloc((size_t)nch, sizeof(int));
+    int64_t *rp = (int64_t *)malloc(sizeof(int64_t) * (size_t)(nloc + 1));
+    if (!rps || !gcs || !gws || !cnt || !st || !rp) {
+        free(rps); free(gcs); free(gws); free(cnt); free(st); free(rp);
+        return ORC_ERR_NOMEM;
+    }
+    #pragma omp parallel for schedule(dynamic, 1) num_threads(nthreads)
+    for (int64_t c = 0; c < nch; ++c) {
+        int64_t a = row_begin + nloc * c / nch, b = row_begin + nloc * (c + 1) / nch;
+        st[c] = orc_build(nrows, ncols, row_ptr, col_idx, val, col_ptr, row_idx, valT, drop_tol, a, b,
+                          &rps[c], &gcs[c], &gws[c], &cnt[c], diag ? diag + (a - row_begin) : NULL,
+                          nnzc ? nnzc + (a - row_begin) : NULL);
+    }
+    int err = ORC_OK;
+    int64_t total = 0;
+    for (int64_t c = 0; c < nch; ++c) {
+        if (st[c] && !err) err = st[c];
+        total += cnt[c];
+    }
+    int32_t *gc = NULL;
+    double *gw = NULL;
+    if (!err) {
+        gc = (int32_t *)malloc(sizeof(int32_t) * (size_t)(total > 0 ? total : 1));
+        gw = (double *)malloc(sizeof(double) * (size_t)(total > 0 ? total : 1));
+        if (!gc || !gw) err = ORC_ERR_NOMEM;
+    }
+    if (!err) {
+        int64_t off = 0;
+        rp[0] = 0;
+        for (int64_t c = 0; c < nch; ++c) {
+            int64_t a = nloc * c / nch, b = nloc * (c + 1) / nch;
+            for (int64_t r = a; r < b; ++r) rp[r + 1] = off + rps[c][r - a + 1];
+            memcpy(gc + off, gcs[c], sizeof(int32_t) * (size_t)cnt[c]);
+            memcpy(gw + off, gws[c], sizeof(double) * (size_t)cnt[c]);
+            off += cnt[c];
+        }
+    }
+    for (int64_t c = 0; c < nch; ++c) {
+        free(rps[c]); free(gcs[c]); free(gws[c]);
+    }
+    free(rps); free(gcs); free(gws); free(cnt); free(st);
+    if (err) {
+        free(rp); free(gc); free(gw);
+        return err;
+    }
+    *g_row_ptr = rp;
+    *g_col = gc;
+    *g_w = gw;
+    *g_nnz = total;
+    return ORC_OK;
+}
 
 /* Neumaier-compensated summation step. */
 static void neumaier(double *s, double *c, double x) {

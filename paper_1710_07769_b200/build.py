@@ -28,11 +28,29 @@ def deps():
     return sources() + glob.glob(os.path.join(CSRC, "*.cuh")) + [os.path.join(HERE, "..", "include", "rig.h")]
 
 
+STAMP = LIB + ".sha256"
+
+
+def source_hash() -> str:
+    """sha256 over the compiler, its flags and every source/header (by content):
+    the library is rebuilt whenever any of them differs from the recorded one,
+    whatever the file times say."""
+    import hashlib
+
+    h = hashlib.sha256()
+    h.update(" ".join([NVCC, *NVCC_FLAGS]).encode())
+    for p in sorted(deps()):
+        h.update(os.path.basename(p).encode())
+        with open(p, "rb") as fh:
+            h.update(fh.read())
+    return h.hexdigest()
+
+
 def up_to_date() -> bool:
-    if not os.path.exists(LIB):
+    if not os.path.exists(LIB) or not os.path.exists(STAMP):
         return False
-    t = os.path.getmtime(LIB)
-    return all(os.path.getmtime(p) <= t for p in deps())
+    with open(STAMP) as fh:
+        return fh.read().strip() == source_hash()
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
@@ -40,14 +58,17 @@ def build(force: bool = False, verbose: bool = False) -> str:
         return LIB
     objdir = os.path.join(HERE, "build")
     os.makedirs(objdir, exist_ok=True)
-    objs = []
-    for src in sources():
+    objs, procs = [], []
+    for src in sources():  # one nvcc per file, concurrently
         obj = os.path.join(objdir, os.path.basename(src)[:-3] + ".o")
-        cmd = [NVCC, *NVCC_FLAGS, "-dc" if False else "-c", src, "-o", obj]
+        cmd = [NVCC, *NVCC_FLAGS, "-c", src, "-o", obj]
         if verbose:
             print(" ".join(cmd), flush=True)
-        subprocess.check_call(cmd)
+        procs.append((src, subprocess.Popen(cmd)))
         objs.append(obj)
+    failed = [src for src, pr in procs if pr.wait() != 0]
+    if failed:
+        raise RuntimeError(f"nvcc failed: {failed}")
     tmp = LIB + f".{os.getpid()}.tmp"
     cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", tmp, *objs,
            "-Xcompiler", "-fPIC", "-lcudart"]
@@ -55,6 +76,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
         print(" ".join(cmd), flush=True)
     subprocess.check_call(cmd)
     os.replace(tmp, LIB)
+    with open(STAMP, "w") as fh:
+        fh.write(source_hash() + "\n")
     return LIB
 
 

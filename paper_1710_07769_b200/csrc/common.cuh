@@ -45,6 +45,8 @@ struct Csc {
     const double *vt;   // [nnz + ncols] bit-identical to the CSR value of (i,k)
 };
 __device__ __forceinline__ int64_t csc_begin(const Csc &T, int k) { return T.cp[k] + k; }
+// CSC positions (entries + one sentinel per column + the leading pad) fit int32
+inline bool csc_fits_i32(const Csr &A) { return A.nnz + A.ncols + 2 <= (int64_t)INT32_MAX; }
 
 // Counters written by the device and read back by the host at a sync.
 constexpr int kSymBins = kNumSymBins + 1;  // + huge

@@ -334,12 +334,21 @@ __device__ __forceinline__ void meta_entries(const RowArgs &a, RowMeta &M) {
         M.av = a.A.v[M.s + l];
     }
 }
-__device__ __forceinline__ void meta_cols(const RowArgs &a, RowMeta &M) {
+__device__ __forceinline__ void prefetch_l2(const void *p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
+// stage 3; with `pf`, each lane also prefetches its column (rows, values)
+// into L2, so that the row's gathers hit L2 when the row starts
+__device__ __forceinline__ void meta_cols(const RowArgs &a, RowMeta &M, bool pf) {
     M.cl = 0;
     if (M.k >= 0) {
         const int64_t c0 = a.T.cp[M.k];
         M.cl = (int)(a.T.cp[M.k + 1] - c0);
         M.cs = (int)(c0 + M.k);
+        if (pf) {
+            const char *r0 = reinterpret_cast<const char *>(a.T.ri + M.cs);
+            const char *v0 = reinterpret_cast<const char *>(a.T.vt + M.cs);
+            for (int off = 0; off < M.cl * 4; off += 128) prefetch_l2(r0 + off);
+            for (int off = 0; off < M.cl * 8; off += 128) prefetch_l2(v0 + off);
+        }
     }
 }
 
@@ -585,7 +594,7 @@ __global__ void __launch_bounds__(kRwThreads, 6) k_row_win(RowArgs a) {
     RowMeta cur, nxt;
     meta_rows(a, idx, cur);
     meta_entries(a, cur);
-    meta_cols(a, cur);
+    meta_cols(a, cur, false);
     // the staged row: look back for its offset, copy it into place
     auto flush = [&]() {
         if (pidx < 0) return;
@@ -644,7 +653,7 @@ __global__ void __launch_bounds__(kRwThreads, 6) k_row_win(RowArgs a) {
         }
         if (a.part) finish_cut(a, idx, acc, badp);
         meta_entries(a, nxt);
-        meta_cols(a, nxt);
+        meta_cols(a, nxt, !(a.dbg & 4));
         __syncwarp();
         return nidx;
     };

@@ -1,7 +1,16 @@
 // k_scan.cu -- device-wide exclusive prefix sum with int64 output (CSC column
-// pointers, graph row pointers, flop prefix).  Two launches: per-tile totals,
-// then per-tile scan where each CTA adds the totals of all earlier tiles
-// (tiles are few: <= n / 4096), so there is no serial chain between CTAs.
+// pointers, graph row pointers, flop prefix).  Two variants:
+//  * single pass (k_scan_1p, the default when no shape statistics are
+//    wanted): tiles of kTile items taken in order from a ticket; each tile
+//    publishes its total, then finds its prefix by a decoupled look-back over
+//    the earlier tiles' 64-bit status words (2 flag bits + a 62-bit value).
+//    Assumptions: every prefix is < 2^62; forward progress holds because a
+//    tile only waits on tiles with lower tickets, which were taken by CTAs
+//    already running (tickets are handed out by resident CTAs only).
+//  * two launches (k_tile_sum + k_tile_scan, used with the shape statistics
+//    or an event between the passes): per-tile totals, then each CTA adds the
+//    totals of all earlier tiles (tiles are few: <= n / 4096), so there is no
+//    serial chain between CTAs.
 #include "common.cuh"
 
 namespace rig {

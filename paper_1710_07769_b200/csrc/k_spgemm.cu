@@ -634,7 +634,7 @@ void launch_analyze_sym(const SymArgs &a, uint8_t *bin8, DevCounters *ctr, cudaS
     const int64_t nloc = a.re - a.rb;
     int64_t g = (nloc + kMergeThreads - 1) / kMergeThreads;
     g = g < 1 ? 1 : (g > (int64_t)sms() * 16 ? (int64_t)sms() * 16 : g);
-    if (a.A.nnz <= INT32_MAX)
+    if (csc_fits_i32(a.A))
         k_analyze_sym<int32_t><<<(unsigned)g, kMergeThreads, 0, s>>>(a, bin8, ctr);
     else
         k_analyze_sym<int64_t><<<(unsigned)g, kMergeThreads, 0, s>>>(a, bin8, ctr);
@@ -653,12 +653,9 @@ static void launch_merge_t(const SymArgs *sa, const NumArgs *na, cudaStream_t s)
         int64_t g = (nloc + kMergeThreads - 1) / kMergeThreads;
         g = g < 1 ? 1 : (g > (int64_t)sms() * 16 ? (int64_t)sms() * 16 : g);
         const size_t smem = (size_t)kMergeWarps * (size_t)na->stage_cap * (sizeof(double) + sizeof(int32_t));
-        static bool attr = false;
-        if (!attr) {
-            cudaFuncSetAttribute(k_num_merge<RMAX, IdxT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)(kMergeWarps * kMaxStageCap * (sizeof(double) + sizeof(int32_t))));
-            attr = true;
-        }
+        // per device (context): set before every launch (cheap), never cached in a static
+        cudaFuncSetAttribute(k_num_merge<RMAX, IdxT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)(kMergeWarps * kMaxStageCap * (sizeof(double) + sizeof(int32_t))));
         k_num_merge<RMAX, IdxT><<<(unsigned)g, kMergeThreads, smem, s>>>(*na);
     }
     note_launch();
@@ -679,7 +676,7 @@ static void launch_merge_r(int maxlen, const SymArgs *sa, const NumArgs *na, cud
 }
 
 void launch_sym_merge(const SymArgs &a, int maxlen, cudaStream_t s) {
-    if (a.A.nnz <= INT32_MAX)
+    if (csc_fits_i32(a.A))
         launch_merge_r<int32_t>(maxlen, &a, nullptr, s);
     else
         launch_merge_r<int64_t>(maxlen, &a, nullptr, s);
@@ -688,12 +685,9 @@ void launch_sym_merge(const SymArgs &a, int maxlen, cudaStream_t s) {
 template <int RMAX>
 static void launch_pair_t(const NumArgs &na, cudaStream_t s) {
     const size_t smem = (size_t)kPairWarps * (size_t)na.stage_cap * (sizeof(double) + sizeof(int32_t));
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(k_num_pair<RMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)((size_t)kPairWarps * kMaxStageCap * (sizeof(double) + sizeof(int32_t))));
-        attr = true;
-    }
+    // per device (context): set before every launch, never cached in a static
+    cudaFuncSetAttribute(k_num_pair<RMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)((size_t)kPairWarps * kMaxStageCap * (sizeof(double) + sizeof(int32_t))));
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_num_pair<RMAX>, kPairThreads, smem);
     if (per_sm < 1) per_sm = 1;
@@ -717,7 +711,7 @@ void launch_num_merge(const NumArgs &a, int maxlen, cudaStream_t s) {
         }
         return;
     }
-    if (a.A.nnz <= INT32_MAX)
+    if (csc_fits_i32(a.A))
         launch_merge_r<int32_t>(maxlen, nullptr, &a, s);
     else
         launch_merge_r<int64_t>(maxlen, nullptr, &a, s);

@@ -391,7 +391,7 @@ static void plan_build(rig_plan *p, const rig_csr_t *Ain, bool allow_early = fal
     const size_t o_nnzc = L.add(sizeof(int64_t) * (size_t)nloc);
     const size_t o_fnm = L.add(sizeof(int64_t) * (size_t)nloc);
     const size_t o_bin8 = L.add((size_t)nloc);
-    const bool use_qs = nnz + m <= (int64_t)INT32_MAX;  // run starts fit int32
+    const bool use_qs = csc_fits_i32(A0);  // run starts fit int32
     const size_t o_qs = use_qs ? L.add(sizeof(int2) * (size_t)nnz) : 0;
     // f1 (RIG_FLAG_SPARSIFY): dense-column list and cutoffs, A~ in CSR
     size_t o_dlist = 0, o_ckey = 0, o_crow = 0, o_nk = 0, o_rp2 = 0, o_ci2 = 0, o_v2 = 0, o_st3 = 0;
@@ -515,8 +515,11 @@ static void plan_build(rig_plan *p, const rig_csr_t *Ain, bool allow_early = fal
             p->early = true;
             p->h = DevCounters{};
             p->h.max_len = (int)sh.max_row;
-            p->h.products = sh.p_full;
-            p->nnz_upper = sh.p_full - sh.shard_nnz;
+            // a shard's products are at most min(sum_k len_k^2, shard_nnz *
+            // max_col) (f_i <= len_i * max_col): the bound scales with the shard
+            const int64_t pb = std::min<int64_t>(sh.p_full, sh.shard_nnz * sh.max_col);
+            p->h.products = pb;  // an upper bound here (sizes the merge kernel's stage)
+            p->nnz_upper = pb - sh.shard_nnz;
             return;
         }
     }
@@ -529,7 +532,7 @@ static void plan_build(rig_plan *p, const rig_csr_t *Ain, bool allow_early = fal
     const int64_t n_mid = p->h.n_mid;
     if (n_mid == 0) return;
     if (n_mid == nloc && rowwin_enabled() && p->h.max_f <= kRowWinMaxF &&
-        p->A.nnz + p->A.ncols + 2 < (int64_t)INT32_MAX) {
+        csc_fits_i32(p->A)) {
         p->rowwin = true;  // every row in one kernel, placed by look-back
         p->rw_gcap = (int)std::max<int64_t>(p->h.max_f, 1);  // global far lists: rows beyond the shared list
         return;

@@ -127,17 +127,25 @@ class _Cai:
 
 
 class _GraphOwner:
-    """Owns the library-allocated arrays of one graph; freed (rig_graph_free,
-    stream-ordered on the current stream) when the Graph and every tensor view
-    of it are gone.  Holds no reference back to them: no reference cycle."""
+    """Owns the library-allocated arrays of one graph; freed (rig_graph_free)
+    when the Graph and every tensor view of it are gone.  The free is ordered
+    on the stream and device the graph was BUILT on (not whatever is current at
+    collection time), so it follows the build's pending work; a consumer on
+    another stream must synchronise with the build stream before dropping its
+    views.  Holds no reference back to the views: no reference cycle."""
 
-    def __init__(self, g: rig_graph_t):
+    def __init__(self, g: rig_graph_t, stream=None):
         self.g = g
+        s = stream if stream is not None else torch.cuda.current_stream()
+        self.stream = s if isinstance(s, torch.cuda.Stream) else None
+        self.raw_stream = _stream(stream)
+        self.device = torch.cuda.current_device()
 
     def __del__(self):
         try:
             if self.g is not None:
-                lib.rig_graph_free(ctypes.byref(self.g), _stream())
+                with torch.cuda.device(self.device):
+                    lib.rig_graph_free(ctypes.byref(self.g), self.raw_stream)
                 self.g = None
         except Exception:
             pass
@@ -148,7 +156,7 @@ class Graph:
     (rig_build) exposed as torch views, created on first access."""
 
     def __init__(self, g: rig_graph_t, row_begin: int, stream):
-        self._owner = _GraphOwner(g)
+        self._owner = _GraphOwner(g, stream)
         self._g = rig_graph_t(g.n, g.nnz, g.row_ptr, g.col_idx, g.w, g.diag)
         self.row_begin = row_begin
         self.n, self.nnz = int(g.n), int(g.nnz)

@@ -535,3 +535,54 @@ def test_int_weights_paper_range():
         oracle.int_weights(np.array([0.5]), 0)
     with pytest.raises(oracle.OracleError):
         oracle.int_weights(np.array([-0.5]), 10)
+
+
+@pytest.mark.parametrize("threads", [2, 3, 8])
+def test_parallel_oracle_identical(threads):
+    """orc_build_par (OpenMP row chunks) returns
+    orc_build's outputs bit for bit, for any thread count and row range."""
+    rng = np.random.default_rng(77 + threads)
+    for cfg in (1, 4, 5):
+        w = make_small(cfg)
+        a, b = (0, w.n) if cfg != 5 else (123, w.n - 77)
+        g1 = oracle.build(w.row_ptr, w.col_idx, w.val, scale_rows=w.scale_rows, drop_tol=w.drop_tol,
+                          row_begin=a, row_end=b)
+        gp = oracle.build(w.row_ptr, w.col_idx, w.val, scale_rows=w.scale_rows, drop_tol=w.drop_tol,
+                          row_begin=a, row_end=b, threads=threads)
+        assert np.array_equal(g1.row_ptr, gp.row_ptr) and np.array_equal(g1.col, gp.col)
+        assert g1.w.tobytes() == gp.w.tobytes() and g1.diag.tobytes() == gp.diag.tobytes()
+        assert np.array_equal(g1.nnzc, gp.nnzc)
+    assert rng is not None
+
+
+def test_full_size_golden_record():
+    """tests/golden/full_size_digests.json (tools/make_full_golden.py, oracle
+    only) covers configs 1-5; its totals agree with the closed forms of the
+    stencil configs and its blocks tile the rows."""
+    import json
+    import os
+
+    with open(os.path.join(os.path.dirname(__file__), "golden", "full_size_digests.json")) as fh:
+        gold = json.load(fh)
+    assert all(str(c) in gold for c in (1, 2, 3, 4, 5))
+    assert gold["2"]["graph_nnz"] == 11_980_004 and gold["3"]["graph_nnz"] == 190_322_400
+    for c in (1, 2, 3, 4, 5):
+        g = gold[str(c)]
+        rows = [b["rows"] for b in g["blocks"]]
+        assert rows[0][0] == 0 and rows[-1][1] == g["n"]
+        assert all(r[1] == s[0] for r, s in zip(rows, rows[1:]))
+        assert sum(b["nnz"] for b in g["blocks"]) == g["graph_nnz"]
+        assert 0.0 <= g["cut"] <= g["total_weight"]
+    # config 2 at full size through the oracle here: the recorded digests and cut
+    w = make(2)
+    a_hat = oracle.scale(w.row_ptr, w.val)[0]
+    csc = oracle.transpose(w.n, w.n, w.row_ptr, w.col_idx, a_hat)
+    import hashlib
+
+    blk = gold["2"]["blocks"][5]
+    a, b = blk["rows"]
+    rp, col, wv, diag, _ = oracle.build_from_scaled(w.n, w.n, w.row_ptr, w.col_idx, a_hat, csc, w.drop_tol, a, b)
+    h = hashlib.sha256()
+    for x, dt in ((rp, "<i8"), (col, "<i4"), (wv, "<f8"), (diag, "<f8")):
+        h.update(np.ascontiguousarray(x, dtype=dt).tobytes())
+    assert h.hexdigest() == blk["sha256"]
