@@ -4,15 +4,17 @@ one synthetic matrix resident in HBM: rig_build (scale, transpose, analyze,
 symbolic, numeric fused with abs/drop/diag-strip, compaction if needed) +
 rig_cutsize (+ NCCL allreduce of the cut when N > 1).
 
-Workload (N=1): BASELINE.json configs[1] -- 2-D convection-diffusion-like
-5-point stencil, n = 1,000,000.  Metric: A.A^T intermediate
-products per second (P / step time), plus build ms and the numeric pass's
-fraction of the measured HBM roofline.
+Workload (N=1, default): BASELINE.json configs[4] -- banded-plus-random,
+n = 4,000,000 (the config with the most work: 2.19e9 products, 1.13e9 graph
+entries).  --config selects another (1-7).  Metric: A.A^T
+intermediate products per second (P / step time), plus build ms and the
+numeric pass's fraction of the HBM roofline (measured copy bandwidth and the
+8.0 TB/s spec).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--impl reference]
 N > 1: launch with torchrun (one rank per GPU); rows of C are sharded by
-flop count (rig_row_split), the cut is allreduced over NCCL, the time is the
-max over ranks.
+flop count (rig_row_split) and built by dist.build_cut_sharded (the cut is
+allreduced over NCCL); the time is the max over ranks.
 """
 from __future__ import annotations
 
@@ -25,11 +27,14 @@ import sys
 import threading
 import time
 
+import numpy as np
+
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "A·A^T intermediate products/s and row-graph build ms; % of HBM roofline"
 L2_FLUSH_BYTES = 512 << 20
+SPEC_HBM_GBS = 8000.0  # B200 HBM3e spec (north star: "~8 TB/s")
 
 
 def parse():
@@ -37,10 +42,11 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", type=int, default=2, help="BASELINE.json config id (1-based); default configs[1]")
+    ap.add_argument("--config", type=int, default=5, help="BASELINE.json config id (1-based); default configs[4]")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--cpu-seconds", type=float, default=12.0, help="bounded oracle sample (cpu_baseline)")
+    ap.add_argument("--ref-step-seconds", type=float, default=3.0, help="--impl reference: oracle work per step")
     ap.add_argument("--clock-ms", type=int, default=100, help="nvidia-smi sampling period (0: off)")
     ap.add_argument("--soak-seconds", type=float, default=1.5,
                     help="untimed steps before the timed region so clocks are sampled under load")
@@ -139,56 +145,110 @@ class ClockSampler:
         return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+class OracleSample:
+    """The oracle as it stands (plain C, oracle/), on a bounded sample of the
+    workload: rows [0, R) of G_RIP (dense-accumulator Gustavson + the cutsize
+    of those rows), the scaling and CSC prepared once beforehand.  R is sized
+    from a short calibration so one sample takes about `seconds`."""
+
+    def __init__(self, w):
+        import oracle
+
+        self.o, self.w = oracle, w
+        t0 = time.perf_counter()
+        self.a_hat = oracle.scale(w.row_ptr, w.val)[0] if w.scale_rows else w.val
+        self.csc = oracle.transpose(w.n, w.ncols, w.row_ptr, w.col_idx, self.a_hat)
+        self.prep_s = time.perf_counter() - t0
+        self.f = oracle.row_products(w.row_ptr, w.col_idx, self.csc[0])[0]
+        self.fpre = np.concatenate([[0], np.cumsum(self.f)])
+
+    def run(self, rows, threads):
+        w = self.w
+        t0 = time.perf_counter()
+        rp, col, wv, _d, _n = self.o.build_from_scaled(w.n, w.ncols, w.row_ptr, w.col_idx, self.a_hat, self.csc,
+                                                       w.drop_tol, 0, rows, threads=threads)
+        self.o.cutsize(rp, col, wv, w.part, w.K)
+        return time.perf_counter() - t0, int(self.fpre[rows])
+
+    def rows_for(self, seconds, threads):
+        n = self.w.n
+        r = min(n, 2048)
+        while True:
+            t, P = self.run(r, threads)
+            if r >= n or t >= 0.25 * seconds:
+                break
+            r = min(n, r * 4)
+        rate = P / max(t, 1e-9)  # products/s
+        want = rate * seconds
+        return int(min(n, max(r, np.searchsorted(self.fpre, want, side="left"))))
+
+
 def cpu_baseline(w, seconds):
-    """The oracle as it stands (single-threaded C, oracle/), timed on this
-    host on repetitions of the full workload, bounded to ~`seconds`."""
+    """cpu_baseline of the JSON line: the oracle on this host, 1 thread and all
+    cores (os.sched_getaffinity), each on a bounded row sample (~seconds/2)."""
     import oracle
 
-    reps, t0 = 0, time.perf_counter()
-    P = None
-    while True:
-        g = oracle.build(w.row_ptr, w.col_idx, w.val, scale_rows=w.scale_rows, drop_tol=w.drop_tol)
-        oracle.cutsize(g.row_ptr, g.col, g.w, w.part, w.K)
-        P = g.products
-        reps += 1
-        el = time.perf_counter() - t0
-        if el >= seconds or reps >= 50:
-            break
-    return {"value": P * reps / el, "unit": "products/s", "cores": 1, "kind": "oracle",
-            "sample": f"full {w.name} workload (scale+CSC+Gustavson+cutsize) x {reps} in {el:.1f}s",
-            "ms_per_step": 1e3 * el / reps}
+    S = OracleSample(w)
+    allc = oracle.default_threads()
+    out = {}
+    for label, th in (("1thread", 1), ("all", allc)):
+        R = S.rows_for(seconds / 2, th)
+        t, P = S.run(R, th)
+        out[label] = (P / t, R, t, P)
+    v, R, t, P = out["all"]
+    v1, R1, t1, P1 = out["1thread"]
+    return {"value": v, "unit": "products/s", "cores": allc, "kind": "oracle",
+            "sample": (f"rows [0, {R}) of {w.name} ({P} products, {t:.1f}s on {allc} threads; "
+                       f"Gustavson + cutsize; scaling + CSC ({S.prep_s:.1f}s, 1 thread) prepared once)"),
+            "value_1thread": v1, "sample_1thread": f"rows [0, {R1}) ({P1} products, {t1:.1f}s)",
+            "cpu_model": cpu_model()}
 
 
 def run_reference(args):
     """--impl reference: the CPU oracle (the only reference this tier has)
-    timed as it stands on the host cores, on our arm's config/metric."""
+    timed as it stands on the host cores, on our arm's config / metric: each
+    step builds a bounded row sample of the workload on all cores (sized to
+    ~--ref-step-seconds)."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     from rig_inputs import make
 
-    w = make(args.config)
     import oracle
 
+    w = make(args.config)
     oracle.build_lib()
+    S = OracleSample(w)
+    th = oracle.default_threads()
+    R = S.rows_for(args.ref_step_seconds, th)
     for _ in range(max(0, min(args.warmup, 1))):
-        oracle.build(w.row_ptr, w.col_idx, w.val, scale_rows=w.scale_rows, drop_tol=w.drop_tol)
-    times, P = [], None
+        S.run(R, th)
+    times, P = [], 0
     for _ in range(args.steps):
-        t0 = time.perf_counter()
-        g = oracle.build(w.row_ptr, w.col_idx, w.val, scale_rows=w.scale_rows, drop_tol=w.drop_tol)
-        oracle.cutsize(g.row_ptr, g.col, g.w, w.part, w.K)
-        times.append(time.perf_counter() - t0)
-        P = g.products
+        t, P = S.run(R, th)
+        times.append(t)
     t = sum(times) / len(times)
     v = P / t
+    sample = (f"rows [0, {R}) of {w.name} per step ({P} products; Gustavson + cutsize on {th} threads; "
+              f"scaling + CSC prepared once, {S.prep_s:.1f}s)")
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "products/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": workload_label(w), "n": w.n, "nnz_A": w.nnz,
-                       "products": P, "K": w.K},
-            "cpu_baseline": {"value": v, "unit": "products/s", "cores": 1, "kind": "oracle",
-                             "sample": f"full {w.name} workload per step (scale+CSC+Gustavson+cutsize)"},
+            "config": {"workload": workload_label(w), "n": w.n, "nnz_A": w.nnz, "K": w.K,
+                       "sample_rows": R, "sample_products": P},
+            "cpu_baseline": {"value": v, "unit": "products/s", "cores": th, "kind": "oracle", "sample": sample,
+                             "cpu_model": cpu_model()},
             "e2e": {"value": v, "unit": "products/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -198,7 +258,6 @@ def main():
     if args.impl == "reference":
         return run_reference(args)
 
-    import numpy as np
     import torch
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -213,6 +272,7 @@ def main():
 
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
+    from paper_1710_07769_b200 import dist as rdist
     from paper_1710_07769_b200 import rig
     from rig_inputs import make
 
@@ -227,11 +287,12 @@ def main():
     cut_buf = torch.empty(1, dtype=torch.float64, device="cuda")
 
     def step():
-        # the whole hot path through the C ABI: a1-a6 (build) + a7 (cutsize)
-        g, cut = rig.rig_build_cut(A, part, w.K, rb, re, w.scale_rows, w.drop_tol, out=cut_buf)
+        # the whole hot path through the C ABI: a1-a6 (build) + a7 (cutsize);
+        # N > 1: this rank's shard, then a8 (NCCL allreduce of the partial cuts)
         if world > 1:
-            dist.all_reduce(cut)  # a8: NCCL allreduce of the partial cutsizes
-        return g, cut
+            g, cut, _ = rdist.build_cut_sharded(A, part, w.K, w.scale_rows, w.drop_tol, split=split)
+            return g, cut
+        return rig.rig_build_cut(A, part, w.K, rb, re, w.scale_rows, w.drop_tol, out=cut_buf)
 
     # warm-up
     for _ in range(max(args.warmup, 3)):
@@ -347,11 +408,12 @@ def main():
 
     peak, peak_src = load_peaks()
     alg = numeric_alg_bytes(w.n, w.nnz, nnz_c) / max(world, 1) if world > 1 else numeric_alg_bytes(w.n, w.nnz, nnz_c)
-    merge_only = "symbolic" not in pass_ms  # every row on the merge path: one kernel does all of a5-a6
-    roof_ms = ker_ms if merge_only else num_ms
-    roof_kernel = ("k_num_pair (a5+a6 fused merge path, two lanes per row, all rows; CUDA events around the launch)"
-                   if merge_only else
-                   "numeric pass (k_num_mid + k_num_huge + k_num_pair + k_copy_rows; CUDA events around the pass)")
+    path = rig.last_path()
+    roof_ms = ker_ms if path in ("merge", "rowwin") else num_ms
+    roof_kernel = {
+        "merge": "k_num_pair (a5+a6 fused merge path, two lanes per row, all rows; CUDA events around the launch)",
+        "rowwin": "k_row_win (a5+a6(+a7 partials) for every row, look-back placement; CUDA events around the launch)",
+    }.get(path, "numeric pass (k_num_mid + k_num_huge + k_num_pair + k_copy_rows; CUDA events around the pass)")
     achieved = alg / (roof_ms * 1e-3) / 1e9
     traffic, traffic_src = load_traffic(args.config)
     line = {
@@ -383,9 +445,12 @@ def main():
         "cut": cut_val,
         "roofline": {"bound": "hbm", "kernel": roof_kernel, "duration_ms": roof_ms,
                      "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "peak_spec": SPEC_HBM_GBS, "frac_spec": achieved / SPEC_HBM_GBS,
                      "traffic": traffic, "alg_bytes": alg,
-                     "alg_bytes_formula": "SURVEY §8(d) F1 = 24(n+1) + 24 nnzA + 12 nnzC",
+                     "alg_bytes_formula": ("SURVEY §8(d) F1 = 24(n+1) + 24 nnzA + 12 nnzC per launch "
+                                           "(nnzC = graph nnz + nonempty rows; entries dropped by drop_tol not counted)"),
                      "peak_source": peak_src, "traffic_source": traffic_src},
+        "numeric_path": path,
         "gpu_launches": launches,
         "clocks": clk,
     }

@@ -289,6 +289,12 @@ RIG_API const char *rig_last_error(void);
 /* Number of kernels this library has launched since it was loaded. */
 RIG_API uint64_t rig_launch_count(void);
 RIG_API const char *rig_version(void);
+/* Numeric path taken by the calling thread's last a5-a6 pass (diagnostics,
+ * bench labels): "merge" (every row on the k-way merge path, k_num_pair),
+ * "rowwin" (no row on the merge path: k_row_win, look-back placement) or
+ * "mixed" (merge rows + mid-row passes + placement copy); "" before any
+ * build.  Thread-local; the pointer stays valid until the thread's next build. */
+RIG_API const char *rig_last_path(void);
 
 #ifdef __cplusplus
 }

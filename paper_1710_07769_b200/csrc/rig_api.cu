@@ -118,6 +118,7 @@ struct Error : std::runtime_error {
 };
 
 static thread_local std::string t_last_error;
+static thread_local std::string t_last_path;
 
 #define CK(call)                                                                                \
     do {                                                                                        \
@@ -673,7 +674,11 @@ static int64_t plan_numeric(rig_plan *p, int32_t *gcol, double *gw, double *diag
     double *cutp = cut ? reinterpret_cast<double *>(wn + o_cutp) : nullptr;
     double *dg = (p->flags & RIG_FLAG_DIAG) ? diag : nullptr;
     const int64_t n_mid = p->h.n_mid;
-    if (p->rowwin) return rowwin_numeric(p, gcol, gw, cap, dg, row_ptr_out, wn, holes_d, used, cutp, cut);
+    if (p->rowwin) {
+        t_last_path = "rowwin";
+        return rowwin_numeric(p, gcol, gw, cap, dg, row_ptr_out, wn, holes_d, used, cutp, cut);
+    }
+    t_last_path = n_mid > 0 ? "mixed" : "merge";
     {
         Prof pf(P_NUMERIC, s);
         if (n_mid > 0) {
@@ -981,7 +986,8 @@ int rig_trim(void) {
     ABI_END
 }
 uint64_t rig_launch_count(void) { return g_launches.load(); }
-const char *rig_version(void) { return "librig 0.2 (sm_100a)"; }
+const char *rig_version(void) { return "librig 0.3 (sm_100a)"; }
+const char *rig_last_path(void) { return t_last_path.c_str(); }
 
 int rig_build(const rig_csr_t *A, int scale_rows, double drop_tol, uint32_t flags, rig_graph_t *out,
               rig_stream_t stream) {

@@ -71,6 +71,7 @@ def _load():
     L.rig_last_error.restype = ctypes.c_char_p
     L.rig_launch_count.restype = ctypes.c_uint64
     L.rig_version.restype = ctypes.c_char_p
+    L.rig_last_path.restype = ctypes.c_char_p
     L.rig_profile_enable.argtypes = [ctypes.c_int]
     L.rig_profile_read.argtypes = [P, P]
     L.rig_pass_name.argtypes = [ctypes.c_int]
@@ -95,6 +96,11 @@ def _check(code):
 def _stream(stream=None):
     s = torch.cuda.current_stream() if stream is None else stream
     return ctypes.c_void_p(s.cuda_stream)
+
+
+def last_path() -> str:
+    """Numeric path of this thread's last build: merge / rowwin / mixed."""
+    return lib.rig_last_path().decode()
 
 
 def launch_count() -> int:
