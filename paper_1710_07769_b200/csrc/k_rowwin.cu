@@ -47,9 +47,9 @@ constexpr int kRwNB = 256;           // sort buckets (shared mode)
 constexpr int kRwGNB = 512;          // sort buckets (global mode)
 constexpr int kRwTcap = 64;          // units per table fill
 constexpr int kRwSmallBucket = 8;    // buckets up to this size: per-lane insertion sort
-constexpr int kRwStageCap = 512;     // entries per staging slot
+constexpr int kRwStageCap = 512;     // entries per staging slot (>= kRwFcap + kRwW)
 #ifndef RIG_RW_DEPTH
-#define RIG_RW_DEPTH 4  // 80 registers without spills (6 CTAs of 128 threads per SM)
+#define RIG_RW_DEPTH 6  // 80 registers without spills (6 CTAs of 128 threads per SM)
 #endif
 constexpr int kRwDepth = RIG_RW_DEPTH;  // units in flight
 
@@ -483,17 +483,18 @@ __device__ __forceinline__ int far_count(const F_ &F, int n, int wbase, double t
     return kept;
 }
 
-// Emit a counted row in ascending j to dst (col, w) from position 0: far
-// below the window, the window (re-zeroed), far above.  Cut edges (j > i,
-// part differs) go to acc; diag[idx] = c_ii.
-template <class F_>
-__device__ __forceinline__ void emit_row(const RowArgs &a, RwSmem &S, const F_ &F, int64_t idx, int n, int nbelow,
-                                         int32_t *dcol, double *dw, bool write, int32_t pi, Comp &acc, int &badp) {
+// Emit a row in ascending j to dst (col, w) from position 0: far below the
+// window, the window (re-zeroed), far above; returns the kept count.  FOLD:
+// group heads fold their far groups here (else far_count stored |c| / -1 in
+// fb).  Cut edges (j > i, part differs) go to acc; diag[idx] = c_ii.
+template <bool FOLD, bool CUT, class F_>
+__device__ __forceinline__ int emit_row(const RowArgs &a, RwSmem &S, const F_ &F, int64_t idx, int n, int nbelow,
+                                        int32_t *dcol, double *dw, bool write, int32_t pi, Comp &acc, int &badp) {
     const int l = lane_id();
     const unsigned lt = lanemask_lt();
     const int64_t i = a.rb + idx;
     const int wbase = (int)i - kRwWH;
-    const bool cut = a.part != nullptr;
+    const bool cut = CUT && a.part != nullptr;
     int o = 0;
     auto put = [&](bool keep, int key, double w) {
         const unsigned bal = __ballot_sync(kFull, keep);
@@ -514,8 +515,19 @@ __device__ __forceinline__ void emit_row(const RowArgs &a, RwSmem &S, const F_ &
                 const int x = F.perm()[p];
                 key = F.fk()[x];
                 if (p == 0 || F.fk()[F.perm()[p - 1]] != key) {
-                    w = F.fb()[x];
-                    keep = w >= 0.0;
+                    if (FOLD) {
+                        double c = __fma_rn(F.a(x), F.fb()[x], +0.0);
+                        for (int q = p + 1; q < n; ++q) {  // the group, in arrival order
+                            const int y = F.perm()[q];
+                            if (F.fk()[y] != key) break;
+                            c = __fma_rn(F.a(y), F.fb()[y], c);
+                        }
+                        w = fabs(c);
+                        keep = w > a.tol;
+                    } else {
+                        w = F.fb()[x];
+                        keep = w >= 0.0;
+                    }
                 }
             }
             if (cut && keep && (int64_t)key > i) {
@@ -547,17 +559,48 @@ __device__ __forceinline__ void emit_row(const RowArgs &a, RwSmem &S, const F_ &
         put(keep, key, w);
     }
     far_range(nbelow, n);
+    return o;
 }
 
-// Copy a staged row (n entries) to the graph at g0 (coalesced, streaming).
-__device__ __forceinline__ void copy_staged(const int32_t *scol, const double *sw, int n, int32_t *gcol, double *gw,
-                                            int64_t g0) {
+// Copy a staged row (n entries) to the graph at g0 (coalesced, streaming;
+// kCopyU rounds of loads in flight), and take the row's cut edges there (j >
+// i, part[j] != part[i]: PAPER.md:393-405) -- the part[] gathers are batched
+// with the copy instead of stalling the emission.
+constexpr int kCopyU = 4;
+__device__ __forceinline__ void copy_staged(const RowArgs &a, const int32_t *scol, const double *sw, int n, int64_t g0,
+                                            bool write, int64_t i, int32_t pi, Comp &acc, int &badp) {
     const int l = lane_id();
-    for (int t = l; t < n; t += 32) {
-        const int32_t c = __ldcs(scol + t);
-        const double w = __ldcs(sw + t);
-        __stcs(gcol + g0 + t, c);
-        __stcs(gw + g0 + t, w);
+    const bool cut = a.part != nullptr;
+    for (int t0 = 0; t0 < n; t0 += 32 * kCopyU) {
+        int32_t c[kCopyU], pj[kCopyU];
+        double w[kCopyU];
+#pragma unroll
+        for (int u = 0; u < kCopyU; ++u) {
+            const int t = t0 + 32 * u + l;
+            c[u] = -1;
+            w[u] = 0.0;
+            if (t < n) {
+                c[u] = __ldcs(scol + t);
+                w[u] = __ldcs(sw + t);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < kCopyU; ++u) {
+            const int t = t0 + 32 * u + l;
+            if (t < n && write) {
+                __stcs(a.gcol + g0 + t, c[u]);
+                __stcs(a.gw + g0 + t, w[u]);
+            }
+            pj[u] = pi;
+            if (cut && (int64_t)c[u] > i) pj[u] = __ldg(&a.part[c[u]]);
+        }
+        if (cut) {
+#pragma unroll
+            for (int u = 0; u < kCopyU; ++u) {
+                badp |= (pj[u] < 0) | (pj[u] >= a.K);
+                if (pj[u] != pi) acc.add(w[u]);
+            }
+        }
     }
 }
 
@@ -596,11 +639,16 @@ __global__ void __launch_bounds__(kRwThreads, 6) k_row_win(RowArgs a) {
     meta_entries(a, cur);
     meta_cols(a, cur, false);
     // the staged row: look back for its offset, copy it into place
+    int32_t ppi = 0;  // part of the staged row
     auto flush = [&]() {
         if (pidx < 0) return;
         const int64_t g0 = lookback(a.chain, pidx, pkept);
         const bool fits = g0 + pkept <= a.cap;
-        if (fits) copy_staged(stc + pslot * kRwStageCap, stw + pslot * kRwStageCap, pkept, a.gcol, a.gw, g0);
+        Comp acc;
+        int badp = a.part ? ((ppi < 0) | (ppi >= a.K)) : 0;
+        copy_staged(a, stc + pslot * kRwStageCap, stw + pslot * kRwStageCap, pkept, g0, fits, a.rb + pidx, ppi, acc,
+                    badp);
+        if (a.part) finish_cut(a, pidx, acc, badp);
         if (l == 0) {
             a.row_ptr[pidx + 1] = g0 + pkept;
             if (pidx == 0) a.row_ptr[0] = 0;
@@ -608,7 +656,7 @@ __global__ void __launch_bounds__(kRwThreads, 6) k_row_win(RowArgs a) {
         }
         pidx = -1;
     };
-    auto finish = [&](const auto &F, int nfar) {
+    auto finish = [&](const auto &F, int nfar, bool shared_list) {
         const int64_t i = a.rb + idx;
         const int wbase = (int)i - kRwWH;
         if (nfar > 1)
@@ -616,42 +664,55 @@ __global__ void __launch_bounds__(kRwThreads, 6) k_row_win(RowArgs a) {
         else if (nfar == 1 && l == 0)
             F.perm()[0] = 0;
         __syncwarp();
-        int nbelow = 0;
-        int kept = far_count(F, nfar, wbase, a.tol, nbelow);
-#pragma unroll
-        for (int t0 = 0; t0 < kRwW; t0 += 32) {
-            const int t = t0 + l;
-            kept += __popc(__ballot_sync(kFull, t < kRwW && t != kRwWH && fabs(S.wv[t]) > a.tol));
-        }
-        // publish the count; take the next ticket now (a ticket taken earlier
-        // would be held while this warp waits, and rows behind it would wait
-        // on it); then place the previously staged row
-        if (l == 0) st_relaxed(&a.chain[idx], (idx == 0 ? kPre : kAgg) | (unsigned long long)kept);
-        int64_t nidx = 0;
-        if (l == 0) nidx = (int64_t)atomicAdd(a.ticket, 1ull);
-        flush();
         Comp acc;
         int badp = a.part ? ((cur.pi < 0) | (cur.pi >= a.K)) : 0;
-        nidx = __shfl_sync(kFull, nidx, 0);
-        meta_rows(a, nidx, nxt);
-        if (staging && kept <= kRwStageCap) {
+        int64_t nidx = 0;
+        if (staging && shared_list) {
+            // one pass: fold, count and write the row into the free staging
+            // slot (kept <= far items + window slots <= kRwStageCap)
+            int nbelow = 0;
+            for (int p0 = 0; p0 < nfar; p0 += 32) {
+                const int p = p0 + l;
+                nbelow += __popc(__ballot_sync(kFull, p < nfar && F.fk()[F.perm()[p]] < wbase));
+            }
             const int slot = pslot ^ 1;
-            emit_row(a, S, F, idx, nfar, nbelow, stc + slot * kRwStageCap, stw + slot * kRwStageCap, true, cur.pi,
-                     acc, badp);
+            const int kept = emit_row<true, false>(a, S, F, idx, nfar, nbelow, stc + slot * kRwStageCap,
+                                                   stw + slot * kRwStageCap, true, cur.pi, acc, badp);
+            // publish the count; take the next ticket now (a ticket taken
+            // earlier would be held while this warp waits, and rows behind it
+            // would wait on it); then place the previously staged row
+            if (l == 0) st_relaxed(&a.chain[idx], (idx == 0 ? kPre : kAgg) | (unsigned long long)kept);
+            if (l == 0) nidx = (int64_t)atomicAdd(a.ticket, 1ull);
+            flush();
             pidx = idx;
             pkept = kept;
             pslot = slot;
-        } else {  // wait for the offset, write in place
+            ppi = cur.pi;
+            nidx = __shfl_sync(kFull, nidx, 0);
+            meta_rows(a, nidx, nxt);
+        } else {  // count, publish, wait for the offset, write in place
+            int nbelow = 0;
+            int kept = far_count(F, nfar, wbase, a.tol, nbelow);
+#pragma unroll
+            for (int t0 = 0; t0 < kRwW; t0 += 32) {
+                const int t = t0 + l;
+                kept += __popc(__ballot_sync(kFull, t != kRwWH && fabs(S.wv[t]) > a.tol));
+            }
+            if (l == 0) st_relaxed(&a.chain[idx], (idx == 0 ? kPre : kAgg) | (unsigned long long)kept);
+            if (l == 0) nidx = (int64_t)atomicAdd(a.ticket, 1ull);
+            flush();
+            nidx = __shfl_sync(kFull, nidx, 0);
+            meta_rows(a, nidx, nxt);
             const int64_t g0 = (a.dbg & 1) ? min(idx * 280, a.cap - 1024) : lookback(a.chain, idx, kept);
             const bool fits = g0 + kept <= a.cap;
-            emit_row(a, S, F, idx, nfar, nbelow, a.gcol + g0, a.gw + g0, fits, cur.pi, acc, badp);
+            emit_row<false, true>(a, S, F, idx, nfar, nbelow, a.gcol + g0, a.gw + g0, fits, cur.pi, acc, badp);
             if (l == 0) {
                 a.row_ptr[idx + 1] = g0 + kept;
                 if (idx == 0) a.row_ptr[0] = 0;
                 if (!fits) atomicOr(a.overflow, 1);
             }
+            if (a.part) finish_cut(a, idx, acc, badp);
         }
-        if (a.part) finish_cut(a, idx, acc, badp);
         meta_entries(a, nxt);
         meta_cols(a, nxt, !(a.dbg & 4));
         __syncwarp();
@@ -677,14 +738,14 @@ __global__ void __launch_bounds__(kRwThreads, 6) k_row_win(RowArgs a) {
         }
         int64_t nidx;
         if (!global) {
-            nidx = finish(FS, nfar);
+            nidx = finish(FS, nfar, true);
         } else {
             nfar = accumulate(a, S, FG, i, cur);
             if (nfar > FG.cap()) {  // cannot happen when gcap >= max f_i (host check)
                 if (l == 0) atomicOr(a.overflow, 2);
                 nfar = FG.cap();
             }
-            nidx = finish(FG, nfar);
+            nidx = finish(FG, nfar, false);
         }
         idx = nidx;
         cur = nxt;
