@@ -295,6 +295,14 @@ RIG_API const char *rig_version(void);
  * "mixed" (merge rows + mid-row passes + placement copy); "" before any
  * build.  Thread-local; the pointer stays valid until the thread's next build. */
 RIG_API const char *rig_last_path(void);
+/* Measurement only (north star "L2 hit rate on the A^T
+ * gathers"): runs a0-a4 on A (device CSR) and then k_gather_probe, the
+ * numeric pass's gather loop (warp per row, ascending rows, every column k
+ * of each row read from the CSC of A_hat) with no accumulation and no
+ * writes, so ncu's L2/DRAM counters of that kernel are the gathers' own.
+ * *checksum_host (may be NULL) receives a checksum of the gathered data.
+ * Synchronises the stream. */
+RIG_API int rig_gather_probe(const rig_csr_t *A, int scale_rows, double *checksum_host, rig_stream_t stream);
 
 #ifdef __cplusplus
 }

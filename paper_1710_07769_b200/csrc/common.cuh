@@ -356,6 +356,11 @@ void launch_row_win(const RowArgs &a, cudaStream_t s);
 // per-row cut sums -> 256 partials (fixed segments) and *used = 256
 void launch_rowcut_partials(const double *cutrow, int64_t n, double *partials, int *used, cudaStream_t s);
 
+// k_probe.cu: gather-only probe of the numeric pass (measurement): sink
+// [gather_probe_warps()] doubles
+int gather_probe_warps();
+void launch_gather_probe(const Csr &A, const Csc &T, int64_t rb, int64_t re, double *sink, cudaStream_t s);
+
 // k_post.cu
 void launch_count_kept(const int64_t *gptr_ub, int64_t nloc, const int32_t *gcol, int64_t *kept, cudaStream_t s);
 void launch_compact_move(const int64_t *gptr_ub, const int64_t *gptr, int64_t nloc, const int32_t *gcol_in,

@@ -989,6 +989,31 @@ uint64_t rig_launch_count(void) { return g_launches.load(); }
 const char *rig_version(void) { return "librig 0.3 (sm_100a)"; }
 const char *rig_last_path(void) { return t_last_path.c_str(); }
 
+int rig_gather_probe(const rig_csr_t *A, int scale_rows, double *checksum_host, rig_stream_t stream) {
+    ABI_BEGIN
+    cudaStream_t s = (cudaStream_t)stream;
+    rig_plan *p = make_plan(A, scale_rows, 0.0, 0, 0, A->nrows, s);
+    try {
+        Arena ar(s);
+        const int nw = gather_probe_warps();
+        double *sink = ar.get<double>(nw);
+        launch_gather_probe(p->A, p->T, 0, A->nrows, sink, s);
+        check_launch("gather probe");
+        std::vector<double> h((size_t)nw);
+        CK(cudaMemcpyAsync(h.data(), sink, sizeof(double) * (size_t)nw, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        double t = 0.0;
+        for (double v : h) t += v;
+        if (checksum_host) *checksum_host = t;
+    } catch (...) {
+        delete p;
+        throw;
+    }
+    delete p;
+    return RIG_OK;
+    ABI_END
+}
+
 int rig_build(const rig_csr_t *A, int scale_rows, double drop_tol, uint32_t flags, rig_graph_t *out,
               rig_stream_t stream) {
     ABI_BEGIN

@@ -98,6 +98,13 @@ def _stream(stream=None):
     return ctypes.c_void_p(s.cuda_stream)
 
 
+def rig_gather_probe(A: CSR, scale_rows=1, stream=None) -> float:
+    """Measurement: the numeric pass's gather loop alone (k_gather_probe)."""
+    out = ctypes.c_double()
+    _check(lib.rig_gather_probe(ctypes.byref(A.c()), int(scale_rows), ctypes.byref(out), _stream(stream)))
+    return out.value
+
+
 def last_path() -> str:
     """Numeric path of this thread's last build: merge / rowwin / mixed."""
     return lib.rig_last_path().decode()
