@@ -613,7 +613,10 @@ __device__ __forceinline__ void finish_cut(const RowArgs &a, int64_t idx, Comp &
     if (__any_sync(kFull, badp) && l == 0) atomicOr(a.bad_part, 1);
 }
 
-__global__ void __launch_bounds__(kRwThreads, 6) k_row_win(RowArgs a) {
+#ifndef RIG_RW_MINB
+#define RIG_RW_MINB 6  // CTAs per SM the register budget is fitted to (shared memory allows 6)
+#endif
+__global__ void __launch_bounds__(kRwThreads, RIG_RW_MINB) k_row_win(RowArgs a) {
     extern __shared__ __align__(16) unsigned char rw_smem[];
     const int wid = threadIdx.x >> 5;
     RwSmem &S = reinterpret_cast<RwSmem *>(rw_smem)[wid];
