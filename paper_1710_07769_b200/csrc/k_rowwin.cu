@@ -40,24 +40,37 @@ namespace rig {
 
 constexpr int kRwThreads = 128;
 constexpr int kRwWarps = kRwThreads / 32;
-constexpr int kRwWH = 128;           // window: -kRwWH <= j - i < kRwWH
+#ifndef RIG_RW_WH
+#define RIG_RW_WH 112
+#endif
+constexpr int kRwWH = RIG_RW_WH;     // window: -kRwWH <= j - i < kRwWH (kRwWH multiple of 16)
 constexpr int kRwW = 2 * kRwWH;      // window slots
-constexpr int kRwFcap = 256;         // far items in shared memory
-constexpr int kRwNB = 256;           // sort buckets (shared mode)
+#ifndef RIG_RW_FCAP
+#define RIG_RW_FCAP 192
+#endif
+constexpr int kRwFcap = RIG_RW_FCAP; // far items in shared memory
+#ifndef RIG_RW_NB
+#define RIG_RW_NB 128
+#endif
+constexpr int kRwNB = RIG_RW_NB;     // sort buckets (shared mode)
 constexpr int kRwGNB = 512;          // sort buckets (global mode)
-constexpr int kRwTcap = 64;          // units per table fill
+#ifndef RIG_RW_TCAP
+#define RIG_RW_TCAP 40
+#endif
+constexpr int kRwTcap = RIG_RW_TCAP; // units per table fill
 constexpr int kRwSmallBucket = 8;    // buckets up to this size: per-lane insertion sort
 constexpr int kRwStageCap = 512;     // entries per staging slot (>= kRwFcap + kRwW)
 #ifndef RIG_RW_DEPTH
-#define RIG_RW_DEPTH 6  // 80 registers without spills (6 CTAs of 128 threads per SM)
+#define RIG_RW_DEPTH 3  // fits the 56-register budget of 9 CTAs per SM
 #endif
 constexpr int kRwDepth = RIG_RW_DEPTH;  // units in flight
 
 struct RwSmem {
     double wv[kRwW];      // window
     double fb[kRwFcap];   // far: a_jk; after the count pass, at a group's head item: |c| (or -1: not kept)
-    double ta[kRwTcap + kRwDepth];   // unit: a_ik (padded: see accumulate)
-    int2 tcs[kRwTcap + kRwDepth];    // unit: (CSC offset of its first lane, lane count); tmp of the bucket rank
+    // units: padded up to a multiple of kRwDepth, plus kRwDepth look-ahead slots
+    double ta[kRwTcap + 2 * kRwDepth];  // unit: a_ik
+    int2 tcs[kRwTcap + 2 * kRwDepth];   // unit: (CSC offset of its first lane, lane count); tmp of the bucket rank
     int fk[kRwFcap];      // far: key j
     int bc[kRwNB];        // bucket cursors / ends
     unsigned bad[kRwNB / 32];
@@ -86,7 +99,7 @@ struct FarS {
     __device__ __forceinline__ unsigned *bad() const { return S->bad; }
     __device__ __forceinline__ uint16_t *perm() const { return S->perm; }
     __device__ __forceinline__ uint16_t *tmp() const { return reinterpret_cast<uint16_t *>(S->tcs); }
-    __device__ __forceinline__ int tmp_cap() const { return kRwTcap * 4; }
+    __device__ __forceinline__ int tmp_cap() const { return (kRwTcap + 2 * kRwDepth) * 4; }
     __device__ __forceinline__ int *nbad_ptr() const { return &S->nbad; }
     __device__ __forceinline__ void nbad_set(int v) const { S->nbad = v; }
     __device__ __forceinline__ int nbad_get() const { return *reinterpret_cast<volatile int *>(&S->nbad); }
@@ -186,7 +199,7 @@ __device__ __forceinline__ int64_t lookback(unsigned long long *chain, int64_t i
 // buckets of <= kRwSmallBucket items; a longer bucket found out of order is
 // ranked by (key, arrival) by the whole warp.
 template <class F_>
-__device__ __forceinline__ void far_sort(const F_ &F, int n) {
+__device__ __forceinline__ bool far_sort(const F_ &F, int n) {
     const int l = lane_id();
     const unsigned lt = lanemask_lt();
     constexpr int NB = F_::nb, PER = NB / 32;
@@ -250,7 +263,7 @@ __device__ __forceinline__ void far_sort(const F_ &F, int n) {
     }
     __syncwarp();
     const int nbad = F.nbad_get();
-    if (nbad == 0) return;
+    if (nbad == 0) return true;
     // one lane per short bad bucket: insertion sort (key ties keep arrival
     // order = item index); long ones (or > 32 bad buckets): the warp ranks
     bool big = nbad > 32;
@@ -275,7 +288,7 @@ __device__ __forceinline__ void far_sort(const F_ &F, int n) {
             big = true;
         }
     }
-    if (!__any_sync(kFull, big)) return;
+    if (!__any_sync(kFull, big)) return true;
     __syncwarp();
     uint16_t *tmp = F.tmp();
     for (int wd = 0; wd < PER; ++wd) {
@@ -284,7 +297,7 @@ __device__ __forceinline__ void far_sort(const F_ &F, int n) {
             const int b = wd * 32 + __ffs(m) - 1;
             m &= m - 1;
             const int e1 = bc[b], e0 = b > 0 ? bc[b - 1] : 0, sz = e1 - e0;
-            if (sz > F.tmp_cap()) continue;  // cannot happen: the tmp holds a whole list
+            if (sz > F.tmp_cap()) return false;  // the caller redoes the row with a global far list
             for (int q = l; q < sz; q += 32) tmp[q] = perm[e0 + q];
             __syncwarp();
             for (int r0 = 0; r0 < sz; r0 += 32) {
@@ -306,6 +319,7 @@ __device__ __forceinline__ void far_sort(const F_ &F, int n) {
             __syncwarp();
         }
     }
+    return true;
 }
 
 struct RowMeta {
@@ -614,7 +628,7 @@ __device__ __forceinline__ void finish_cut(const RowArgs &a, int64_t idx, Comp &
 }
 
 #ifndef RIG_RW_MINB
-#define RIG_RW_MINB 6  // CTAs per SM the register budget is fitted to (shared memory allows 6)
+#define RIG_RW_MINB 9  // CTAs per SM the register budget (56) is fitted to; shared memory allows 9
 #endif
 __global__ void __launch_bounds__(kRwThreads, RIG_RW_MINB) k_row_win(RowArgs a) {
     extern __shared__ __align__(16) unsigned char rw_smem[];
@@ -662,11 +676,6 @@ __global__ void __launch_bounds__(kRwThreads, RIG_RW_MINB) k_row_win(RowArgs a) 
     auto finish = [&](const auto &F, int nfar, bool shared_list) {
         const int64_t i = a.rb + idx;
         const int wbase = (int)i - kRwWH;
-        if (nfar > 1)
-            far_sort(F, nfar);
-        else if (nfar == 1 && l == 0)
-            F.perm()[0] = 0;
-        __syncwarp();
         Comp acc;
         int badp = a.part ? ((cur.pi < 0) | (cur.pi >= a.K)) : 0;
         int64_t nidx = 0;
@@ -733,7 +742,17 @@ __global__ void __launch_bounds__(kRwThreads, RIG_RW_MINB) k_row_win(RowArgs a) 
         }
         if (!global) {
             nfar = accumulate(a, S, FS, i, cur);
-            if (nfar > FS.cap()) {  // far list overflow: redo with the global far list
+            // far list overflow, or a long out-of-order sort bucket beyond the
+            // shared scratch: redo the row with the global far list
+            bool redo = nfar > FS.cap();
+            if (!redo) {
+                if (nfar > 1)
+                    redo = !far_sort(FS, nfar);
+                else if (nfar == 1 && l == 0)
+                    FS.perm()[0] = 0;
+                __syncwarp();
+            }
+            if (redo) {
                 for (int t = l; t < kRwW; t += 32) S.wv[t] = +0.0;
                 __syncwarp();
                 global = true;
@@ -748,6 +767,11 @@ __global__ void __launch_bounds__(kRwThreads, RIG_RW_MINB) k_row_win(RowArgs a) 
                 if (l == 0) atomicOr(a.overflow, 2);
                 nfar = FG.cap();
             }
+            if (nfar > 1)
+                far_sort(FG, nfar);  // tmp_cap = gcap: always sorts
+            else if (nfar == 1 && l == 0)
+                FG.perm()[0] = 0;
+            __syncwarp();
             nidx = finish(FG, nfar, false);
         }
         idx = nidx;
