@@ -43,7 +43,7 @@ constexpr int kRwWarps = kRwThreads / 32;
 #ifndef RIG_RW_WH
 #define RIG_RW_WH 112
 #endif
-constexpr int kRwWH = RIG_RW_WH;     // window: -kRwWH <= j - i < kRwWH (kRwWH multiple of 16)
+constexpr int kRwWH = RIG_RW_WH;     // window: -kRwWH <= j - i < kRwWH
 constexpr int kRwW = 2 * kRwWH;      // window slots
 #ifndef RIG_RW_FCAP
 #define RIG_RW_FCAP 192
@@ -66,7 +66,7 @@ constexpr int kRwStageCap = 512;     // entries per staging slot (>= kRwFcap + k
 constexpr int kRwDepth = RIG_RW_DEPTH;  // units in flight
 
 struct RwSmem {
-    double wv[kRwW];      // window
+    double wv[kRwW];      // window (every access is guarded by t < kRwW)
     double fb[kRwFcap];   // far: a_jk; after the count pass, at a group's head item: |c| (or -1: not kept)
     // units: padded up to a multiple of kRwDepth, plus kRwDepth look-ahead slots
     double ta[kRwTcap + 2 * kRwDepth];  // unit: a_ik
@@ -708,7 +708,7 @@ __global__ void __launch_bounds__(kRwThreads, RIG_RW_MINB) k_row_win(RowArgs a) 
 #pragma unroll
             for (int t0 = 0; t0 < kRwW; t0 += 32) {
                 const int t = t0 + l;
-                kept += __popc(__ballot_sync(kFull, t != kRwWH && fabs(S.wv[t]) > a.tol));
+                kept += __popc(__ballot_sync(kFull, t < kRwW && t != kRwWH && fabs(S.wv[t]) > a.tol));
             }
             if (l == 0) st_relaxed(&a.chain[idx], (idx == 0 ? kPre : kAgg) | (unsigned long long)kept);
             if (l == 0) nidx = (int64_t)atomicAdd(a.ticket, 1ull);
