@@ -346,6 +346,14 @@ struct RowArgs {
     int gcap;
     int32_t *stage_col;  // [rowwin_stage_entries()] per-warp staging slots
     double *stage_w;
+    // temp mode (mixed path's mid rows; list != null): rows list[0..*count_dev)
+    // written exactly to tcol/tw at toff[r], cnt[r] = kept + 1; no look-back
+    const int32_t *list;
+    const int64_t *count_dev;
+    const int64_t *toff;
+    int32_t *tcol;
+    double *tw;
+    int64_t *cnt;
     int dbg;          // RIG_DEBUG_MASK experiments (0 in normal operation)
 };
 int rowwin_grid();

@@ -323,6 +323,7 @@ __device__ __forceinline__ bool far_sort(const F_ &F, int n) {
 }
 
 struct RowMeta {
+    int64_t i = 0;       // global row id
     int64_t s = 0, e = 0;
     int k = 0;           // lane t: column of entry t
     int cs = 0, cl = 0;  // lane t: CSC offset (sentinel layout) and length of column k
@@ -332,10 +333,12 @@ struct RowMeta {
 
 // Row metadata in three dependent stages (row pointers; entries; column
 // bounds), issued at points of the previous row where their latency hides.
-__device__ __forceinline__ void meta_rows(const RowArgs &a, int64_t idx, RowMeta &M) {
+template <bool TEMP>
+__device__ __forceinline__ void meta_rows(const RowArgs &a, int64_t idx, int64_t nrows, RowMeta &M) {
     M.s = M.e = 0;
-    if (idx >= a.nloc) return;
-    const int64_t i = a.rb + idx;
+    if (idx >= nrows) return;
+    const int64_t i = TEMP ? (int64_t)a.list[idx] : a.rb + idx;  // TEMP: the mixed path's row list
+    if (TEMP) M.i = i;
     M.s = a.A.rp[i];
     M.e = a.A.rp[i + 1];
     if (a.part) M.pi = __ldg(&a.part[i]);
@@ -502,11 +505,11 @@ __device__ __forceinline__ int far_count(const F_ &F, int n, int wbase, double t
 // group heads fold their far groups here (else far_count stored |c| / -1 in
 // fb).  Cut edges (j > i, part differs) go to acc; diag[idx] = c_ii.
 template <bool FOLD, bool CUT, class F_>
-__device__ __forceinline__ int emit_row(const RowArgs &a, RwSmem &S, const F_ &F, int64_t idx, int n, int nbelow,
+__device__ __forceinline__ int emit_row(const RowArgs &a, RwSmem &S, const F_ &F, int64_t i, int64_t r, int n,
+                                        int nbelow,
                                         int32_t *dcol, double *dw, bool write, int32_t pi, Comp &acc, int &badp) {
     const int l = lane_id();
     const unsigned lt = lanemask_lt();
-    const int64_t i = a.rb + idx;
     const int wbase = (int)i - kRwWH;
     const bool cut = CUT && a.part != nullptr;
     int o = 0;
@@ -562,7 +565,7 @@ __device__ __forceinline__ int emit_row(const RowArgs &a, RwSmem &S, const F_ &F
             c = S.wv[t];
             S.wv[t] = +0.0;
         }
-        if (t == kRwWH && a.diag) a.diag[idx] = c;
+        if (t == kRwWH && a.diag) a.diag[r] = c;
         const double w = fabs(c);
         const bool keep = t < kRwW && t != kRwWH && w > a.tol;
         if (cut && keep && t > kRwWH) {
@@ -630,6 +633,11 @@ __device__ __forceinline__ void finish_cut(const RowArgs &a, int64_t idx, Comp &
 #ifndef RIG_RW_MINB
 #define RIG_RW_MINB 9  // CTAs per SM the register budget (56) is fitted to; shared memory allows 9
 #endif
+// TEMP = false: every row of the shard, placed by look-back (row-window
+// path).  TEMP = true: the rows of a.list (mixed path's mid rows), each
+// written with its exact kept count to the temporary at toff[r] (cnt[r] =
+// kept + 1, as the mid kernels); k_copy_rows places them and takes their cut.
+template <bool TEMP>
 __global__ void __launch_bounds__(kRwThreads, RIG_RW_MINB) k_row_win(RowArgs a) {
     extern __shared__ __align__(16) unsigned char rw_smem[];
     const int wid = threadIdx.x >> 5;
@@ -648,17 +656,18 @@ __global__ void __launch_bounds__(kRwThreads, RIG_RW_MINB) k_row_win(RowArgs a) 
     const bool staging = !(a.dbg & 2);
     int64_t pidx = -1;  // staged row waiting for its offset
     int pkept = 0, pslot = 0;
+    const int64_t nrows = TEMP ? *a.count_dev : a.nloc;
     int64_t idx = 0;
     if (l == 0) idx = (int64_t)atomicAdd(a.ticket, 1ull);
     idx = __shfl_sync(kFull, idx, 0);
     RowMeta cur, nxt;
-    meta_rows(a, idx, cur);
+    meta_rows<TEMP>(a, idx, nrows, cur);
     meta_entries(a, cur);
     meta_cols(a, cur, false);
     // the staged row: look back for its offset, copy it into place
     int32_t ppi = 0;  // part of the staged row
     auto flush = [&]() {
-        if (pidx < 0) return;
+        if (TEMP || pidx < 0) return;
         const int64_t g0 = lookback(a.chain, pidx, pkept);
         const bool fits = g0 + pkept <= a.cap;
         Comp acc;
@@ -674,12 +683,27 @@ __global__ void __launch_bounds__(kRwThreads, RIG_RW_MINB) k_row_win(RowArgs a) 
         pidx = -1;
     };
     auto finish = [&](const auto &F, int nfar, bool shared_list) {
-        const int64_t i = a.rb + idx;
+        const int64_t i = TEMP ? cur.i : a.rb + idx;
         const int wbase = (int)i - kRwWH;
         Comp acc;
         int badp = a.part ? ((cur.pi < 0) | (cur.pi >= a.K)) : 0;
         int64_t nidx = 0;
-        if (staging && shared_list) {
+        if constexpr (TEMP) {
+            // exact row into the temporary (room f_i - len_i >= kept), one pass
+            if (l == 0) nidx = (int64_t)atomicAdd(a.ticket, 1ull);
+            int nbelow = 0;
+            for (int p0 = 0; p0 < nfar; p0 += 32) {
+                const int p = p0 + l;
+                nbelow += __popc(__ballot_sync(kFull, p < nfar && F.fk()[F.perm()[p]] < wbase));
+            }
+            const int64_t r = i - a.rb;
+            const int64_t t0 = a.toff[r];
+            const int kept = emit_row<true, false>(a, S, F, i, r, nfar, nbelow, a.tcol + t0, a.tw + t0, true, cur.pi,
+                                                   acc, badp);
+            if (l == 0) a.cnt[r] = kept + 1;  // the graph scan subtracts the diagonal slot
+            nidx = __shfl_sync(kFull, nidx, 0);
+            meta_rows<TEMP>(a, nidx, nrows, nxt);
+        } else if (staging && shared_list) {
             // one pass: fold, count and write the row into the free staging
             // slot (kept <= far items + window slots <= kRwStageCap)
             int nbelow = 0;
@@ -688,7 +712,7 @@ __global__ void __launch_bounds__(kRwThreads, RIG_RW_MINB) k_row_win(RowArgs a) 
                 nbelow += __popc(__ballot_sync(kFull, p < nfar && F.fk()[F.perm()[p]] < wbase));
             }
             const int slot = pslot ^ 1;
-            const int kept = emit_row<true, false>(a, S, F, idx, nfar, nbelow, stc + slot * kRwStageCap,
+            const int kept = emit_row<true, false>(a, S, F, i, idx, nfar, nbelow, stc + slot * kRwStageCap,
                                                    stw + slot * kRwStageCap, true, cur.pi, acc, badp);
             // publish the count; take the next ticket now (a ticket taken
             // earlier would be held while this warp waits, and rows behind it
@@ -701,7 +725,7 @@ __global__ void __launch_bounds__(kRwThreads, RIG_RW_MINB) k_row_win(RowArgs a) 
             pslot = slot;
             ppi = cur.pi;
             nidx = __shfl_sync(kFull, nidx, 0);
-            meta_rows(a, nidx, nxt);
+            meta_rows<TEMP>(a, nidx, nrows, nxt);
         } else {  // count, publish, wait for the offset, write in place
             int nbelow = 0;
             int kept = far_count(F, nfar, wbase, a.tol, nbelow);
@@ -714,10 +738,10 @@ __global__ void __launch_bounds__(kRwThreads, RIG_RW_MINB) k_row_win(RowArgs a) 
             if (l == 0) nidx = (int64_t)atomicAdd(a.ticket, 1ull);
             flush();
             nidx = __shfl_sync(kFull, nidx, 0);
-            meta_rows(a, nidx, nxt);
+            meta_rows<TEMP>(a, nidx, nrows, nxt);
             const int64_t g0 = (a.dbg & 1) ? min(idx * 280, a.cap - 1024) : lookback(a.chain, idx, kept);
             const bool fits = g0 + kept <= a.cap;
-            emit_row<false, true>(a, S, F, idx, nfar, nbelow, a.gcol + g0, a.gw + g0, fits, cur.pi, acc, badp);
+            emit_row<false, true>(a, S, F, i, idx, nfar, nbelow, a.gcol + g0, a.gw + g0, fits, cur.pi, acc, badp);
             if (l == 0) {
                 a.row_ptr[idx + 1] = g0 + kept;
                 if (idx == 0) a.row_ptr[0] = 0;
@@ -730,8 +754,8 @@ __global__ void __launch_bounds__(kRwThreads, RIG_RW_MINB) k_row_win(RowArgs a) 
         __syncwarp();
         return nidx;
     };
-    while (idx < a.nloc) {
-        const int64_t i = a.rb + idx;
+    while (idx < nrows) {
+        const int64_t i = TEMP ? cur.i : a.rb + idx;
         const bool one_batch = cur.e - cur.s <= 32;
         int nfar = 0;
         bool global = !one_batch;
@@ -802,9 +826,9 @@ static int rowwin_ctas_per_sm() {
     if (dev < 0 || dev >= 64) dev = 0;
     if (!cache[dev]) {
         const size_t smem = (size_t)kRwWarps * sizeof(RwSmem);
-        cudaFuncSetAttribute(k_row_win, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(k_row_win<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         int per_sm = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_row_win, kRwThreads, smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_row_win<false>, kRwThreads, smem);
         cache[dev] = per_sm > 0 ? per_sm : 1;
     }
     return cache[dev];
@@ -817,8 +841,13 @@ int rowwin_max_gcap() { return 65535; }  // perm entries are 16-bit
 
 void launch_row_win(const RowArgs &a, cudaStream_t s) {
     const size_t smem = (size_t)kRwWarps * sizeof(RwSmem);
-    cudaFuncSetAttribute(k_row_win, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_row_win<<<rowwin_grid(), kRwThreads, smem, s>>>(a);
+    if (a.list) {
+        cudaFuncSetAttribute(k_row_win<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        k_row_win<true><<<rowwin_grid(), kRwThreads, smem, s>>>(a);
+    } else {
+        cudaFuncSetAttribute(k_row_win<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        k_row_win<false><<<rowwin_grid(), kRwThreads, smem, s>>>(a);
+    }
     note_launch();
 }
 

@@ -352,6 +352,8 @@ struct rig_plan {
     bool rowwin = false;    // no row on the merge path: one row-window kernel places every
                             // row straight into the graph (k_rowwin.cu, no temporary)
     int rw_gcap = 0;        // its global far-list capacity (0: shared lists only)
+    bool mid_rowwin = false;  // mixed path: mid rows through k_row_win (temp mode) instead of the mid passes
+    void *mid_rw_scratch = nullptr;  // its global far lists + ticket
     explicit rig_plan(cudaStream_t st) : s(st), arena(st) {}
 };
 
@@ -558,6 +560,12 @@ static void plan_build(rig_plan *p, const rig_csr_t *Ain, bool allow_early = fal
     // far lists of the global-far-list pass (rows that can outgrow the 768-item list)
     const bool need_gfar = p->h.max_f > kMidBigFarCapHost;
     const size_t o_gfar = need_gfar ? LB.add(mid_gfar_scratch_bytes()) : 0;
+    // mid rows (f_i <= 2^kSymBinMaxLog / 2) through k_row_win in temp mode:
+    // global far lists of that capacity, + a zeroed ticket
+    p->mid_rowwin = rowwin_enabled() && csc_fits_i32(p->A);
+    constexpr int kMidMaxF = 1 << (kSymBinMaxLog - 1);
+    p->rw_gcap = (int)std::min<int64_t>(std::max<int64_t>(p->h.max_f, 1), kMidMaxF);
+    const size_t o_mrw = p->mid_rowwin ? LB.add(256 + rowwin_scratch_bytes(p->rw_gcap)) : 0;
     size_t o_huge = 0;
     if (need_huge) {
         p->huge_slots_n = huge_slots(n, p->h.max_f > kMidSmallCap ? n_mid : std::min<int64_t>(n_mid, 8),
@@ -569,6 +577,7 @@ static void plan_build(rig_plan *p, const rig_csr_t *Ain, bool allow_early = fal
     p->lists = reinterpret_cast<int32_t *>(wb + o_lists);
     p->defer = reinterpret_cast<int32_t *>(wb + o_defer);
     p->gfar = need_gfar ? wb + o_gfar : nullptr;
+    p->mid_rw_scratch = p->mid_rowwin ? wb + o_mrw : nullptr;
     p->tcol = reinterpret_cast<int32_t *>(wb + o_tcol);
     p->tw = reinterpret_cast<double *>(wb + o_tw);
     if (need_huge) {
@@ -684,6 +693,61 @@ static int64_t plan_numeric(rig_plan *p, int32_t *gcol, double *gw, double *diag
         if (n_mid > 0) {
             MidArgs ma{p->A,     p->T,     p->rb,  p->lists, p->ctr->list_count, p->toff, p->tcol, p->tw,
                        p->nnzc,  p->defer, p->ctr->defer_count, dg, p->tol, debug_mask()};
+            if (p->mid_rowwin) {
+                // mid rows (f_i <= 2048): k_row_win in temp mode, nothing deferred;
+                // huge rows: wide window -> global far list -> CTA per row
+                auto *ticket = reinterpret_cast<unsigned long long *>(p->mid_rw_scratch);
+                CK(cudaMemsetAsync(ticket, 0, 256, s));
+                RowArgs ra{};
+                ra.A = p->A;
+                ra.T = p->T;
+                ra.rb = p->rb;
+                ra.nloc = p->nloc;
+                ra.ticket = ticket;
+                ra.diag = dg;
+                ra.tol = p->tol;
+                ra.gscratch = static_cast<unsigned char *>(p->mid_rw_scratch) + 256;
+                ra.gcap = p->rw_gcap;
+                ra.overflow = holes_d + 0;  // bit 1 only (capacity bug); read with the holes flag
+                ra.list = p->lists;
+                ra.count_dev = p->ctr->list_count;
+                ra.toff = p->toff;
+                ra.tcol = p->tcol;
+                ra.tw = p->tw;
+                ra.cnt = p->nnzc;
+                ra.dbg = debug_mask();
+                {
+                    Prof pk(P_KERNEL, s);
+                    launch_row_win(ra, s);
+                }
+                check_launch("mid rows (row-window, temp mode)");
+                MidArgs wd = ma;
+                wd.defer_list = p->defer + 2 * n_mid;
+                wd.defer_count = p->ctr->defer_count + 2;
+                wd.list = p->lists + n_mid;  // f_i beyond the mid bins
+                wd.count = p->ctr->list_count + 1;
+                launch_num_mid_wide(wd, s);
+                check_launch("huge rows (wide window)");
+                MidArgs hu = ma;
+                hu.list = p->defer + 2 * n_mid;
+                hu.count = p->ctr->defer_count + 2;
+                if (p->gfar) {
+                    MidArgs gf = ma;
+                    gf.list = p->defer + 2 * n_mid;
+                    gf.count = p->ctr->defer_count + 2;
+                    gf.defer_list = p->defer + 3 * n_mid;
+                    gf.defer_count = p->ctr->defer_count + 3;
+                    gf.fscratch = p->gfar;
+                    gf.fscratch_bytes = (int64_t)mid_gfar_scratch_bytes();
+                    gf.fnm = p->fnm;
+                    launch_num_mid_gfar(gf, s);
+                    check_launch("huge rows (global far lists)");
+                    hu.list = p->defer + 3 * n_mid;
+                    hu.count = p->ctr->defer_count + 3;
+                }
+                launch_num_huge(hu, p->huge_slots_n, p->huge_scratch, s);
+                check_launch("huge rows");
+            } else {
             {
                 Prof pk(P_KERNEL, s);
                 launch_num_mid(ma, kMidSmallCap, s);
@@ -731,6 +795,7 @@ static int64_t plan_numeric(rig_plan *p, int32_t *gcol, double *gw, double *diag
                 }
                 launch_num_huge(hu, p->huge_slots_n, p->huge_scratch, s);
                 check_launch("deferred rows");
+            }
             }
         }
         {
