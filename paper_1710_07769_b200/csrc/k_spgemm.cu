@@ -305,6 +305,9 @@ __device__ __forceinline__ int tree_min(const int (&h)[N]) {
     return v[0];
 }
 
+#ifndef RIG_PAIR_LOOKAHEAD
+#define RIG_PAIR_LOOKAHEAD 0  // measured: 1 (next key loaded one advance ahead) is 2-5 % slower on configs 2-3
+#endif
 // One half row.  q0[t]: CSC position of run t's first (ascending) or last
 // (descending) entry, or -1 for an empty run (t >= len).  Kept entries go to
 // the swizzled output stage at tile index ob, ob +- 1, ...  Returns the count.
@@ -314,6 +317,10 @@ __device__ __forceinline__ int pair_half_row(const NumArgs &a, bool desc, int64_
                                              int32_t pi, int &badp) {
     int h[R], q[R];
     double av[R], hv[R];
+#if RIG_PAIR_LOOKAHEAD
+    int h2[R];  // each run's NEXT key, loaded one advance ahead: the min of a
+                // step never waits on the load issued by the step before it
+#endif
     const int xm = desc ? -1 : 0;
     const int step = desc ? -1 : 1;
 #pragma unroll
@@ -322,9 +329,15 @@ __device__ __forceinline__ int pair_half_row(const NumArgs &a, bool desc, int64_
         av[t] = av0[t];
         h[t] = INT_MAX;
         hv[t] = 0.0;
+#if RIG_PAIR_LOOKAHEAD
+        h2[t] = INT_MAX;
+#endif
         if (q[t] >= 0) {
             h[t] = a.T.ri[q[t]] ^ xm;
             hv[t] = a.T.vt[q[t]];
+#if RIG_PAIR_LOOKAHEAD
+            h2[t] = a.T.ri[q[t] + step] ^ xm;
+#endif
         }
     }
     const int ik = (int)i ^ xm;
@@ -343,7 +356,12 @@ __device__ __forceinline__ int pair_half_row(const NumArgs &a, bool desc, int64_
                 acc = __fma_rn(av[t], hv[t], acc);
                 q[t] += step;  // ascending lanes stop at i, descending ones
                                // at i too: a run is never left
+#if RIG_PAIR_LOOKAHEAD
+                h[t] = h2[t];
+                h2[t] = a.T.ri[q[t] + step] ^ xm;  // at most two past the run (readable pads / sentinels)
+#else
                 h[t] = a.T.ri[q[t]] ^ xm;
+#endif
                 hv[t] = a.T.vt[q[t]];
             }
         }

@@ -389,8 +389,10 @@ static void plan_build(rig_plan *p, const rig_csr_t *Ain, bool allow_early = fal
     const size_t o_ahat = p->scale ? L.add(sizeof(double) * (size_t)nnz) : 0;
     // + one sentinel per column, + one leading pad entry: a descending merge
     // lane's last advance may read the entry before its run (never used)
-    const size_t o_ri = L.add(sizeof(int32_t) * (size_t)(nnz + m + 2));
-    const size_t o_vt = L.add(sizeof(double) * (size_t)(nnz + m + 1));
+    // two readable pad entries lead the arrays: the merge lanes' look-ahead
+    // reads up to two entries before a run (never used)
+    const size_t o_ri = L.add(sizeof(int32_t) * (size_t)(nnz + m + 3));
+    const size_t o_vt = L.add(sizeof(double) * (size_t)(nnz + m + 2));
     const size_t o_nnzc = L.add(sizeof(int64_t) * (size_t)nloc);
     const size_t o_fnm = L.add(sizeof(int64_t) * (size_t)nloc);
     const size_t o_bin8 = L.add((size_t)nloc);
@@ -414,8 +416,8 @@ static void plan_build(rig_plan *p, const rig_csr_t *Ain, bool allow_early = fal
     unsigned *cnt = reinterpret_cast<unsigned *>(ws + o_cnt);
     int64_t *cp = reinterpret_cast<int64_t *>(ws + o_cp);
     double *ahat = p->scale ? reinterpret_cast<double *>(ws + o_ahat) : nullptr;
-    int32_t *ri = reinterpret_cast<int32_t *>(ws + o_ri) + 1;
-    double *vt = reinterpret_cast<double *>(ws + o_vt) + 1;
+    int32_t *ri = reinterpret_cast<int32_t *>(ws + o_ri) + 2;
+    double *vt = reinterpret_cast<double *>(ws + o_vt) + 2;
     p->nnzc = reinterpret_cast<int64_t *>(ws + o_nnzc);
     int64_t *fnm = reinterpret_cast<int64_t *>(ws + o_fnm);
     p->fnm = fnm;
