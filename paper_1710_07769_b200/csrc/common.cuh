@@ -11,6 +11,24 @@
 
 namespace rig {
 
+// Bounds checks of the debug build (-DRIG_DEBUG_CHECKS, tools/build_variant.sh):
+// compute-sanitizer is closed on this GPU pool, so the kernels check their own
+// shared and global indices there and trap on a violation.
+#ifdef RIG_DEBUG_CHECKS
+#define RIG_CHECK(c)                                                                                  \
+    do {                                                                                              \
+        if (!(c)) {                                                                                   \
+            printf("RIG_CHECK failed: %s at %s:%d (block %d thread %d)\n", #c, __FILE__, __LINE__,    \
+                   (int)blockIdx.x, (int)threadIdx.x);                                                \
+            __trap();                                                                                 \
+        }                                                                                             \
+    } while (0)
+#else
+#define RIG_CHECK(c) \
+    do {             \
+    } while (0)
+#endif
+
 constexpr unsigned kFull = 0xffffffffu;
 constexpr int kWarp = 32;
 

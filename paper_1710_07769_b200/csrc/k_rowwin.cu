@@ -240,7 +240,10 @@ __device__ __forceinline__ bool far_sort(const F_ &F, int n) {
         const int p = p0 + l;
         const int b = p < n ? bucket(fk[p]) : NB + l;
         const unsigned g = __match_any_sync(kFull, b);
-        if (p < n) perm[bc[b] + __popc(g & lt)] = (uint16_t)p;
+        if (p < n) {
+            RIG_CHECK(b >= 0 && b < NB && bc[b] + __popc(g & lt) < n);
+            perm[bc[b] + __popc(g & lt)] = (uint16_t)p;
+        }
         __syncwarp();
         if (p < n && (g & lt) == 0) bc[b] += __popc(g);
         __syncwarp();
@@ -298,6 +301,7 @@ __device__ __forceinline__ bool far_sort(const F_ &F, int n) {
             m &= m - 1;
             const int e1 = bc[b], e0 = b > 0 ? bc[b - 1] : 0, sz = e1 - e0;
             if (sz > F.tmp_cap()) return false;  // the caller redoes the row with a global far list
+            RIG_CHECK(e0 >= 0 && e1 <= n && sz >= 0);
             for (int q = l; q < sz; q += 32) tmp[q] = perm[e0 + q];
             __syncwarp();
             for (int r0 = 0; r0 < sz; r0 += 32) {
@@ -399,6 +403,7 @@ __device__ __forceinline__ int accumulate(const RowArgs &a, RwSmem &S, const F_ 
         auto apply = [&](int j, double b, double at, int u) {
             const int d = j - wbase;
             const bool near = (unsigned)d < (unsigned)kRwW;
+            RIG_CHECK(j >= -1 && j < a.A.nrows);
             if (near) S.wv[d] = __fma_rn(at, b, S.wv[d]);
             const bool far = !near && j >= 0;
             const unsigned fm = __ballot_sync(kFull, far);
@@ -414,9 +419,12 @@ __device__ __forceinline__ int accumulate(const RowArgs &a, RwSmem &S, const F_ 
             // the pipeline
             const int Up = (U + kRwDepth - 1) / kRwDepth * kRwDepth;
             for (int c = 0, ex = incl - nch; c < nch; ++c) {
+                RIG_CHECK(ex + c < kRwTcap + 2 * kRwDepth);
+                RIG_CHECK(cs >= 0 && (int64_t)cs + cl <= a.A.nnz + a.A.ncols);
                 S.tcs[ex + c] = make_int2(cs + 32 * c, min(32, cl - 32 * c));
                 S.ta[ex + c] = av;
             }
+            RIG_CHECK(Up + kRwDepth <= kRwTcap + 2 * kRwDepth);
             if (l < Up + kRwDepth - U) {
                 S.tcs[U + l] = make_int2(0, 0);
                 S.ta[U + l] = 0.0;
@@ -700,6 +708,7 @@ __global__ void __launch_bounds__(kRwThreads, RIG_RW_MINB) k_row_win(RowArgs a) 
             const int64_t t0 = a.toff[r];
             const int kept = emit_row<true, false>(a, S, F, i, r, nfar, nbelow, a.tcol + t0, a.tw + t0, true, cur.pi,
                                                    acc, badp);
+            RIG_CHECK(kept <= a.toff[r + 1] - a.toff[r]);
             if (l == 0) a.cnt[r] = kept + 1;  // the graph scan subtracts the diagonal slot
             nidx = __shfl_sync(kFull, nidx, 0);
             meta_rows<TEMP>(a, nidx, nrows, nxt);
@@ -714,6 +723,7 @@ __global__ void __launch_bounds__(kRwThreads, RIG_RW_MINB) k_row_win(RowArgs a) 
             const int slot = pslot ^ 1;
             const int kept = emit_row<true, false>(a, S, F, i, idx, nfar, nbelow, stc + slot * kRwStageCap,
                                                    stw + slot * kRwStageCap, true, cur.pi, acc, badp);
+            RIG_CHECK(kept <= kRwStageCap);
             // publish the count; take the next ticket now (a ticket taken
             // earlier would be held while this warp waits, and rows behind it
             // would wait on it); then place the previously staged row

@@ -61,6 +61,27 @@ def main():
     g2 = rig.rig_build(A, 1, 0.05, rig.RIG_FLAG_VALIDATE)
     torch.cuda.synchronize()
     print("mixed ok", g.nnz, g2.nnz)
+    # row-window path: every row off the merge path; random rows take the
+    # global far list (and the capacity retry), banded rows the window
+    rng = np.random.default_rng(3)
+    n = 3000
+    rows, cols = [], []
+    for r in range(n):
+        if r < n // 2:
+            cc = rng.choice(n, int(rng.integers(9, 31)), replace=False)
+        else:
+            cc = np.unique(np.concatenate([[r], np.clip(r + rng.integers(-60, 61, 20), 0, n - 1),
+                                           rng.integers(0, n, 2)]))
+        rows += [r] * cc.size
+        cols += list(cc)
+    key = np.unique(np.array(rows, np.int64) * n + np.array(cols, np.int64))
+    rows, cols = key // n, key % n
+    rp, ci, v = from_triplets(n, n, rows, cols, rng.standard_normal(rows.size))
+    A = rig.CSR(rp, ci, v)
+    part = torch.as_tensor(rng.integers(0, 8, n).astype(np.int32), device="cuda")
+    g, cut = rig.rig_build_cut(A, part, 8, 0, n, 1, 0.0, rig.RIG_FLAG_DIAG)
+    torch.cuda.synchronize()
+    print("rowwin ok", g.nnz, rig.last_path(), float(cut.item()))
 
 
 if __name__ == "__main__":
