@@ -265,12 +265,20 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if args.gpus != world and world > 1:
         print(f"warning: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
+    # BENCH_SHARE_GPU=1 / BENCH_DIST_BACKEND=gloo: exercise the N > 1 code path
+    # on a one-GPU box (every rank on cuda:0, gloo); the numbers mean nothing then
+    if os.environ.get("BENCH_SHARE_GPU") == "1":
+        local = 0
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = os.environ.get("BENCH_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
 
     from paper_1710_07769_b200 import dist as rdist
     from paper_1710_07769_b200 import rig
