@@ -519,7 +519,8 @@ static int sms() {
 
 // a3 + a4 fused for the merge path: per row, f_i = sum of column lengths;
 // merge-path rows get their structural nnz(C_i) right away, the others are
-// binned for the warp-hash / huge symbolic kernels by ceil(log2(2 f_i)).
+// binned by ceil(log2(2 f_i)): the mid bins go to the mid-row kernel (k_row_win in temp mode), the
+// huge bin (f_i > 2048) to the wide-window / global-far-list / CTA-per-row chain.
 template <typename IdxT>
 __global__ void __launch_bounds__(kMergeThreads) k_analyze_sym(SymArgs a, uint8_t *bin8, DevCounters *ctr) {
     const int64_t nloc = a.re - a.rb;

@@ -3,9 +3,10 @@
 // in the kernels of k_*.cu; this file only sequences them and reads back the
 // few counters that size allocations.
 //
-// Host-overhead budget (DESIGN.md §4.4): a build makes one workspace
-// allocation per phase (stream-ordered pool), two memsets, two host syncs
-// (reading counters into pinned host memory) and ~10 kernel launches.
+// Host-overhead budget (DESIGN.md §4.5): a build makes one workspace
+// allocation per phase (stream-ordered pool, cached per thread), a few
+// memsets, one or two host syncs (counters read into pinned host memory) and
+// 10-20 kernel launches depending on the path (merge / row-window / mixed).
 #include <atomic>
 #include <cmath>
 #include <cstdio>

@@ -213,13 +213,13 @@ def test_sym_transpose_path(rig):
 
 
 def test_long_rows_and_columns(rig):
-    """Warp-hash, huge-row and long-column-sort paths."""
+    """Mid-row (global far list), huge-row and long-column-sort paths."""
     rng = np.random.default_rng(11)
     n = 20000
     rows, cols = [], []
-    # row 0: 3000 distinct columns (f > 2048 -> huge symbolic and numeric)
+    # row 0: 3000 distinct columns (f > 2048: the huge-row chain)
     c0 = rng.choice(n, 3000, replace=False); rows += [0] * 3000; cols += list(c0)
-    # rows 1..200: 20..600 entries (warp-hash bins)
+    # rows 1..200: 20..600 entries (mid bins: the row-window kernel, global far lists)
     for r in range(1, 201):
         k = int(rng.integers(20, 600))
         cc = rng.choice(n, k, replace=False); rows += [r] * k; cols += list(cc)
