@@ -372,6 +372,12 @@ struct RowArgs {
     int32_t *tcol;
     double *tw;
     int64_t *cnt;
+    // temp mode: rows with f_i = fnm[r] + len_i > fskip are not processed but
+    // appended to fskip_list (k_row_cta takes them)
+    const int64_t *fnm;
+    int64_t fskip;
+    int32_t *fskip_list;
+    int64_t *fskip_count;
     int dbg;          // RIG_DEBUG_MASK experiments (0 in normal operation)
 };
 int rowwin_grid();
@@ -379,6 +385,31 @@ size_t rowwin_scratch_bytes(int gcap);
 size_t rowwin_stage_entries();
 int rowwin_max_gcap();
 void launch_row_win(const RowArgs &a, cudaStream_t s);
+// k_rowcta.cu: CTA per row (shared-memory expand / stable radix sort / fold)
+// for long rows of scattered columns, temp mode like the mid-row kernels.
+struct RcArgs {
+    Csr A;
+    Csc T;
+    int64_t rb;
+    const int32_t *list0;  // rows (global ids); list0 then list1
+    const int64_t *count0;
+    const int32_t *list1;  // may be null
+    const int64_t *count1;
+    int32_t *rest;         // rows with f_i > fmax (for the huge-row chain)
+    int64_t *rest_count;
+    unsigned long long *ticket;  // zeroed
+    const int64_t *fnm;    // [nloc] f_i - len_i
+    const int64_t *toff;
+    int32_t *tcol;
+    double *tw;
+    int64_t *cnt;
+    double *diag;
+    double tol;
+    int fmax;              // items per row held in shared memory
+};
+size_t rowcta_smem_bytes(int fmax);
+void launch_row_cta(const RcArgs &a, cudaStream_t s);
+
 // per-row cut sums -> 256 partials (fixed segments) and *used = 256
 void launch_rowcut_partials(const double *cutrow, int64_t n, double *partials, int *used, cudaStream_t s);
 

@@ -766,6 +766,21 @@ __global__ void __launch_bounds__(kRwThreads, RIG_RW_MINB) k_row_win(RowArgs a) 
     };
     while (idx < nrows) {
         const int64_t i = TEMP ? cur.i : a.rb + idx;
+        if (TEMP && a.fskip_list && a.fnm[i - a.rb] + (cur.e - cur.s) > a.fskip) {
+            // long row: left to the CTA-per-row kernel
+            int64_t nidx = 0;
+            if (l == 0) {
+                a.fskip_list[atomicAdd((unsigned long long *)a.fskip_count, 1ull)] = (int32_t)i;
+                nidx = (int64_t)atomicAdd(a.ticket, 1ull);
+            }
+            nidx = __shfl_sync(kFull, nidx, 0);
+            meta_rows<TEMP>(a, nidx, nrows, nxt);
+            meta_entries(a, nxt);
+            meta_cols(a, nxt, false);
+            idx = nidx;
+            cur = nxt;
+            continue;
+        }
         const bool one_batch = cur.e - cur.s <= 32;
         int nfar = 0;
         bool global = !one_batch;

@@ -146,6 +146,17 @@ static int64_t sym_min_nnz() {
 // the merge path and the longest row has at most kRowWinMaxF products;
 // RIG_ROWWIN=0 turns it off (tests compare both paths).
 constexpr int64_t kRowWinMaxF = 1024;
+// mixed path: rows with f_i > kRowCtaMinF go from the row-window kernel to the
+// CTA-per-row kernel, which holds up to kRowCtaMaxF products in shared memory
+// (RIG_CTA_MINF / RIG_CTA_MAXF override them: experiments)
+static int64_t env_i64(const char *name, int64_t dflt) {
+    const char *e = getenv(name);
+    return e ? atoll(e) : dflt;
+}
+// (measured on configs 4 and 6: 256 / 1280 best; a second launch with large
+// shared arrays, one CTA per SM, takes the rows up to kRowCtaBigF)
+static const int64_t kRowCtaMinF = env_i64("RIG_CTA_MINF", 256), kRowCtaMaxF = env_i64("RIG_CTA_MAXF", 1280),
+                     kRowCtaBigF = env_i64("RIG_CTA_BIGF", 0);  // measured slower (5120: +0.65 ms, 7168: +0.87 ms on config 4): off
 static bool rowwin_enabled() {
     static int v = -1;
     if (v < 0) {
@@ -554,7 +565,7 @@ static void plan_build(rig_plan *p, const rig_csr_t *Ain, bool allow_early = fal
     const size_t o_toff = LB.add(sizeof(int64_t) * (size_t)(nloc + 1));
     const size_t o_st2 = LB.add(scan_tmp_bytes(nloc));
     const size_t o_lists = LB.add(sizeof(int32_t) * 2 * (size_t)n_mid);
-    const size_t o_defer = LB.add(sizeof(int32_t) * 4 * (size_t)n_mid);
+    const size_t o_defer = LB.add(sizeof(int32_t) * 5 * (size_t)n_mid);
     const size_t o_bcnt = LB.add(sizeof(unsigned) * nbc);
     const size_t o_boff = LB.add(sizeof(int64_t) * (nbc + 1));
     const size_t o_bst = LB.add(scan_tmp_bytes((int64_t)nbc));
@@ -699,8 +710,13 @@ static int64_t plan_numeric(rig_plan *p, int32_t *gcol, double *gw, double *diag
             if (p->mid_rowwin) {
                 // mid rows (f_i <= 2048): k_row_win in temp mode, nothing deferred;
                 // huge rows: wide window -> global far list -> CTA per row
+                // header: row-window ticket, CTA ticket, long-row count, rest count
                 auto *ticket = reinterpret_cast<unsigned long long *>(p->mid_rw_scratch);
                 CK(cudaMemsetAsync(ticket, 0, 256, s));
+                int64_t *long_count = reinterpret_cast<int64_t *>(ticket + 2);
+                int64_t *rest_count = reinterpret_cast<int64_t *>(ticket + 3);
+                int32_t *long_list = p->defer;           // rows left by the row-window kernel
+                int32_t *rest_list = p->defer + n_mid;   // rows beyond the CTA kernel's shared arrays
                 RowArgs ra{};
                 ra.A = p->A;
                 ra.T = p->T;
@@ -719,16 +735,60 @@ static int64_t plan_numeric(rig_plan *p, int32_t *gcol, double *gw, double *diag
                 ra.tw = p->tw;
                 ra.cnt = p->nnzc;
                 ra.dbg = debug_mask();
+                ra.fnm = p->fnm;
+                ra.fskip = kRowCtaMinF;
+                ra.fskip_list = long_list;
+                ra.fskip_count = long_count;
                 {
                     Prof pk(P_KERNEL, s);
                     launch_row_win(ra, s);
                 }
                 check_launch("mid rows (row-window, temp mode)");
+                // long rows of scattered columns (f_i > kRowCtaMinF, mid and huge
+                // bins): CTA per row in shared memory; beyond its arrays, the chain
+                RcArgs rc{};
+                rc.A = p->A;
+                rc.T = p->T;
+                rc.rb = p->rb;
+                rc.list0 = long_list;
+                rc.count0 = long_count;
+                rc.list1 = p->lists + n_mid;
+                rc.count1 = p->ctr->list_count + 1;
+                rc.rest = rest_list;
+                rc.rest_count = rest_count;
+                rc.ticket = ticket + 1;
+                rc.fnm = p->fnm;
+                rc.toff = p->toff;
+                rc.tcol = p->tcol;
+                rc.tw = p->tw;
+                rc.cnt = p->nnzc;
+                rc.diag = dg;
+                rc.tol = p->tol;
+                rc.fmax = (int)std::min<int64_t>(std::max<int64_t>(p->h.max_f, 1), kRowCtaMaxF);
+                launch_row_cta(rc, s);
+                check_launch("long rows (CTA per row)");
+                int32_t *rest2_list = rest_list;
+                int64_t *rest2_count = rest_count;
+                if (p->h.max_f > rc.fmax && kRowCtaBigF > rc.fmax) {  // longer rows: big shared arrays, 1 CTA per SM
+                    RcArgs rb2 = rc;
+                    rb2.list0 = rest_list;
+                    rb2.count0 = rest_count;
+                    rb2.list1 = nullptr;
+                    rb2.count1 = nullptr;
+                    rest2_list = p->defer + 4 * n_mid;
+                    rest2_count = reinterpret_cast<int64_t *>(ticket + 5);
+                    rb2.rest = rest2_list;
+                    rb2.rest_count = rest2_count;
+                    rb2.ticket = ticket + 4;
+                    rb2.fmax = (int)std::min<int64_t>(p->h.max_f, kRowCtaBigF);
+                    launch_row_cta(rb2, s);
+                    check_launch("long rows (CTA per row, big)");
+                }
                 MidArgs wd = ma;
                 wd.defer_list = p->defer + 2 * n_mid;
                 wd.defer_count = p->ctr->defer_count + 2;
-                wd.list = p->lists + n_mid;  // f_i beyond the mid bins
-                wd.count = p->ctr->list_count + 1;
+                wd.list = rest2_list;
+                wd.count = rest2_count;
                 launch_num_mid_wide(wd, s);
                 check_launch("huge rows (wide window)");
                 MidArgs hu = ma;
