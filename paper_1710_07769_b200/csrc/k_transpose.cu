@@ -15,6 +15,8 @@
 // CSC layout: column k occupies [cp[k] + k, cp[k+1] + k) followed by one
 // sentinel (row = INT_MAX, value 0) at cp[k+1] + k, so consumers walking a
 // column need no end bound (csc_begin()).  Rows ascend within each column.
+#include <algorithm>
+
 #include "common.cuh"
 
 namespace rig {
@@ -32,6 +34,10 @@ constexpr int kBucketTarget = RIG_BUCKET_TARGET;
 #define RIG_BUCKET_SLOTS 640
 #endif
 constexpr int kBucketSlots = RIG_BUCKET_SLOTS;
+#ifndef RIG_SMALL_BUCKET_SLOTS
+#define RIG_SMALL_BUCKET_SLOTS 256
+#endif
+constexpr int kSmallBucketSlots = RIG_SMALL_BUCKET_SLOTS, kSmallBucketCols = 64;
 
 struct __align__(16) Rec {
     int32_t col, row;
@@ -210,19 +216,22 @@ constexpr int kSortWarps = kSortThreads / 32;
 // entries and sentinels, in rank order -- is written with fully coalesced
 // stores.  Buckets that do not fit are listed for
 // k_bucket_sort_big.
-template <bool RANK>
+// SLOTS / MAXC: shared capacity of a bucket (records + sentinels) and of its
+// column count; a small instantiation (more warps per SM) serves matrices
+// whose buckets are small, larger buckets go to the big list as usual.
+template <bool RANK, int SLOTS = kBucketSlots, int MAXC = kMaxBucketCols>
 __global__ void __launch_bounds__(kSortThreads) k_bucket_sort(const Rec *__restrict__ rec,
                                                               const int64_t *__restrict__ cp, int64_t ncols,
                                                               int32_t *ri, double *vt, int shift, int *big_list,
                                                               int *big_count, const int *guard) {
     if (guard_skip(guard)) return;
-    __shared__ int32_t s_ri[kSortWarps][kBucketSlots];
-    __shared__ double s_vt[kSortWarps][kBucketSlots];
-    constexpr int RS = RANK ? kBucketSlots : 1;
+    __shared__ int32_t s_ri[kSortWarps][SLOTS];
+    __shared__ double s_vt[kSortWarps][SLOTS];
+    constexpr int RS = RANK ? SLOTS : 1;
     __shared__ uint16_t s_col[kSortWarps][RS];  // local column of a slot (0xffff: sentinel)
     __shared__ uint16_t s_inv[kSortWarps][RS];  // sorted position -> slot
-    __shared__ uint16_t s_off[kSortWarps][kMaxBucketCols + 1];
-    __shared__ unsigned s_cur[kSortWarps][kMaxBucketCols];
+    __shared__ uint16_t s_off[kSortWarps][MAXC + 1];
+    __shared__ unsigned s_cur[kSortWarps][MAXC];
     const int w = threadIdx.x >> 5, l = lane_id();
     int32_t *sr = s_ri[w];
     double *sv = s_vt[w];
@@ -238,7 +247,7 @@ __global__ void __launch_bounds__(kSortThreads) k_bucket_sort(const Rec *__restr
         const int ncb = (int)min((int64_t)bcols, ncols - c0);
         const int64_t e0 = cp[c0];
         const int64_t E = cp[c0 + ncb] - e0;
-        if (E + ncb > kBucketSlots) {
+        if (E + ncb > SLOTS || ncb > MAXC) {
             if (l == 0) big_list[atomicAdd(big_count, 1)] = (int)b;
             continue;
         }
@@ -407,7 +416,17 @@ void launch_transpose(const Csr &A, int scale, const int64_t *cp, double *ahat, 
         g = g < cap ? g : cap;
         // big[0] = count of big buckets, big[1..] = their ids
         // long columns: parallel ranking; short ones: per-lane insertion sorts
-        if (A.nnz > (int64_t)12 * A.ncols)
+        // buckets of <= ~200 records on average (2^shift <= 64 columns): the
+        // small-capacity instantiation (a third of the shared memory per warp)
+        const int64_t mean_bucket = A.nnz / (nb > 0 ? nb : 1) + (1 << shift);
+        const bool small = (1 << shift) <= kSmallBucketCols && mean_bucket <= kSmallBucketSlots * 3 / 4;
+        if (A.nnz > (int64_t)12 * A.ncols && small)
+            k_bucket_sort<true, kSmallBucketSlots, kSmallBucketCols><<<(unsigned)std::min<int64_t>(
+                                                                          (nb + kSortWarps - 1) / kSortWarps,
+                                                                          (int64_t)num_sms() * 24),
+                                                                      kSortThreads, 0, s>>>(
+                static_cast<const Rec *>(rec), cp, A.ncols, ri, vt, shift, big + 1, big, guard);
+        else if (A.nnz > (int64_t)12 * A.ncols)
             k_bucket_sort<true><<<(unsigned)g, kSortThreads, 0, s>>>(static_cast<const Rec *>(rec), cp, A.ncols, ri,
                                                                      vt, shift, big + 1, big, guard);
         else
