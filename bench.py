@@ -384,6 +384,23 @@ def main():
         my_ms, num_ms, ker_ms = float(t[0]), float(t[1]), float(t[2])
     cut_val = float(cut.item())
 
+    # ---- device memory of one build (library pool high-water mark; the
+    # inputs A and part live in torch's allocator, the rest in the pool)
+    torch.cuda.synchronize()
+    rig.rig_mem_stats(reset=True)
+    g, _c = step()
+    torch.cuda.synchronize()
+    pool_now, pool_high = rig.rig_mem_stats()
+    a_bytes = 8 * (w.n + 1) + 12 * w.nnz
+    csc_bytes = 8 * (w.ncols + 1) + 12 * (w.nnz + w.ncols)
+    graph_bytes = 8 * (re - rb + 1) + 12 * g.nnz
+    del g
+    mem = {"pool_high_gb": pool_high / 1e9, "inputs_gb": (a_bytes + 4 * w.n) / 1e9,
+           "a_csc_graph_gb": (a_bytes + csc_bytes + graph_bytes) / 1e9,
+           "ratio": (pool_high + a_bytes + 4 * w.n) / (a_bytes + csc_bytes + graph_bytes),
+           "note": "peak = library pool high-water mark during one build (workspaces + graph) + inputs; "
+                   "ratio against A + CSC of A_hat + the exact graph"}
+
     # ---- e2e through the C ABI from pinned host buffers (N=1 path)
     e2e = None
     if world == 1:
@@ -461,6 +478,7 @@ def main():
         "numeric_path": path,
         "gpu_launches": launches,
         "clocks": clk,
+        "device_memory": mem,
     }
     if e2e:
         line["e2e"] = e2e

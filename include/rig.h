@@ -302,6 +302,11 @@ RIG_API const char *rig_last_path(void);
  * writes, so ncu's L2/DRAM counters of that kernel are the gathers' own.
  * *checksum_host (may be NULL) receives a checksum of the gathered data.
  * Synchronises the stream. */
+/* Measurement: the current device's stream-ordered memory pool (which holds
+ * every library allocation: workspaces, library-owned graphs) -- bytes in use
+ * now and the high-water mark since the last reset (reset = 1 clears it
+ * after reading). */
+RIG_API int rig_mem_stats(uint64_t *used_now, uint64_t *used_high, int reset);
 RIG_API int rig_gather_probe(const rig_csr_t *A, int scale_rows, double *checksum_host, rig_stream_t stream);
 
 #ifdef __cplusplus

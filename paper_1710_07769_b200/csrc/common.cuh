@@ -339,6 +339,7 @@ void launch_copy_rows(const int32_t *list, const int64_t *count, int64_t rb, con
 size_t huge_scratch_bytes(int64_t nrows, int slots, bool numeric);
 size_t huge_bitmap_bytes(int64_t nrows, int slots);  // zeroed prefix of the scratch
 int huge_slots(int64_t nrows, int64_t n_huge, bool heavy);  // heavy: the shard has huge rows
+int huge_slots_rw(int64_t nrows, int64_t n_reach, int64_t per_sm);  // row-window mixed path
 void launch_num_huge(const MidArgs &a, int slots, void *scratch, cudaStream_t s);
 
 // k_rowwin.cu: every row of the shard in one kernel, placed straight into the

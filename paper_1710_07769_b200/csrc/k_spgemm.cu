@@ -767,6 +767,16 @@ size_t huge_scratch_bytes(int64_t nrows, int slots, bool numeric) {
 #ifndef RIG_HUGE_PER_SM
 #define RIG_HUGE_PER_SM 8
 #endif
+int huge_slots_rw(int64_t nrows, int64_t n_reach, int64_t per_sm) {
+    const size_t per = huge_scratch_bytes(nrows, 1, true);
+    size_t fr = 0, tot = 0;
+    cudaMemGetInfo(&fr, &tot);
+    const size_t bud = std::min(((size_t)RIG_HUGE_BUDGET_GB << 30), fr / 4 ? fr / 4 : (size_t)1);
+    int64_t s = std::min<int64_t>(per_sm * (int64_t)sms(), n_reach);
+    s = std::min<int64_t>(s, (int64_t)(bud / (per ? per : 1)));
+    return (int)std::max<int64_t>(s, 1);
+}
+
 int huge_slots(int64_t nrows, int64_t n_huge, bool heavy) {
     const size_t per = huge_scratch_bytes(nrows, 1, true);
     static size_t free_q = 0;

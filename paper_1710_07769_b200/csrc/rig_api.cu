@@ -156,7 +156,8 @@ static int64_t env_i64(const char *name, int64_t dflt) {
 // (measured on configs 4 and 6: 256 / 1280 best; a second launch with large
 // shared arrays, one CTA per SM, takes the rows up to kRowCtaBigF)
 static const int64_t kRowCtaMinF = env_i64("RIG_CTA_MINF", 256), kRowCtaMaxF = env_i64("RIG_CTA_MAXF", 1280),
-                     kRowCtaBigF = env_i64("RIG_CTA_BIGF", 0);  // measured slower (5120: +0.65 ms, 7168: +0.87 ms on config 4): off
+                     kRowCtaBigF = env_i64("RIG_CTA_BIGF", 0);
+static const int64_t kHugePerSmRw = env_i64("RIG_HUGE_PER_SM_RW", 4);  // measured 1, 2, 4, 8: 4 (half the memory of 8, same time)  // huge-kernel slots per SM on the row-window mixed path  // measured slower (5120: +0.65 ms, 7168: +0.87 ms on config 4): off
 static bool rowwin_enabled() {
     static int v = -1;
     if (v < 0) {
@@ -582,8 +583,16 @@ static void plan_build(rig_plan *p, const rig_csr_t *Ain, bool allow_early = fal
     const size_t o_mrw = p->mid_rowwin ? LB.add(256 + rowwin_scratch_bytes(p->rw_gcap)) : 0;
     size_t o_huge = 0;
     if (need_huge) {
-        p->huge_slots_n = huge_slots(n, p->h.max_f > kMidSmallCap ? n_mid : std::min<int64_t>(n_mid, 8),
-                                     p->h.sym_count[kNumSymBins] > 0);
+        if (p->mid_rowwin) {
+            // only rows with f_i > kRowCtaMaxF can reach the huge kernel (the
+            // row-window and CTA kernels take the rest): at most the rows of
+            // the last mid bin and the huge bin; few slots (each is O(n) memory)
+            const int64_t reach = p->h.sym_count[kNumSymBins - 1] + p->h.sym_count[kNumSymBins];
+            p->huge_slots_n = huge_slots_rw(n, std::max<int64_t>(reach, 1), kHugePerSmRw);
+        } else {
+            p->huge_slots_n = huge_slots(n, p->h.max_f > kMidSmallCap ? n_mid : std::min<int64_t>(n_mid, 8),
+                                         p->h.sym_count[kNumSymBins] > 0);
+        }
         o_huge = LB.add(huge_scratch_bytes(n, p->huge_slots_n, true));
     }
     unsigned char *wb = p->cached ? ws_get(1, LB.bytes, s) : p->arena.raw(LB.bytes);
@@ -1116,6 +1125,25 @@ int rig_trim(void) {
 uint64_t rig_launch_count(void) { return g_launches.load(); }
 const char *rig_version(void) { return "librig 0.3 (sm_100a)"; }
 const char *rig_last_path(void) { return t_last_path.c_str(); }
+
+int rig_mem_stats(uint64_t *used_now, uint64_t *used_high, int reset) {
+    ABI_BEGIN
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    cudaMemPool_t pool;
+    CK(cudaDeviceGetDefaultMemPool(&pool, dev));
+    unsigned long long cur = 0, high = 0;  // cuuint64_t
+    CK(cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &cur));
+    CK(cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemHigh, &high));
+    if (used_now) *used_now = (uint64_t)cur;
+    if (used_high) *used_high = (uint64_t)high;
+    if (reset) {
+        unsigned long long zero = 0;
+        CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrUsedMemHigh, &zero));
+    }
+    return RIG_OK;
+    ABI_END
+}
 
 int rig_gather_probe(const rig_csr_t *A, int scale_rows, double *checksum_host, rig_stream_t stream) {
     ABI_BEGIN

@@ -98,6 +98,14 @@ def _stream(stream=None):
     return ctypes.c_void_p(s.cuda_stream)
 
 
+def rig_mem_stats(reset=False):
+    """(bytes in use, high-water mark) of the device's stream-ordered pool,
+    which holds every library allocation."""
+    now, high = ctypes.c_uint64(), ctypes.c_uint64()
+    _check(lib.rig_mem_stats(ctypes.byref(now), ctypes.byref(high), int(bool(reset))))
+    return now.value, high.value
+
+
 def rig_gather_probe(A: CSR, scale_rows=1, stream=None) -> float:
     """Measurement: the numeric pass's gather loop alone (k_gather_probe)."""
     out = ctypes.c_double()

@@ -26,7 +26,7 @@ def test_header_symbols_exported(rig):
                 "rig_last_error", "rig_launch_count", "rig_version", "rig_profile_enable", "rig_profile_read", "rig_trim",
                 "rig_pass_name", "rig_partition_ip", "rig_partition_ip_finalize", "rig_sparsify",
                 "rig_csr_free", "rig_int_weights", "rig_hem_match", "rig_coarsen", "rig_coarse_free",
-                "rig_last_path", "rig_gather_probe"}
+                "rig_last_path", "rig_gather_probe", "rig_mem_stats"}
     assert set(names) == expected
     so = ctypes.CDLL(rig.LIB_PATH)
     for n in names:
