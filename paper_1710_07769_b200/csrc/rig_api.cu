@@ -153,11 +153,14 @@ static int64_t env_i64(const char *name, int64_t dflt) {
     const char *e = getenv(name);
     return e ? atoll(e) : dflt;
 }
-// (measured on configs 4 and 6: 256 / 1280 best; a second launch with large
-// shared arrays, one CTA per SM, takes the rows up to kRowCtaBigF)
+// Measured on configs 4 and 6: 256 / 1280 best.  kRowCtaBigF > 0 adds a
+// second launch with large shared arrays (one CTA per SM) for the rows up to
+// it: measured slower (5120: +0.65 ms, 7168: +0.87 ms on config 4), so off.
 static const int64_t kRowCtaMinF = env_i64("RIG_CTA_MINF", 256), kRowCtaMaxF = env_i64("RIG_CTA_MAXF", 1280),
                      kRowCtaBigF = env_i64("RIG_CTA_BIGF", 0);
-static const int64_t kHugePerSmRw = env_i64("RIG_HUGE_PER_SM_RW", 4);  // measured 1, 2, 4, 8: 4 (half the memory of 8, same time)  // huge-kernel slots per SM on the row-window mixed path  // measured slower (5120: +0.65 ms, 7168: +0.87 ms on config 4): off
+// huge-kernel slots per SM on the row-window mixed path (each slot is O(n)
+// memory); measured 1, 2, 4, 8: 4 is as fast as 8 with half the memory
+static const int64_t kHugePerSmRw = env_i64("RIG_HUGE_PER_SM_RW", 4);
 static bool rowwin_enabled() {
     static int v = -1;
     if (v < 0) {
