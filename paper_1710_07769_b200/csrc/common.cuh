@@ -86,7 +86,9 @@ struct DevCounters {
     int64_t p_full;        // sum over columns of len^2 = products of the full matrix (>= the shard's)
     int64_t max_row;       // longest row of A in the shard
     int64_t shard_nnz;     // entries of A in the shard's rows
+    int64_t min_row_c;     // kMinRowBias - (shortest A row in the shard); 0: no row
 };
+constexpr int64_t kMinRowBias = int64_t(1) << 40;
 
 __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
 

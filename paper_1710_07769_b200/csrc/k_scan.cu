@@ -61,7 +61,7 @@ __global__ void __launch_bounds__(kScanThreads) k_tile_sum(const T *__restrict__
     if (guard_skip(guard)) return;
     const int64_t base = blockIdx.x * kTile;
     int64_t s = 0;
-    unsigned long long ps = 0, mc = 0, mr = 0;
+    unsigned long long ps = 0, mc = 0, mr = 0, mn = 0;  // mn: max of kMinRowBias - len
 #pragma unroll
     for (int j = 0; j < kScanItems; ++j) {
         const int64_t i = base + (int64_t)j * kScanThreads + threadIdx.x;
@@ -79,18 +79,24 @@ __global__ void __launch_bounds__(kScanThreads) k_tile_sum(const T *__restrict__
         const int64_t stride = (int64_t)gridDim.x * kScanThreads;
 #pragma unroll 8
         for (int64_t i = so.rb + blockIdx.x * (int64_t)kScanThreads + threadIdx.x; i < so.re; i += stride)
-            mr = max(mr, (unsigned long long)(so.rp[i + 1] - so.rp[i]));
+        {
+            const unsigned long long len = (unsigned long long)(so.rp[i + 1] - so.rp[i]);
+            mr = max(mr, len);
+            mn = max(mn, (unsigned long long)kMinRowBias - len);
+        }
         ps = warp_sum(ps);
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
             mc = max(mc, __shfl_xor_sync(kFull, mc, o));
             mr = max(mr, __shfl_xor_sync(kFull, mr, o));
+            mn = max(mn, __shfl_xor_sync(kFull, mn, o));
         }
-        __shared__ unsigned long long red[3][kScanThreads / 32];
+        __shared__ unsigned long long red[4][kScanThreads / 32];
         if (lane_id() == 0) {
             red[0][threadIdx.x >> 5] = ps;
             red[1][threadIdx.x >> 5] = mc;
             red[2][threadIdx.x >> 5] = mr;
+            red[3][threadIdx.x >> 5] = mn;
         }
         __syncthreads();
         if (threadIdx.x == 0) {
@@ -98,10 +104,12 @@ __global__ void __launch_bounds__(kScanThreads) k_tile_sum(const T *__restrict__
                 ps += red[0][k];
                 mc = max(mc, red[1][k]);
                 mr = max(mr, red[2][k]);
+                mn = max(mn, red[3][k]);
             }
             if (ps) atomicAdd((unsigned long long *)&so.ctr->p_full, ps);
             if (mc) atomicMax((unsigned long long *)&so.ctr->max_col, mc);
             if (mr) atomicMax((unsigned long long *)&so.ctr->max_row, mr);
+            if (mn) atomicMax((unsigned long long *)&so.ctr->min_row_c, mn);
             if (blockIdx.x == 0) so.ctr->shard_nnz = so.rp[so.re] - so.rp[so.rb];
         }
     }

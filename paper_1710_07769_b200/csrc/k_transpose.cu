@@ -615,26 +615,31 @@ __global__ void __launch_bounds__(kSymThreads, RIG_SYM_MINB) k_sym_transpose(Csr
 __global__ void k_sym_shape(const int64_t *__restrict__ rp, int64_t n, int64_t rb, int64_t re, DevCounters *ctr,
                             const int *fail) {
     if (*reinterpret_cast<const volatile int *>(fail)) return;
-    unsigned long long ps = 0, mc = 0, mr = 0;
+    unsigned long long ps = 0, mc = 0, mr = 0, mn = 0;  // mn: max of kMinRowBias - len
 #pragma unroll 4
     for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
         const unsigned long long len = (unsigned long long)(rp[k + 1] - rp[k]);
         ps += len * len;
         mc = max(mc, len);
-        if (k >= rb && k < re) mr = max(mr, len);
+        if (k >= rb && k < re) {
+            mr = max(mr, len);
+            mn = max(mn, (unsigned long long)kMinRowBias - len);
+        }
     }
     ps = warp_sum(ps);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
         mc = max(mc, __shfl_xor_sync(kFull, mc, o));
         mr = max(mr, __shfl_xor_sync(kFull, mr, o));
+        mn = max(mn, __shfl_xor_sync(kFull, mn, o));
     }
-    __shared__ unsigned long long red[3][8];  // one atomic per counter per CTA (<= 256 threads)
+    __shared__ unsigned long long red[4][8];  // one atomic per counter per CTA (<= 256 threads)
     const int w = threadIdx.x >> 5;
     if (lane_id() == 0) {
         red[0][w] = ps;
         red[1][w] = mc;
         red[2][w] = mr;
+        red[3][w] = mn;
     }
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -642,10 +647,12 @@ __global__ void k_sym_shape(const int64_t *__restrict__ rp, int64_t n, int64_t r
             ps += red[0][k];
             mc = max(mc, red[1][k]);
             mr = max(mr, red[2][k]);
+            mn = max(mn, red[3][k]);
         }
         if (ps) atomicAdd((unsigned long long *)&ctr->p_full, ps);
         if (mc) atomicMax((unsigned long long *)&ctr->max_col, mc);
         if (mr) atomicMax((unsigned long long *)&ctr->max_row, mr);
+        if (mn) atomicMax((unsigned long long *)&ctr->min_row_c, mn);
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) ctr->shard_nnz = rp[re] - rp[rb];
 }

@@ -146,6 +146,9 @@ static int64_t sym_min_nnz() {
 // the merge path and the longest row has at most kRowWinMaxF products;
 // RIG_ROWWIN=0 turns it off (tests compare both paths).
 constexpr int64_t kRowWinMaxF = 1024;
+// the same decision from the shape statistics alone uses the looser bound
+// f_i <= max_row * max_col (config 5: 23 * ~50 against its true max 636)
+constexpr int64_t kRowWinEarlyBound = 2048;
 // mixed path: rows with f_i > kRowCtaMinF go from the row-window kernel to the
 // CTA-per-row kernel, which holds up to kRowCtaMaxF products in shared memory
 // (RIG_CTA_MINF / RIG_CTA_MAXF override them: experiments)
@@ -520,6 +523,28 @@ static void plan_build(rig_plan *p, const rig_csr_t *Ain, bool allow_early = fal
     }
     // a3 + a4 (merge rows): products, merge-row nnzC, paths of the others
     p->qs = use_qs ? reinterpret_cast<int2 *>(ws + o_qs) : nullptr;
+    if (ev_shape && rowwin_enabled() && csc_fits_i32(p->A)) {
+        // row-window path decided from the shape statistics alone (read back
+        // while the transpose runs): every row longer than the merge path
+        // takes, and f_i <= max_row * max_col small enough.  No analysis and
+        // no synchronisation until the end (errors are read there).
+        CK(cudaEventSynchronize(ev_shape));
+        const DevCounters &sh = hs->shape;
+        const int64_t min_row = sh.min_row_c ? kMinRowBias - sh.min_row_c : 0;
+        const int64_t fbound = sh.max_row * sh.max_col;
+        if (nloc > 0 && min_row > kMergeMaxLen && fbound <= kRowWinEarlyBound) {
+            p->early = true;
+            p->rowwin = true;
+            p->h = DevCounters{};
+            const int64_t pb = std::min<int64_t>(sh.p_full, sh.shard_nnz * sh.max_col);
+            p->h.products = pb;  // an upper bound here
+            p->h.max_f = fbound;
+            p->h.n_mid = nloc;
+            p->nnz_upper = pb - sh.shard_nnz;
+            p->rw_gcap = (int)std::max<int64_t>(fbound, 1);
+            return;
+        }
+    }
     SymArgs sa{p->A, p->T, p->rb, p->re, p->nnzc, fnm, p->qs};
     if (nloc > 0) {
         Prof pf(P_ANALYZE, s);
@@ -685,7 +710,9 @@ static int64_t rowwin_numeric(rig_plan *p, int32_t *gcol, double *gw, int64_t ca
     HostStage *hs = host_stage();
     CK(cudaMemcpyAsync(&hs->holes, flag_d, sizeof(int), cudaMemcpyDeviceToHost, s));
     CK(cudaMemcpyAsync(&hs->v[0], row_ptr_out + p->nloc, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    if (p->early) CK(cudaMemcpyAsync(&hs->ctr.err, &p->ctr->err, sizeof(int), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
+    if (p->early && hs->ctr.err) throw Error(err_to_code(hs->ctr.err), err_msg(err_to_code(hs->ctr.err)));
     if (hs->holes & 2) throw Error(RIG_ERR_CUDA, "row-window far list capacity exceeded");
     if (hs->holes & 1) throw NeedCapacity{hs->v[0]};
     return hs->v[0];
