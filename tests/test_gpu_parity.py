@@ -331,6 +331,78 @@ def test_row_window_path(rig, seed):
         plan.destroy()
 
 
+@pytest.mark.parametrize("seed", range(2))
+def test_long_scattered_rows_cta(rig, seed):
+    """Mixed path: short merge rows plus rows of 20..150 scattered columns
+    (f_i ~ 100..1500: the row-window kernel in temp mode below 256 products,
+    k_row_cta -- CTA per row, shared-memory radix sort -- up to 1280, the
+    huge-row chain beyond).  Values with exact ties force cancellations and
+    equal-key groups; drops; diag; cut; a shard."""
+    rng = np.random.default_rng(77 + seed)
+    n = 12000
+    rows, cols = [], []
+    for r in range(n):
+        k = int(rng.integers(20, 150)) if r % 11 == 0 else int(rng.integers(1, 6))
+        cc = rng.choice(n, k, replace=False)
+        rows += [r] * k; cols += list(cc)
+    rows += list(range(n)); cols += list(range(n))
+    rows, cols = np.array(rows), np.array(cols)
+    key = np.unique(rows.astype(np.int64) * n + cols)
+    rows, cols = key // n, key % n
+    vals = rng.standard_normal(rows.size)
+    vals[rng.random(rows.size) < 0.25] = 1.0
+    vals[rng.random(rows.size) < 0.25] = -1.0
+    rp, ci, v = from_triplets(n, n, rows, cols, vals)
+    K = 16
+    part = rng.integers(0, K, n).astype(np.int32)
+    tpart = torch.as_tensor(part, device="cuda")
+    A = rig.CSR(rp, ci, v)
+    for scale, tol in ((1, 0.0), (0, 0.5)):
+        orc = oracle.build(rp, ci, v, scale_rows=scale, drop_tol=tol)
+        g = rig.rig_build(A, scale, tol, rig.RIG_FLAG_DIAG)
+        assert rig.last_path() == "mixed"
+        assert_graph_equal(to_np(g.row_ptr), to_np(g.col_idx), to_np(g.w), orc, to_np(g.diag))
+        ocut = oracle.cutsize(orc.row_ptr, orc.col, orc.w, part, K)[0]
+        gc, cut = rig.rig_build_cut(A, tpart, K, 0, n, scale, tol)
+        assert_graph_equal(to_np(gc.row_ptr), to_np(gc.col_idx), to_np(gc.w), orc)
+        assert abs(cut.item() - ocut) <= REL * ocut
+    a, b = 3001, 9002
+    o3 = oracle.build(rp, ci, v, scale_rows=1, drop_tol=0.0, row_begin=a, row_end=b)
+    g3 = rig.rig_build_rows(A, a, b, 1, 0.0)
+    assert_graph_equal(to_np(g3.row_ptr), to_np(g3.col_idx), to_np(g3.w), o3)
+
+
+def test_row_window_early_errors(rig):
+    """The row-window path decided before the analysis (every row long):
+    device errors raised by the scaling are still reported (read at the final
+    synchronisation): a NaN value and an all-zero row."""
+    rng = np.random.default_rng(5)
+    n = 3000
+    rows, cols = [], []
+    for r in range(n):  # 12 distinct columns within 20 of the diagonal, + the diagonal
+        lo, hi = max(0, r - 20), min(n, r + 21)
+        cc = np.unique(np.concatenate([[r], rng.choice(np.arange(lo, hi), 12, replace=False)]))
+        rows += [r] * cc.size; cols += list(cc)
+    rows, cols = np.array(rows), np.array(cols)
+    vals = rng.standard_normal(rows.size)
+    rp, ci, v = from_triplets(n, n, rows, cols, vals)
+    assert np.diff(rp).min() > 8
+    g = rig.rig_build(rig.CSR(rp, ci, v), 1, 0.0)
+    assert rig.last_path() == "rowwin"
+    orc = oracle.build(rp, ci, v, scale_rows=1, drop_tol=0.0)
+    assert_graph_equal(to_np(g.row_ptr), to_np(g.col_idx), to_np(g.w), orc)
+    bad = v.copy()
+    bad[17] = np.nan
+    with pytest.raises(rig.RigError) as e:
+        rig.rig_build(rig.CSR(rp, ci, bad), 1, 0.0)
+    assert e.value.code == rig.RIG_ERR_NONFINITE
+    z = v.copy()
+    z[rp[100]:rp[101]] = 0.0
+    with pytest.raises(rig.RigError) as e:
+        rig.rig_build(rig.CSR(rp, ci, z), 1, 0.0)
+    assert e.value.code == rig.RIG_ERR_ZERO_ROW
+
+
 def test_mid_row_passes_long_far_lists(rig):
     """Rows of 800..3500 random columns (every key far from the diagonal) run
     through the mid pass, the 768-item far-list pass, the wide window and the
