@@ -199,22 +199,18 @@ __device__ __forceinline__ int64_t lookback(unsigned long long *chain, int64_t i
 // buckets of <= kRwSmallBucket items; a longer bucket found out of order is
 // ranked by (key, arrival) by the whole warp.
 template <class F_>
-__device__ __forceinline__ bool far_sort(const F_ &F, int n) {
+__device__ __forceinline__ bool far_sort(const F_ &F, int n, int key_bits) {
     const int l = lane_id();
     const unsigned lt = lanemask_lt();
     constexpr int NB = F_::nb, PER = NB / 32;
+    constexpr int NBB = NB == 128 ? 7 : (NB == 256 ? 8 : (NB == 512 ? 9 : (NB == 64 ? 6 : 10)));
+    static_assert((1 << NBB) == NB, "NB must be a power of two in [64, 1024]");
     int *fk = F.fk(), *bc = F.bc();
     uint16_t *perm = F.perm();
-    int mn = INT_MAX, mx = INT_MIN;
-    for (int p = l; p < n; p += 32) {
-        const int k = fk[p];
-        mn = min(mn, k);
-        mx = max(mx, k);
-    }
-    mn = __reduce_min_sync(kFull, mn);
-    mx = __reduce_max_sync(kFull, mx);
-    const float scale = (float)NB / ((float)((int64_t)mx - mn) + 1.0f);
-    auto bucket = [&](int k) { return min(NB - 1, (int)(__int2float_rz(k - mn) * scale)); };
+    // fixed-width value buckets over [0, 2^key_bits) (keys are row ids):
+    // monotone in the key, no min / max pass
+    const int sh = key_bits > NBB ? key_bits - NBB : 0;
+    auto bucket = [&](int k) { return k >> sh; };
 #pragma unroll
     for (int u = 0; u < PER; ++u) bc[l * PER + u] = 0;
     if (l < PER) F.bad()[l] = 0u;
@@ -665,6 +661,7 @@ __global__ void __launch_bounds__(kRwThreads, RIG_RW_MINB) k_row_win(RowArgs a) 
     int64_t pidx = -1;  // staged row waiting for its offset
     int pkept = 0, pslot = 0;
     const int64_t nrows = TEMP ? *a.count_dev : a.nloc;
+    const int key_bits = a.A.nrows > 1 ? 64 - __clzll((unsigned long long)(a.A.nrows - 1)) : 1;  // keys < 2^key_bits
     int64_t idx = 0;
     if (l == 0) idx = (int64_t)atomicAdd(a.ticket, 1ull);
     idx = __shfl_sync(kFull, idx, 0);
@@ -796,7 +793,7 @@ __global__ void __launch_bounds__(kRwThreads, RIG_RW_MINB) k_row_win(RowArgs a) 
             bool redo = nfar > FS.cap();
             if (!redo) {
                 if (nfar > 1)
-                    redo = !far_sort(FS, nfar);
+                    redo = !far_sort(FS, nfar, key_bits);
                 else if (nfar == 1 && l == 0)
                     FS.perm()[0] = 0;
                 __syncwarp();
@@ -817,7 +814,7 @@ __global__ void __launch_bounds__(kRwThreads, RIG_RW_MINB) k_row_win(RowArgs a) 
                 nfar = FG.cap();
             }
             if (nfar > 1)
-                far_sort(FG, nfar);  // tmp_cap = gcap: always sorts
+                far_sort(FG, nfar, key_bits);  // tmp_cap = gcap: always sorts
             else if (nfar == 1 && l == 0)
                 FG.perm()[0] = 0;
             __syncwarp();
