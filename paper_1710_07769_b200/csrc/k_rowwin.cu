@@ -466,6 +466,26 @@ __device__ __forceinline__ int accumulate(const RowArgs &a, RwSmem &S, const F_ 
     return nfar;
 }
 
+// Number of sorted far items with key < wbase (the far keys are either
+// below the window or above it): two rounds of 32 probes narrow the
+// boundary instead of a pass over every item.
+template <class F_>
+__device__ __forceinline__ int far_below(const F_ &F, int n, int wbase) {
+    const int l = lane_id();
+    int lo = 0, hi = n;  // boundary in [lo, hi]
+    while (hi - lo > 32) {
+        const int step = (hi - lo + 31) / 32;
+        const int p = lo + l * step;  // probe positions lo, lo + step, ...
+        const bool below = p < hi && F.fk()[F.perm()[p]] < wbase;
+        const int c = __popc(__ballot_sync(kFull, below));  // probes below: a prefix
+        const int nlo = lo + (c > 0 ? (c - 1) * step + 1 : 0);
+        hi = min(hi, lo + c * step);
+        lo = nlo;
+    }
+    const int p = lo + l;
+    return lo + __popc(__ballot_sync(kFull, p < hi && F.fk()[F.perm()[p]] < wbase));
+}
+
 // Count pass over a sorted far list: the head of each equal-key group folds
 // the group in arrival order (the R4 chain of that key) and stores |c| (or
 // -1: not kept) in fb of the head item.  Returns kept far entries; nbelow =
@@ -587,7 +607,7 @@ __device__ __forceinline__ int emit_row(const RowArgs &a, RwSmem &S, const F_ &F
 // kCopyU rounds of loads in flight), and take the row's cut edges there (j >
 // i, part[j] != part[i]: PAPER.md:393-405) -- the part[] gathers are batched
 // with the copy instead of stalling the emission.
-constexpr int kCopyU = 4;
+constexpr int kCopyU = 3;  // 3 rounds of 32 per iteration: a config-5 row (~283 entries) is 3 iterations
 __device__ __forceinline__ void copy_staged(const RowArgs &a, const int32_t *scol, const double *sw, int n, int64_t g0,
                                             bool write, int64_t i, int32_t pi, Comp &acc, int &badp) {
     const int l = lane_id();
@@ -696,11 +716,7 @@ __global__ void __launch_bounds__(kRwThreads, RIG_RW_MINB) k_row_win(RowArgs a) 
         if constexpr (TEMP) {
             // exact row into the temporary (room f_i - len_i >= kept), one pass
             if (l == 0) nidx = (int64_t)atomicAdd(a.ticket, 1ull);
-            int nbelow = 0;
-            for (int p0 = 0; p0 < nfar; p0 += 32) {
-                const int p = p0 + l;
-                nbelow += __popc(__ballot_sync(kFull, p < nfar && F.fk()[F.perm()[p]] < wbase));
-            }
+            const int nbelow = far_below(F, nfar, wbase);
             const int64_t r = i - a.rb;
             const int64_t t0 = a.toff[r];
             const int kept = emit_row<true, false>(a, S, F, i, r, nfar, nbelow, a.tcol + t0, a.tw + t0, true, cur.pi,
@@ -712,11 +728,7 @@ __global__ void __launch_bounds__(kRwThreads, RIG_RW_MINB) k_row_win(RowArgs a) 
         } else if (staging && shared_list) {
             // one pass: fold, count and write the row into the free staging
             // slot (kept <= far items + window slots <= kRwStageCap)
-            int nbelow = 0;
-            for (int p0 = 0; p0 < nfar; p0 += 32) {
-                const int p = p0 + l;
-                nbelow += __popc(__ballot_sync(kFull, p < nfar && F.fk()[F.perm()[p]] < wbase));
-            }
+            const int nbelow = far_below(F, nfar, wbase);
             const int slot = pslot ^ 1;
             const int kept = emit_row<true, false>(a, S, F, i, idx, nfar, nbelow, stc + slot * kRwStageCap,
                                                    stw + slot * kRwStageCap, true, cur.pi, acc, badp);
