@@ -298,6 +298,43 @@ __device__ __forceinline__ bool far_sort(const F_ &F, int n, int key_bits) {
             const int e1 = bc[b], e0 = b > 0 ? bc[b - 1] : 0, sz = e1 - e0;
             if (sz > F.tmp_cap()) return false;  // the caller redoes the row with a global far list
             RIG_CHECK(e0 >= 0 && e1 <= n && sz >= 0);
+            if (sz <= 32) {
+                // the bucket in arrival order is a few ascending runs (one per
+                // column it holds keys of): an item's rank = its index in its
+                // run + for every other run, the items before it (keys < its
+                // key; <= for earlier runs: equal keys keep arrival order),
+                // found by a binary search over that run's lanes
+                const int x = l < sz ? (int)perm[e0 + l] : 0;
+                const int kx = l < sz ? fk[x] : INT_MAX;
+                const int kp = __shfl_up_sync(kFull, kx, 1);
+                const unsigned starts = __ballot_sync(kFull, l < sz && (l == 0 || kx < kp));
+                const int rs = 31 - __clz(starts & (0xffffffffu >> (31 - l)));  // my run's start
+                int rank = l - rs;
+                unsigned m = starts;
+                while (m) {
+                    const int s0 = __ffs(m) - 1;
+                    m &= m - 1;
+                    const int s1 = m ? __ffs(m) - 1 : sz;  // run [s0, s1)
+                    const bool earlier = s0 < rs;
+                    int lo = s0, hi = s1;
+#pragma unroll
+                    for (int it = 0; it < 5; ++it) {  // runs are <= 32 long
+                        const int mid = (lo + hi) >> 1;
+                        const int km = __shfl_sync(kFull, kx, mid & 31);
+                        if (lo < hi) {
+                            if (earlier ? km <= kx : km < kx)
+                                lo = mid + 1;
+                            else
+                                hi = mid;
+                        }
+                    }
+                    if (s0 != rs) rank += lo - s0;
+                }
+                __syncwarp();
+                if (l < sz) perm[e0 + rank] = (uint16_t)x;
+                __syncwarp();
+                continue;
+            }
             for (int q = l; q < sz; q += 32) tmp[q] = perm[e0 + q];
             __syncwarp();
             for (int r0 = 0; r0 < sz; r0 += 32) {
