@@ -769,9 +769,19 @@ size_t huge_scratch_bytes(int64_t nrows, int slots, bool numeric) {
 #endif
 int huge_slots_rw(int64_t nrows, int64_t n_reach, int64_t per_sm) {
     const size_t per = huge_scratch_bytes(nrows, 1, true);
-    size_t fr = 0, tot = 0;
-    cudaMemGetInfo(&fr, &tot);
-    const size_t bud = std::min(((size_t)RIG_HUGE_BUDGET_GB << 30), fr / 4 ? fr / 4 : (size_t)1);
+    // budget from the device's TOTAL memory (fixed per device): a budget that
+    // followed the current free memory would change the workspace size from
+    // build to build and defeat the workspace cache (a regrow costs ms)
+    static size_t quarter[64] = {0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64) dev = 0;
+    if (!quarter[dev]) {
+        size_t fr = 0, tot = 0;
+        cudaMemGetInfo(&fr, &tot);
+        quarter[dev] = tot / 4 ? tot / 4 : 1;
+    }
+    const size_t bud = std::min(((size_t)RIG_HUGE_BUDGET_GB << 30), quarter[dev]);
     int64_t s = std::min<int64_t>(per_sm * (int64_t)sms(), n_reach);
     s = std::min<int64_t>(s, (int64_t)(bud / (per ? per : 1)));
     return (int)std::max<int64_t>(s, 1);

@@ -129,9 +129,19 @@ __global__ void RIG_SCATTER_BOUNDS k_bucket_scatter(Csr A, int scale, double *__
         constexpr int U = RIG_SCATTER_U;  // chunks per group: their bucket atomics are in flight together
         for (int64_t g0 = lo; g0 < hi; g0 += 32 * U) {
             int kk[U], row[U], bb[U];
-            double xx[U];
+            double xx[U], av[U];
             unsigned gg[U];
             unsigned long long off[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {  // every chunk's loads first: in flight together
+                const int64_t p = g0 + 32 * u + l;
+                kk[u] = 0;
+                av[u] = 0.0;
+                if (p < hi) {
+                    kk[u] = A.ci[p];
+                    av[u] = A.v[p];
+                }
+            }
 #pragma unroll
             for (int u = 0; u < U; ++u) {
                 const int64_t c0 = g0 + 32 * u;
@@ -144,12 +154,9 @@ __global__ void RIG_SCATTER_BOUNDS k_bucket_scatter(Csr A, int scale, double *__
                 const double rn = shfl_d(nrm, row[u]), ry = shfl_d(y, row[u]);
                 const int64_t p = c0 + l;
                 const bool valid = p < hi;
-                kk[u] = 0;
                 xx[u] = 0.0;
                 if (valid) {
-                    kk[u] = A.ci[p];
-                    const double av = A.v[p];
-                    xx[u] = scale ? div_rn_fast(av, rn, ry) : av;
+                    xx[u] = scale ? div_rn_fast(av[u], rn, ry) : av[u];
                     if (scale) ahat[p] = xx[u];
                 }
                 bb[u] = valid ? (kk[u] >> shift) : -1 - l;
