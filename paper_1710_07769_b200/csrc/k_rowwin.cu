@@ -59,7 +59,10 @@ constexpr int kRwGNB = 512;          // sort buckets (global mode)
 #endif
 constexpr int kRwTcap = RIG_RW_TCAP; // units per table fill
 constexpr int kRwSmallBucket = 8;    // buckets up to this size: per-lane insertion sort
-constexpr int kRwStageCap = 512;     // entries per staging slot (>= kRwFcap + kRwW)
+constexpr int kRwStageCap = 512;     // entries per staging slot (>= kRwFcap + kRwW); slots are 128-byte aligned
+#ifndef RIG_RW_DISCARD
+#define RIG_RW_DISCARD 1
+#endif
 #ifndef RIG_RW_DEPTH
 #define RIG_RW_DEPTH 3  // fits the 56-register budget of 9 CTAs per SM
 #endif
@@ -680,6 +683,17 @@ __device__ __forceinline__ void copy_staged(const RowArgs &a, const int32_t *sco
             }
         }
     }
+#if RIG_RW_DISCARD
+    // the staged lines are dead now: drop them from L2 without a write-back
+    // (a dirty staged line would otherwise reach DRAM when evicted)
+    __syncwarp();
+    const int lc = (n * 4 + 127) / 128, lw = (n * 8 + 127) / 128;
+    for (int t = l; t < lc + lw; t += 32) {
+        const char *pl = t < lc ? reinterpret_cast<const char *>(scol) + 128 * t
+                                : reinterpret_cast<const char *>(sw) + 128 * (t - lc);
+        asm volatile("discard.global.L2 [%0], 128;" ::"l"(pl) : "memory");
+    }
+#endif
 }
 
 __device__ __forceinline__ void finish_cut(const RowArgs &a, int64_t idx, Comp &acc, int badp) {
