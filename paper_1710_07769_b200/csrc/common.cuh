@@ -409,8 +409,16 @@ struct RcArgs {
     double *diag;
     double tol;
     int fmax;              // items per row held in shared memory
+    // RANGE launch (skey != null): rows with fmax < f_i <= scap go through
+    // key ranges, staged in per-CTA slices of global scratch
+    int32_t *skey;         // [grid][2][scap]
+    double *sval;          // [grid][4][scap]
+    int64_t scap;
 };
-size_t rowcta_smem_bytes(int fmax);
+size_t rowcta_smem_bytes(int fmax, bool range);
+size_t rowcta_scratch_bytes(int64_t scap, int grid);
+int rowcta_grid(int fmax, bool range);
+int rowcta_range_fmax();  // fmax of the RANGE launch (warps x items per warp range)
 void launch_row_cta(const RcArgs &a, cudaStream_t s);
 
 // per-row cut sums -> 256 partials (fixed segments) and *used = 256

@@ -156,11 +156,14 @@ static int64_t env_i64(const char *name, int64_t dflt) {
     const char *e = getenv(name);
     return e ? atoll(e) : dflt;
 }
-// Measured on configs 4 and 6: 256 / 1280 best.  kRowCtaBigF > 0 adds a
-// second launch with large shared arrays (one CTA per SM) for the rows up to
-// it: measured slower (5120: +0.65 ms, 7168: +0.87 ms on config 4), so off.
+// Measured on configs 4 and 6: 256 / 1280 best.  Longer rows (after the
+// wide-window pass) take a second launch (k_row_cta<RANGE>, larger arrays):
+// rows beyond its arrays go through key ranges, staged in per-CTA slices of
+// global scratch of up to kLongScratchMB in all; the rows it cannot take
+// (beyond a slice, or a crowded key sub-bucket) fall to the global-far-list
+// and CTA-accumulator kernels, whose scratch is then allocated.
 static const int64_t kRowCtaMinF = env_i64("RIG_CTA_MINF", 256), kRowCtaMaxF = env_i64("RIG_CTA_MAXF", 1280),
-                     kRowCtaBigF = env_i64("RIG_CTA_BIGF", 0);
+                     kLongScratchMB = env_i64("RIG_LONG_SCRATCH_MB", 1024);
 // huge-kernel slots per SM on the row-window mixed path (each slot is O(n)
 // memory); measured 1, 2, 4, 8: 4 is as fast as 8 with half the memory
 static const int64_t kHugePerSmRw = env_i64("RIG_HUGE_PER_SM_RW", 4);
@@ -373,6 +376,9 @@ struct rig_plan {
     int rw_gcap = 0;        // its global far-list capacity (0: shared lists only)
     bool mid_rowwin = false;  // mixed path: mid rows through k_row_win (temp mode) instead of the mid passes
     void *mid_rw_scratch = nullptr;  // its global far lists + ticket
+    void *long_scratch = nullptr;    // k_row_cta<RANGE> slices (mid_rowwin, max f_i > kRowCtaMaxF)
+    int64_t long_scap = 0;
+    int long_grid = 0;
     explicit rig_plan(cudaStream_t st) : s(st), arena(st) {}
 };
 
@@ -588,7 +594,6 @@ static void plan_build(rig_plan *p, const rig_csr_t *Ain, bool allow_early = fal
     // the huge path takes the huge bin and every row the mid kernel defers (far
     // list beyond its capacity, or far keys crowding one sort bucket); with
     // short rows only the latter can happen, so a few slots suffice
-    const bool need_huge = true;
     const size_t nbc = bins_count_elems(nloc);
     Layout LB;
     const size_t o_toff = LB.add(sizeof(int64_t) * (size_t)(nloc + 1));
@@ -601,37 +606,40 @@ static void plan_build(rig_plan *p, const rig_csr_t *Ain, bool allow_early = fal
     const size_t o_tcol = LB.add(sizeof(int32_t) * (size_t)p->h.mid_slots);
     const size_t o_tw = LB.add(sizeof(double) * (size_t)p->h.mid_slots);
     // far lists of the global-far-list pass (rows that can outgrow the 768-item list)
-    const bool need_gfar = p->h.max_f > kMidBigFarCapHost;
-    const size_t o_gfar = need_gfar ? LB.add(mid_gfar_scratch_bytes()) : 0;
     // mid rows (f_i <= 2^kSymBinMaxLog / 2) through k_row_win in temp mode:
     // global far lists of that capacity, + a zeroed ticket
     p->mid_rowwin = rowwin_enabled() && csc_fits_i32(p->A);
+    const bool need_gfar = p->h.max_f > kMidBigFarCapHost;
+    const size_t o_gfar = need_gfar && !p->mid_rowwin ? LB.add(mid_gfar_scratch_bytes()) : 0;
     constexpr int kMidMaxF = 1 << (kSymBinMaxLog - 1);
     p->rw_gcap = (int)std::min<int64_t>(std::max<int64_t>(p->h.max_f, 1), kMidMaxF);
     const size_t o_mrw = p->mid_rowwin ? LB.add(256 + rowwin_scratch_bytes(p->rw_gcap)) : 0;
-    size_t o_huge = 0;
-    if (need_huge) {
-        if (p->mid_rowwin) {
-            // only rows with f_i > kRowCtaMaxF can reach the huge kernel (the
-            // row-window and CTA kernels take the rest): at most the rows of
-            // the last mid bin and the huge bin; few slots (each is O(n) memory)
-            const int64_t reach = p->h.sym_count[kNumSymBins - 1] + p->h.sym_count[kNumSymBins];
-            p->huge_slots_n = huge_slots_rw(n, std::max<int64_t>(reach, 1), kHugePerSmRw);
-        } else {
-            p->huge_slots_n = huge_slots(n, p->h.max_f > kMidSmallCap ? n_mid : std::min<int64_t>(n_mid, 8),
-                                         p->h.sym_count[kNumSymBins] > 0);
+    size_t o_huge = 0, o_long = 0;
+    if (p->mid_rowwin) {
+        // the global-far-list and huge kernels get their scratch only if rows
+        // reach them (plan_numeric, after the range launch)
+        if (p->h.max_f > kRowCtaMaxF) {
+            p->long_grid = rowcta_grid(rowcta_range_fmax(), true);
+            const int64_t per_item = (int64_t)rowcta_scratch_bytes(1, p->long_grid);
+            p->long_scap = std::min<int64_t>(p->h.max_f, (kLongScratchMB << 20) / per_item);
+            if (p->long_scap > rowcta_range_fmax()) o_long = LB.add(rowcta_scratch_bytes(p->long_scap, p->long_grid));
+            else p->long_scap = 0;
         }
+    } else {
+        p->huge_slots_n = huge_slots(n, p->h.max_f > kMidSmallCap ? n_mid : std::min<int64_t>(n_mid, 8),
+                                     p->h.sym_count[kNumSymBins] > 0);
         o_huge = LB.add(huge_scratch_bytes(n, p->huge_slots_n, true));
     }
     unsigned char *wb = p->cached ? ws_get(1, LB.bytes, s) : p->arena.raw(LB.bytes);
     p->toff = reinterpret_cast<int64_t *>(wb + o_toff);
     p->lists = reinterpret_cast<int32_t *>(wb + o_lists);
     p->defer = reinterpret_cast<int32_t *>(wb + o_defer);
-    p->gfar = need_gfar ? wb + o_gfar : nullptr;
+    p->gfar = need_gfar && !p->mid_rowwin ? wb + o_gfar : nullptr;
     p->mid_rw_scratch = p->mid_rowwin ? wb + o_mrw : nullptr;
+    p->long_scratch = p->long_scap ? wb + o_long : nullptr;
     p->tcol = reinterpret_cast<int32_t *>(wb + o_tcol);
     p->tw = reinterpret_cast<double *>(wb + o_tw);
-    if (need_huge) {
+    if (!p->mid_rowwin) {
         p->huge_scratch = wb + o_huge;
         CK(cudaMemsetAsync(p->huge_scratch, 0, huge_bitmap_bytes(n, p->huge_slots_n), s));
     }
@@ -806,49 +814,68 @@ static int64_t plan_numeric(rig_plan *p, int32_t *gcol, double *gw, double *diag
                 rc.fmax = (int)std::min<int64_t>(std::max<int64_t>(p->h.max_f, 1), kRowCtaMaxF);
                 launch_row_cta(rc, s);
                 check_launch("long rows (CTA per row)");
-                int32_t *rest2_list = rest_list;
-                int64_t *rest2_count = rest_count;
-                if (p->h.max_f > rc.fmax && kRowCtaBigF > rc.fmax) {  // longer rows: big shared arrays, 1 CTA per SM
-                    RcArgs rb2 = rc;
-                    rb2.list0 = rest_list;
-                    rb2.count0 = rest_count;
-                    rb2.list1 = nullptr;
-                    rb2.count1 = nullptr;
-                    rest2_list = p->defer + 4 * n_mid;
-                    rest2_count = reinterpret_cast<int64_t *>(ticket + 5);
-                    rb2.rest = rest2_list;
-                    rb2.rest_count = rest2_count;
-                    rb2.ticket = ticket + 4;
-                    rb2.fmax = (int)std::min<int64_t>(p->h.max_f, kRowCtaBigF);
-                    launch_row_cta(rb2, s);
-                    check_launch("long rows (CTA per row, big)");
-                }
+                // the rest: a wide-window pass (|j - i| < 2048: banded / FEM
+                // rows) ...
                 MidArgs wd = ma;
                 wd.defer_list = p->defer + 2 * n_mid;
                 wd.defer_count = p->ctr->defer_count + 2;
-                wd.list = rest2_list;
-                wd.count = rest2_count;
+                wd.list = rest_list;
+                wd.count = rest_count;
                 launch_num_mid_wide(wd, s);
-                check_launch("huge rows (wide window)");
-                MidArgs hu = ma;
-                hu.list = p->defer + 2 * n_mid;
-                hu.count = p->ctr->defer_count + 2;
-                if (p->gfar) {
-                    MidArgs gf = ma;
-                    gf.list = p->defer + 2 * n_mid;
-                    gf.count = p->ctr->defer_count + 2;
-                    gf.defer_list = p->defer + 3 * n_mid;
-                    gf.defer_count = p->ctr->defer_count + 3;
-                    gf.fscratch = p->gfar;
-                    gf.fscratch_bytes = (int64_t)mid_gfar_scratch_bytes();
-                    gf.fnm = p->fnm;
-                    launch_num_mid_gfar(gf, s);
-                    check_launch("huge rows (global far lists)");
-                    hu.list = p->defer + 3 * n_mid;
-                    hu.count = p->ctr->defer_count + 3;
+                check_launch("long rows (wide window)");
+                // ... then key ranges through the CTA kernel's larger arrays
+                int32_t *last_list = p->defer + 2 * n_mid;
+                int64_t *last_count = p->ctr->defer_count + 2;
+                if (p->long_scratch) {
+                    RcArgs rl = rc;
+                    rl.list0 = last_list;
+                    rl.count0 = last_count;
+                    rl.list1 = nullptr;
+                    rl.count1 = nullptr;
+                    last_list = p->defer + 4 * n_mid;
+                    last_count = reinterpret_cast<int64_t *>(ticket + 5);
+                    rl.rest = last_list;
+                    rl.rest_count = last_count;
+                    rl.ticket = ticket + 4;
+                    rl.fmax = rowcta_range_fmax();
+                    rl.skey = static_cast<int32_t *>(p->long_scratch);
+                    rl.sval = reinterpret_cast<double *>(rl.skey + (size_t)2 * p->long_scap * p->long_grid);
+                    rl.scap = p->long_scap;
+                    launch_row_cta(rl, s);
+                    check_launch("long rows (CTA per row, key ranges)");
                 }
-                launch_num_huge(hu, p->huge_slots_n, p->huge_scratch, s);
-                check_launch("huge rows");
+                // rows left (beyond the scratch slices or a crowded key bucket):
+                // global far lists, then the CTA accumulator kernel, with their
+                // scratch allocated now
+                HostStage *hs = host_stage();
+                CK(cudaMemcpyAsync(&hs->v[1], last_count, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+                CK(cudaStreamSynchronize(s));
+                const int64_t n_last = hs->v[1];
+                if (n_last > 0) {
+                    const int64_t n = p->A.nrows;
+                    MidArgs hu = ma;
+                    hu.list = last_list;
+                    hu.count = last_count;
+                    if (p->h.max_f > kMidBigFarCapHost) {
+                        MidArgs gf = ma;
+                        gf.list = last_list;
+                        gf.count = last_count;
+                        gf.defer_list = p->defer + 3 * n_mid;
+                        gf.defer_count = p->ctr->defer_count + 3;
+                        gf.fscratch = tmp_arena.raw(mid_gfar_scratch_bytes());
+                        gf.fscratch_bytes = (int64_t)mid_gfar_scratch_bytes();
+                        gf.fnm = p->fnm;
+                        launch_num_mid_gfar(gf, s);
+                        check_launch("long rows (global far lists)");
+                        hu.list = p->defer + 3 * n_mid;
+                        hu.count = p->ctr->defer_count + 3;
+                    }
+                    p->huge_slots_n = huge_slots_rw(n, n_last, kHugePerSmRw);
+                    p->huge_scratch = tmp_arena.raw(huge_scratch_bytes(n, p->huge_slots_n, true));
+                    CK(cudaMemsetAsync(p->huge_scratch, 0, huge_bitmap_bytes(n, p->huge_slots_n), s));
+                    launch_num_huge(hu, p->huge_slots_n, p->huge_scratch, s);
+                    check_launch("huge rows");
+                }
             } else {
             {
                 Prof pk(P_KERNEL, s);
@@ -935,7 +962,7 @@ static int64_t plan_numeric(rig_plan *p, int32_t *gcol, double *gw, double *diag
             };
             launch_copy_rows(p->lists, p->ctr->list_count, p->rb, p->toff, row_ptr_out, p->tcol, p->tw, gcol, gw,
                              co(1), s);
-            if (p->huge_scratch)
+            if (p->huge_scratch || p->h.sym_count[kNumSymBins] > 0)  // the huge bin's rows
                 launch_copy_rows(p->lists + n_mid, p->ctr->list_count + 1, p->rb, p->toff, row_ptr_out, p->tcol, p->tw,
                                  gcol, gw, co(2), s);
         }

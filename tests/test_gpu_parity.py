@@ -372,6 +372,31 @@ def test_long_scattered_rows_cta(rig, seed):
     assert_graph_equal(to_np(g3.row_ptr), to_np(g3.col_idx), to_np(g3.w), o3)
 
 
+@pytest.mark.parametrize("env", [{}, {"RIG_LONG_SCRATCH_MB": "100"}, {"RIG_LONG_SCRATCH_MB": "1"}])
+def test_long_rows_key_ranges(rig, env):
+    """Long rows of scattered columns (tests/long_rows_check.py): the CTA
+    kernel's key-range launch (crowded buckets split further), a crowded key
+    falling to the global far-list / accumulator kernels (scratch allocated
+    on demand), a shard.  With RIG_LONG_SCRATCH_MB=100 the longest rows
+    exceed the slices and fall back too; with RIG_LONG_SCRATCH_MB=1 there is
+    no range launch and every long row takes the fallback chain."""
+    if not env:
+        import long_rows_check
+
+        long_rows_check.run(0)
+        return
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    e = dict(os.environ, PYTHONPATH=os.pathsep.join([root, os.path.join(root, "tests")]), **env)
+    r = subprocess.run([sys.executable, os.path.join(root, "tests", "long_rows_check.py")], env=e, cwd=root,
+                       capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-4000:]
+    assert "long rows ok" in r.stdout
+
+
 def test_row_window_early_errors(rig):
     """The row-window path decided before the analysis (every row long):
     device errors raised by the scaling are still reported (read at the final

@@ -5,7 +5,9 @@ import csv, io, subprocess, sys
 rep, units = sys.argv[1], float(sys.argv[2]) if len(sys.argv) > 2 else 1.0
 kre = sys.argv[3] if len(sys.argv) > 3 else None
 cmd = ["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"]
-if kre:
+if kre and kre.startswith("skip="):  # select the report's n-th launch instead of a name
+    cmd += ["--launch-skip", kre[5:], "--launch-count", "1"]
+elif kre:
     cmd += ["--kernel-name", f"regex:{kre}"]
 out = subprocess.run(cmd, capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(out)))
