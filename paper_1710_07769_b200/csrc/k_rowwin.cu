@@ -139,6 +139,24 @@ struct FarG {
     }
 };
 
+// Per-lane cut sum of one row.  The terms are positive weights |c_ij|, about
+// 10 per lane on banded rows: plain summation has relative error <= 10 eps
+// per lane and 5 eps in the lane tree (finish_cut), far inside the 1e-12
+// cutsize tolerance; the per-row sums are then added with Neumaier
+// compensation (k_rowcut_partials).  RIG_RW_CUT_COMP=1: Neumaier per lane.
+#ifndef RIG_RW_CUT_COMP
+#define RIG_RW_CUT_COMP 0
+#endif
+#if RIG_RW_CUT_COMP
+using CutSum = Comp;
+#else
+struct CutSum {
+    double s = 0.0;
+    __device__ __forceinline__ void add(double x) { s += x; }
+    __device__ __forceinline__ double value() const { return s; }
+};
+#endif
+
 // ---- look-back status words: count | kAgg (count published), prefix | kPre
 constexpr unsigned long long kAgg = 1ull << 62, kPre = 2ull << 62, kValMask = (1ull << 62) - 1;
 __device__ __forceinline__ void st_relaxed(unsigned long long *p, unsigned long long v) {
@@ -362,9 +380,12 @@ __device__ __forceinline__ bool far_sort(const F_ &F, int n, int key_bits) {
     return true;
 }
 
+// 32-bit row ids and entry offsets: on this path nnz + ncols < 2^31 (CSC
+// offsets fit int32), so rows and A's entry offsets fit too -- fewer live
+// registers in the row loop (the kernel runs at 56 registers)
 struct RowMeta {
-    int64_t i = 0;       // global row id
-    int64_t s = 0, e = 0;
+    int i = 0;           // global row id
+    int s = 0, e = 0;
     int k = 0;           // lane t: column of entry t
     int cs = 0, cl = 0;  // lane t: CSC offset (sentinel layout) and length of column k
     double av = 0.0;     // lane t: a_hat_ik
@@ -374,13 +395,13 @@ struct RowMeta {
 // Row metadata in three dependent stages (row pointers; entries; column
 // bounds), issued at points of the previous row where their latency hides.
 template <bool TEMP>
-__device__ __forceinline__ void meta_rows(const RowArgs &a, int64_t idx, int64_t nrows, RowMeta &M) {
+__device__ __forceinline__ void meta_rows(const RowArgs &a, int idx, int nrows, RowMeta &M) {
     M.s = M.e = 0;
     if (idx >= nrows) return;
-    const int64_t i = TEMP ? (int64_t)a.list[idx] : a.rb + idx;  // TEMP: the mixed path's row list
+    const int i = TEMP ? a.list[idx] : (int)a.rb + idx;  // TEMP: the mixed path's row list
     if (TEMP) M.i = i;
-    M.s = a.A.rp[i];
-    M.e = a.A.rp[i + 1];
+    M.s = (int)a.A.rp[i];
+    M.e = (int)a.A.rp[i + 1];
     if (a.part) M.pi = __ldg(&a.part[i]);
 }
 __device__ __forceinline__ void meta_entries(const RowArgs &a, RowMeta &M) {
@@ -412,14 +433,14 @@ __device__ __forceinline__ void meta_cols(const RowArgs &a, RowMeta &M, bool pf)
 // Accumulate row i (window + far list).  Returns the number of far products
 // (> F.cap(): the list overflowed and is incomplete).
 template <class F_>
-__device__ __forceinline__ int accumulate(const RowArgs &a, RwSmem &S, const F_ &F, int64_t i,
+__device__ __forceinline__ int accumulate(const RowArgs &a, RwSmem &S, const F_ &F, int i,
                                           const RowMeta &M) {
     const int l = lane_id();
     const unsigned lt = lanemask_lt();
-    const int wbase = (int)i - kRwWH;
+    const int wbase = i - kRwWH;
     int nfar = 0;
-    for (int64_t bb = M.s; bb < M.e; bb += 32) {
-        const int nent = (int)min((int64_t)32, M.e - bb);
+    for (int bb = M.s; bb < M.e; bb += 32) {
+        const int nent = min(32, M.e - bb);
         int cs = 0, cl = 0;
         double av = 0.0;
         if (bb == M.s) {
@@ -569,9 +590,9 @@ __device__ __forceinline__ int far_count(const F_ &F, int n, int wbase, double t
 // group heads fold their far groups here (else far_count stored |c| / -1 in
 // fb).  Cut edges (j > i, part differs) go to acc; diag[idx] = c_ii.
 template <bool FOLD, bool CUT, class F_>
-__device__ __forceinline__ int emit_row(const RowArgs &a, RwSmem &S, const F_ &F, int64_t i, int64_t r, int n,
+__device__ __forceinline__ int emit_row(const RowArgs &a, RwSmem &S, const F_ &F, int i, int r, int n,
                                         int nbelow,
-                                        int32_t *dcol, double *dw, bool write, int32_t pi, Comp &acc, int &badp) {
+                                        int32_t *dcol, double *dw, bool write, int32_t pi, CutSum &acc, int &badp) {
     const int l = lane_id();
     const unsigned lt = lanemask_lt();
     const int wbase = (int)i - kRwWH;
@@ -611,7 +632,7 @@ __device__ __forceinline__ int emit_row(const RowArgs &a, RwSmem &S, const F_ &F
                     }
                 }
             }
-            if (cut && keep && (int64_t)key > i) {
+            if (cut && keep && key > i) {
                 const int32_t pj = __ldg(&a.part[key]);
                 badp |= (pj < 0) | (pj >= a.K);
                 if (pj != pi) acc.add(w);
@@ -649,7 +670,7 @@ __device__ __forceinline__ int emit_row(const RowArgs &a, RwSmem &S, const F_ &F
 // with the copy instead of stalling the emission.
 constexpr int kCopyU = 3;  // 3 rounds of 32 per iteration: a config-5 row (~283 entries) is 3 iterations
 __device__ __forceinline__ void copy_staged(const RowArgs &a, const int32_t *scol, const double *sw, int n, int64_t g0,
-                                            bool write, int64_t i, int32_t pi, Comp &acc, int &badp) {
+                                            bool write, int i, int32_t pi, CutSum &acc, int &badp) {
     const int l = lane_id();
     const bool cut = a.part != nullptr;
     for (int t0 = 0; t0 < n; t0 += 32 * kCopyU) {
@@ -673,7 +694,7 @@ __device__ __forceinline__ void copy_staged(const RowArgs &a, const int32_t *sco
                 __stcs(a.gw + g0 + t, w[u]);
             }
             pj[u] = pi;
-            if (cut && (int64_t)c[u] > i) pj[u] = __ldg(&a.part[c[u]]);
+            if (cut && c[u] > i) pj[u] = __ldg(&a.part[c[u]]);
         }
         if (cut) {
 #pragma unroll
@@ -696,7 +717,7 @@ __device__ __forceinline__ void copy_staged(const RowArgs &a, const int32_t *sco
 #endif
 }
 
-__device__ __forceinline__ void finish_cut(const RowArgs &a, int64_t idx, Comp &acc, int badp) {
+__device__ __forceinline__ void finish_cut(const RowArgs &a, int idx, CutSum &acc, int badp) {
     const int l = lane_id();
     double v = acc.value();  // fixed lane tree: deterministic per row
 #pragma unroll
@@ -729,12 +750,12 @@ __global__ void __launch_bounds__(kRwThreads, RIG_RW_MINB) k_row_win(RowArgs a) 
     int32_t *stc = a.stage_col + gw * 2 * kRwStageCap;
     double *stw = a.stage_w + gw * 2 * kRwStageCap;
     const bool staging = !(a.dbg & 2);
-    int64_t pidx = -1;  // staged row waiting for its offset
+    int pidx = -1;  // staged row waiting for its offset
     int pkept = 0, pslot = 0;
-    const int64_t nrows = TEMP ? *a.count_dev : a.nloc;
+    const int nrows = (int)(TEMP ? *a.count_dev : a.nloc);
     const int key_bits = a.A.nrows > 1 ? 64 - __clzll((unsigned long long)(a.A.nrows - 1)) : 1;  // keys < 2^key_bits
-    int64_t idx = 0;
-    if (l == 0) idx = (int64_t)atomicAdd(a.ticket, 1ull);
+    int idx = 0;
+    if (l == 0) idx = (int)atomicAdd(a.ticket, 1ull);
     idx = __shfl_sync(kFull, idx, 0);
     RowMeta cur, nxt;
     meta_rows<TEMP>(a, idx, nrows, cur);
@@ -746,9 +767,9 @@ __global__ void __launch_bounds__(kRwThreads, RIG_RW_MINB) k_row_win(RowArgs a) 
         if (TEMP || pidx < 0) return;
         const int64_t g0 = lookback(a.chain, pidx, pkept);
         const bool fits = g0 + pkept <= a.cap;
-        Comp acc;
+        CutSum acc;
         int badp = a.part ? ((ppi < 0) | (ppi >= a.K)) : 0;
-        copy_staged(a, stc + pslot * kRwStageCap, stw + pslot * kRwStageCap, pkept, g0, fits, a.rb + pidx, ppi, acc,
+        copy_staged(a, stc + pslot * kRwStageCap, stw + pslot * kRwStageCap, pkept, g0, fits, (int)a.rb + pidx, ppi, acc,
                     badp);
         if (a.part) finish_cut(a, pidx, acc, badp);
         if (l == 0) {
@@ -759,16 +780,16 @@ __global__ void __launch_bounds__(kRwThreads, RIG_RW_MINB) k_row_win(RowArgs a) 
         pidx = -1;
     };
     auto finish = [&](const auto &F, int nfar, bool shared_list) {
-        const int64_t i = TEMP ? cur.i : a.rb + idx;
+        const int i = TEMP ? cur.i : (int)a.rb + idx;
         const int wbase = (int)i - kRwWH;
-        Comp acc;
+        CutSum acc;
         int badp = a.part ? ((cur.pi < 0) | (cur.pi >= a.K)) : 0;
-        int64_t nidx = 0;
+        int nidx = 0;
         if constexpr (TEMP) {
             // exact row into the temporary (room f_i - len_i >= kept), one pass
-            if (l == 0) nidx = (int64_t)atomicAdd(a.ticket, 1ull);
+            if (l == 0) nidx = (int)atomicAdd(a.ticket, 1ull);
             const int nbelow = far_below(F, nfar, wbase);
-            const int64_t r = i - a.rb;
+            const int r = i - (int)a.rb;
             const int64_t t0 = a.toff[r];
             const int kept = emit_row<true, false>(a, S, F, i, r, nfar, nbelow, a.tcol + t0, a.tw + t0, true, cur.pi,
                                                    acc, badp);
@@ -788,7 +809,7 @@ __global__ void __launch_bounds__(kRwThreads, RIG_RW_MINB) k_row_win(RowArgs a) 
             // earlier would be held while this warp waits, and rows behind it
             // would wait on it); then place the previously staged row
             if (l == 0) st_relaxed(&a.chain[idx], (idx == 0 ? kPre : kAgg) | (unsigned long long)kept);
-            if (l == 0) nidx = (int64_t)atomicAdd(a.ticket, 1ull);
+            if (l == 0) nidx = (int)atomicAdd(a.ticket, 1ull);
             flush();
             pidx = idx;
             pkept = kept;
@@ -805,11 +826,11 @@ __global__ void __launch_bounds__(kRwThreads, RIG_RW_MINB) k_row_win(RowArgs a) 
                 kept += __popc(__ballot_sync(kFull, t < kRwW && t != kRwWH && fabs(S.wv[t]) > a.tol));
             }
             if (l == 0) st_relaxed(&a.chain[idx], (idx == 0 ? kPre : kAgg) | (unsigned long long)kept);
-            if (l == 0) nidx = (int64_t)atomicAdd(a.ticket, 1ull);
+            if (l == 0) nidx = (int)atomicAdd(a.ticket, 1ull);
             flush();
             nidx = __shfl_sync(kFull, nidx, 0);
             meta_rows<TEMP>(a, nidx, nrows, nxt);
-            const int64_t g0 = (a.dbg & 1) ? min(idx * 280, a.cap - 1024) : lookback(a.chain, idx, kept);
+            const int64_t g0 = (a.dbg & 1) ? min((int64_t)idx * 280, a.cap - 1024) : lookback(a.chain, idx, kept);
             const bool fits = g0 + kept <= a.cap;
             emit_row<false, true>(a, S, F, i, idx, nfar, nbelow, a.gcol + g0, a.gw + g0, fits, cur.pi, acc, badp);
             if (l == 0) {
@@ -825,13 +846,13 @@ __global__ void __launch_bounds__(kRwThreads, RIG_RW_MINB) k_row_win(RowArgs a) 
         return nidx;
     };
     while (idx < nrows) {
-        const int64_t i = TEMP ? cur.i : a.rb + idx;
+        const int i = TEMP ? cur.i : (int)a.rb + idx;
         if (TEMP && a.fskip_list && a.fnm[i - a.rb] + (cur.e - cur.s) > a.fskip) {
             // long row: left to the CTA-per-row kernel
-            int64_t nidx = 0;
+            int nidx = 0;
             if (l == 0) {
                 a.fskip_list[atomicAdd((unsigned long long *)a.fskip_count, 1ull)] = (int32_t)i;
-                nidx = (int64_t)atomicAdd(a.ticket, 1ull);
+                nidx = (int)atomicAdd(a.ticket, 1ull);
             }
             nidx = __shfl_sync(kFull, nidx, 0);
             meta_rows<TEMP>(a, nidx, nrows, nxt);
@@ -867,7 +888,7 @@ __global__ void __launch_bounds__(kRwThreads, RIG_RW_MINB) k_row_win(RowArgs a) 
                 global = true;
             }
         }
-        int64_t nidx;
+        int nidx;
         if (!global) {
             nidx = finish(FS, nfar, true);
         } else {
