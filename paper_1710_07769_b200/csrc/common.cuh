@@ -134,6 +134,7 @@ int num_sms();
 // ---------------------------------------------------------------- kernels
 // k_prep.cu
 void launch_validate(const Csr &A, int *err, cudaStream_t s);
+void launch_part_check(const int32_t *part, int64_t n, int32_t K, int *bad, cudaStream_t s);
 void launch_col_hist(const Csr &A, unsigned *cnt, unsigned *rank /*nullable*/, cudaStream_t s,
                      const int *guard = nullptr);
 // k_transpose.cu: bucketed a1 + a2 (see there for the CSC layout with sentinels)
@@ -236,6 +237,17 @@ struct Comp {
     __device__ __forceinline__ double value() const { return s + c; }
 };
 
+// Per-lane cut sum inside the fused numeric kernels.  The terms are positive
+// weights |c_ij| (no cancellation), a few to a few hundred per lane: plain
+// summation has relative error <= (terms) * eps, far inside the 1e-12
+// cutsize tolerance; the per-lane / per-row sums are then combined in fixed
+// trees and Neumaier-compensated segments (deterministic).
+struct CutSum {
+    double s = 0.0;
+    __device__ __forceinline__ void add(double x) { s += x; }
+    __device__ __forceinline__ double value() const { return s; }
+};
+
 // Sum of one double per thread over the CTA in a fixed tree order; thread 0
 // gets the result.  All threads must call it.
 template <int NT>
@@ -288,6 +300,7 @@ void launch_analyze_sym(const SymArgs &a, uint8_t *bin8, DevCounters *ctr, cudaS
 // maxlen: longest A row on the merge path in the shard (DevCounters::max_len)
 void launch_sym_merge(const SymArgs &a, int maxlen, cudaStream_t s);
 void launch_num_merge(const NumArgs &a, int maxlen, cudaStream_t s);
+
 // Rows off the merge path (k_midrow.cu, k_spgemm.cu huge path): each row is
 // written with its exact kept entries to a temporary at toff[r] and
 // cnt[r] = kept + 1 (the graph scan subtracts the diagonal slot); k_copy_rows
@@ -461,5 +474,63 @@ void launch_coarse_rows(int pass, const int64_t *rp, const int32_t *col, const i
                         const int32_t *cmap, const int32_t *lead, int64_t nc, int64_t *ccnt, const int64_t *crp,
                         int32_t *ccol, int64_t *cw, uint64_t *gscratch, int64_t gcap, int big_warps,
                         cudaStream_t s);
+
+// ---- decoupled look-back over per-item status words (row-window rows):
+// count | kAgg (count published), prefix | kPre
+constexpr unsigned long long kAgg = 1ull << 62, kPre = 2ull << 62, kValMask = (1ull << 62) - 1;
+__device__ __forceinline__ void st_relaxed(unsigned long long *p, unsigned long long v) {
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;\n" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_relaxed(const unsigned long long *p) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];\n" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
+// Exclusive prefix of row idx's count; idx's own status is already published
+// (kAgg, or kPre for idx 0).  All lanes call it; lane 0 publishes idx's
+// inclusive prefix.  Every lower ticket is held by a running warp, which
+// publishes its count without waiting on anything: the walk ends.
+__device__ __forceinline__ int64_t lookback(unsigned long long *chain, int64_t idx, int64_t c) {
+    const int l = lane_id();
+    if (idx == 0) return 0;
+    int64_t excl = 0;
+    int64_t base = idx - 1;
+    while (true) {
+        const int64_t j = base - l;
+        unsigned long long v = j >= 0 ? ld_relaxed(&chain[j]) : kPre;
+        unsigned zm = __ballot_sync(kFull, (v >> 62) == 0);
+        unsigned pm = __ballot_sync(kFull, (v & kPre) != 0);
+        // wait for the nearest unpublished predecessor that is needed (one
+        // lane polls one word with backoff: no polling storm on the
+        // frontier's cache lines), then look at the window again
+        while (true) {
+            const int fp = pm ? __ffs(pm) - 1 : 31;
+            const unsigned need = fp == 31 ? kFull : ((2u << fp) - 1u);
+            const unsigned wz = zm & need;
+            if (!wz) break;
+            const int t = __ffs(wz) - 1;
+            if (l == t) {
+                unsigned ns = 64;
+                do {
+                    __nanosleep(ns);
+                    ns = ns < 2048 ? ns * 2 : 2048;
+                    v = ld_relaxed(&chain[j]);
+                } while ((v >> 62) == 0);
+            }
+            __syncwarp();
+            zm = __ballot_sync(kFull, (v >> 62) == 0);
+            pm = __ballot_sync(kFull, (v & kPre) != 0);
+        }
+        const int fp = pm ? __ffs(pm) - 1 : 31;
+        const unsigned need = fp == 31 ? kFull : ((2u << fp) - 1u);
+        const int64_t add = ((need >> l) & 1u) ? (int64_t)(v & kValMask) : 0;
+        excl += warp_sum(add);
+        if (pm) break;
+        base -= 32;
+    }
+    if (l == 0) st_relaxed(&chain[idx], kPre | (unsigned long long)(excl + c));
+    return excl;
+}
 
 }  // namespace rig

@@ -46,6 +46,26 @@ void launch_validate(const Csr &A, int *err, cudaStream_t s) {
     note_launch();
 }
 
+// Partition ids (a7): every part[v], v < n, in [0, K) -- the oracle's check
+// (orc_cutsize) -- else *bad = 1 and the fused cut becomes NaN.  One read of
+// part[] up front, so the fused numeric kernels gather part[j] unchecked.
+__global__ void k_part_check(const int32_t *__restrict__ part, int64_t n, int32_t K, int *bad) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    int b = 0;
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += stride) {
+        const int32_t x = part[v];
+        b |= (x < 0) | (x >= K);
+    }
+    if (__syncthreads_or(b) && threadIdx.x == 0) atomicOr(bad, 1);
+}
+
+void launch_part_check(const int32_t *part, int64_t n, int32_t K, int *bad, cudaStream_t s) {
+    if (n <= 0) return;
+    const int64_t g = std::min<int64_t>((n + 255) / 256, (int64_t)num_sms() * 8);
+    k_part_check<<<(unsigned)g, 256, 0, s>>>(part, n, K, bad);
+    note_launch();
+}
+
 // ------------------------------------------------------------------ a2 (histogram)
 // Column counts; with `rank`, also each entry's arrival slot in its column
 // (the returned old count), so the scatter needs no atomics.

@@ -304,11 +304,31 @@ __device__ int rc_warp_range(const RcArgs &a, const RcWarp &W, const int32_t *gk
                              double *ow) {
     const int l = lane_id();
     const unsigned lt = lanemask_lt();
-    for (int p = l; p < m; p += 32) {
-        W.k0[p] = (unsigned)(gk[p] - klo);
-        W.x0[p] = (uint16_t)p;
-        W.ia[p] = ga[p];
-        W.ib[p] = gb[p];
+    constexpr int U = 4;  // rounds per step: their global loads in flight together
+    for (int p0 = l; p0 < m; p0 += 32 * U) {
+        int kk[U];
+        double xa[U], xb[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int p = p0 + 32 * u;
+            kk[u] = 0;
+            xa[u] = xb[u] = 0.0;
+            if (p < m) {
+                kk[u] = gk[p];
+                xa[u] = ga[p];
+                xb[u] = gb[p];
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int p = p0 + 32 * u;
+            if (p < m) {
+                W.k0[p] = (unsigned)(kk[u] - klo);
+                W.x0[p] = (uint16_t)p;
+                W.ia[p] = xa[u];
+                W.ib[p] = xb[u];
+            }
+        }
     }
     __syncwarp();
     unsigned *kin = W.k0, *kout = W.k1;
@@ -464,42 +484,55 @@ __device__ __noinline__ bool rc_range_row(const RcArgs &a, const RcSmem &S, int6
     for (int b = tid; b < kRcWarps * kRcBins; b += kRcThreads) S.hist[b] = 0;
     __syncthreads();
     unsigned *hw = S.hist + w * kRcBins;
-    for (int p0 = w0; p0 < w1; p0 += 32) {
-        const int p = p0 + l;
-        int dg = kRcBins + l;
-        if (p < w1) {
-            const int k = gk0[p];
-            if (k != (int)i) dg = k >> bsh;
+    constexpr int U = 4;  // rounds per step: their global loads in flight together
+    for (int p00 = w0; p00 < w1; p00 += 32 * U) {
+        int kk[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int p = p00 + 32 * u + l;
+            kk[u] = p < w1 ? gk0[p] : -1;
         }
-        const unsigned g = __match_any_sync(kFull, dg);
-        if (dg < kRcBins && (g & lt) == 0) hw[dg] += __popc(g);
-        __syncwarp();
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int dg = (kk[u] >= 0 && kk[u] != (int)i) ? kk[u] >> bsh : kRcBins + l;
+            const unsigned g = __match_any_sync(kFull, dg);
+            if (dg < kRcBins && (g & lt) == 0) hw[dg] += __popc(g);
+            __syncwarp();
+        }
     }
     __syncthreads();
     int start;
     const int bcnt = rc_offsets(S.hist, S.ws, &start);
     S.bst[tid] = start;
     if (tid == kRcThreads - 1) S.bst[kRcBins] = start + bcnt;
-    for (int p0 = w0; p0 < w1; p0 += 32) {
-        const int p = p0 + l;
-        int k = 0, dg = kRcBins + l;
-        double x = 0.0, y = 0.0;
-        if (p < w1) {
-            k = gk0[p];
-            if (k != (int)i) dg = k >> bsh;
-            x = ga0[p];
-            y = gb0[p];
+    for (int p00 = w0; p00 < w1; p00 += 32 * U) {
+        int kk[U];
+        double xx[U], yy[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int p = p00 + 32 * u + l;
+            kk[u] = -1;
+            xx[u] = yy[u] = 0.0;
+            if (p < w1) {
+                kk[u] = gk0[p];
+                xx[u] = ga0[p];
+                yy[u] = gb0[p];
+            }
         }
-        const unsigned g = __match_any_sync(kFull, dg);
-        if (dg < kRcBins) {
-            const int pos = (int)hw[dg] + __popc(g & lt);
-            gk1[pos] = k;
-            ga1[pos] = x;
-            gb1[pos] = y;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int dg = (kk[u] >= 0 && kk[u] != (int)i) ? kk[u] >> bsh : kRcBins + l;
+            const unsigned g = __match_any_sync(kFull, dg);
+            if (dg < kRcBins) {
+                const int pos = (int)hw[dg] + __popc(g & lt);
+                gk1[pos] = kk[u];
+                ga1[pos] = xx[u];
+                gb1[pos] = yy[u];
+            }
+            __syncwarp();
+            if (dg < kRcBins && (g & lt) == 0) hw[dg] += __popc(g);
+            __syncwarp();
         }
-        __syncwarp();
-        if (dg < kRcBins && (g & lt) == 0) hw[dg] += __popc(g);
-        __syncwarp();
     }
     __syncthreads();
     // ---- 3. ranges of consecutive buckets (in parallel, bucket per thread):

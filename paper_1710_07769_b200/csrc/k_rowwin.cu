@@ -139,80 +139,13 @@ struct FarG {
     }
 };
 
-// Per-lane cut sum of one row.  The terms are positive weights |c_ij|, about
-// 10 per lane on banded rows: plain summation has relative error <= 10 eps
-// per lane and 5 eps in the lane tree (finish_cut), far inside the 1e-12
-// cutsize tolerance; the per-row sums are then added with Neumaier
-// compensation (k_rowcut_partials).  RIG_RW_CUT_COMP=1: Neumaier per lane.
-#ifndef RIG_RW_CUT_COMP
-#define RIG_RW_CUT_COMP 0
-#endif
+// Cut sums: CutSum (common.cuh), plain per-lane sums of positive weights;
+// RIG_RW_CUT_COMP=1: Neumaier per lane instead.
 #if RIG_RW_CUT_COMP
-using CutSum = Comp;
-#else
-struct CutSum {
-    double s = 0.0;
-    __device__ __forceinline__ void add(double x) { s += x; }
-    __device__ __forceinline__ double value() const { return s; }
-};
+#define CutSum Comp
 #endif
 
-// ---- look-back status words: count | kAgg (count published), prefix | kPre
-constexpr unsigned long long kAgg = 1ull << 62, kPre = 2ull << 62, kValMask = (1ull << 62) - 1;
-__device__ __forceinline__ void st_relaxed(unsigned long long *p, unsigned long long v) {
-    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;\n" ::"l"(p), "l"(v) : "memory");
-}
-__device__ __forceinline__ unsigned long long ld_relaxed(const unsigned long long *p) {
-    unsigned long long v;
-    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];\n" : "=l"(v) : "l"(p) : "memory");
-    return v;
-}
-
-// Exclusive prefix of row idx's count; idx's own status is already published
-// (kAgg, or kPre for idx 0).  All lanes call it; lane 0 publishes idx's
-// inclusive prefix.  Every lower ticket is held by a running warp, which
-// publishes its count without waiting on anything: the walk ends.
-__device__ __forceinline__ int64_t lookback(unsigned long long *chain, int64_t idx, int64_t c) {
-    const int l = lane_id();
-    if (idx == 0) return 0;
-    int64_t excl = 0;
-    int64_t base = idx - 1;
-    while (true) {
-        const int64_t j = base - l;
-        unsigned long long v = j >= 0 ? ld_relaxed(&chain[j]) : kPre;
-        unsigned zm = __ballot_sync(kFull, (v >> 62) == 0);
-        unsigned pm = __ballot_sync(kFull, (v & kPre) != 0);
-        // wait for the nearest unpublished predecessor that is needed (one
-        // lane polls one word with backoff: no polling storm on the
-        // frontier's cache lines), then look at the window again
-        while (true) {
-            const int fp = pm ? __ffs(pm) - 1 : 31;
-            const unsigned need = fp == 31 ? kFull : ((2u << fp) - 1u);
-            const unsigned wz = zm & need;
-            if (!wz) break;
-            const int t = __ffs(wz) - 1;
-            if (l == t) {
-                unsigned ns = 64;
-                do {
-                    __nanosleep(ns);
-                    ns = ns < 2048 ? ns * 2 : 2048;
-                    v = ld_relaxed(&chain[j]);
-                } while ((v >> 62) == 0);
-            }
-            __syncwarp();
-            zm = __ballot_sync(kFull, (v >> 62) == 0);
-            pm = __ballot_sync(kFull, (v & kPre) != 0);
-        }
-        const int fp = pm ? __ffs(pm) - 1 : 31;
-        const unsigned need = fp == 31 ? kFull : ((2u << fp) - 1u);
-        const int64_t add = ((need >> l) & 1u) ? (int64_t)(v & kValMask) : 0;
-        excl += warp_sum(add);
-        if (pm) break;
-        base -= 32;
-    }
-    if (l == 0) st_relaxed(&chain[idx], kPre | (unsigned long long)(excl + c));
-    return excl;
-}
+// look-back status words and lookback(): common.cuh
 
 // Stable sort of the n far items by key: F.perm()[sorted position] = item
 // (items are numbered in arrival order).  Value buckets (monotone fp32 map of
@@ -592,7 +525,7 @@ __device__ __forceinline__ int far_count(const F_ &F, int n, int wbase, double t
 template <bool FOLD, bool CUT, class F_>
 __device__ __forceinline__ int emit_row(const RowArgs &a, RwSmem &S, const F_ &F, int i, int r, int n,
                                         int nbelow,
-                                        int32_t *dcol, double *dw, bool write, int32_t pi, CutSum &acc, int &badp) {
+                                        int32_t *dcol, double *dw, bool write, int32_t pi, CutSum &acc) {
     const int l = lane_id();
     const unsigned lt = lanemask_lt();
     const int wbase = (int)i - kRwWH;
@@ -634,7 +567,6 @@ __device__ __forceinline__ int emit_row(const RowArgs &a, RwSmem &S, const F_ &F
             }
             if (cut && keep && key > i) {
                 const int32_t pj = __ldg(&a.part[key]);
-                badp |= (pj < 0) | (pj >= a.K);
                 if (pj != pi) acc.add(w);
             }
             put(keep, key, w);
@@ -655,7 +587,6 @@ __device__ __forceinline__ int emit_row(const RowArgs &a, RwSmem &S, const F_ &F
         const bool keep = t < kRwW && t != kRwWH && w > a.tol;
         if (cut && keep && t > kRwWH) {
             const int32_t pj = __ldg(&a.part[key]);
-            badp |= (pj < 0) | (pj >= a.K);
             if (pj != pi) acc.add(w);
         }
         put(keep, key, w);
@@ -670,9 +601,10 @@ __device__ __forceinline__ int emit_row(const RowArgs &a, RwSmem &S, const F_ &F
 // with the copy instead of stalling the emission.
 constexpr int kCopyU = 3;  // 3 rounds of 32 per iteration: a config-5 row (~283 entries) is 3 iterations
 __device__ __forceinline__ void copy_staged(const RowArgs &a, const int32_t *scol, const double *sw, int n, int64_t g0,
-                                            bool write, int i, int32_t pi, CutSum &acc, int &badp) {
+                                            bool write, int i, int32_t pi, CutSum &acc) {
     const int l = lane_id();
     const bool cut = a.part != nullptr;
+#pragma unroll 1
     for (int t0 = 0; t0 < n; t0 += 32 * kCopyU) {
         int32_t c[kCopyU], pj[kCopyU];
         double w[kCopyU];
@@ -699,7 +631,6 @@ __device__ __forceinline__ void copy_staged(const RowArgs &a, const int32_t *sco
         if (cut) {
 #pragma unroll
             for (int u = 0; u < kCopyU; ++u) {
-                badp |= (pj[u] < 0) | (pj[u] >= a.K);
                 if (pj[u] != pi) acc.add(w[u]);
             }
         }
@@ -717,13 +648,13 @@ __device__ __forceinline__ void copy_staged(const RowArgs &a, const int32_t *sco
 #endif
 }
 
-__device__ __forceinline__ void finish_cut(const RowArgs &a, int idx, CutSum &acc, int badp) {
+// part[] ids were range-checked up front (k_part_check): no check here
+__device__ __forceinline__ void finish_cut(const RowArgs &a, int idx, CutSum &acc) {
     const int l = lane_id();
     double v = acc.value();  // fixed lane tree: deterministic per row
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(kFull, v, off);
     if (l == 0) a.cutrow[idx] = v;
-    if (__any_sync(kFull, badp) && l == 0) atomicOr(a.bad_part, 1);
 }
 
 #ifndef RIG_RW_MINB
@@ -768,10 +699,8 @@ __global__ void __launch_bounds__(kRwThreads, RIG_RW_MINB) k_row_win(RowArgs a) 
         const int64_t g0 = lookback(a.chain, pidx, pkept);
         const bool fits = g0 + pkept <= a.cap;
         CutSum acc;
-        int badp = a.part ? ((ppi < 0) | (ppi >= a.K)) : 0;
-        copy_staged(a, stc + pslot * kRwStageCap, stw + pslot * kRwStageCap, pkept, g0, fits, (int)a.rb + pidx, ppi, acc,
-                    badp);
-        if (a.part) finish_cut(a, pidx, acc, badp);
+        copy_staged(a, stc + pslot * kRwStageCap, stw + pslot * kRwStageCap, pkept, g0, fits, (int)a.rb + pidx, ppi, acc);
+        if (a.part) finish_cut(a, pidx, acc);
         if (l == 0) {
             a.row_ptr[pidx + 1] = g0 + pkept;
             if (pidx == 0) a.row_ptr[0] = 0;
@@ -783,7 +712,6 @@ __global__ void __launch_bounds__(kRwThreads, RIG_RW_MINB) k_row_win(RowArgs a) 
         const int i = TEMP ? cur.i : (int)a.rb + idx;
         const int wbase = (int)i - kRwWH;
         CutSum acc;
-        int badp = a.part ? ((cur.pi < 0) | (cur.pi >= a.K)) : 0;
         int nidx = 0;
         if constexpr (TEMP) {
             // exact row into the temporary (room f_i - len_i >= kept), one pass
@@ -792,7 +720,7 @@ __global__ void __launch_bounds__(kRwThreads, RIG_RW_MINB) k_row_win(RowArgs a) 
             const int r = i - (int)a.rb;
             const int64_t t0 = a.toff[r];
             const int kept = emit_row<true, false>(a, S, F, i, r, nfar, nbelow, a.tcol + t0, a.tw + t0, true, cur.pi,
-                                                   acc, badp);
+                                                   acc);
             RIG_CHECK(kept <= a.toff[r + 1] - a.toff[r]);
             if (l == 0) a.cnt[r] = kept + 1;  // the graph scan subtracts the diagonal slot
             nidx = __shfl_sync(kFull, nidx, 0);
@@ -803,7 +731,7 @@ __global__ void __launch_bounds__(kRwThreads, RIG_RW_MINB) k_row_win(RowArgs a) 
             const int nbelow = far_below(F, nfar, wbase);
             const int slot = pslot ^ 1;
             const int kept = emit_row<true, false>(a, S, F, i, idx, nfar, nbelow, stc + slot * kRwStageCap,
-                                                   stw + slot * kRwStageCap, true, cur.pi, acc, badp);
+                                                   stw + slot * kRwStageCap, true, cur.pi, acc);
             RIG_CHECK(kept <= kRwStageCap);
             // publish the count; take the next ticket now (a ticket taken
             // earlier would be held while this warp waits, and rows behind it
@@ -832,13 +760,13 @@ __global__ void __launch_bounds__(kRwThreads, RIG_RW_MINB) k_row_win(RowArgs a) 
             meta_rows<TEMP>(a, nidx, nrows, nxt);
             const int64_t g0 = (a.dbg & 1) ? min((int64_t)idx * 280, a.cap - 1024) : lookback(a.chain, idx, kept);
             const bool fits = g0 + kept <= a.cap;
-            emit_row<false, true>(a, S, F, i, idx, nfar, nbelow, a.gcol + g0, a.gw + g0, fits, cur.pi, acc, badp);
+            emit_row<false, true>(a, S, F, i, idx, nfar, nbelow, a.gcol + g0, a.gw + g0, fits, cur.pi, acc);
             if (l == 0) {
                 a.row_ptr[idx + 1] = g0 + kept;
                 if (idx == 0) a.row_ptr[0] = 0;
                 if (!fits) atomicOr(a.overflow, 1);
             }
-            if (a.part) finish_cut(a, idx, acc, badp);
+            if (a.part) finish_cut(a, idx, acc);
         }
         meta_entries(a, nxt);
         meta_cols(a, nxt, !(a.dbg & 4));

@@ -69,7 +69,7 @@ __device__ __forceinline__ int64_t sym_merge_row(const Csr &A, const Csc &T, int
 // With a.part set, kept edges (i,j), j > i, part[j] != pi also go to `cut`.
 template <int R, typename IdxT>
 __device__ __forceinline__ void num_merge_row(const NumArgs &a, int64_t i, int64_t r, int64_t s, int32_t *oc,
-                                              double *ow, int64_t ub, Comp &cut, int32_t pi, int &badp) {
+                                              double *ow, int64_t ub, CutSum &cut, int32_t pi) {
     int32_t h[R];
     IdxT q[R];
     double av[R], hv[R];
@@ -127,7 +127,6 @@ __device__ __forceinline__ void num_merge_row(const NumArgs &a, int64_t i, int64
                 ow[o] = w;
                 ++o;
                 if (a.part && (int64_t)m > i) {
-                    badp |= (pend_pj < 0) | (pend_pj >= a.K);
                     if (pend_pj != pi) cut.add(pend_w);
                     pend_pj = a.part[m];
                     pend_w = w;
@@ -136,7 +135,6 @@ __device__ __forceinline__ void num_merge_row(const NumArgs &a, int64_t i, int64
         }
     }
     if (a.part) {
-        badp |= (pend_pj < 0) | (pend_pj >= a.K);
         if (pend_pj != pi) cut.add(pend_w);
     }
     if (o < ub) {
@@ -186,8 +184,7 @@ __global__ void __launch_bounds__(kMergeThreads) k_num_merge(NumArgs a) {
     int32_t *st_cp = reinterpret_cast<int32_t *>(merge_smem + (size_t)kMergeWarps * cap * sizeof(double)) + (size_t)w * cap;
     const int64_t nloc = a.re - a.rb;
     const int64_t ntiles = (nloc + 31) / 32;
-    Comp cut;
-    int badp = 0;
+    CutSum cut;
     for (int64_t tile = (int64_t)blockIdx.x * kMergeWarps + w; tile < ntiles;
          tile += (int64_t)gridDim.x * kMergeWarps) {
         const int64_t r0 = tile * 32;
@@ -206,20 +203,19 @@ __global__ void __launch_bounds__(kMergeThreads) k_num_merge(NumArgs a) {
             int32_t pi = 0;
             if (a.part) {
                 pi = a.part[i];
-                badp |= (pi < 0) | (pi >= a.K);
             }
             switch (len) {
                 case 0:
                     if (a.diag) a.diag[r] = 0.0;
                     break;
-                case 1: num_merge_row<1, IdxT>(a, i, r, s, oc, ow, ub, cut, pi, badp); break;
-                case 2: num_merge_row<2, IdxT>(a, i, r, s, oc, ow, ub, cut, pi, badp); break;
-                case 3: num_merge_row<3, IdxT>(a, i, r, s, oc, ow, ub, cut, pi, badp); break;
-                case 4: num_merge_row<4, IdxT>(a, i, r, s, oc, ow, ub, cut, pi, badp); break;
-                case 5: if constexpr (RMAX >= 5) num_merge_row<5, IdxT>(a, i, r, s, oc, ow, ub, cut, pi, badp); break;
-                case 6: if constexpr (RMAX >= 6) num_merge_row<6, IdxT>(a, i, r, s, oc, ow, ub, cut, pi, badp); break;
-                case 7: if constexpr (RMAX >= 7) num_merge_row<7, IdxT>(a, i, r, s, oc, ow, ub, cut, pi, badp); break;
-                case 8: if constexpr (RMAX >= 8) num_merge_row<8, IdxT>(a, i, r, s, oc, ow, ub, cut, pi, badp); break;
+                case 1: num_merge_row<1, IdxT>(a, i, r, s, oc, ow, ub, cut, pi); break;
+                case 2: num_merge_row<2, IdxT>(a, i, r, s, oc, ow, ub, cut, pi); break;
+                case 3: num_merge_row<3, IdxT>(a, i, r, s, oc, ow, ub, cut, pi); break;
+                case 4: num_merge_row<4, IdxT>(a, i, r, s, oc, ow, ub, cut, pi); break;
+                case 5: if constexpr (RMAX >= 5) num_merge_row<5, IdxT>(a, i, r, s, oc, ow, ub, cut, pi); break;
+                case 6: if constexpr (RMAX >= 6) num_merge_row<6, IdxT>(a, i, r, s, oc, ow, ub, cut, pi); break;
+                case 7: if constexpr (RMAX >= 7) num_merge_row<7, IdxT>(a, i, r, s, oc, ow, ub, cut, pi); break;
+                case 8: if constexpr (RMAX >= 8) num_merge_row<8, IdxT>(a, i, r, s, oc, ow, ub, cut, pi); break;
                 default: break;
             }
         }
@@ -238,7 +234,6 @@ __global__ void __launch_bounds__(kMergeThreads) k_num_merge(NumArgs a) {
             a.cutp[blockIdx.x] = v;
             if (blockIdx.x == 0) *a.cut_used = (int)gridDim.x;
         }
-        if (__syncthreads_or(badp) && threadIdx.x == 0) atomicOr(a.bad_part, 1);
     }
 }
 
@@ -308,13 +303,23 @@ __device__ __forceinline__ int tree_min(const int (&h)[N]) {
 #ifndef RIG_PAIR_LOOKAHEAD
 #define RIG_PAIR_LOOKAHEAD 0  // measured: 1 (next key loaded one advance ahead) is 2-5 % slower on configs 2-3
 #endif
+// Output of a half row: the swizzled shared stage (tile index e, stepping +-1).
+struct OutStage {
+    unsigned oc0, ow0, e, step;
+    __device__ __forceinline__ void put(int j, double w) {
+        const unsigned x = out_swz(e);
+        sts_s32(oc0 + 4 * x, j);
+        sts_f64(ow0 + 8 * x, w);
+        e += step;
+    }
+};
 // One half row.  q0[t]: CSC position of run t's first (ascending) or last
 // (descending) entry, or -1 for an empty run (t >= len).  Kept entries go to
-// the swizzled output stage at tile index ob, ob +- 1, ...  Returns the count.
-template <int R>
+// `out` in the lane's direction.  CUT: the descending lane's kept edges
+// (j > i) with part[j] != pi go to `cut`.  Returns the count.
+template <int R, bool CUT = true, class Out>
 __device__ __forceinline__ int pair_half_row(const NumArgs &a, bool desc, int64_t i, int64_t r, const int *q0,
-                                             const double *av0, unsigned oc0, unsigned ow0, unsigned ob, Comp &cut,
-                                             int32_t pi, int &badp) {
+                                             const double *av0, Out &out, CutSum &cut, int32_t pi) {
     int h[R], q[R];
     double av[R], hv[R];
 #if RIG_PAIR_LOOKAHEAD
@@ -341,8 +346,7 @@ __device__ __forceinline__ int pair_half_row(const NumArgs &a, bool desc, int64_
         }
     }
     const int ik = (int)i ^ xm;
-    unsigned oe = ob;
-    const unsigned ostep = desc ? 0xffffffffu : 1u;
+    const bool cut_on = CUT && desc && a.part;
     int o = 0;
     int32_t pend_pj = pi;
     double pend_w = 0.0;
@@ -372,33 +376,28 @@ __device__ __forceinline__ int pair_half_row(const NumArgs &a, bool desc, int64_
         const double w = fabs(acc);
         if (w > a.tol) {
             const int j = m ^ xm;
-            const unsigned e = out_swz(oe);
-            sts_s32(oc0 + 4 * e, j);
-            sts_f64(ow0 + 8 * e, w);
-            oe += ostep;
+            out.put(j, w);
             ++o;
-            if (desc && a.part) {  // j > i: each undirected edge counted once
-                badp |= (pend_pj < 0) | (pend_pj >= a.K);
+            if (cut_on) {  // j > i: each undirected edge counted once
                 if (pend_pj != pi) cut.add(pend_w);
                 pend_pj = a.part[j];
                 pend_w = w;
             }
         }
     }
-    if (desc && a.part) {
-        badp |= (pend_pj < 0) | (pend_pj >= a.K);
+    if (cut_on) {
         if (pend_pj != pi) cut.add(pend_w);
     }
     return o;
 }
 
-template <int RMAX>
+template <int RMAX, bool CUT = true, class Out>
 __device__ __forceinline__ int pair_half_row_r(int len, const NumArgs &a, bool desc, int64_t i, int64_t r,
-                                               const int *q0, const double *av0, unsigned oc0, unsigned ow0,
-                                               unsigned ob, Comp &cut, int32_t pi, int &badp) {
-    if (len <= 2) return pair_half_row<2>(a, desc, i, r, q0, av0, oc0, ow0, ob, cut, pi, badp);
-    if (RMAX > 4 && len <= 4) return pair_half_row<4>(a, desc, i, r, q0, av0, oc0, ow0, ob, cut, pi, badp);
-    return pair_half_row<RMAX>(a, desc, i, r, q0, av0, oc0, ow0, ob, cut, pi, badp);
+                                               const int *q0, const double *av0, Out &out, CutSum &cut,
+                                               int32_t pi) {
+    if (len <= 2) return pair_half_row<2, CUT>(a, desc, i, r, q0, av0, out, cut, pi);
+    if (RMAX > 4 && len <= 4) return pair_half_row<4, CUT>(a, desc, i, r, q0, av0, out, cut, pi);
+    return pair_half_row<RMAX, CUT>(a, desc, i, r, q0, av0, out, cut, pi);
 }
 
 // Rows whose output does not fit the stage are merged by num_merge_row with
@@ -416,8 +415,7 @@ __global__ void RIG_PAIR_BOUNDS k_num_pair(NumArgs a) {
     const unsigned oc0 = smem_u32(st_cp), ow0 = smem_u32(st_wp);
     const int64_t nloc = a.re - a.rb;
     const int64_t ntiles = (nloc + kPairRows - 1) / kPairRows;
-    Comp cut;
-    int badp = 0;
+    CutSum cut;
     for (int64_t tile = (int64_t)blockIdx.x * kPairWarps + w; tile < ntiles; tile += (int64_t)gridDim.x * kPairWarps) {
         const int64_t r0 = tile * kPairRows;
         const int rows = (int)min((int64_t)kPairRows, nloc - r0);
@@ -439,7 +437,6 @@ __global__ void RIG_PAIR_BOUNDS k_num_pair(NumArgs a) {
             ub = a.gptr[r + 1] - gr;
             if (a.part) {
                 pi = a.part[i];
-                badp |= (pi < 0) | (pi >= a.K);
             }
         }
         // the row's runs and values, loaded before the merge-row test (run 0's
@@ -459,19 +456,20 @@ __global__ void RIG_PAIR_BOUNDS k_num_pair(NumArgs a) {
         int o = 0;
         if (mrow && staged) {
             const unsigned ob = (unsigned)(gr - g0) + (desc ? (unsigned)(ub - 1) : 0u);
-            o = pair_half_row_r<RMAX>(len, a, desc, i, r, qv, av, oc0, ow0, ob, cut, pi, badp);
+            OutStage out{oc0, ow0, ob, desc ? 0xffffffffu : 1u};
+            o = pair_half_row_r<RMAX>(len, a, desc, i, r, qv, av, out, cut, pi);
         } else if (mrow && !desc) {  // output beyond the stage: direct global stores
             int32_t *oc = a.gcol + gr;
             double *ow = a.gw + gr;
             switch (len) {
-                case 1: num_merge_row<1, int32_t>(a, i, r, s, oc, ow, ub, cut, pi, badp); break;
-                case 2: num_merge_row<2, int32_t>(a, i, r, s, oc, ow, ub, cut, pi, badp); break;
-                case 3: num_merge_row<3, int32_t>(a, i, r, s, oc, ow, ub, cut, pi, badp); break;
-                case 4: num_merge_row<4, int32_t>(a, i, r, s, oc, ow, ub, cut, pi, badp); break;
-                case 5: if constexpr (RMAX >= 5) num_merge_row<5, int32_t>(a, i, r, s, oc, ow, ub, cut, pi, badp); break;
-                case 6: if constexpr (RMAX >= 6) num_merge_row<6, int32_t>(a, i, r, s, oc, ow, ub, cut, pi, badp); break;
-                case 7: if constexpr (RMAX >= 7) num_merge_row<7, int32_t>(a, i, r, s, oc, ow, ub, cut, pi, badp); break;
-                case 8: if constexpr (RMAX >= 8) num_merge_row<8, int32_t>(a, i, r, s, oc, ow, ub, cut, pi, badp); break;
+                case 1: num_merge_row<1, int32_t>(a, i, r, s, oc, ow, ub, cut, pi); break;
+                case 2: num_merge_row<2, int32_t>(a, i, r, s, oc, ow, ub, cut, pi); break;
+                case 3: num_merge_row<3, int32_t>(a, i, r, s, oc, ow, ub, cut, pi); break;
+                case 4: num_merge_row<4, int32_t>(a, i, r, s, oc, ow, ub, cut, pi); break;
+                case 5: if constexpr (RMAX >= 5) num_merge_row<5, int32_t>(a, i, r, s, oc, ow, ub, cut, pi); break;
+                case 6: if constexpr (RMAX >= 6) num_merge_row<6, int32_t>(a, i, r, s, oc, ow, ub, cut, pi); break;
+                case 7: if constexpr (RMAX >= 7) num_merge_row<7, int32_t>(a, i, r, s, oc, ow, ub, cut, pi); break;
+                case 8: if constexpr (RMAX >= 8) num_merge_row<8, int32_t>(a, i, r, s, oc, ow, ub, cut, pi); break;
                 default: break;
             }
         } else if (qr < rows && len == 0 && !desc) {
@@ -508,7 +506,6 @@ __global__ void RIG_PAIR_BOUNDS k_num_pair(NumArgs a) {
             a.cutp[blockIdx.x] = v;
             if (blockIdx.x == 0) *a.cut_used = (int)gridDim.x;
         }
-        if (__syncthreads_or(badp) && threadIdx.x == 0) atomicOr(a.bad_part, 1);
     }
 }
 

@@ -744,6 +744,9 @@ static int64_t plan_numeric(rig_plan *p, int32_t *gcol, double *gw, double *diag
     double *cutp = cut ? reinterpret_cast<double *>(wn + o_cutp) : nullptr;
     double *dg = (p->flags & RIG_FLAG_DIAG) ? diag : nullptr;
     const int64_t n_mid = p->h.n_mid;
+    // a7's partition ids range-checked once (the fused kernels gather part[j]
+    // unchecked); an id outside [0, K) makes the cut NaN (launch_cut_final)
+    if (cut) launch_part_check(cut->part, p->A.nrows, cut->K, badp, s);
     if (p->rowwin) {
         t_last_path = "rowwin";
         return rowwin_numeric(p, gcol, gw, cap, dg, row_ptr_out, wn, holes_d, used, cutp, cut);
