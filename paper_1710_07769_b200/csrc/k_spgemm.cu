@@ -707,6 +707,13 @@ static void launch_pair_t(const NumArgs &na, cudaStream_t s) {
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_num_pair<RMAX>, kPairThreads, smem);
     if (per_sm < 1) per_sm = 1;
+    // resident CTAs per SM (grid-stride kernel): RIG_PAIR_CTAS caps them
+    // (measured: capping below the occupancy limit is slower on configs 2-4)
+    static const int cap_sm = [] {
+        const char *e = getenv("RIG_PAIR_CTAS");
+        return e ? atoi(e) : 0;
+    }();
+    if (cap_sm > 0 && per_sm > cap_sm) per_sm = cap_sm;
     const int64_t nloc = na.re - na.rb;
     const int64_t ntiles = (nloc + kPairRows - 1) / kPairRows;
     int64_t g = (ntiles + kPairWarps - 1) / kPairWarps;
