@@ -400,6 +400,7 @@ int rowwin_grid();
 size_t rowwin_scratch_bytes(int gcap);
 size_t rowwin_stage_entries();
 int rowwin_max_gcap();
+int64_t rowwin_max_rows();
 void launch_row_win(const RowArgs &a, cudaStream_t s);
 // k_rowcta.cu: CTA per row (shared-memory expand / stable radix sort / fold)
 // for long rows of scattered columns, temp mode like the mid-row kernels.

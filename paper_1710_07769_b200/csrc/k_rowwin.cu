@@ -67,6 +67,10 @@ constexpr int kRwStageCap = 512;     // entries per staging slot (>= kRwFcap + k
 #define RIG_RW_DEPTH 3  // fits the 56-register budget of 9 CTAs per SM
 #endif
 constexpr int kRwDepth = RIG_RW_DEPTH;  // units in flight
+// shared far items: the unit (< 2^kFarPack table slots) packed under the key
+constexpr int kFarPack = 6;
+static_assert(kRwTcap + 2 * kRwDepth <= (1 << kFarPack), "unit ids must fit kFarPack bits");
+constexpr int64_t kRowWinMaxRows = int64_t{1} << (31 - kFarPack);  // packed keys fit int32
 
 struct RwSmem {
     double wv[kRwW];      // window (every access is guarded by t < kRwW)
@@ -74,13 +78,12 @@ struct RwSmem {
     // units: padded up to a multiple of kRwDepth, plus kRwDepth look-ahead slots
     double ta[kRwTcap + 2 * kRwDepth];  // unit: a_ik
     int2 tcs[kRwTcap + 2 * kRwDepth];   // unit: (CSC offset of its first lane, lane count); tmp of the bucket rank
-    int fk[kRwFcap];      // far: key j
+    int fk[kRwFcap];      // far: key j << kFarPack | unit (a_ik = ta[unit]); rows < 2^25 on this path
     int bc[kRwNB];        // bucket cursors / ends
     unsigned bad[kRwNB / 32];
     int nbad;
     int badlist[32];
     uint16_t perm[kRwFcap];
-    uint8_t fu[kRwFcap];  // far: unit (a_ik = ta[unit])
 };
 
 // far list storage: shared memory (FarS, one batch of <= 32 entries and
@@ -89,12 +92,13 @@ struct RwSmem {
 struct FarS {
     RwSmem *S;
     static constexpr int nb = kRwNB;
+    static constexpr int pack = kFarPack;  // raw = key << pack | unit: ordered by (key, unit) = (key, arrival)
     __device__ __forceinline__ int cap() const { return kRwFcap; }
-    __device__ __forceinline__ double a(int x) const { return S->ta[S->fu[x]]; }
+    __device__ __forceinline__ double a(int x) const { return S->ta[S->fk[x] & ((1 << kFarPack) - 1)]; }
+    __device__ __forceinline__ int key(int x) const { return S->fk[x] >> kFarPack; }
     __device__ __forceinline__ void put(int pos, int j, double b, double, int u) const {
-        S->fk[pos] = j;
+        S->fk[pos] = (j << kFarPack) | u;
         S->fb[pos] = b;
-        S->fu[pos] = (uint8_t)u;
     }
     __device__ __forceinline__ double *fb() const { return S->fb; }
     __device__ __forceinline__ int *fk() const { return S->fk; }
@@ -118,6 +122,7 @@ struct FarG {
     unsigned char *base;
     int gcap;
     static constexpr int nb = kRwGNB;
+    static constexpr int pack = 0;  // raw = key
     __device__ __forceinline__ int cap() const { return gcap; }
     __device__ __forceinline__ double *fa() const { return reinterpret_cast<double *>(base); }
     __device__ __forceinline__ double *fb() const { return fa() + gcap; }
@@ -132,6 +137,7 @@ struct FarG {
     __device__ __forceinline__ int nbad_get() const { return *reinterpret_cast<volatile int *>(nbad_ptr()); }
     __device__ __forceinline__ int *badlist() const { return nbad_ptr() + 1; }
     __device__ __forceinline__ double a(int x) const { return fa()[x]; }
+    __device__ __forceinline__ int key(int x) const { return fk()[x]; }
     __device__ __forceinline__ void put(int pos, int j, double b, double at, int) const {
         fk()[pos] = j;
         fb()[pos] = b;
@@ -148,7 +154,8 @@ struct FarG {
 // look-back status words and lookback(): common.cuh
 
 // Stable sort of the n far items by key: F.perm()[sorted position] = item
-// (items are numbered in arrival order).  Value buckets (monotone fp32 map of
+// (items are numbered in arrival order).  Sorts the raw values fk[] (key <<
+// F_::pack | unit in the shared list: unique, ordered by (key, arrival)).  Value buckets (monotone fp32 map of
 // key - min) filled in arrival order; each lane insertion-sorts its own
 // buckets of <= kRwSmallBucket items; a longer bucket found out of order is
 // ranked by (key, arrival) by the whole warp.
@@ -161,9 +168,10 @@ __device__ __forceinline__ bool far_sort(const F_ &F, int n, int key_bits) {
     static_assert((1 << NBB) == NB, "NB must be a power of two in [64, 1024]");
     int *fk = F.fk(), *bc = F.bc();
     uint16_t *perm = F.perm();
-    // fixed-width value buckets over [0, 2^key_bits) (keys are row ids):
+    // fixed-width value buckets over [0, 2^raw_bits) (keys are row ids):
     // monotone in the key, no min / max pass
-    const int sh = key_bits > NBB ? key_bits - NBB : 0;
+    const int raw_bits = key_bits + F_::pack;
+    const int sh = raw_bits > NBB ? raw_bits - NBB : 0;
     auto bucket = [&](int k) { return k >> sh; };
 #pragma unroll
     for (int u = 0; u < PER; ++u) bc[l * PER + u] = 0;
@@ -470,14 +478,14 @@ __device__ __forceinline__ int far_below(const F_ &F, int n, int wbase) {
     while (hi - lo > 32) {
         const int step = (hi - lo + 31) / 32;
         const int p = lo + l * step;  // probe positions lo, lo + step, ...
-        const bool below = p < hi && F.fk()[F.perm()[p]] < wbase;
+        const bool below = p < hi && F.key(F.perm()[p]) < wbase;
         const int c = __popc(__ballot_sync(kFull, below));  // probes below: a prefix
         const int nlo = lo + (c > 0 ? (c - 1) * step + 1 : 0);
         hi = min(hi, lo + c * step);
         lo = nlo;
     }
     const int p = lo + l;
-    return lo + __popc(__ballot_sync(kFull, p < hi && F.fk()[F.perm()[p]] < wbase));
+    return lo + __popc(__ballot_sync(kFull, p < hi && F.key(F.perm()[p]) < wbase));
 }
 
 // Count pass over a sorted far list: the head of each equal-key group folds
@@ -489,7 +497,6 @@ __device__ __forceinline__ int far_count(const F_ &F, int n, int wbase, double t
     const int l = lane_id();
     int kept = 0;
     nbelow = 0;
-    const int *fk = F.fk();
     const uint16_t *perm = F.perm();
     double *fb = F.fb();
     for (int p0 = 0; p0 < n; p0 += 32) {
@@ -497,13 +504,13 @@ __device__ __forceinline__ int far_count(const F_ &F, int n, int wbase, double t
         bool keep = false, below = false;
         if (p < n) {
             const int x = perm[p];
-            const int key = fk[x];
+            const int key = F.key(x);
             below = key < wbase;
-            if (p == 0 || fk[perm[p - 1]] != key) {
+            if (p == 0 || F.key(perm[p - 1]) != key) {
                 double acc = __fma_rn(F.a(x), fb[x], +0.0);
                 for (int q = p + 1; q < n; ++q) {
                     const int y = perm[q];
-                    if (fk[y] != key) break;
+                    if (F.key(y) != key) break;
                     acc = __fma_rn(F.a(y), fb[y], acc);
                 }
                 const double w = fabs(acc);
@@ -548,13 +555,13 @@ __device__ __forceinline__ int emit_row(const RowArgs &a, RwSmem &S, const F_ &F
             double w = 0.0;
             if (p < f1) {
                 const int x = F.perm()[p];
-                key = F.fk()[x];
-                if (p == 0 || F.fk()[F.perm()[p - 1]] != key) {
+                key = F.key(x);
+                if (p == 0 || F.key(F.perm()[p - 1]) != key) {
                     if (FOLD) {
                         double c = __fma_rn(F.a(x), F.fb()[x], +0.0);
                         for (int q = p + 1; q < n; ++q) {  // the group, in arrival order
                             const int y = F.perm()[q];
-                            if (F.fk()[y] != key) break;
+                            if (F.key(y) != key) break;
                             c = __fma_rn(F.a(y), F.fb()[y], c);
                         }
                         w = fabs(c);
@@ -872,6 +879,7 @@ int rowwin_grid() { return num_sms() * rowwin_ctas_per_sm(); }
 size_t rowwin_scratch_bytes(int gcap) { return (size_t)rowwin_grid() * kRwWarps * rw_slice_bytes(gcap); }
 size_t rowwin_stage_entries() { return (size_t)rowwin_grid() * kRwWarps * 2 * kRwStageCap; }
 int rowwin_max_gcap() { return 65535; }  // perm entries are 16-bit
+int64_t rowwin_max_rows() { return kRowWinMaxRows; }  // packed far keys (key << kFarPack | unit) fit int32
 
 void launch_row_win(const RowArgs &a, cudaStream_t s) {
     const size_t smem = (size_t)kRwWarps * sizeof(RwSmem);

@@ -167,7 +167,13 @@ static const int64_t kRowCtaMinF = env_i64("RIG_CTA_MINF", 256), kRowCtaMaxF = e
 // huge-kernel slots per SM on the row-window mixed path (each slot is O(n)
 // memory); measured 1, 2, 4, 8: 4 is as fast as 8 with half the memory
 static const int64_t kHugePerSmRw = env_i64("RIG_HUGE_PER_SM_RW", 4);
-static bool rowwin_enabled() {
+static bool rowwin_enabled_env();
+// the row-window kernel (row-window and mixed paths) needs int32 CSC offsets
+// and row ids below 2^25 (its shared far list packs the unit under the key)
+static bool rowwin_ok(const Csr &A) {
+    return rowwin_enabled_env() && csc_fits_i32(A) && A.nrows <= rowwin_max_rows();
+}
+static bool rowwin_enabled_env() {
     static int v = -1;
     if (v < 0) {
         const char *e = getenv("RIG_ROWWIN");
@@ -529,7 +535,7 @@ static void plan_build(rig_plan *p, const rig_csr_t *Ain, bool allow_early = fal
     }
     // a3 + a4 (merge rows): products, merge-row nnzC, paths of the others
     p->qs = use_qs ? reinterpret_cast<int2 *>(ws + o_qs) : nullptr;
-    if (ev_shape && rowwin_enabled() && csc_fits_i32(p->A)) {
+    if (ev_shape && rowwin_ok(p->A)) {
         // row-window path decided from the shape statistics alone (read back
         // while the transpose runs): every row longer than the merge path
         // takes, and f_i <= max_row * max_col small enough.  No analysis and
@@ -583,8 +589,7 @@ static void plan_build(rig_plan *p, const rig_csr_t *Ain, bool allow_early = fal
     p->nnz_upper = p->h.products - p->h.nnz_rows;
     const int64_t n_mid = p->h.n_mid;
     if (n_mid == 0) return;
-    if (n_mid == nloc && rowwin_enabled() && p->h.max_f <= kRowWinMaxF &&
-        csc_fits_i32(p->A)) {
+    if (n_mid == nloc && rowwin_ok(p->A) && p->h.max_f <= kRowWinMaxF) {
         p->rowwin = true;  // every row in one kernel, placed by look-back
         p->rw_gcap = (int)std::max<int64_t>(p->h.max_f, 1);  // global far lists: rows beyond the shared list
         return;
@@ -608,7 +613,7 @@ static void plan_build(rig_plan *p, const rig_csr_t *Ain, bool allow_early = fal
     // far lists of the global-far-list pass (rows that can outgrow the 768-item list)
     // mid rows (f_i <= 2^kSymBinMaxLog / 2) through k_row_win in temp mode:
     // global far lists of that capacity, + a zeroed ticket
-    p->mid_rowwin = rowwin_enabled() && csc_fits_i32(p->A);
+    p->mid_rowwin = rowwin_ok(p->A);
     const bool need_gfar = p->h.max_f > kMidBigFarCapHost;
     const size_t o_gfar = need_gfar && !p->mid_rowwin ? LB.add(mid_gfar_scratch_bytes()) : 0;
     constexpr int kMidMaxF = 1 << (kSymBinMaxLog - 1);

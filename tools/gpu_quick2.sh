@@ -1,0 +1,7 @@
+# Build, selected GPU parity tests ($TESTK), bench of $CONFIGS (10 steps).
+python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1 || { tail gpurun_out/build.log; exit 1; }
+timeout 900 python -m pytest tests -m gpu -x -q ${TESTK:+-k "$TESTK"} > gpurun_out/gputests.log 2>&1; tail -2 gpurun_out/gputests.log
+for c in ${CONFIGS:-5}; do
+  timeout 300 python bench.py --config $c --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/bench_c$c.json 2> gpurun_out/bench_c$c.err
+  python tools/bench_table.py gpurun_out/bench_c$c.json
+done
