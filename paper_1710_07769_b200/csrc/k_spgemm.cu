@@ -300,6 +300,9 @@ __device__ __forceinline__ int tree_min(const int (&h)[N]) {
     return v[0];
 }
 
+#ifndef RIG_PAIR_WARP_DISPATCH
+#define RIG_PAIR_WARP_DISPATCH 1  // measured: configs 2-4 numeric 3-5 % faster than per-lane widths
+#endif
 #ifndef RIG_PAIR_LOOKAHEAD
 #define RIG_PAIR_LOOKAHEAD 0  // measured: 1 (next key loaded one advance ahead) is 2-5 % slower on configs 2-3
 #endif
@@ -454,10 +457,18 @@ __global__ void RIG_PAIR_BOUNDS k_num_pair(NumArgs a) {
             }
         }
         int o = 0;
+#if RIG_PAIR_WARP_DISPATCH
+        // merge width chosen per warp (the tile's longest merge row): one
+        // instantiation runs, instead of the lanes of different widths
+        // running theirs one after another (mixed lengths: power-law rows)
+        const int wlen = (int)__reduce_max_sync(kFull, (unsigned)((mrow && staged) ? len : 0));
+#else
+        const int wlen = len;
+#endif
         if (mrow && staged) {
             const unsigned ob = (unsigned)(gr - g0) + (desc ? (unsigned)(ub - 1) : 0u);
             OutStage out{oc0, ow0, ob, desc ? 0xffffffffu : 1u};
-            o = pair_half_row_r<RMAX>(len, a, desc, i, r, qv, av, out, cut, pi);
+            o = pair_half_row_r<RMAX>(wlen, a, desc, i, r, qv, av, out, cut, pi);
         } else if (mrow && !desc) {  // output beyond the stage: direct global stores
             int32_t *oc = a.gcol + gr;
             double *ow = a.gw + gr;
