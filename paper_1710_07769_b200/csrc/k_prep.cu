@@ -88,8 +88,58 @@ __global__ void k_col_hist(const int32_t *__restrict__ ci, int64_t nnz, unsigned
     }
 }
 
+// Column counts without ranks, privatised: each CTA counts a chunk of
+// kHistChunk consecutive entries into a shared window of kHistWin columns
+// starting just below the chunk's first column (banded / stencil rows keep
+// most columns near the row index, so most entries stay on chip), entries
+// outside the window go straight to global atomics, and the window's
+// non-zero bins are added to the global counts once.  Counts are sums:
+// the result does not depend on the order.
+constexpr int kHistThreads = 256, kHistWin = 2048, kHistChunk = 4096, kHistSlack = 64;
+__global__ void __launch_bounds__(kHistThreads) k_col_hist_win(const int32_t *__restrict__ ci, int64_t nnz,
+                                                                int64_t ncols, unsigned *cnt, const int *guard) {
+    if (guard_skip(guard)) return;
+    __shared__ unsigned h[kHistWin];
+    const int64_t nch = (nnz + kHistChunk - 1) / kHistChunk;
+    for (int64_t c = blockIdx.x; c < nch; c += gridDim.x) {
+        const int64_t e0 = c * kHistChunk, e1 = min(nnz, e0 + kHistChunk);
+        for (int t = threadIdx.x; t < kHistWin; t += kHistThreads) h[t] = 0u;
+        const int64_t base = max((int64_t)0, (int64_t)__ldg(&ci[e0]) - kHistSlack);
+        __syncthreads();
+        for (int64_t p0 = e0 + threadIdx.x; p0 < e1; p0 += 4 * kHistThreads) {  // 4 loads in flight
+            int k[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int64_t p = p0 + (int64_t)u * kHistThreads;
+                k[u] = p < e1 ? __ldcs(&ci[p]) : -1;
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                if (k[u] < 0) continue;
+                const int64_t d = (int64_t)k[u] - base;
+                if (d >= 0 && d < kHistWin)
+                    atomicAdd(&h[d], 1u);
+                else
+                    atomicAdd(&cnt[k[u]], 1u);
+            }
+        }
+        __syncthreads();
+        for (int t = threadIdx.x; t < kHistWin; t += kHistThreads) {
+            const unsigned v = h[t];
+            if (v && base + t < ncols) atomicAdd(&cnt[base + t], v);
+        }
+        __syncthreads();
+    }
+}
+
 void launch_col_hist(const Csr &A, unsigned *cnt, unsigned *rank, cudaStream_t s, const int *guard) {
-    k_col_hist<<<grid_for(A.nnz, 256, 16), 256, 0, s>>>(A.ci, A.nnz, cnt, rank, guard);
+    if (rank) {
+        k_col_hist<<<grid_for(A.nnz, 256, 16), 256, 0, s>>>(A.ci, A.nnz, cnt, rank, guard);
+    } else {
+        const int64_t nch = (A.nnz + kHistChunk - 1) / kHistChunk;
+        const int64_t g = std::min<int64_t>(nch, (int64_t)num_sms() * 16);
+        k_col_hist_win<<<(unsigned)std::max<int64_t>(g, 1), kHistThreads, 0, s>>>(A.ci, A.nnz, A.ncols, cnt, guard);
+    }
     note_launch();
 }
 
