@@ -331,6 +331,47 @@ def test_row_window_path(rig, seed):
         plan.destroy()
 
 
+@pytest.mark.parametrize("kind", ["rowwin", "merge"])
+def test_cut_partition_runs(rig, kind):
+    """The fused kernels skip the part[] gather of edges (i, j) with i < j <
+    pnext[i] (same block; k_part_next): partitions whose runs end exactly at
+    chunk edges (4096 rows), span several chunks, alternate every row, one
+    block for all rows (K = 1, cut 0), a single boundary at the last row, and
+    random ids -- the cut vs the oracle on 20000 rows through the row-window
+    kernel (banded rows) and the merge kernel (5-point stencil rows)."""
+    rng = np.random.default_rng(4242)
+    n = 20000
+    rows, cols = [], []
+    for r in range(n):
+        if kind == "rowwin":
+            off = rng.choice(np.r_[-40:0, 1:41], 12, replace=False)  # every row > 8 entries
+            cc = np.unique(np.concatenate([[r], (r + off) % n, rng.integers(0, n, 2)]))
+        else:
+            cc = np.unique([(r + d) % n for d in (-100, -1, 0, 1, 100)])
+        rows += [r] * cc.size; cols += list(cc)
+    rp, ci, v = from_triplets(n, n, np.array(rows), np.array(cols), rng.uniform(-1, 1, len(rows)))
+    A = rig.CSR(rp, ci, v)
+    orc = oracle.build(rp, ci, v, scale_rows=1, drop_tol=0.0)
+    idx = np.arange(n)
+    parts = {
+        "chunk_edges": (idx // 4096, 5),
+        "long_runs": (idx // 9000, 3),
+        "alternate": (idx % 2, 2),
+        "one_block": (np.zeros(n, np.int64), 1),
+        "last_row": ((idx == n - 1).astype(np.int64), 2),
+        "runs_of_7": ((idx // 7) % 4, 4),
+        "random": (rng.integers(0, 16, n), 16),
+    }
+    for name, (pt, K) in parts.items():
+        part = pt.astype(np.int32)
+        ocut = oracle.cutsize(orc.row_ptr, orc.col, orc.w, part, K)[0]
+        _, cut = rig.rig_build_cut(A, torch.as_tensor(part, device="cuda"), K, 0, n, 1, 0.0)
+        assert rig.last_path() == kind, name
+        assert abs(cut.item() - ocut) <= REL * max(ocut, 1e-300), name
+        if K == 1:
+            assert cut.item() == 0.0
+
+
 @pytest.mark.parametrize("seed", range(2))
 def test_long_scattered_rows_cta(rig, seed):
     """Mixed path: short merge rows plus rows of 20..150 scattered columns
