@@ -333,9 +333,8 @@ def test_row_window_path(rig, seed):
 
 @pytest.mark.parametrize("kind", ["rowwin", "merge"])
 def test_cut_partition_runs(rig, kind):
-    """The fused kernels skip the part[] gather of edges (i, j) with i < j <
-    pnext[i] (same block; k_part_next): partitions whose runs end exactly at
-    chunk edges (4096 rows), span several chunks, alternate every row, one
+    """The fused cut under partitions of every run structure: runs ending at
+    4096-row edges, spanning several thousand rows, alternating every row, one
     block for all rows (K = 1, cut 0), a single boundary at the last row, and
     random ids -- the cut vs the oracle on 20000 rows through the row-window
     kernel (banded rows) and the merge kernel (5-point stencil rows)."""
