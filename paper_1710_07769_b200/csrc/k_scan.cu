@@ -304,8 +304,33 @@ void scan_u32_shape(const unsigned *in, int64_t n, int64_t *out, void *tmp, DevC
     int64_t *ts = static_cast<int64_t *>(tmp);
     k_tile_sum<unsigned><<<(unsigned)ntiles, kScanThreads, 0, s>>>(in, n, ScanOp::Identity, ts,
                                                                     ShapeOut{ctr, rp, rb, re}, guard);
-    cudaMemcpyAsync(host_copy, ctr, sizeof(DevCounters), cudaMemcpyDeviceToHost, s);
-    cudaEventRecord(ready, s);
+    // the statistics go to the host from a side stream (per thread and
+    // device), so the build's stream never waits on the PCIe round trip; the
+    // host reads only the shape fields, which nothing on `s` writes again
+    // before the host has waited on `ready`
+    struct Side {
+        int dev = -1;
+        cudaStream_t st = nullptr;
+        cudaEvent_t done = nullptr;
+    };
+    static thread_local Side side[8];
+    int dev = 0;
+    cudaGetDevice(&dev);
+    Side *sd = dev >= 0 && dev < 8 ? &side[dev] : nullptr;
+    if (sd && !sd->st) {
+        if (cudaStreamCreateWithFlags(&sd->st, cudaStreamNonBlocking) != cudaSuccess ||
+            cudaEventCreateWithFlags(&sd->done, cudaEventDisableTiming) != cudaSuccess)
+            sd->st = nullptr;
+    }
+    if (sd && sd->st) {
+        cudaEventRecord(sd->done, s);
+        cudaStreamWaitEvent(sd->st, sd->done, 0);
+        cudaMemcpyAsync(host_copy, ctr, sizeof(DevCounters), cudaMemcpyDeviceToHost, sd->st);
+        cudaEventRecord(ready, sd->st);
+    } else {
+        cudaMemcpyAsync(host_copy, ctr, sizeof(DevCounters), cudaMemcpyDeviceToHost, s);
+        cudaEventRecord(ready, s);
+    }
     k_tile_scan<unsigned><<<(unsigned)ntiles, kScanThreads, 0, s>>>(in, n, ScanOp::Identity, ts, ntiles, out, guard);
     note_launch(2);
 }
