@@ -415,6 +415,8 @@ struct RcArgs {
     int32_t *rest;         // rows with f_i > fmax (for the huge-row chain)
     int64_t *rest_count;
     unsigned long long *ticket;  // zeroed
+    unsigned long long *ticket2; // zeroed, or null: one round (else the rows with f_i > bigf go first)
+    int64_t bigf;
     const int64_t *fnm;    // [nloc] f_i - len_i
     const int64_t *toff;
     int32_t *tcol;

@@ -624,10 +624,6 @@ __device__ __noinline__ bool rc_range_row(const RcArgs &a, const RcSmem &S, int6
     return true;
 }
 
-#ifndef RIG_RC_BIGF
-#define RIG_RC_BIGF 4096  // measured: 2048 / 4096 / 8192 / 16384, 4096 best on configs 4 and 6
-#endif
-constexpr int64_t kRcBigF = RIG_RC_BIGF;  // RANGE launch: rows with more products start first
 #ifndef RIG_RC_MINB
 #define RIG_RC_MINB 2
 #endif
@@ -639,12 +635,12 @@ __global__ void __launch_bounds__(kRcThreads, RANGE ? RIG_RC_MINB : 1) k_row_cta
     const int tid = threadIdx.x;
     const int64_t n0 = *a.count0, n1 = a.list1 ? *a.count1 : 0;
     const int passes = rc_passes(a.A.nrows);
-    // RANGE launch: two rounds over the list, the rows beyond kRcBigF first
-    // (longest work first: a long row started last would hold the launch's
-    // tail), a ticket each (a.ticket[0], a.ticket[2])
-    for (int round = 0; round < (RANGE ? 2 : 1); ++round)
+    // with ticket2: two rounds over the list, the rows beyond bigf products
+    // first (longest work first: a long row started last would hold the
+    // launch's tail), a ticket each
+    for (int round = 0; round < (a.ticket2 ? 2 : 1); ++round)
     for (;;) {
-        if (tid == 0) S.misc[0] = (int64_t)atomicAdd(a.ticket + 2 * round, 1ull);
+        if (tid == 0) S.misc[0] = (int64_t)atomicAdd(round ? a.ticket2 : a.ticket, 1ull);
         __syncthreads();
         const int64_t t = S.misc[0];
         __syncthreads();
@@ -653,7 +649,7 @@ __global__ void __launch_bounds__(kRcThreads, RANGE ? RIG_RC_MINB : 1) k_row_cta
         const int64_t r = i - a.rb;
         const int64_t s = a.A.rp[i], e = a.A.rp[i + 1];
         const int64_t f = a.fnm[r] + (e - s);
-        if (RANGE && ((f > kRcBigF) != (round == 0))) continue;
+        if (a.ticket2 && ((f > a.bigf) != (round == 0))) continue;
         if (f > F) {
             const bool done = RANGE && f <= a.scap && rc_range_row(a, S, i, r, s, e, (int)f);
             if (!done && tid == 0) a.rest[atomicAdd((unsigned long long *)a.rest_count, 1ull)] = (int32_t)i;

@@ -164,6 +164,10 @@ static int64_t env_i64(const char *name, int64_t dflt) {
 // and CTA-accumulator kernels, whose scratch is then allocated.
 static const int64_t kRowCtaMinF = env_i64("RIG_CTA_MINF", 256), kRowCtaMaxF = env_i64("RIG_CTA_MAXF", 1280),
                      kLongScratchMB = env_i64("RIG_LONG_SCRATCH_MB", 1024);
+// longest rows first in the CTA-per-row launches (two rounds over the list):
+// the shared-memory launch (0: one round) and the key-range launch
+// (measured on configs 4 and 6: 4096 best of 2048-16384 for the latter)
+static const int64_t kRowCtaBigF0 = env_i64("RIG_CTA_BIGF0", 0), kRowCtaBigF1 = env_i64("RIG_CTA_BIGF1", 4096);
 // huge-kernel slots per SM on the row-window mixed path (each slot is O(n)
 // memory); measured 1, 2, 4, 8: 4 is as fast as 8 with half the memory
 static const int64_t kHugePerSmRw = env_i64("RIG_HUGE_PER_SM_RW", 4);
@@ -820,6 +824,8 @@ static int64_t plan_numeric(rig_plan *p, int32_t *gcol, double *gw, double *diag
                 rc.diag = dg;
                 rc.tol = p->tol;
                 rc.fmax = (int)std::min<int64_t>(std::max<int64_t>(p->h.max_f, 1), kRowCtaMaxF);
+                rc.ticket2 = kRowCtaBigF0 > 0 ? ticket + 7 : nullptr;  // longest rows first
+                rc.bigf = kRowCtaBigF0;
                 launch_row_cta(rc, s);
                 check_launch("long rows (CTA per row)");
                 // the rest: a wide-window pass (|j - i| < 2048: banded / FEM
@@ -845,6 +851,8 @@ static int64_t plan_numeric(rig_plan *p, int32_t *gcol, double *gw, double *diag
                     rl.rest = last_list;
                     rl.rest_count = last_count;
                     rl.ticket = ticket + 4;
+                    rl.ticket2 = ticket + 6;  // rows beyond kRowCtaBigF1 products first
+                    rl.bigf = kRowCtaBigF1;
                     rl.fmax = rowcta_range_fmax();
                     rl.skey = static_cast<int32_t *>(p->long_scratch);
                     rl.sval = reinterpret_cast<double *>(rl.skey + (size_t)2 * p->long_scap * p->long_grid);
