@@ -12,6 +12,8 @@ for c in 1 2 3 4 5 6 7; do
 done
 timeout 900 python bench.py > gpurun_out/bench_default.json 2> gpurun_out/bench_default.err
 timeout 900 python bench.py --impl reference --steps 5 --warmup 1 > gpurun_out/bench_reference.json 2> gpurun_out/bench_reference.err
+# the N > 1 bench path (row shards + allreduce) with 2 ranks sharing the one GPU (gloo): a path check, not a number
+BENCH_SHARE_GPU=1 BENCH_DIST_BACKEND=gloo timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29533 bench.py --gpus 2 --config 2 --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/bench_2ranks_shared.json 2> gpurun_out/bench_2ranks_shared.err
 CONFIGS="2 3 4 5 6 7" bash tools/gpu_launches.sh > /dev/null 2>&1
 B="python bench.py --steps 2 --warmup 3 --no-cpu-baseline --soak-seconds 0 --clock-ms 0"
 ncu --set full --import-source on --clock-control none -k regex:"k_row_win" -s 1 -c 1 -o gpurun_out/full_c5 $B --config 5 > gpurun_out/ncu_full_c5.log 2>&1

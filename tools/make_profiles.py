@@ -30,7 +30,8 @@ def main(tag):
     os.makedirs(P, exist_ok=True)
     copies = {"gputests.log": f"{tag}_gpu_tests.txt", "smoke.log": f"{tag}_smoke.txt",
               "bench_default.json": f"{tag}_bench_default.json", "bench_reference.json": f"{tag}_bench_reference.json",
-              "rc_bench_all_configs.jsonl": f"{tag}_bench_all_configs.jsonl"}
+              "rc_bench_all_configs.jsonl": f"{tag}_bench_all_configs.jsonl",
+              "bench_2ranks_shared.json": f"{tag}_bench_2ranks_shared_gpu.json"}
     for src, dst in copies.items():
         if os.path.exists(os.path.join(G, src)):
             shutil.copy(os.path.join(G, src), os.path.join(P, dst))
