@@ -212,8 +212,9 @@ struct NumArgs {
     double tol;
     int *holes;
     // fused a7 (optional, part == nullptr: off): every kept edge (i,j) with
-    // j > i and part[i] != part[j] is added to a per-thread Neumaier sum; each
-    // CTA writes its sum to cutp[blockIdx.x] (deterministic order).
+    // j > i and part[i] != part[j] is added to a per-thread sum (CutSum in the
+    // merge kernels, Neumaier in the others); each CTA writes its sum to
+    // cutp[blockIdx.x] (deterministic order).
     const int32_t *part;
     int32_t K;
     double *cutp;

@@ -21,16 +21,18 @@
 //    never kept, since kept means |c| > drop_tol >= 0).  Invalid lanes of a
 //    unit carry j = -1, b = 0: never far, and near only on the slot of key
 //    -1, which no real key uses and which stays +0.0.
-//  * far keys are appended (key, a_jk, unit) to a far list in arrival (=
-//    ascending k) order.  The list is sorted stably by key: value buckets
-//    filled in arrival order; each lane then insertion-sorts its own short
-//    buckets (key ties keep arrival order), and the warp ranks the rare long
-//    bucket found out of order.  Equal keys are folded in arrival order.
-//  * count pass (kept: j != i and |c| > tol; the folded
-//    far values are kept for the emission), publish the count, then the
-//    emission writes far-below, window, far-above in ascending j; the row's
-//    cut edges (j > i, part[i] != part[j]) go to a per-row
-//    Neumaier sum, summed later in a fixed tree (deterministic).
+//  * far keys are appended (key << 6 | unit, a_jk) to a far list in arrival
+//    (= ascending k) order; the packed words are unique and ordered by (key,
+//    arrival), so sorting them is the stable key sort: value buckets filled
+//    in arrival order; each lane then insertion-sorts its own short buckets,
+//    and the warp ranks the rare long bucket found out of order.  Equal keys
+//    are folded in arrival order.
+//  * one pass folds, counts (kept: j != i and |c| > tol, PAPER.md:295-315,
+//    352) and writes the row in ascending j (far-below, window, far-above)
+//    to the warp's staging slot; the count is published, and the row is
+//    copied to its offset after the warp's next row; the row's cut edges (j
+//    > i, part[i] != part[j]) go to per-lane sums there,
+//    reduced in fixed trees (deterministic).
 //  * rows of more than 32 entries or more than kRwTcap units, and rows whose
 //    far list outgrows the shared one, run with their far list in a per-warp
 //    slice of global scratch (capacity >= the largest f_i, host-checked).
