@@ -608,7 +608,10 @@ __device__ __forceinline__ int emit_row(const RowArgs &a, RwSmem &S, const F_ &F
 // kCopyU rounds of loads in flight), and take the row's cut edges there (j >
 // i, part[j] != part[i]: PAPER.md:393-405) -- the part[] gathers are batched
 // with the copy instead of stalling the emission.
-constexpr int kCopyU = 3;  // 3 rounds of 32 per iteration: a config-5 row (~283 entries) is 3 iterations
+#ifndef RIG_RW_COPYU
+#define RIG_RW_COPYU 3
+#endif
+constexpr int kCopyU = RIG_RW_COPYU;  // 3 rounds of 32 per iteration: a config-5 row (~283 entries) is 3 iterations
 __device__ __forceinline__ void copy_staged(const RowArgs &a, const int32_t *scol, const double *sw, int n, int64_t g0,
                                             bool write, int i, int32_t pi, CutSum &acc) {
     const int l = lane_id();
