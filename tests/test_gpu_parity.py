@@ -212,6 +212,22 @@ def test_sym_transpose_path(rig):
     assert "sym path ok" in r.stdout
 
 
+def test_without_row_window(rig):
+    """The path without the row-window kernel (what n >= 2^25 rows take; forced
+    by RIG_ROWWIN=0 in a fresh process, tests/no_rowwin_check.py): the older
+    mid-row passes and the CTA accumulator, graph and cut vs the oracle."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, RIG_ROWWIN="0", PYTHONPATH=root)
+    r = subprocess.run([sys.executable, os.path.join(root, "tests", "no_rowwin_check.py")], env=env, cwd=root,
+                       capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-4000:]
+    assert "no-rowwin paths ok" in r.stdout
+
+
 def test_long_rows_and_columns(rig):
     """Mid-row (global far list), huge-row and long-column-sort paths."""
     rng = np.random.default_rng(11)
