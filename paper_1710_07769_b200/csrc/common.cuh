@@ -300,7 +300,7 @@ constexpr int kCutLaunches = 8;  // merge, mid small, mid big, huge (+ spare slo
 // a3 + a4(merge rows) fused: products, merge-row nnzC, bins for the others
 // bin8[r]: symbolic bin of row r, or kBinNone on the merge path;
 // ctr->sym_count / n_mid: bin totals.
-void launch_analyze_sym(const SymArgs &a, uint8_t *bin8, DevCounters *ctr, cudaStream_t s);
+void launch_analyze_sym(const SymArgs &a, uint8_t *bin8, DevCounters *ctr, bool warp_width, cudaStream_t s);
 // maxlen: longest A row on the merge path in the shard (DevCounters::max_len)
 void launch_sym_merge(const SymArgs &a, int maxlen, cudaStream_t s);
 void launch_num_merge(const NumArgs &a, int maxlen, cudaStream_t s);

@@ -26,6 +26,52 @@ static int g_sms_cache = 0;
 // folded in ascending k: c_ij = fma(a_ik, a_jk, c_ij) -- the ordered chain.
 // IdxT: int32 CSC offsets when nnz < 2^31 (fewer registers), else int64.
 // Columns end in an INT_MAX sentinel (csc_begin), so a run needs no end bound.
+// The same merge at width R for a row of len <= R entries (runs t >= len are
+// empty): a warp runs ONE width -- its longest merge row's -- instead of the
+// lanes of different lengths running their instantiations one after another.
+template <int R, typename IdxT>
+__device__ __forceinline__ int64_t sym_merge_row_w(const Csr &A, const Csc &T, int64_t s, int len, int2 *qs,
+                                                   int64_t *f_out) {
+    int32_t h[R];
+    IdxT q[R];
+    int64_t f = 0;
+    int32_t cl[R];
+#pragma unroll
+    for (int t = 0; t < R; ++t) {
+        q[t] = 0;
+        cl[t] = 0;
+        if (t < len) {
+            const int k = A.ci[s + t];
+            const int64_t c0 = T.cp[k], c1 = T.cp[k + 1];
+            q[t] = (IdxT)(c0 + k);
+            cl[t] = (int32_t)min(c1 - c0, (int64_t)INT32_MAX);
+            f += c1 - c0;
+        }
+    }
+    *f_out = f;
+    if (f > kMergeMaxF) return -1;
+    if (qs) {
+#pragma unroll
+        for (int t = 0; t < R; ++t)
+            if (t < len) qs[s + t] = make_int2((int32_t)q[t], cl[t]);
+    }
+#pragma unroll
+    for (int t = 0; t < R; ++t) h[t] = t < len ? T.ri[q[t]] : INT_MAX;
+    int64_t cnt = 0;
+    while (true) {
+        int m = h[0];
+#pragma unroll
+        for (int t = 1; t < R; ++t) m = min(m, h[t]);
+        if (m == INT_MAX) break;
+        ++cnt;
+#pragma unroll
+        for (int t = 0; t < R; ++t) {
+            if (h[t] == m) h[t] = T.ri[++q[t]];
+        }
+    }
+    return cnt;
+}
+
 template <int R, typename IdxT>
 __device__ __forceinline__ int64_t sym_merge_row(const Csr &A, const Csc &T, int64_t s, int2 *qs = nullptr,
                                                  int64_t *f_out = nullptr) {
@@ -529,8 +575,15 @@ static int sms() {
 // merge-path rows get their structural nnz(C_i) right away, the others are
 // binned by ceil(log2(2 f_i)): the mid bins go to the mid-row kernel (k_row_win in temp mode), the
 // huge bin (f_i > 2048) to the wide-window / global-far-list / CTA-per-row chain.
-template <typename IdxT>
-__global__ void __launch_bounds__(kMergeThreads) k_analyze_sym(SymArgs a, uint8_t *bin8, DevCounters *ctr) {
+// WW: merge width per warp (the warp's longest merge row) instead of per lane,
+// for shards whose row lengths vary inside a warp (power-law rows: every lane
+// length ran its instantiation in turn); 3 CTAs per SM leave it unspilled.
+// Measured: config 4 analysis 0.404 -> 0.268 ms; on stencils (uniform rows)
+// per lane is faster (config 3 0.685 vs 0.708 ms), so the host picks.  Per
+// lane at 4 CTAs per SM (64 registers, the width it was tuned at; 96 unbounded:
+// config 3 0.685 -> 0.852 ms).
+template <typename IdxT, bool WW>
+__global__ void __launch_bounds__(kMergeThreads, WW ? 3 : 4) k_analyze_sym(SymArgs a, uint8_t *bin8, DevCounters *ctr) {
     const int64_t nloc = a.re - a.rb;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     int64_t local = 0, nnzr = 0, maxf = 0, slots = 0;
@@ -575,21 +628,40 @@ __global__ void __launch_bounds__(kMergeThreads) k_analyze_sym(SymArgs a, uint8_
             part = warp_sum(part);
             if (lane == u) fi = part;
         }
+        const int len = valid ? (int)min(e - s, (int64_t)kMergeMaxLen + 1) : 0;
+        int64_t c = len == 0 ? 0 : -1;  // merge count (an empty row: 0); -1: off the merge path
+        if constexpr (WW) {
+            // merge width per warp: the longest merge row of the warp (rows of
+            // <= 8 entries: f_i and, if small enough, the count in one pass)
+            const int wl = (int)__reduce_max_sync(kFull, (unsigned)(len <= kMergeMaxLen ? len : 0));
+            if (len >= 1 && len <= kMergeMaxLen) {
+                switch (wl) {
+                    case 1: c = sym_merge_row_w<1, IdxT>(a.A, a.T, s, len, a.qs, &fi); break;
+                    case 2: c = sym_merge_row_w<2, IdxT>(a.A, a.T, s, len, a.qs, &fi); break;
+                    case 3: c = sym_merge_row_w<3, IdxT>(a.A, a.T, s, len, a.qs, &fi); break;
+                    case 4: c = sym_merge_row_w<4, IdxT>(a.A, a.T, s, len, a.qs, &fi); break;
+                    case 5: c = sym_merge_row_w<5, IdxT>(a.A, a.T, s, len, a.qs, &fi); break;
+                    case 6: c = sym_merge_row_w<6, IdxT>(a.A, a.T, s, len, a.qs, &fi); break;
+                    case 7: c = sym_merge_row_w<7, IdxT>(a.A, a.T, s, len, a.qs, &fi); break;
+                    default: c = sym_merge_row_w<8, IdxT>(a.A, a.T, s, len, a.qs, &fi); break;
+                }
+            }
+        } else {
+            if (!valid) continue;
+            switch (len) {  // rows of <= 8 entries: f_i and, if small enough, the count in one pass
+                case 1: c = sym_merge_row<1, IdxT>(a.A, a.T, s, a.qs, &fi); break;
+                case 2: c = sym_merge_row<2, IdxT>(a.A, a.T, s, a.qs, &fi); break;
+                case 3: c = sym_merge_row<3, IdxT>(a.A, a.T, s, a.qs, &fi); break;
+                case 4: c = sym_merge_row<4, IdxT>(a.A, a.T, s, a.qs, &fi); break;
+                case 5: c = sym_merge_row<5, IdxT>(a.A, a.T, s, a.qs, &fi); break;
+                case 6: c = sym_merge_row<6, IdxT>(a.A, a.T, s, a.qs, &fi); break;
+                case 7: c = sym_merge_row<7, IdxT>(a.A, a.T, s, a.qs, &fi); break;
+                case 8: c = sym_merge_row<8, IdxT>(a.A, a.T, s, a.qs, &fi); break;
+                default: break;
+            }
+        }
         if (!valid) continue;
         nnzr += e - s;
-        const int len = (int)min(e - s, (int64_t)kMergeMaxLen + 1);
-        int64_t c = len == 0 ? 0 : -1;  // merge count (an empty row: 0); -1: off the merge path
-        switch (len) {  // rows of <= 8 entries: f_i and, if small enough, the count in one pass
-            case 1: c = sym_merge_row<1, IdxT>(a.A, a.T, s, a.qs, &fi); break;
-            case 2: c = sym_merge_row<2, IdxT>(a.A, a.T, s, a.qs, &fi); break;
-            case 3: c = sym_merge_row<3, IdxT>(a.A, a.T, s, a.qs, &fi); break;
-            case 4: c = sym_merge_row<4, IdxT>(a.A, a.T, s, a.qs, &fi); break;
-            case 5: c = sym_merge_row<5, IdxT>(a.A, a.T, s, a.qs, &fi); break;
-            case 6: c = sym_merge_row<6, IdxT>(a.A, a.T, s, a.qs, &fi); break;
-            case 7: c = sym_merge_row<7, IdxT>(a.A, a.T, s, a.qs, &fi); break;
-            case 8: c = sym_merge_row<8, IdxT>(a.A, a.T, s, a.qs, &fi); break;
-            default: break;
-        }
         local += fi;
         if (len <= kMergeMaxLen && c >= 0) {
             maxlen = max(maxlen, len);
@@ -657,14 +729,19 @@ __global__ void __launch_bounds__(kMergeThreads) k_analyze_sym(SymArgs a, uint8_
     }
 }
 
-void launch_analyze_sym(const SymArgs &a, uint8_t *bin8, DevCounters *ctr, cudaStream_t s) {
+void launch_analyze_sym(const SymArgs &a, uint8_t *bin8, DevCounters *ctr, bool warp_width, cudaStream_t s) {
     const int64_t nloc = a.re - a.rb;
     int64_t g = (nloc + kMergeThreads - 1) / kMergeThreads;
     g = g < 1 ? 1 : (g > (int64_t)sms() * 16 ? (int64_t)sms() * 16 : g);
-    if (csc_fits_i32(a.A))
-        k_analyze_sym<int32_t><<<(unsigned)g, kMergeThreads, 0, s>>>(a, bin8, ctr);
+    const bool i32 = csc_fits_i32(a.A);
+    if (warp_width && i32)
+        k_analyze_sym<int32_t, true><<<(unsigned)g, kMergeThreads, 0, s>>>(a, bin8, ctr);
+    else if (warp_width)
+        k_analyze_sym<int64_t, true><<<(unsigned)g, kMergeThreads, 0, s>>>(a, bin8, ctr);
+    else if (i32)
+        k_analyze_sym<int32_t, false><<<(unsigned)g, kMergeThreads, 0, s>>>(a, bin8, ctr);
     else
-        k_analyze_sym<int64_t><<<(unsigned)g, kMergeThreads, 0, s>>>(a, bin8, ctr);
+        k_analyze_sym<int64_t, false><<<(unsigned)g, kMergeThreads, 0, s>>>(a, bin8, ctr);
     note_launch();
 }
 

@@ -539,6 +539,9 @@ static void plan_build(rig_plan *p, const rig_csr_t *Ain, bool allow_early = fal
     }
     // a3 + a4 (merge rows): products, merge-row nnzC, paths of the others
     p->qs = use_qs ? reinterpret_cast<int2 *>(ws + o_qs) : nullptr;
+    // analysis merge width per warp when row lengths vary widely (some rows
+    // off the merge path: power-law shards), per lane otherwise (k_spgemm.cu)
+    bool an_warp_width = false;
     if (ev_shape && rowwin_ok(p->A)) {
         // row-window path decided from the shape statistics alone (read back
         // while the transpose runs): every row longer than the merge path
@@ -548,6 +551,7 @@ static void plan_build(rig_plan *p, const rig_csr_t *Ain, bool allow_early = fal
         const DevCounters &sh = hs->shape;
         const int64_t min_row = sh.min_row_c ? kMinRowBias - sh.min_row_c : 0;
         const int64_t fbound = sh.max_row * sh.max_col;
+        an_warp_width = sh.max_row > kMergeMaxLen;
         if (nloc > 0 && min_row > kMergeMaxLen && fbound <= kRowWinEarlyBound) {
             p->early = true;
             p->rowwin = true;
@@ -564,7 +568,7 @@ static void plan_build(rig_plan *p, const rig_csr_t *Ain, bool allow_early = fal
     SymArgs sa{p->A, p->T, p->rb, p->re, p->nnzc, fnm, p->qs};
     if (nloc > 0) {
         Prof pf(P_ANALYZE, s);
-        launch_analyze_sym(sa, bin8, p->ctr, s);
+        launch_analyze_sym(sa, bin8, p->ctr, an_warp_width, s);
     }
     check_launch("analyze");
     if (ev_shape) {
