@@ -60,7 +60,10 @@ constexpr int kRwGNB = 512;          // sort buckets (global mode)
 #define RIG_RW_TCAP 40
 #endif
 constexpr int kRwTcap = RIG_RW_TCAP; // units per table fill
-constexpr int kRwSmallBucket = 8;    // buckets up to this size: per-lane insertion sort
+#ifndef RIG_RW_SMALLB
+#define RIG_RW_SMALLB 8
+#endif
+constexpr int kRwSmallBucket = RIG_RW_SMALLB;  // buckets up to this size: per-lane insertion sort
 constexpr int kRwStageCap = 512;     // entries per staging slot (>= kRwFcap + kRwW); slots are 128-byte aligned
 #ifndef RIG_RW_DISCARD
 #define RIG_RW_DISCARD 1
