@@ -217,6 +217,9 @@ __global__ void k_bucket_init(const int64_t *__restrict__ cp, int64_t nb, int sh
 #ifndef RIG_RANK_U4
 #define RIG_RANK_U4 1
 #endif
+#ifndef RIG_SMALL_RANK
+#define RIG_SMALL_RANK 1  // small buckets: rank (1) or per-lane insertion sorts (0; measured)
+#endif
 constexpr int kSortThreads = 64;  // 2 warps: one bucket per warp
 constexpr int kSortWarps = kSortThreads / 32;
 
@@ -446,7 +449,7 @@ void launch_transpose(const Csr &A, int scale, const int64_t *cp, double *ahat, 
         const int64_t mean_bucket = A.nnz / (nb > 0 ? nb : 1) + (1 << shift);
         const bool small = (1 << shift) <= kSmallBucketCols && mean_bucket <= kSmallBucketSlots * 3 / 4;
         if (A.nnz > (int64_t)12 * A.ncols && small)
-            k_bucket_sort<true, kSmallBucketSlots, kSmallBucketCols><<<(unsigned)std::min<int64_t>(
+            k_bucket_sort<RIG_SMALL_RANK != 0, kSmallBucketSlots, kSmallBucketCols><<<(unsigned)std::min<int64_t>(
                                                                           (nb + kSortWarps - 1) / kSortWarps,
                                                                           (int64_t)num_sms() * 24),
                                                                       kSortThreads, 0, s>>>(
